@@ -1,0 +1,198 @@
+/*
+ * reattn_cuda.h — the C-ABI boundary of the B200-native ReAttention hot path.
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.  Every
+ * function returns a reattn_status; on failure reattn_last_error(ctx) holds the message,
+ * worded exactly as the reference's exception (so the C++ shim in include/reattn/ can
+ * rethrow the same type and text).
+ *
+ * Each entry point replaces one reference function of
+ * /root/reference/proj/include/reattn/ (cited per declaration).  The reference has no FFI
+ * of its own: its boundary is the header-only C++ API, which include/reattn/*.hpp
+ * re-creates on top of this ABI.
+ *
+ * Device pointers ("_dev") are CUDA global memory of the context's device; all work is
+ * enqueued on the context's stream.  Functions documented "synchronous" return after the
+ * stream drained.  The whole hot path (scan -> vote/spans/scope -> attention) runs
+ * without host round trips and can be captured in a CUDA graph (reattn_plan_*).
+ */
+#ifndef REATTN_CUDA_H
+#define REATTN_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define REATTN_ABI_VERSION 1
+
+typedef struct reattn_ctx reattn_ctx;
+typedef struct reattn_cache reattn_cache;
+typedef struct reattn_rope reattn_rope;
+typedef struct reattn_plan reattn_plan;
+
+typedef enum {
+    REATTN_OK = 0,
+    REATTN_EINVAL = 1,   /* std::invalid_argument */
+    REATTN_ERANGE = 2,   /* std::out_of_range */
+    REATTN_ELOGIC = 3,   /* std::logic_error */
+    REATTN_ECUDA = 4,    /* CUDA runtime / device failure */
+    REATTN_ERUNTIME = 5  /* std::runtime_error */
+} reattn_status;
+
+typedef enum { REATTN_F32 = 0, REATTN_BF16 = 1 } reattn_dtype;
+typedef enum { REATTN_SPAN_ALIGNED = 0, REATTN_SPAN_CENTERED = 1 } reattn_span_mode;
+/* model.hpp:19 AttentionMode */
+typedef enum { REATTN_MODE_FULL = 0, REATTN_MODE_WINDOW = 1, REATTN_MODE_REATTENTION = 2 } reattn_mode;
+/* Lane arithmetic of the fp32 score dot (dense_matrix.hpp:41-56); the reference compiles
+ * `l += a*b` either unfused or as an FMA depending on compiler/ISA/d. */
+typedef enum { REATTN_LANES_UNFUSED = 0, REATTN_LANES_FMA = 1 } reattn_lanes;
+
+/* selection.hpp:127-152 SelectionConfig (tile_size only bounds the reference's CPU scratch;
+ * it never changes results and is ignored here). */
+typedef struct {
+    uint64_t k, k_prime, span_m, tile_size, l_global, l_local, l_chunk;
+    int32_t span_mode;
+    int32_t reserved;
+} reattn_selection_config;
+
+/* engine.hpp:481-495 RunStats (per step; the C++ shim folds it into the caller's RunStats) */
+typedef struct {
+    uint64_t max_position_used;
+    uint64_t ood_positions;
+    int32_t coverage_total;
+    int32_t reserved;
+    double entropy_max;
+    double entropy_sum;
+    uint64_t entropy_rows;
+    uint64_t scope_len;
+    uint64_t n_spans;
+    uint64_t coverage;
+    uint64_t peak_scratch_bytes;
+} reattn_step_stats;
+
+/* ---- context --------------------------------------------------------------------- */
+const char* reattn_version(void);
+int reattn_ctx_create(int device, reattn_ctx** out);
+void reattn_ctx_destroy(reattn_ctx* ctx);
+const char* reattn_last_error(const reattn_ctx* ctx);
+int reattn_ctx_set_stream(reattn_ctx* ctx, void* cuda_stream);
+void* reattn_ctx_stream(const reattn_ctx* ctx);
+int reattn_ctx_set_lanes(reattn_ctx* ctx, int lanes);
+int reattn_ctx_synchronize(reattn_ctx* ctx);
+int reattn_ctx_num_sms(const reattn_ctx* ctx);
+/* device memory helpers for callers without their own allocator (the C++ shim) */
+int reattn_malloc(reattn_ctx* ctx, uint64_t bytes, void** out_dev);
+int reattn_free(reattn_ctx* ctx, void* dev);
+int reattn_memcpy_h2d(reattn_ctx* ctx, void* dst_dev, const void* src_host, uint64_t bytes);
+int reattn_memcpy_d2h(reattn_ctx* ctx, void* dst_host, const void* src_dev, uint64_t bytes);
+
+/* ---- device KV cache: kv_cache.hpp:38-118 SegmentedKvCache ------------------------ */
+/* Head-major [n_kv][capacity][d] storage of `dtype` for K and V; indices are append rank. */
+int reattn_cache_create(reattn_ctx* ctx, uint64_t n_kv, uint64_t d, uint64_t l_global,
+                        uint64_t l_local_max, uint64_t capacity, int dtype, reattn_cache** out);
+void reattn_cache_destroy(reattn_cache* cache);
+/* Grow the storage to new_capacity rows per head (existing rows are kept). */
+int reattn_cache_reserve(reattn_ctx* ctx, reattn_cache* cache, uint64_t new_capacity);
+/* kv_cache.hpp:54-68 append: rows x (n_kv*d) fp32 in DenseMatrix layout (host or device). */
+int reattn_cache_append(reattn_ctx* ctx, reattn_cache* cache, const float* keys,
+                        const float* values, uint64_t rows, int src_on_device);
+/* Declare `total` rows already written into the storage (bulk fills, e.g. benchmarks). */
+int reattn_cache_set_total(reattn_ctx* ctx, reattn_cache* cache, uint64_t total);
+/* kv_cache.hpp:70-87 accessors */
+int reattn_cache_info(const reattn_cache* cache, uint64_t* n_kv, uint64_t* d, uint64_t* l_global,
+                      uint64_t* l_local_max, uint64_t* capacity, uint64_t* total,
+                      uint64_t* global_end, uint64_t* local_start, int* dtype);
+void* reattn_cache_keys(const reattn_cache* cache);
+void* reattn_cache_values(const reattn_cache* cache);
+
+/* ---- rotary table: rope.hpp:317-366 RotaryTable ----------------------------------- */
+int reattn_rope_create(reattn_ctx* ctx, uint64_t head_dim, double base, uint64_t max_position,
+                       reattn_rope** out);
+void reattn_rope_destroy(reattn_rope* rope);
+/* host copies of the float tables [max_position][head_dim/2] (may be NULL) */
+int reattn_rope_tables_host(const reattn_rope* rope, float* cos_host, float* sin_host);
+/* rope.hpp:368-377 rope_rotate on device rows [n_rows][head_dim]; positions on the host.
+ * Synchronous.  Position >= max_position -> REATTN_ERANGE "position out of pretrained range". */
+int reattn_rope_rotate(reattn_ctx* ctx, const reattn_rope* rope, float* rows_dev,
+                       const uint64_t* positions_host, uint64_t n_rows);
+
+/* ---- selection: selection.hpp:275-456 --------------------------------------------- */
+/* fused_topk_scores (selection.hpp:275).  q_dev: [n_q][n_heads*d] fp32.  keys_dev: head-major
+ * [n_kv][head_stride][d] of key_dtype, middle row 0 at row `row0` of every head, `count`
+ * middle rows.  Outputs [n_kv][n_q][k] (score desc, index asc); *n_out = min(k, count).
+ * *scratch_bytes = device workspace of the call (constant in `count`).  Synchronous. */
+int reattn_fused_topk(reattn_ctx* ctx, const float* q_dev, uint64_t n_q, uint64_t n_heads,
+                      const void* keys_dev, int key_dtype, uint64_t n_kv, uint64_t head_stride,
+                      uint64_t row0, uint64_t count, uint64_t d, uint64_t k,
+                      uint32_t* idx_out_dev, float* score_out_dev, uint64_t* n_out,
+                      uint64_t* scratch_bytes);
+/* tally_candidates + vote (selection.hpp:359-393) over a flat candidate list.  Synchronous. */
+int reattn_vote(reattn_ctx* ctx, const uint32_t* idx_dev, const float* score_dev, uint64_t n,
+                uint64_t k_prime, uint32_t* winners_dev, uint64_t* n_winners);
+/* tally_candidates (selection.hpp:359-383): every distinct index, ranked by (votes desc,
+ * max score desc, index asc), with its votes and max score.  Synchronous. */
+int reattn_tally(reattn_ctx* ctx, const uint32_t* idx_dev, const float* score_dev, uint64_t n,
+                 uint32_t* idx_out_dev, uint32_t* votes_out_dev, float* score_out_dev,
+                 uint64_t* n_unique);
+/* expand_spans (selection.hpp:425-456).  Synchronous. */
+int reattn_expand_spans(reattn_ctx* ctx, const uint32_t* winners_dev, uint64_t n, uint64_t span_m,
+                        uint64_t middle_len, int span_mode, uint32_t* begin_dev,
+                        uint32_t* end_dev, uint64_t* n_spans);
+
+/* ---- scope + attention ------------------------------------------------------------ */
+/* assemble_scope (scope.hpp:248-289).  Spans index the middle.  src_dev receives the
+ * scope-row -> cache-row table (capacity >= window); keys/values_out_dev (nullable)
+ * receive fp32 [n_kv][L][d] copies.  Synchronous. */
+int reattn_assemble_scope(reattn_ctx* ctx, const reattn_cache* cache, const uint32_t* span_b_dev,
+                          const uint32_t* span_e_dev, uint64_t n_spans, uint64_t window,
+                          uint32_t* src_dev, float* keys_out_dev, float* values_out_dev,
+                          uint64_t* length);
+/* attend (attend.hpp:404-456).  q [n_q][d], k [L][d], v [L][dv] fp32 device rows;
+ * out [n_q][dv], entropy [n_q] (f64).  Synchronous. */
+int reattn_attend(reattn_ctx* ctx, const float* q_dev, uint64_t n_q, const float* k_dev,
+                  const float* v_dev, uint64_t L, uint64_t d, uint64_t dv, int has_boundary,
+                  uint64_t boundary, float* out_dev, double* entropy_dev);
+/* attend_step (engine.hpp:501-572): selection (gated as engine.hpp:516), scope, RoPE at
+ * compact positions, attention.  q_dev [n_q][n_head*d] pre-rotation; out_dev
+ * [n_q][n_head*d].  span_b/e_host (nullable, capacity >= k_prime) receive the spans,
+ * entropy_host (nullable, [n_q][n_head]) the row entropies.  Synchronous. */
+int reattn_attend_step(reattn_ctx* ctx, const reattn_cache* cache, const reattn_rope* rope,
+                       const float* q_dev, uint64_t n_q, uint64_t n_head,
+                       const reattn_selection_config* cfg, int mode, float* out_dev,
+                       reattn_step_stats* stats, uint64_t* span_b_host, uint64_t* span_e_host,
+                       double* entropy_host);
+
+/* ---- plans: one attend_step shape captured as a CUDA graph ------------------------ */
+/* The plan owns its q/out device buffers and workspace; launching it replays the whole
+ * step (scan, vote/spans/scope, attention, combine) with no host synchronisation. */
+int reattn_plan_create(reattn_ctx* ctx, const reattn_cache* cache, const reattn_rope* rope,
+                       uint64_t n_q, uint64_t n_head, const reattn_selection_config* cfg,
+                       int mode, reattn_plan** out);
+void reattn_plan_destroy(reattn_plan* plan);
+float* reattn_plan_q(const reattn_plan* plan);
+float* reattn_plan_out(const reattn_plan* plan);
+/* asynchronous replay on the context stream */
+int reattn_plan_launch(reattn_plan* plan);
+/* enqueue only the plan's K-scan kernel (no graph) so callers can time it with events */
+int reattn_plan_launch_scan(reattn_plan* plan);
+/* end to end from host memory: H2D q, replay, D2H out, synchronise */
+int reattn_plan_run_host(reattn_plan* plan, const float* q_host, float* out_host);
+/* synchronise and read the last replay's stats (errors surface here) */
+int reattn_plan_stats(reattn_plan* plan, reattn_step_stats* stats);
+/* kernels per replay, and the algorithmic bytes of the dominant kernel (the K scan) */
+int reattn_plan_info(const reattn_plan* plan, uint64_t* kernels_per_step,
+                     uint64_t* scan_bytes, uint64_t* scope_bytes);
+
+/* ---- synthetic inputs (tests and benchmarks; not on the hot path) ---------------- */
+/* dst[i] = splitmix64(seed, offset+i) mapped to [-1, 1) (24 significant bits), stored as
+ * fp32 or bf16 (round to nearest even). */
+int reattn_synth_uniform(reattn_ctx* ctx, void* dst_dev, uint64_t n, int dtype, uint64_t seed,
+                         uint64_t offset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* REATTN_CUDA_H */

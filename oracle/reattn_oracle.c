@@ -412,6 +412,18 @@ int oracle_attend_step(const float* q_pre, size_t n_q, size_t n_head, const floa
     return ORACLE_OK;
 }
 
+/* Host twin of the library's synthetic generator (misc.cu synth_value). */
+void oracle_synth_uniform(uint64_t seed, uint64_t offset, uint64_t n, float* out, int bf16) {
+    for (uint64_t e = 0; e < n; ++e) {
+        uint64_t z = seed * 0x9E3779B97F4A7C15ull + (offset + e) + 0x632BE59BD9B4E019ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const float v = (float)(z >> 40) * (1.0f / 8388608.0f) - 1.0f;
+        out[e] = bf16 ? oracle_round_bf16(v) : v;
+    }
+}
+
 float oracle_round_bf16(float x) {
     uint32_t u;
     memcpy(&u, &x, 4);

@@ -102,6 +102,9 @@ int oracle_attend_step(const float* q_pre, size_t n_q, size_t n_head, const floa
 
 /* bf16 round-to-nearest-even of an fp32 value, returned as fp32 (test input helper). */
 float oracle_round_bf16(float x);
+/* splitmix64(seed, offset+i) -> [-1, 1) (24 significant bits), optionally bf16-rounded;
+ * identical to the library's reattn_synth_uniform (test/bench input generator). */
+void oracle_synth_uniform(uint64_t seed, uint64_t offset, uint64_t n, float* out, int bf16);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,675 @@
+// K4+K5 — scope gather + RoPE at compact positions + finite-scope attention, split-KV.
+//
+// Restates (reference /root/reference/proj/include/reattn/):
+//   assemble_scope copies        scope.hpp:274-287  (fused: rows are gathered straight from
+//                                                    the cache through the scope table)
+//   RotaryTable::rotate_row      rope.hpp:347-358   (keys at compact i, queries at L'-n_q+i,
+//                                                    engine.hpp:536-551; unfused fp32 ops)
+//   attend                       attend.hpp:404-456 (scale 1/sqrt(d) in double, causal
+//                                                    boundary, f64 state incl. the entropy
+//                                                    numerator B = sum (s-m) e^{s-m})
+//   dot_f64                      dense_matrix.hpp:59-74 (exact 8-lane order, so logits are
+//                                                    bit-identical for identical inputs)
+// Each CTA owns one KV head, a block of query rows (GQA-packed: every q head of the group
+// shares the gathered K/V rows) and a contiguous range of scope rows, processed in chunks
+// of kAttnSplit rows with an online (m, A, B, acc) merge.  Partial states of the key
+// ranges are merged by attend_combine in split order (deterministic).
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace reattn_dev;
+
+namespace reattn_impl {
+
+namespace {
+
+constexpr int kAttnThreads = 256;
+constexpr int kQRows = 16;  // query rows per CTA (>= group)
+
+struct AttnLaunch {
+    AttnArgs a;
+    int qb;          // query positions per CTA
+    int qr;          // query rows per CTA = qb * group
+    int n_qblocks;
+    int n_splits;
+    int chunks_per_split;
+    int direct;      // n_splits == 1: write the final output directly
+};
+
+__device__ __forceinline__ uint32_t scope_len(const AttnArgs& a) {
+    return a.hdr ? a.hdr->L : a.L_host;
+}
+
+template <typename T>
+__device__ __forceinline__ float ld_elem(const void* base, size_t i) {
+    return load_as_float<T>((const T*)base + i);
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(kAttnThreads) attend_split_kernel(const AttnLaunch P) {
+    const AttnArgs& a = P.a;
+    if (a.hdr && a.hdr->error != 0) return;
+    const uint32_t L = scope_len(a);
+    const int split = blockIdx.x, kv = blockIdx.y, qblk = blockIdx.z;
+    const int d = a.d, dv = a.dv, G = a.group, QR = P.qr;
+    const int KS = d + 1;  // padded smem row strides (bank-conflict-free scalar access)
+    const int VS = dv;
+    const uint32_t key_begin = (uint32_t)split * P.chunks_per_split * kAttnSplit;
+    extern __shared__ double asm_[];
+    double* lg = asm_;                              // [QR][kAttnSplit]
+    double* acc = lg + QR * kAttnSplit;             // [QR][dv]
+    double* st = acc + (size_t)QR * dv;             // [QR][3] m, A, B
+    float* qs = (float*)(st + QR * 3);              // [QR][KS]
+    float* ks = qs + QR * KS;                       // [kAttnSplit][KS]
+    float* vs = ks + kAttnSplit * KS;               // [kAttnSplit][VS]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = kAttnThreads / 32;
+    const uint32_t boundary = a.boundary_is_tail ? (L - (uint32_t)a.n_q) : a.boundary_host;
+    const double scale = 1.0 / sqrt((double)d);
+
+    // ---- queries: rotated at L'-n_q+i (engine.hpp:546-551) ----
+    const int half = d / 2;
+    for (int e = tid; e < QR * d; e += kAttnThreads) {
+        const int r = e / d, c = e % d;
+        const int i = qblk * P.qb + r / G;
+        const int h = kv * G + r % G;
+        float val = 0.0f;
+        if (i < a.n_q) {
+            const float* qrow = a.q + (size_t)i * a.q_row_stride + (size_t)h * d;
+            if (a.rope_cos && c < 2 * half) {
+                const int j = c >> 1;
+                const uint32_t pos = L - (uint32_t)a.n_q + (uint32_t)i;
+                const float cs = a.rope_cos[(size_t)pos * half + j];
+                const float sn = a.rope_sin[(size_t)pos * half + j];
+                const float x = qrow[2 * j], y = qrow[2 * j + 1];
+                val = (c & 1) ? __fadd_rn(__fmul_rn(x, sn), __fmul_rn(y, cs))
+                              : __fsub_rn(__fmul_rn(x, cs), __fmul_rn(y, sn));
+            } else {
+                val = qrow[c];
+            }
+        }
+        qs[r * KS + c] = val;
+    }
+    for (int e = tid; e < QR * dv; e += kAttnThreads) acc[e] = 0.0;
+    for (int r = tid; r < QR; r += kAttnThreads) {
+        st[r * 3 + 0] = -INFINITY;
+        st[r * 3 + 1] = 0.0;
+        st[r * 3 + 2] = 0.0;
+    }
+    __syncthreads();
+
+    for (int ch = 0; ch < P.chunks_per_split; ++ch) {
+        const uint32_t k0 = key_begin + (uint32_t)ch * kAttnSplit;
+        if (k0 >= L) break;
+        const int nk = (int)min((uint32_t)kAttnSplit, L - k0);
+        // ---- gather K (rotated at compact position) and V rows (scope.hpp:282-286) ----
+        for (int e = tid; e < nk * d; e += kAttnThreads) {
+            const int r = e / d, c = e % d;
+            const uint32_t sr = k0 + r;
+            const uint32_t cr = a.src ? a.src[sr] : sr;
+            const size_t rowb = ((size_t)kv * a.head_stride + cr) * d;
+            float val;
+            if (a.rope_cos && c < 2 * half) {
+                const int j = c >> 1;
+                const float x = ld_elem<KT>(a.k_base, rowb + 2 * j);
+                const float y = ld_elem<KT>(a.k_base, rowb + 2 * j + 1);
+                const float cs = a.rope_cos[(size_t)sr * half + j];
+                const float sn = a.rope_sin[(size_t)sr * half + j];
+                val = (c & 1) ? __fadd_rn(__fmul_rn(x, sn), __fmul_rn(y, cs))
+                              : __fsub_rn(__fmul_rn(x, cs), __fmul_rn(y, sn));
+            } else {
+                val = ld_elem<KT>(a.k_base, rowb + c);
+            }
+            ks[r * KS + c] = val;
+        }
+        for (int e = tid; e < nk * dv; e += kAttnThreads) {
+            const int r = e / dv, c = e % dv;
+            const uint32_t sr = k0 + r;
+            const uint32_t cr = a.src ? a.src[sr] : sr;
+            vs[r * VS + c] = ld_elem<KT>(a.v_base, ((size_t)kv * a.head_stride + cr) * dv + c);
+        }
+        __syncthreads();
+        // ---- logits: exact dot_f64 lane order, times 1/sqrt(d) (attend.hpp:430) ----
+        for (int e = tid; e < QR * kAttnSplit; e += kAttnThreads) {
+            const int r = e / kAttnSplit, j = e % kAttnSplit;
+            const int i = qblk * P.qb + r / G;
+            double s = -INFINITY;
+            const uint32_t key = k0 + j;
+            const bool vis = j < nk && i < a.n_q &&
+                             (!a.causal || (uint64_t)key < (uint64_t)boundary + i + 1);
+            if (vis) {
+                const float* qv = qs + r * KS;
+                const float* kr = ks + j * KS;
+                double l[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                int c = 0;
+                for (; c + 8 <= d; c += 8) {
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) l[t] = fma((double)qv[c + t], (double)kr[c + t], l[t]);
+                }
+                for (; c < d; ++c) l[0] = fma((double)qv[c], (double)kr[c], l[0]);
+                s = (((l[0] + l[1]) + (l[2] + l[3])) + ((l[4] + l[5]) + (l[6] + l[7]))) * scale;
+            }
+            lg[r * kAttnSplit + j] = s;
+        }
+        __syncthreads();
+        // ---- online softmax update per row (attend.hpp:432-447) ----
+        for (int r = warp; r < QR; r += nwarps) {
+            double mx = -INFINITY;
+            for (int j = lane; j < nk; j += 32) mx = fmax(mx, lg[r * kAttnSplit + j]);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, off));
+            const double m_old = st[r * 3 + 0];
+            const double m_new = fmax(m_old, mx);
+            double sa = 0.0, sb = 0.0;
+            if (m_new != -INFINITY) {
+                for (int j = lane; j < nk; j += 32) {
+                    const double s = lg[r * kAttnSplit + j];
+                    double w = 0.0;
+                    if (s != -INFINITY) {
+                        w = exp(s - m_new);
+                        sa += w;
+                        sb += (s - m_new) * w;
+                    }
+                    lg[r * kAttnSplit + j] = w;
+                }
+            } else {
+                for (int j = lane; j < nk; j += 32) lg[r * kAttnSplit + j] = 0.0;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                sa += __shfl_xor_sync(0xFFFFFFFFu, sa, off);
+                sb += __shfl_xor_sync(0xFFFFFFFFu, sb, off);
+            }
+            double rs = 1.0;
+            if (lane == 0) {
+                const double A = st[r * 3 + 1], B = st[r * 3 + 2];
+                if (m_new == -INFINITY) {
+                    rs = 1.0;
+                } else if (A == 0.0) {
+                    st[r * 3 + 1] = sa;
+                    st[r * 3 + 2] = sb;
+                    rs = 0.0;
+                } else {
+                    rs = exp(m_old - m_new);
+                    st[r * 3 + 1] = A * rs + sa;
+                    st[r * 3 + 2] = rs * (B + (m_old - m_new) * A) + sb;
+                }
+                st[r * 3 + 0] = m_new;
+            }
+            rs = __shfl_sync(0xFFFFFFFFu, rs, 0);
+            for (int c = lane; c < dv; c += 32) acc[r * dv + c] *= rs;
+        }
+        __syncthreads();
+        // ---- value accumulation (attend.hpp:436, :445) ----
+        for (int e = tid; e < QR * dv; e += kAttnThreads) {
+            const int r = e / dv, c = e % dv;
+            const double* w = lg + r * kAttnSplit;
+            double s = acc[e];
+            for (int j = 0; j < nk; ++j) s = fma(w[j], (double)vs[j * VS + c], s);
+            acc[e] = s;
+        }
+        __syncthreads();
+    }
+
+    // ---- emit: final output (single split) or the partial state ----
+    for (int e = tid; e < QR * dv; e += kAttnThreads) {
+        const int r = e / dv, c = e % dv;
+        const int i = qblk * P.qb + r / G;
+        if (i >= a.n_q) continue;
+        const int g = r % G;
+        if (P.direct) {
+            const double A = st[r * 3 + 1];
+            a.out[(size_t)i * a.n_head * dv + (size_t)(kv * G + g) * dv + c] = (float)(acc[e] / A);
+        } else {
+            const size_t row = ((size_t)split * a.n_kv + kv) * ((size_t)a.n_q * G) + (size_t)i * G + g;
+            double* p = a.part + row * (3 + dv);
+            p[3 + c] = acc[e];
+            if (c == 0) {
+                p[0] = st[r * 3 + 0];
+                p[1] = st[r * 3 + 1];
+                p[2] = st[r * 3 + 2];
+            }
+        }
+    }
+    if (P.direct) {
+        for (int r = tid; r < QR; r += kAttnThreads) {
+            const int i = qblk * P.qb + r / G;
+            if (i >= a.n_q) continue;
+            const double A = st[r * 3 + 1], B = st[r * 3 + 2];
+            const double h = log(A) - B / A;
+            a.entropy[(size_t)i * a.n_head + kv * G + r % G] = h < 0.0 ? 0.0 : h;
+        }
+    }
+}
+
+// merge the split partials of one (query, head) row in split order
+__global__ void __launch_bounds__(128) attend_combine_kernel(const AttnLaunch P) {
+    const AttnArgs& a = P.a;
+    if (a.hdr && a.hdr->error != 0) return;
+    const uint32_t L = scope_len(a);
+    const int i = blockIdx.x / a.n_head, h = blockIdx.x % a.n_head;
+    const int kv = h / a.group, g = h % a.group;
+    const int dv = a.dv;
+    const uint32_t keys_per_split = (uint32_t)P.chunks_per_split * kAttnSplit;
+    const int ns = (int)min((uint32_t)P.n_splits, (L + keys_per_split - 1) / keys_per_split);
+    __shared__ double s_w[1024];
+    __shared__ double s_res[3];
+    if (threadIdx.x == 0) {
+        double M = -INFINITY;
+        for (int s = 0; s < ns; ++s) {
+            const size_t row = ((size_t)s * a.n_kv + kv) * ((size_t)a.n_q * a.group) + (size_t)i * a.group + g;
+            const double* p = a.part + row * (3 + dv);
+            if (p[1] > 0.0) M = fmax(M, p[0]);
+        }
+        double A = 0.0, B = 0.0;
+        for (int s = 0; s < ns; ++s) {
+            const size_t row = ((size_t)s * a.n_kv + kv) * ((size_t)a.n_q * a.group) + (size_t)i * a.group + g;
+            const double* p = a.part + row * (3 + dv);
+            double w = 0.0;
+            if (p[1] > 0.0) {
+                w = exp(p[0] - M);
+                A += p[1] * w;
+                B += w * (p[2] + (p[0] - M) * p[1]);
+            }
+            if (s < 1024) s_w[s] = w;
+        }
+        s_res[0] = A;
+        s_res[1] = B;
+        const double hh = log(A) - B / A;
+        a.entropy[(size_t)i * a.n_head + h] = hh < 0.0 ? 0.0 : hh;
+    }
+    __syncthreads();
+    const double A = s_res[0];
+    for (int c = threadIdx.x; c < dv; c += blockDim.x) {
+        double acc = 0.0;
+        for (int s = 0; s < ns; ++s) {
+            const double w = s_w[s];
+            if (w == 0.0) continue;
+            const size_t row = ((size_t)s * a.n_kv + kv) * ((size_t)a.n_q * a.group) + (size_t)i * a.group + g;
+            acc = fma(a.part[row * (3 + dv) + 3 + c], w, acc);
+        }
+        a.out[(size_t)i * a.n_head * dv + (size_t)h * dv + c] = (float)(acc / A);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Decode specialisation (n_q == 1, d == dv == 128, group <= 8): one CTA per (32-row slice
+// of the scope, kv head).  16-byte vectorised gathers through the scope table with RoPE
+// applied in registers; logits in f64 with the exact dot_f64 lane order: four threads per
+// key, each owning two of the eight lanes for every q head of the GQA group (each K element
+// is converted to f64 once and reused by the whole group), the fixed reduction tree
+// finished with two shuffles; f64 softmax state.  Slice partials are merged by
+// attend_decode_combine.
+constexpr int kDecChunk = 32;
+constexpr int kDecThreads = 128;
+constexpr int kDecD = 128;
+constexpr int kDecKSF = kDecD + 8;   // fp32 K row stride (conflict-free LDS.64 per half-warp)
+constexpr int kDecPart = kDecD + 4;  // partial row: m, A, B, pad, acc[128] (16-B aligned)
+
+struct DecodeArgs {
+    AttnArgs a;
+    int n_chunks;  // grid.x (upper bound from L_max)
+};
+
+template <typename KT>
+__device__ __forceinline__ void load8(const KT* p, float (&v)[8]);
+template <>
+__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float (&v)[8]) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        v[2 * i] = __uint_as_float(u[i] << 16);
+        v[2 * i + 1] = __uint_as_float(u[i] & 0xFFFF0000u);
+    }
+}
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, float (&v)[8]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+constexpr size_t decode_smem_bytes() {
+    return (size_t)(8 * kDecD + 8 * kDecChunk + 32) * sizeof(double) +
+           (size_t)kDecChunk * kDecKSF * sizeof(float) + (size_t)kDecChunk * kDecD * sizeof(float);
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(kDecThreads) attend_decode_kernel(const DecodeArgs P) {
+    const AttnArgs& a = P.a;
+    if (a.hdr && a.hdr->error != 0) return;
+    const uint32_t L = scope_len(a);
+    const int chunk = blockIdx.x, kv = blockIdx.y;
+    const uint32_t k0 = (uint32_t)chunk * kDecChunk;
+    if (k0 >= L) return;
+    const int nk = (int)min((uint32_t)kDecChunk, L - k0);
+    const int G = a.group;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    extern __shared__ __align__(16) double dsm[];
+    double* qd = dsm;                              // [8][kDecD]
+    double* lg = qd + 8 * kDecD;                   // [8][kDecChunk]
+    double* st = lg + 8 * kDecChunk;               // [8][3] (+pad)
+    float* ks = (float*)(st + 32);                 // [kDecChunk][kDecKSF]
+    float* vs = ks + kDecChunk * kDecKSF;          // [kDecChunk][kDecD]
+    constexpr int half = kDecD / 2;
+
+    // ---- gather K (RoPE at compact position k0+r) and V through the scope table;
+    //      all loads of the thread issued before any use ----
+    constexpr int kIter = kDecChunk * (kDecD / 8) / kDecThreads;  // 4
+    uint32_t cr[kIter];
+#pragma unroll
+    for (int i = 0; i < kIter; ++i) {
+        const int e = tid + i * kDecThreads, r = e >> 4;
+        cr[i] = r < nk ? (a.src ? __ldg(a.src + k0 + r) : k0 + r) : 0u;
+    }
+    float kf[kIter][8], vf[kIter][8];
+    float4 c4[kIter], s4[kIter];
+#pragma unroll
+    for (int i = 0; i < kIter; ++i) {
+        const int e = tid + i * kDecThreads, r = e >> 4, c8 = (e & 15) * 8;
+        if (r < nk) {
+            const size_t rowb = ((size_t)kv * a.head_stride + cr[i]) * kDecD + c8;
+            load8<KT>((const KT*)a.k_base + rowb, kf[i]);
+            load8<KT>((const KT*)a.v_base + rowb, vf[i]);
+            if (a.rope_cos) {
+                c4[i] = __ldg(reinterpret_cast<const float4*>(a.rope_cos + (size_t)(k0 + r) * half + c8 / 2));
+                s4[i] = __ldg(reinterpret_cast<const float4*>(a.rope_sin + (size_t)(k0 + r) * half + c8 / 2));
+            }
+        }
+    }
+    // queries of the group, rotated at L'-1 (engine.hpp:546-551), kept as f64
+    const uint32_t qpos = L - 1u;
+    for (int e = tid; e < G * half; e += kDecThreads) {
+        const int g = e / half, j = e % half;
+        const float* qrow = a.q + (size_t)(kv * G + g) * kDecD;
+        const float x = qrow[2 * j], y = qrow[2 * j + 1];
+        float rx = x, ry = y;
+        if (a.rope_cos) {
+            const float cs = a.rope_cos[(size_t)qpos * half + j];
+            const float sn = a.rope_sin[(size_t)qpos * half + j];
+            rx = __fsub_rn(__fmul_rn(x, cs), __fmul_rn(y, sn));
+            ry = __fadd_rn(__fmul_rn(x, sn), __fmul_rn(y, cs));
+        }
+        qd[g * kDecD + 2 * j] = (double)rx;
+        qd[g * kDecD + 2 * j + 1] = (double)ry;
+    }
+#pragma unroll
+    for (int i = 0; i < kIter; ++i) {
+        const int e = tid + i * kDecThreads, r = e >> 4, c8 = (e & 15) * 8;
+        if (r < nk) {
+            if (a.rope_cos) {
+                const float cc[4] = {c4[i].x, c4[i].y, c4[i].z, c4[i].w};
+                const float ss[4] = {s4[i].x, s4[i].y, s4[i].z, s4[i].w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float x = kf[i][2 * t], y = kf[i][2 * t + 1];
+                    kf[i][2 * t] = __fsub_rn(__fmul_rn(x, cc[t]), __fmul_rn(y, ss[t]));
+                    kf[i][2 * t + 1] = __fadd_rn(__fmul_rn(x, ss[t]), __fmul_rn(y, cc[t]));
+                }
+            }
+            float4* kr = reinterpret_cast<float4*>(ks + r * kDecKSF + c8);
+            kr[0] = make_float4(kf[i][0], kf[i][1], kf[i][2], kf[i][3]);
+            kr[1] = make_float4(kf[i][4], kf[i][5], kf[i][6], kf[i][7]);
+            float4* vr = reinterpret_cast<float4*>(vs + r * kDecD + c8);
+            vr[0] = make_float4(vf[i][0], vf[i][1], vf[i][2], vf[i][3]);
+            vr[1] = make_float4(vf[i][4], vf[i][5], vf[i][6], vf[i][7]);
+        }
+    }
+    __syncthreads();
+    // ---- logits (attend.hpp:430): thread (key j, lane pair p) accumulates lanes 2p, 2p+1
+    //      of dot_f64 for every head; the tree ((l0+l1)+(l2+l3))+((l4+l5)+(l6+l7)) is
+    //      finished across the 4 threads of the key with shuffles (exact order) ----
+    {
+        const double scale = 1.0 / sqrt((double)kDecD);
+        const int j = tid >> 2, p = tid & 3;
+        double acc[8][2];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) acc[g][0] = acc[g][1] = 0.0;
+        if (j < nk) {
+            const float* kr = ks + j * kDecKSF + 2 * p;
+#pragma unroll 4
+            for (int c = 0; c < kDecD / 8; ++c) {
+                const float2 k2 = *reinterpret_cast<const float2*>(kr + 8 * c);
+                const double ka = (double)k2.x, kb = (double)k2.y;
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    if (g < G) {
+                        const double2 q2 =
+                            *reinterpret_cast<const double2*>(qd + g * kDecD + 8 * c + 2 * p);
+                        acc[g][0] = fma(q2.x, ka, acc[g][0]);
+                        acc[g][1] = fma(q2.y, kb, acc[g][1]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            if (g < G) {
+                double s = acc[g][0] + acc[g][1];
+                s = s + __shfl_xor_sync(0xFFFFFFFFu, s, 1);
+                s = s + __shfl_xor_sync(0xFFFFFFFFu, s, 2);
+                if (p == 0) lg[g * kDecChunk + j] = j < nk ? s * scale : -INFINITY;
+            }
+        }
+    }
+    __syncthreads();
+    // ---- per-head softmax statistics of this slice (one warp per head) ----
+    for (int g = warp; g < G; g += kDecThreads / 32) {
+        const double s = lane < nk ? lg[g * kDecChunk + lane] : -INFINITY;
+        double m = s;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xFFFFFFFFu, m, off));
+        const double w = lane < nk ? exp(s - m) : 0.0;
+        double A = w, B = lane < nk ? (s - m) * w : 0.0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            A += __shfl_xor_sync(0xFFFFFFFFu, A, off);
+            B += __shfl_xor_sync(0xFFFFFFFFu, B, off);
+        }
+        lg[g * kDecChunk + lane] = w;
+        if (lane == 0) {
+            st[g * 3 + 0] = m;
+            st[g * 3 + 1] = A;
+            st[g * 3 + 2] = B;
+        }
+    }
+    __syncthreads();
+    // ---- values: thread c owns output column c for every head of the group ----
+    const int c = tid;
+    double acc[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) acc[g] = 0.0;
+    for (int j = 0; j < nk; ++j) {
+        const double v = (double)vs[j * kDecD + c];
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+            if (g < G) acc[g] = fma(lg[g * kDecChunk + j], v, acc[g]);
+    }
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        if (g < G) {
+            double* p = a.part + (((size_t)chunk * a.n_kv + kv) * G + g) * kDecPart;
+            p[4 + c] = acc[g];
+            if (c < 3) p[c] = st[g * 3 + c];
+        }
+    }
+}
+
+// Merge the slices of one q head: weights in parallel, then 8 warps each sum a strided
+// subset of slices (lanes own 4 columns, 16-byte loads), reduced in a fixed order.
+constexpr int kCombThreads = 256;
+__global__ void __launch_bounds__(kCombThreads) attend_decode_combine(const DecodeArgs P) {
+    const AttnArgs& a = P.a;
+    if (a.hdr && a.hdr->error != 0) return;
+    const uint32_t L = scope_len(a);
+    const int h = blockIdx.x;
+    const int kv = h / a.group, g = h % a.group;
+    const int ns = (int)((L + kDecChunk - 1) / kDecChunk);
+    constexpr int NW = kCombThreads / 32;
+    __shared__ double w_s[2048];
+    __shared__ double red[NW][kDecD];
+    __shared__ double rs[NW][3];
+    __shared__ double s_M, s_A;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    auto prow = [&](int s) {
+        return a.part + (((size_t)s * a.n_kv + kv) * a.group + g) * kDecPart;
+    };
+    double m = -INFINITY;
+    for (int s = tid; s < ns; s += kCombThreads) m = fmax(m, prow(s)[0]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xFFFFFFFFu, m, off));
+    if (lane == 0) rs[warp][0] = m;
+    __syncthreads();
+    if (tid == 0) {
+        double M = rs[0][0];
+        for (int w = 1; w < NW; ++w) M = fmax(M, rs[w][0]);
+        s_M = M;
+    }
+    __syncthreads();
+    const double M = s_M;
+    double A = 0.0, B = 0.0;
+    for (int s = tid; s < ns; s += kCombThreads) {
+        const double* p = prow(s);
+        const double w = exp(p[0] - M);
+        w_s[s] = w;
+        A += p[1] * w;
+        B += w * (p[2] + (p[0] - M) * p[1]);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        A += __shfl_xor_sync(0xFFFFFFFFu, A, off);
+        B += __shfl_xor_sync(0xFFFFFFFFu, B, off);
+    }
+    if (lane == 0) {
+        rs[warp][1] = A;
+        rs[warp][2] = B;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double At = 0.0, Bt = 0.0;
+        for (int w = 0; w < NW; ++w) {
+            At += rs[w][1];
+            Bt += rs[w][2];
+        }
+        s_A = At;
+        const double hh = log(At) - Bt / At;
+        a.entropy[h] = hh < 0.0 ? 0.0 : hh;
+    }
+    // value rows: warp w sums slices w, w+NW, ...; lane owns columns 4*lane .. 4*lane+3
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int s = warp; s < ns; s += NW) {
+        const double2* p = reinterpret_cast<const double2*>(prow(s) + 4 + 4 * lane);
+        const double2 x = p[0], y = p[1];
+        const double w = w_s[s];
+        acc[0] = fma(x.x, w, acc[0]);
+        acc[1] = fma(x.y, w, acc[1]);
+        acc[2] = fma(y.x, w, acc[2]);
+        acc[3] = fma(y.y, w, acc[3]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) red[warp][4 * lane + u] = acc[u];
+    __syncthreads();
+    if (tid < kDecD) {
+        double t = 0.0;
+        for (int w = 0; w < NW; ++w) t += red[w][tid];
+        a.out[(size_t)h * kDecD + tid] = (float)(t / s_A);
+    }
+}
+
+bool decode_eligible(const AttnArgs& a, uint32_t L_max) {
+    return a.n_q == 1 && a.d == kDecD && a.dv == kDecD && a.group >= 1 && a.group <= 8 &&
+           a.causal && a.boundary_is_tail && L_max <= 2048u * kDecChunk &&
+           (a.dtype == kBF16 || a.dtype == kF32);
+}
+
+AttnLaunch plan_attend(const AttnArgs& a, uint32_t L_max, int num_sms) {
+    AttnLaunch P;
+    P.a = a;
+    P.qb = std::min(std::max(1, a.n_q), std::max(1, kQRows / std::max(1, a.group)));
+    P.qr = P.qb * a.group;
+    P.n_qblocks = (a.n_q + P.qb - 1) / P.qb;
+    const int chunks = std::max<int>(1, (int)((L_max + kAttnSplit - 1) / kAttnSplit));
+    const int base = a.n_kv * P.n_qblocks;
+    const int target = 2 * num_sms;
+    int splits = std::max(1, std::min(chunks, (target + base - 1) / base));
+    P.chunks_per_split = (chunks + splits - 1) / splits;
+    P.n_splits = (chunks + P.chunks_per_split - 1) / P.chunks_per_split;
+    P.direct = P.n_splits == 1;
+    return P;
+}
+
+size_t attend_smem(const AttnLaunch& P) {
+    const int d = P.a.d, dv = P.a.dv, QR = P.qr;
+    return (size_t)QR * kAttnSplit * 8 + (size_t)QR * dv * 8 + (size_t)QR * 3 * 8 +
+           (size_t)QR * (d + 1) * 4 + (size_t)kAttnSplit * (d + 1) * 4 +
+           (size_t)kAttnSplit * dv * 4;
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+}  // namespace
+
+size_t attend_workspace(const AttnArgs& a, uint32_t L_max) {
+    if (decode_eligible(a, L_max)) {
+        const size_t nc = (L_max + kDecChunk - 1) / kDecChunk;
+        return nc * a.n_kv * a.group * kDecPart * sizeof(double);
+    }
+    const AttnLaunch P = plan_attend(a, L_max, sm_count());
+    if (P.direct) return 0;
+    return (size_t)P.n_splits * a.n_kv * a.n_q * a.group * (3 + a.dv) * sizeof(double);
+}
+
+int attend_kernel_count(const AttnArgs& a, uint32_t L_max) {
+    if (decode_eligible(a, L_max)) return 2;
+    return attend_workspace(a, L_max) ? 2 : 1;
+}
+
+cudaError_t launch_attend(const AttnArgs& a, uint32_t L_max, cudaStream_t s) {
+    if (decode_eligible(a, L_max)) {
+        DecodeArgs D;
+        D.a = a;
+        D.n_chunks = (int)((L_max + kDecChunk - 1) / kDecChunk);
+        dim3 grid(D.n_chunks, a.n_kv);
+        const size_t smem = decode_smem_bytes();
+        if (a.dtype == kBF16) {
+            cudaFuncSetAttribute(attend_decode_kernel<__nv_bfloat16>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attend_decode_kernel<__nv_bfloat16><<<grid, kDecThreads, smem, s>>>(D);
+        } else {
+            cudaFuncSetAttribute(attend_decode_kernel<float>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attend_decode_kernel<float><<<grid, kDecThreads, smem, s>>>(D);
+        }
+        attend_decode_combine<<<a.n_head, kCombThreads, 0, s>>>(D);
+        return cudaGetLastError();
+    }
+    const AttnLaunch P = plan_attend(a, L_max, sm_count());
+    const size_t smem = attend_smem(P);
+    dim3 grid(P.n_splits, a.n_kv, P.n_qblocks);
+    if (a.dtype == kBF16) {
+        cudaFuncSetAttribute(attend_split_kernel<__nv_bfloat16>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attend_split_kernel<__nv_bfloat16><<<grid, kAttnThreads, smem, s>>>(P);
+    } else {
+        cudaFuncSetAttribute(attend_split_kernel<float>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attend_split_kernel<float><<<grid, kAttnThreads, smem, s>>>(P);
+    }
+    if (!P.direct) attend_combine_kernel<<<a.n_q * a.n_head, 128, 0, s>>>(P);
+    return cudaGetLastError();
+}
+
+}  // namespace reattn_impl

@@ -1,0 +1,990 @@
+// C-ABI implementation (include/reattn_cuda.h): contexts, device KV cache, rotary tables,
+// the synchronous reference-shaped entry points and CUDA-graph step plans.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/reattn_cuda.h"
+#include "kernels.h"
+
+using namespace reattn_impl;
+
+struct reattn_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int lanes = REATTN_LANES_UNFUSED;
+    int num_sms = 148;
+    std::string err;
+    void* arena = nullptr;  // scratch for synchronous calls
+    size_t arena_bytes = 0;
+};
+
+struct reattn_cache {
+    uint64_t n_kv, d, l_global, l_local_max, capacity, total = 0;
+    int dtype;
+    void* keys = nullptr;
+    void* values = nullptr;
+    uint64_t global_end() const { return std::min(total, l_global); }
+    uint64_t local_start() const {
+        const uint64_t g = global_end();
+        return total - std::min(total - g, l_local_max);
+    }
+};
+
+struct reattn_rope {
+    uint64_t head_dim, max_position;
+    double base;
+    std::vector<float> cos_h, sin_h;
+    float* cos_d = nullptr;
+    float* sin_d = nullptr;
+};
+
+namespace {
+
+int set_err(reattn_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+#define CU(ctx, call)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return set_err((ctx), REATTN_ECUDA,                                         \
+                           std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " \
+                               #call);                                                  \
+    } while (0)
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// bump allocator over a device region
+struct Carver {
+    uint8_t* base;
+    size_t off = 0;
+    size_t cap;
+    template <typename T>
+    T* take(size_t n) {
+        off = align_up(off, 256);
+        T* p = (T*)(base ? base + off : nullptr);
+        off += std::max<size_t>(n, 1) * sizeof(T);
+        return p;
+    }
+};
+
+int ensure_arena(reattn_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->arena_bytes) return REATTN_OK;
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->arena) CU(ctx, cudaFree(ctx->arena));
+    ctx->arena = nullptr;
+    ctx->arena_bytes = 0;
+    const size_t nb = align_up(bytes + bytes / 4, 1 << 20);
+    CU(ctx, cudaMalloc(&ctx->arena, nb));
+    CU(ctx, cudaMemset(ctx->arena, 0, nb));
+    ctx->arena_bytes = nb;
+    return REATTN_OK;
+}
+
+int status_from_scope(reattn_ctx* ctx, int32_t e) {
+    switch (e) {
+        case kScopeOk: return REATTN_OK;
+        case kScopeErrWindow: return set_err(ctx, REATTN_EINVAL, "scope exceeds pretrain window");
+        case kScopeErrSpanRange:
+            return set_err(ctx, REATTN_ERANGE, "assemble_scope: span outside middle");
+        case kScopeErrQueryLong:
+            return set_err(ctx, REATTN_ELOGIC, "attend_step: query block longer than scope");
+        case kScopeErrWinnerRange:
+            return set_err(ctx, REATTN_ERANGE, "expand_spans: winner outside middle");
+        case kScopeErrTooMany:
+            return set_err(ctx, REATTN_ERUNTIME, "vote: candidate count exceeds device capacity");
+        default: return set_err(ctx, REATTN_ERUNTIME, "device scope error");
+    }
+}
+
+// ---- scan dispatch -------------------------------------------------------------------
+struct ScanPlan {
+    ScanArgs a;
+    bool fast = false;
+    CUtensorMap map;
+    size_t ws_bytes = 0;
+};
+
+int plan_scan(reattn_ctx* ctx, ScanPlan& sp) {
+    sp.fast = scan_fast_supported(sp.a);
+    sp.ws_bytes = 0;
+    if (sp.fast) {
+        sp.ws_bytes = scan_fast_workspace(sp.a, ctx->num_sms);
+        if (!make_key_tensor_map(&sp.map, sp.a.keys, sp.a.dtype, sp.a.d,
+                                 (uint64_t)sp.a.n_kv * sp.a.head_stride,
+                                 scan_fast_box_rows(sp.a.dtype)))
+            sp.fast = false;  // layout the TMA unit cannot describe: exact generic path
+    }
+    if (!sp.fast && sp.a.k > kGenericMaxK)
+        return set_err(ctx, REATTN_EINVAL, "fused_topk_scores: k exceeds device capacity (7936)");
+    return REATTN_OK;
+}
+
+// The fast scan's last-CTA ticket lives at offset 0 of its workspace and is re-armed by
+// the kernel itself.  Plans own private, zero-initialised workspaces; the synchronous
+// entry points share the context arena, so they clear the ticket first (zero_ticket).
+int enqueue_scan(reattn_ctx* ctx, const ScanPlan& sp, void* ws, cudaStream_t s,
+                 bool zero_ticket) {
+    if (sp.fast && zero_ticket) CU(ctx, cudaMemsetAsync(ws, 0, 256, s));
+    if (sp.fast)
+        CU(ctx, launch_scan_fast(sp.a, sp.map, ws, ctx->num_sms, s));
+    else
+        CU(ctx, launch_scan_generic(sp.a, s));
+    return REATTN_OK;
+}
+
+// ---- attend_step pipeline --------------------------------------------------------------
+struct StepPlan {
+    // shape
+    uint64_t n_q, n_head, n_kv, d, group, g_end, l_start, total, middle, window;
+    uint64_t kk;  // min(k, middle) when selecting
+    bool select = false;
+    uint32_t L_upper = 0;
+    reattn_selection_config cfg;
+    ScanPlan scan;
+    // device buffers
+    uint32_t* cand_idx = nullptr;
+    float* cand_score = nullptr;
+    void* scan_ws = nullptr;
+    uint32_t* winners = nullptr;
+    uint32_t* span_b = nullptr;
+    uint32_t* span_e = nullptr;
+    uint32_t* scope_src = nullptr;
+    ScopeHeader* hdr = nullptr;
+    double* part = nullptr;
+    double* entropy = nullptr;
+    size_t part_bytes = 0;
+    size_t scratch_bytes = 0;
+    uint64_t kernels = 0;
+};
+
+int plan_step(reattn_ctx* ctx, const reattn_cache* cache, const reattn_rope* rope, uint64_t n_q,
+              uint64_t n_head, const reattn_selection_config* cfg, int mode, StepPlan& P,
+              const float* q_dev, float* out_dev) {
+    if (n_head % cache->n_kv != 0)
+        return set_err(ctx, REATTN_EINVAL, "attend_step: n_head must be a multiple of kv heads");
+    if (rope->head_dim != cache->d)
+        return set_err(ctx, REATTN_EINVAL, "attend_step: rotary head_dim != cache d_head");
+    if (cfg->k == 0) return set_err(ctx, REATTN_EINVAL, "selection: k must be >= 1");
+    if (cfg->span_m == 0) return set_err(ctx, REATTN_EINVAL, "selection: span_m must be >= 1");
+    P.cfg = *cfg;
+    P.n_q = n_q;
+    P.n_head = n_head;
+    P.n_kv = cache->n_kv;
+    P.d = cache->d;
+    P.group = n_head / cache->n_kv;
+    P.total = cache->total;
+    P.g_end = cache->global_end();
+    P.l_start = cache->local_start();
+    P.middle = P.l_start - P.g_end;
+    P.window = rope->max_position;
+    P.select = mode == REATTN_MODE_REATTENTION && cfg->k_prime > 0 && P.middle > 0;
+    P.kk = std::min<uint64_t>(cfg->k, P.middle);
+    const uint64_t local = P.total - P.l_start;
+    uint64_t sel_rows = P.select ? std::min<uint64_t>(P.middle, cfg->k_prime * cfg->span_m) : 0;
+    P.L_upper = (uint32_t)std::min<uint64_t>(P.window, P.g_end + sel_rows + local);
+    if (P.total >= (1ull << 32) || P.window >= (1ull << 31))
+        return set_err(ctx, REATTN_EINVAL, "attend_step: cache too long for 32-bit indices");
+    if (P.select) {
+        const uint64_t n_cand = P.n_kv * n_q * P.kk;
+        if (n_cand > kVoteMaxSmem)
+            return set_err(ctx, REATTN_ERUNTIME,
+                           "vote: candidate count exceeds device capacity (8192)");
+        ScanArgs& a = P.scan.a;
+        a.q = q_dev;
+        a.n_q = (int)n_q;
+        a.n_heads = (int)n_head;
+        a.n_kv = (int)P.n_kv;
+        a.d = (int)P.d;
+        a.keys = cache->keys;
+        a.dtype = cache->dtype;
+        a.head_stride = cache->capacity;
+        a.row0 = P.g_end;
+        a.count = (uint32_t)P.middle;
+        a.k = (int)cfg->k;
+        a.lanes = ctx->lanes;
+        int rc = plan_scan(ctx, P.scan);
+        if (rc) return rc;
+    }
+    (void)out_dev;
+    return REATTN_OK;
+}
+
+AttnArgs step_attn_args(const StepPlan& P, const reattn_cache* cache, const reattn_rope* rope,
+                        const float* q_dev, float* out_dev) {
+    AttnArgs a;
+    a.q = q_dev;
+    a.q_row_stride = P.n_head * P.d;
+    a.n_q = (int)P.n_q;
+    a.n_head = (int)P.n_head;
+    a.n_kv = (int)P.n_kv;
+    a.group = (int)P.group;
+    a.d = (int)P.d;
+    a.dv = (int)P.d;
+    a.k_base = cache->keys;
+    a.v_base = cache->values;
+    a.dtype = cache->dtype;
+    a.head_stride = cache->capacity;
+    a.src = P.scope_src;
+    a.hdr = P.hdr;
+    a.L_host = 0;
+    a.rope_cos = rope->cos_d;
+    a.rope_sin = rope->sin_d;
+    a.causal = 1;
+    a.boundary_is_tail = 1;
+    a.boundary_host = 0;
+    a.part = P.part;
+    a.out = out_dev;
+    a.entropy = P.entropy;
+    return a;
+}
+
+// carve (or size, when base == nullptr) the step buffers
+void carve_step(StepPlan& P, const reattn_cache* cache, const reattn_rope* rope, Carver& c) {
+    const uint64_t ncand = P.select ? P.n_kv * P.n_q * P.cfg.k : 1;
+    P.cand_idx = c.take<uint32_t>(ncand);
+    P.cand_score = c.take<float>(ncand);
+    P.scan_ws = c.take<uint8_t>(P.scan.ws_bytes);
+    const uint64_t kp = std::max<uint64_t>(1, P.cfg.k_prime);
+    P.winners = c.take<uint32_t>(kp);
+    P.span_b = c.take<uint32_t>(kp);
+    P.span_e = c.take<uint32_t>(kp);
+    P.scope_src = c.take<uint32_t>(std::max<uint64_t>(1, P.L_upper));
+    P.hdr = c.take<ScopeHeader>(1);
+    AttnArgs a = step_attn_args(P, cache, rope, nullptr, nullptr);
+    P.part_bytes = attend_workspace(a, std::max<uint32_t>(1, P.L_upper));
+    P.part = c.take<double>(P.part_bytes / sizeof(double) + 1);
+    P.entropy = c.take<double>(std::max<uint64_t>(1, P.n_q * P.n_head));
+    P.scratch_bytes = c.off;
+}
+
+int enqueue_step(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache, const reattn_rope* rope,
+                 const float* q_dev, float* out_dev, cudaStream_t s, bool zero_ticket) {
+    P.kernels = 0;
+    SelectArgs sa;
+    std::memset(&sa, 0, sizeof(sa));
+    if (P.select) {
+        sa.cand_idx = P.cand_idx;
+        sa.cand_score = P.cand_score;
+        sa.n_lists = (uint32_t)(P.n_kv * P.n_q);
+        sa.list_len = (uint32_t)P.kk;
+        sa.list_stride = (uint32_t)P.cfg.k;
+        sa.k_prime = (uint32_t)P.cfg.k_prime;
+    }
+    sa.span_m = (uint32_t)P.cfg.span_m;
+    sa.middle_len = (uint32_t)P.middle;
+    sa.span_mode = P.cfg.span_mode;
+    sa.build_scope = 1;
+    sa.g_end = (uint32_t)P.g_end;
+    sa.l_start = (uint32_t)P.l_start;
+    sa.total = (uint32_t)P.total;
+    sa.window = (uint32_t)P.window;
+    sa.n_q = (uint32_t)P.n_q;
+    sa.winners = P.winners;
+    sa.span_b = P.span_b;
+    sa.span_e = P.span_e;
+    sa.scope_src = P.scope_src;
+    sa.hdr = P.hdr;
+    // Decode: <= 32 candidates -> vote/spans/scope run in the fast scan's last CTA (one
+    // launch fewer, no host round trip); otherwise the standalone select kernel.
+    bool fused = false;
+    if (P.select) {
+        P.scan.a.q = q_dev;
+        P.scan.a.idx_out = P.cand_idx;
+        P.scan.a.score_out = P.cand_score;
+        fused = P.scan.fast && P.n_kv * P.n_q * P.kk <= kSmallSelectMax;
+        P.scan.a.fuse_select = fused ? 1 : 0;
+        if (fused) {
+            SmallSelectIO& io = P.scan.a.sel;
+            io.k_prime = sa.k_prime;
+            io.span_m = sa.span_m;
+            io.middle_len = sa.middle_len;
+            io.span_mode = sa.span_mode;
+            io.g_end = sa.g_end;
+            io.l_start = sa.l_start;
+            io.total = sa.total;
+            io.window = sa.window;
+            io.n_q = sa.n_q;
+            io.winners = sa.winners;
+            io.span_b = sa.span_b;
+            io.span_e = sa.span_e;
+            io.scope_src = sa.scope_src;
+            io.hdr = sa.hdr;
+        }
+        int rc = enqueue_scan(ctx, P.scan, P.scan_ws, s, zero_ticket);
+        if (rc) return rc;
+        ++P.kernels;
+    }
+    if (!fused) {
+        CU(ctx, launch_select(sa, s));
+        ++P.kernels;
+    }
+    if (P.n_q > 0) {
+        AttnArgs a = step_attn_args(P, cache, rope, q_dev, out_dev);
+        CU(ctx, launch_attend(a, std::max<uint32_t>(1, P.L_upper), s));
+        P.kernels += attend_kernel_count(a, std::max<uint32_t>(1, P.L_upper));
+    }
+    return REATTN_OK;
+}
+
+int finish_step_stats(reattn_ctx* ctx, const StepPlan& P, const ScopeHeader& h,
+                      reattn_step_stats* st, double* entropy_host) {
+    int rc = status_from_scope(ctx, h.error);
+    if (rc) return rc;
+    if (P.n_q == 0 && h.L == 0) return set_err(ctx, REATTN_EINVAL, "empty key set");
+    std::vector<double> ent(P.n_q * P.n_head);
+    if (!ent.empty())
+        CU(ctx, cudaMemcpy(ent.data(), P.entropy, ent.size() * sizeof(double),
+                           cudaMemcpyDeviceToHost));
+    if (entropy_host) std::copy(ent.begin(), ent.end(), entropy_host);
+    if (st) {
+        std::memset(st, 0, sizeof(*st));
+        double mx = 0.0, sum = 0.0;
+        for (uint64_t hh = 0; hh < P.n_head; ++hh)
+            for (uint64_t i = 0; i < P.n_q; ++i) {
+                const double e = ent[i * P.n_head + hh];
+                mx = std::max(mx, e);
+                sum += e;
+            }
+        st->entropy_max = mx;
+        st->entropy_sum = sum;
+        st->entropy_rows = P.n_q * P.n_head;
+        st->scope_len = h.L;
+        st->max_position_used = h.L ? h.L - 1 : 0;
+        st->ood_positions = 0;  // every position < L' <= window (checked on device)
+        st->n_spans = h.n_spans;
+        st->coverage = h.coverage;
+        st->coverage_total = h.coverage == P.middle ? 1 : 0;
+        st->peak_scratch_bytes = P.scratch_bytes;
+    }
+    return REATTN_OK;
+}
+
+}  // namespace
+
+struct reattn_plan {
+    reattn_ctx* ctx;
+    const reattn_cache* cache;
+    const reattn_rope* rope;
+    StepPlan P;
+    void* mem = nullptr;
+    float* q = nullptr;
+    float* out = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};
+
+extern "C" {
+
+const char* reattn_version(void) { return "reattn-b200 0.1 (sm_100a)"; }
+
+int reattn_ctx_create(int device, reattn_ctx** out) {
+    auto* ctx = new reattn_ctx();
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete ctx;
+        *out = nullptr;
+        return REATTN_ECUDA;
+    }
+    ctx->own_stream = true;
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    *out = ctx;
+    return REATTN_OK;
+}
+
+void reattn_ctx_destroy(reattn_ctx* ctx) {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->arena) cudaFree(ctx->arena);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* reattn_last_error(const reattn_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+int reattn_ctx_set_stream(reattn_ctx* ctx, void* s) {
+    if (ctx->own_stream) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+        ctx->own_stream = false;
+    }
+    ctx->stream = (cudaStream_t)s;
+    return REATTN_OK;
+}
+void* reattn_ctx_stream(const reattn_ctx* ctx) { return (void*)ctx->stream; }
+
+int reattn_ctx_set_lanes(reattn_ctx* ctx, int lanes) {
+    if (lanes != REATTN_LANES_UNFUSED && lanes != REATTN_LANES_FMA)
+        return set_err(ctx, REATTN_EINVAL, "unknown lane arithmetic");
+    ctx->lanes = lanes;
+    return REATTN_OK;
+}
+int reattn_ctx_synchronize(reattn_ctx* ctx) {
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+int reattn_ctx_num_sms(const reattn_ctx* ctx) { return ctx->num_sms; }
+
+int reattn_malloc(reattn_ctx* ctx, uint64_t bytes, void** out) {
+    *out = nullptr;
+    CU(ctx, cudaMalloc(out, std::max<uint64_t>(bytes, 1)));
+    return REATTN_OK;
+}
+int reattn_free(reattn_ctx* ctx, void* p) {
+    if (p) CU(ctx, cudaFree(p));
+    return REATTN_OK;
+}
+int reattn_memcpy_h2d(reattn_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+    if (!bytes) return REATTN_OK;
+    CU(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+int reattn_memcpy_d2h(reattn_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+    if (!bytes) return REATTN_OK;
+    CU(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+// ---- cache ---------------------------------------------------------------------------
+int reattn_cache_create(reattn_ctx* ctx, uint64_t n_kv, uint64_t d, uint64_t l_global,
+                        uint64_t l_local_max, uint64_t capacity, int dtype, reattn_cache** out) {
+    *out = nullptr;
+    if (n_kv == 0 || d == 0)
+        return set_err(ctx, REATTN_EINVAL, "cache needs at least one head and a positive head dim");
+    if (l_local_max == 0) return set_err(ctx, REATTN_EINVAL, "l_local_max must be positive");
+    if (dtype != REATTN_F32 && dtype != REATTN_BF16)
+        return set_err(ctx, REATTN_EINVAL, "cache: unknown dtype");
+    auto* c = new reattn_cache();
+    c->n_kv = n_kv;
+    c->d = d;
+    c->l_global = l_global;
+    c->l_local_max = l_local_max;
+    c->capacity = std::max<uint64_t>(capacity, 1);
+    c->dtype = dtype;
+    const size_t bytes = n_kv * c->capacity * d * (dtype == REATTN_BF16 ? 2 : 4);
+    cudaError_t e = cudaMalloc(&c->keys, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&c->values, bytes);
+    if (e != cudaSuccess) {
+        if (c->keys) cudaFree(c->keys);
+        delete c;
+        return set_err(ctx, REATTN_ECUDA, std::string("cache allocation: ") + cudaGetErrorString(e));
+    }
+    *out = c;
+    return REATTN_OK;
+}
+
+void reattn_cache_destroy(reattn_cache* c) {
+    if (!c) return;
+    cudaFree(c->keys);
+    cudaFree(c->values);
+    delete c;
+}
+
+int reattn_cache_append(reattn_ctx* ctx, reattn_cache* c, const float* keys, const float* values,
+                        uint64_t rows, int src_on_device) {
+    if (rows == 0) return REATTN_OK;
+    if (c->total + rows > c->capacity)
+        return set_err(ctx, REATTN_ERUNTIME, "cache append: capacity exceeded");
+    const size_t bytes = rows * c->n_kv * c->d * sizeof(float);
+    const float* ks = keys;
+    const float* vs = values;
+    if (!src_on_device) {
+        int rc = ensure_arena(ctx, 2 * bytes + 512);
+        if (rc) return rc;
+        float* kd = (float*)ctx->arena;
+        float* vd = (float*)((uint8_t*)ctx->arena + align_up(bytes, 256));
+        CU(ctx, cudaMemcpyAsync(kd, keys, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        CU(ctx, cudaMemcpyAsync(vd, values, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        ks = kd;
+        vs = vd;
+    }
+    CU(ctx, launch_cache_append(ks, c->keys, c->dtype, rows, c->n_kv, c->d, c->capacity, c->total,
+                                ctx->stream));
+    CU(ctx, launch_cache_append(vs, c->values, c->dtype, rows, c->n_kv, c->d, c->capacity,
+                                c->total, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    c->total += rows;  // boundaries follow kv_cache.hpp:65-67 (computed on demand)
+    return REATTN_OK;
+}
+
+int reattn_cache_reserve(reattn_ctx* ctx, reattn_cache* c, uint64_t cap) {
+    if (cap <= c->capacity) return REATTN_OK;
+    const uint64_t esz = c->dtype == REATTN_BF16 ? 2 : 4;
+    void* nk = nullptr;
+    void* nv = nullptr;
+    CU(ctx, cudaMalloc(&nk, c->n_kv * cap * c->d * esz));
+    CU(ctx, cudaMalloc(&nv, c->n_kv * cap * c->d * esz));
+    if (c->total) {
+        const size_t w = c->total * c->d * esz;
+        CU(ctx, cudaMemcpy2DAsync(nk, cap * c->d * esz, c->keys, c->capacity * c->d * esz, w,
+                                  c->n_kv, cudaMemcpyDeviceToDevice, ctx->stream));
+        CU(ctx, cudaMemcpy2DAsync(nv, cap * c->d * esz, c->values, c->capacity * c->d * esz, w,
+                                  c->n_kv, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    cudaFree(c->keys);
+    cudaFree(c->values);
+    c->keys = nk;
+    c->values = nv;
+    c->capacity = cap;
+    return REATTN_OK;
+}
+
+int reattn_cache_set_total(reattn_ctx* ctx, reattn_cache* c, uint64_t total) {
+    if (total > c->capacity) return set_err(ctx, REATTN_EINVAL, "cache: total exceeds capacity");
+    c->total = total;
+    return REATTN_OK;
+}
+
+int reattn_cache_info(const reattn_cache* c, uint64_t* n_kv, uint64_t* d, uint64_t* l_global,
+                      uint64_t* l_local_max, uint64_t* capacity, uint64_t* total,
+                      uint64_t* global_end, uint64_t* local_start, int* dtype) {
+    if (n_kv) *n_kv = c->n_kv;
+    if (d) *d = c->d;
+    if (l_global) *l_global = c->l_global;
+    if (l_local_max) *l_local_max = c->l_local_max;
+    if (capacity) *capacity = c->capacity;
+    if (total) *total = c->total;
+    if (global_end) *global_end = c->global_end();
+    if (local_start) *local_start = c->local_start();
+    if (dtype) *dtype = c->dtype;
+    return REATTN_OK;
+}
+void* reattn_cache_keys(const reattn_cache* c) { return c->keys; }
+void* reattn_cache_values(const reattn_cache* c) { return c->values; }
+
+// ---- rope ----------------------------------------------------------------------------
+int reattn_rope_create(reattn_ctx* ctx, uint64_t head_dim, double base, uint64_t max_position,
+                       reattn_rope** out) {
+    *out = nullptr;
+    if (head_dim == 0 || head_dim % 2 != 0)
+        return set_err(ctx, REATTN_EINVAL, "rotary head_dim must be even and positive");
+    if (!(base > 0.0)) return set_err(ctx, REATTN_EINVAL, "rotary base must be positive");
+    if (max_position == 0)
+        return set_err(ctx, REATTN_EINVAL, "rotary max_position must be positive");
+    auto* r = new reattn_rope();
+    r->head_dim = head_dim;
+    r->max_position = max_position;
+    r->base = base;
+    const uint64_t half = head_dim / 2;
+    // table constant: float(cos/sin(p * base^(-2i/d))) computed in double (rope.hpp:325-337)
+    std::vector<double> inv(half);
+    for (uint64_t i = 0; i < half; ++i) inv[i] = std::pow(base, -2.0 * double(i) / double(head_dim));
+    r->cos_h.resize(max_position * half);
+    r->sin_h.resize(max_position * half);
+    for (uint64_t p = 0; p < max_position; ++p)
+        for (uint64_t i = 0; i < half; ++i) {
+            const double ang = double(p) * inv[i];
+            r->cos_h[p * half + i] = float(std::cos(ang));
+            r->sin_h[p * half + i] = float(std::sin(ang));
+        }
+    const size_t bytes = r->cos_h.size() * sizeof(float);
+    cudaError_t e = cudaMalloc(&r->cos_d, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&r->sin_d, bytes);
+    if (e == cudaSuccess) e = cudaMemcpy(r->cos_d, r->cos_h.data(), bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(r->sin_d, r->sin_h.data(), bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(r->cos_d);
+        cudaFree(r->sin_d);
+        delete r;
+        return set_err(ctx, REATTN_ECUDA, std::string("rope upload: ") + cudaGetErrorString(e));
+    }
+    *out = r;
+    return REATTN_OK;
+}
+
+void reattn_rope_destroy(reattn_rope* r) {
+    if (!r) return;
+    cudaFree(r->cos_d);
+    cudaFree(r->sin_d);
+    delete r;
+}
+
+int reattn_rope_tables_host(const reattn_rope* r, float* c, float* s) {
+    if (c) std::copy(r->cos_h.begin(), r->cos_h.end(), c);
+    if (s) std::copy(r->sin_h.begin(), r->sin_h.end(), s);
+    return REATTN_OK;
+}
+
+int reattn_rope_rotate(reattn_ctx* ctx, const reattn_rope* r, float* rows, const uint64_t* pos,
+                       uint64_t n_rows) {
+    if (n_rows == 0) return REATTN_OK;
+    std::vector<uint32_t> p32(n_rows);
+    for (uint64_t i = 0; i < n_rows; ++i) {
+        if (pos[i] >= r->max_position)
+            return set_err(ctx, REATTN_ERANGE, "position out of pretrained range");
+        p32[i] = (uint32_t)pos[i];
+    }
+    int rc = ensure_arena(ctx, n_rows * 4 + 256);
+    if (rc) return rc;
+    CU(ctx, cudaMemcpyAsync(ctx->arena, p32.data(), n_rows * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CU(ctx, launch_rope_rotate(rows, (const uint32_t*)ctx->arena, n_rows, r->head_dim, r->cos_d,
+                               r->sin_d, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+// ---- selection ---------------------------------------------------------------------------
+int reattn_fused_topk(reattn_ctx* ctx, const float* q_dev, uint64_t n_q, uint64_t n_heads,
+                      const void* keys_dev, int key_dtype, uint64_t n_kv, uint64_t head_stride,
+                      uint64_t row0, uint64_t count, uint64_t d, uint64_t k, uint32_t* idx_out,
+                      float* score_out, uint64_t* n_out, uint64_t* scratch_bytes) {
+    if (n_kv == 0 || n_heads % n_kv != 0)
+        return set_err(ctx, REATTN_EINVAL, "fused_topk_scores: n_heads must be a multiple of kv heads");
+    if (k == 0) return set_err(ctx, REATTN_EINVAL, "selection: k must be >= 1");
+    if (count >= (1ull << 32)) return set_err(ctx, REATTN_EINVAL, "fused_topk_scores: middle too long");
+    if (n_out) *n_out = std::min(k, count);
+    ScanPlan sp;
+    ScanArgs& a = sp.a;
+    a.q = q_dev;
+    a.n_q = (int)n_q;
+    a.n_heads = (int)n_heads;
+    a.n_kv = (int)n_kv;
+    a.d = (int)d;
+    a.keys = keys_dev;
+    a.dtype = key_dtype;
+    a.head_stride = head_stride;
+    a.row0 = row0;
+    a.count = (uint32_t)count;
+    a.k = (int)k;
+    a.lanes = ctx->lanes;
+    a.idx_out = idx_out;
+    a.score_out = score_out;
+    int rc = plan_scan(ctx, sp);
+    if (rc) return rc;
+    // fixed workspace: independent of `count` (the scratch contract, test_selection.cpp:228)
+    const size_t ws_fixed = scan_fast_workspace(a, ctx->num_sms);
+    if (scratch_bytes) *scratch_bytes = ws_fixed + n_q * n_kv * k * 8;
+    if (count == 0 || n_q == 0) return REATTN_OK;
+    rc = ensure_arena(ctx, ws_fixed + 256);
+    if (rc) return rc;
+    rc = enqueue_scan(ctx, sp, ctx->arena, ctx->stream, true);
+    if (rc) return rc;
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_vote(reattn_ctx* ctx, const uint32_t* idx_dev, const float* score_dev, uint64_t n,
+                uint64_t k_prime, uint32_t* winners_dev, uint64_t* n_winners) {
+    *n_winners = 0;
+    if (k_prime == 0 || n == 0) return REATTN_OK;
+    if (n > kVoteMaxSmem)
+        return set_err(ctx, REATTN_ERUNTIME, "vote: candidate count exceeds device capacity (8192)");
+    int rc = ensure_arena(ctx, 4096);
+    if (rc) return rc;
+    SelectArgs sa;
+    std::memset(&sa, 0, sizeof(sa));
+    sa.cand_idx = idx_dev;
+    sa.cand_score = score_dev;
+    sa.n_lists = 1;
+    sa.list_len = (uint32_t)n;
+    sa.list_stride = (uint32_t)n;
+    sa.k_prime = (uint32_t)std::min<uint64_t>(k_prime, n);
+    sa.winners = winners_dev;
+    sa.hdr = (ScopeHeader*)ctx->arena;
+    CU(ctx, launch_select(sa, ctx->stream));
+    ScopeHeader h;
+    CU(ctx, cudaMemcpyAsync(&h, sa.hdr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    rc = status_from_scope(ctx, h.error);
+    if (rc) return rc;
+    *n_winners = h.n_winners;
+    return REATTN_OK;
+}
+
+int reattn_tally(reattn_ctx* ctx, const uint32_t* idx_dev, const float* score_dev, uint64_t n,
+                 uint32_t* idx_out, uint32_t* votes_out, float* score_out, uint64_t* n_unique) {
+    *n_unique = 0;
+    if (n == 0) return REATTN_OK;
+    if (n > kVoteMaxSmem)
+        return set_err(ctx, REATTN_ERUNTIME, "vote: candidate count exceeds device capacity (8192)");
+    int rc = ensure_arena(ctx, 4096);
+    if (rc) return rc;
+    SelectArgs sa;
+    std::memset(&sa, 0, sizeof(sa));
+    sa.cand_idx = idx_dev;
+    sa.cand_score = score_dev;
+    sa.n_lists = 1;
+    sa.list_len = (uint32_t)n;
+    sa.list_stride = (uint32_t)n;
+    sa.k_prime = (uint32_t)n;
+    sa.winners = idx_out;
+    sa.rank_votes = votes_out;
+    sa.rank_score = score_out;
+    sa.hdr = (ScopeHeader*)ctx->arena;
+    CU(ctx, launch_select(sa, ctx->stream));
+    ScopeHeader h;
+    CU(ctx, cudaMemcpyAsync(&h, sa.hdr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    rc = status_from_scope(ctx, h.error);
+    if (rc) return rc;
+    *n_unique = h.n_winners;
+    return REATTN_OK;
+}
+
+int reattn_expand_spans(reattn_ctx* ctx, const uint32_t* winners_dev, uint64_t n, uint64_t span_m,
+                        uint64_t middle_len, int span_mode, uint32_t* begin_dev,
+                        uint32_t* end_dev, uint64_t* n_spans) {
+    *n_spans = 0;
+    if (span_m == 0) return set_err(ctx, REATTN_EINVAL, "selection: span_m must be >= 1");
+    if (n == 0 || middle_len == 0) return REATTN_OK;
+    int rc = ensure_arena(ctx, 4096);
+    if (rc) return rc;
+    SelectArgs sa;
+    std::memset(&sa, 0, sizeof(sa));
+    sa.winners_in = winners_dev;
+    sa.n_winners_in = (uint32_t)n;
+    sa.k_prime = (uint32_t)n;
+    sa.span_m = (uint32_t)span_m;
+    sa.middle_len = (uint32_t)middle_len;
+    sa.span_mode = span_mode;
+    sa.winners = const_cast<uint32_t*>(winners_dev);
+    sa.span_b = begin_dev;
+    sa.span_e = end_dev;
+    sa.hdr = (ScopeHeader*)ctx->arena;
+    CU(ctx, launch_select(sa, ctx->stream));
+    ScopeHeader h;
+    CU(ctx, cudaMemcpyAsync(&h, sa.hdr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    rc = status_from_scope(ctx, h.error);
+    if (rc) return rc;
+    *n_spans = h.n_spans;
+    return REATTN_OK;
+}
+
+int reattn_assemble_scope(reattn_ctx* ctx, const reattn_cache* c, const uint32_t* span_b_dev,
+                          const uint32_t* span_e_dev, uint64_t n_spans, uint64_t window,
+                          uint32_t* src_dev, float* keys_out, float* values_out,
+                          uint64_t* length) {
+    int rc = ensure_arena(ctx, 4096);
+    if (rc) return rc;
+    SelectArgs sa;
+    std::memset(&sa, 0, sizeof(sa));
+    sa.span_b_in = span_b_dev;
+    sa.span_e_in = span_e_dev;
+    sa.n_spans_in = (uint32_t)n_spans;
+    if (n_spans == 0) {  // an empty SpanSet: still "given", never voted
+        sa.span_b_in = span_b_dev ? span_b_dev : (const uint32_t*)ctx->arena;
+        sa.span_e_in = sa.span_b_in;
+    }
+    sa.middle_len = (uint32_t)(c->local_start() - c->global_end());
+    sa.build_scope = 1;
+    sa.g_end = (uint32_t)c->global_end();
+    sa.l_start = (uint32_t)c->local_start();
+    sa.total = (uint32_t)c->total;
+    sa.window = (uint32_t)std::min<uint64_t>(window, 0xFFFFFFFFull);
+    sa.n_q = 0;
+    sa.scope_src = src_dev;
+    sa.hdr = (ScopeHeader*)((uint8_t*)ctx->arena + 256);
+    CU(ctx, launch_select(sa, ctx->stream));
+    ScopeHeader h;
+    CU(ctx, cudaMemcpyAsync(&h, sa.hdr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    rc = status_from_scope(ctx, h.error);
+    if (rc) return rc;
+    *length = h.L;
+    if (h.L && keys_out)
+        CU(ctx, launch_gather(c->keys, c->dtype, c->n_kv, c->d, c->capacity, src_dev, h.L,
+                              keys_out, ctx->stream));
+    if (h.L && values_out)
+        CU(ctx, launch_gather(c->values, c->dtype, c->n_kv, c->d, c->capacity, src_dev, h.L,
+                              values_out, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_attend(reattn_ctx* ctx, const float* q_dev, uint64_t n_q, const float* k_dev,
+                  const float* v_dev, uint64_t L, uint64_t d, uint64_t dv, int has_boundary,
+                  uint64_t boundary, float* out_dev, double* entropy_dev) {
+    if (L == 0) return set_err(ctx, REATTN_EINVAL, "empty key set");
+    if (d > 4096 || dv > 4096) return set_err(ctx, REATTN_EINVAL, "attend: head dim too large");
+    if (n_q == 0) return REATTN_OK;
+    AttnArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.q = q_dev;
+    a.q_row_stride = d;
+    a.n_q = (int)n_q;
+    a.n_head = 1;
+    a.n_kv = 1;
+    a.group = 1;
+    a.d = (int)d;
+    a.dv = (int)dv;
+    a.dtype = kF32;
+    a.head_stride = 0;
+    a.src = nullptr;
+    a.hdr = nullptr;
+    a.L_host = (uint32_t)L;
+    a.causal = has_boundary ? 1 : 0;
+    a.boundary_is_tail = 0;
+    a.boundary_host = (uint32_t)std::min<uint64_t>(boundary, 0xFFFFFFF0ull);
+    a.out = out_dev;
+    a.entropy = entropy_dev;
+    // k and v have different row widths: run them as separate bases (head_stride unused)
+    a.k_base = k_dev;
+    a.v_base = v_dev;
+    const size_t ws = attend_workspace(a, (uint32_t)L);
+    int rc = ensure_arena(ctx, ws + 256);
+    if (rc) return rc;
+    a.part = (double*)ctx->arena;
+    CU(ctx, launch_attend(a, (uint32_t)L, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_attend_step(reattn_ctx* ctx, const reattn_cache* cache, const reattn_rope* rope,
+                       const float* q_dev, uint64_t n_q, uint64_t n_head,
+                       const reattn_selection_config* cfg, int mode, float* out_dev,
+                       reattn_step_stats* stats, uint64_t* span_b_host, uint64_t* span_e_host,
+                       double* entropy_host) {
+    StepPlan P;
+    int rc = plan_step(ctx, cache, rope, n_q, n_head, cfg, mode, P, q_dev, out_dev);
+    if (rc) return rc;
+    Carver sizer{nullptr, 0, 0};
+    carve_step(P, cache, rope, sizer);
+    rc = ensure_arena(ctx, sizer.off + 256);
+    if (rc) return rc;
+    Carver c{(uint8_t*)ctx->arena, 0, ctx->arena_bytes};
+    carve_step(P, cache, rope, c);
+    rc = enqueue_step(ctx, P, cache, rope, q_dev, out_dev, ctx->stream, true);
+    if (rc) return rc;
+    ScopeHeader h;
+    CU(ctx, cudaMemcpyAsync(&h, P.hdr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    rc = finish_step_stats(ctx, P, h, stats, entropy_host);
+    if (rc) return rc;
+    if (span_b_host && h.n_spans) {
+        std::vector<uint32_t> b(h.n_spans), e(h.n_spans);
+        CU(ctx, cudaMemcpy(b.data(), P.span_b, h.n_spans * 4, cudaMemcpyDeviceToHost));
+        CU(ctx, cudaMemcpy(e.data(), P.span_e, h.n_spans * 4, cudaMemcpyDeviceToHost));
+        for (uint32_t i = 0; i < h.n_spans; ++i) {
+            span_b_host[i] = b[i];
+            span_e_host[i] = e[i];
+        }
+    }
+    return REATTN_OK;
+}
+
+// ---- plans ---------------------------------------------------------------------------
+int reattn_plan_create(reattn_ctx* ctx, const reattn_cache* cache, const reattn_rope* rope,
+                       uint64_t n_q, uint64_t n_head, const reattn_selection_config* cfg,
+                       int mode, reattn_plan** out) {
+    *out = nullptr;
+    auto* p = new reattn_plan();
+    p->ctx = ctx;
+    p->cache = cache;
+    p->rope = rope;
+    int rc = plan_step(ctx, cache, rope, n_q, n_head, cfg, mode, p->P, nullptr, nullptr);
+    if (rc) {
+        delete p;
+        return rc;
+    }
+    Carver sizer{nullptr, 0, 0};
+    sizer.take<float>(n_q * n_head * cache->d);
+    sizer.take<float>(n_q * n_head * cache->d);
+    carve_step(p->P, cache, rope, sizer);
+    cudaError_t e = cudaMalloc(&p->mem, sizer.off + 256);
+    if (e == cudaSuccess) e = cudaMemset(p->mem, 0, sizer.off + 256);
+    if (e != cudaSuccess) {
+        delete p;
+        return set_err(ctx, REATTN_ECUDA, std::string("plan allocation: ") + cudaGetErrorString(e));
+    }
+    Carver c{(uint8_t*)p->mem, 0, sizer.off + 256};
+    p->q = c.take<float>(n_q * n_head * cache->d);
+    p->out = c.take<float>(n_q * n_head * cache->d);
+    carve_step(p->P, cache, rope, c);
+    // capture the step as a graph on a private stream
+    cudaStream_t cs;
+    CU(ctx, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CU(ctx, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    rc = enqueue_step(ctx, p->P, cache, rope, p->q, p->out, cs, false);
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(cs, &g);
+    cudaStreamDestroy(cs);
+    if (rc || ce != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        cudaFree(p->mem);
+        delete p;
+        return rc ? rc : set_err(ctx, REATTN_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    }
+    p->graph = g;
+    e = cudaGraphInstantiate(&p->exec, g, 0);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(g);
+        cudaFree(p->mem);
+        delete p;
+        return set_err(ctx, REATTN_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    }
+    *out = p;
+    return REATTN_OK;
+}
+
+void reattn_plan_destroy(reattn_plan* p) {
+    if (!p) return;
+    cudaDeviceSynchronize();  // never touches the (possibly destroyed) context stream
+    if (p->exec) cudaGraphExecDestroy(p->exec);
+    if (p->graph) cudaGraphDestroy(p->graph);
+    cudaFree(p->mem);
+    delete p;
+}
+float* reattn_plan_q(const reattn_plan* p) { return p->q; }
+float* reattn_plan_out(const reattn_plan* p) { return p->out; }
+
+int reattn_plan_launch(reattn_plan* p) {
+    CU(p->ctx, cudaGraphLaunch(p->exec, p->ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_plan_launch_scan(reattn_plan* p) {
+    if (!p->P.select) return REATTN_OK;
+    return enqueue_scan(p->ctx, p->P.scan, p->P.scan_ws, p->ctx->stream, false);
+}
+
+int reattn_plan_run_host(reattn_plan* p, const float* q_host, float* out_host) {
+    const size_t bytes = p->P.n_q * p->P.n_head * p->cache->d * sizeof(float);
+    reattn_ctx* ctx = p->ctx;
+    CU(ctx, cudaMemcpyAsync(p->q, q_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    CU(ctx, cudaGraphLaunch(p->exec, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(out_host, p->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_plan_stats(reattn_plan* p, reattn_step_stats* st) {
+    reattn_ctx* ctx = p->ctx;
+    ScopeHeader h;
+    CU(ctx, cudaMemcpyAsync(&h, p->P.hdr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return finish_step_stats(ctx, p->P, h, st, nullptr);
+}
+
+int reattn_plan_info(const reattn_plan* p, uint64_t* kernels, uint64_t* scan_bytes,
+                     uint64_t* scope_bytes) {
+    const uint64_t esz = p->cache->dtype == REATTN_BF16 ? 2 : 4;
+    if (kernels) *kernels = p->P.kernels;
+    if (scan_bytes) *scan_bytes = p->P.select ? p->P.n_kv * p->P.middle * p->P.d * esz : 0;
+    if (scope_bytes) *scope_bytes = p->P.n_kv * (uint64_t)p->P.L_upper * 2 * p->P.d * esz;
+    return REATTN_OK;
+}
+
+int reattn_synth_uniform(reattn_ctx* ctx, void* dst, uint64_t n, int dtype, uint64_t seed,
+                         uint64_t offset) {
+    if (n == 0) return REATTN_OK;
+    CU(ctx, launch_synth_uniform(dst, dtype, n, seed, offset, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+}  // extern "C"

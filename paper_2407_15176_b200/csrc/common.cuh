@@ -1,0 +1,184 @@
+// Shared sm_100a device helpers: mbarrier / TMA PTX wrappers, packed f32x2 math,
+// total-order keys for (score desc, index asc) selection.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace reattn_dev {
+
+constexpr uint32_t kNoIndex = 0xFFFFFFFFu;
+constexpr int kLanesUnfused = 0;  // dot lane update: round(a*b) then round(l + p)
+constexpr int kLanesFma = 1;      // dot lane update: fma(a, b, l)
+
+// ---------------------------------------------------------------------------------
+// Ordering: the reference ranks top-k entries by score descending, then index
+// ascending (selection.hpp:76-80, :127-134), and compares scores with ==, so -0.0
+// and +0.0 are equal.  better(a, b) is that strict total order.
+__device__ __forceinline__ bool better(float sa, uint32_t ia, float sb, uint32_t ib) {
+    return sa > sb || (sa == sb && ia < ib);
+}
+
+// Monotone map float -> uint32 (larger float => larger key), -0.0 folded onto +0.0.
+__device__ __forceinline__ uint32_t float_key(float f) {
+    uint32_t u = __float_as_uint(f);
+    if (u == 0x80000000u) u = 0u;
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key_float(uint32_t k) {
+    uint32_t u = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+    return __uint_as_float(u);
+}
+// 64-bit composite: larger == better under (score desc, index asc).
+__device__ __forceinline__ unsigned long long topk_key(float s, uint32_t idx) {
+    return ((unsigned long long)float_key(s) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
+}
+__device__ __forceinline__ uint32_t key_index(unsigned long long k) {
+    return 0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull);
+}
+__device__ __forceinline__ float key_score(unsigned long long k) {
+    return key_float((uint32_t)(k >> 32));
+}
+
+// ---------------------------------------------------------------------------------
+// Packed fp32x2 arithmetic (sm_100+): each half is an IEEE-rounded fp32 op, so the
+// results are bit-identical to the scalar __fmul_rn / __fadd_rn / __fmaf_rn.
+typedef unsigned long long f2_t;
+
+__device__ __forceinline__ f2_t f2_pack(uint32_t lo, uint32_t hi) {
+    f2_t d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "r"(lo), "r"(hi));
+    return d;
+}
+__device__ __forceinline__ f2_t f2_packf(float lo, float hi) {
+    return f2_pack(__float_as_uint(lo), __float_as_uint(hi));
+}
+__device__ __forceinline__ float f2_lo(f2_t v) {
+    uint32_t lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+    return __uint_as_float(lo);
+}
+__device__ __forceinline__ float f2_hi(f2_t v) {
+    uint32_t lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+    return __uint_as_float(hi);
+}
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
+    f2_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+    f2_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// acc + p with p a product that must stay unfused.  ptxas contracts mul.rn.f32x2 feeding
+// add.rn.f32x2 into FFMA2 even with explicit rounding and --fmad=false; routing the product
+// through an integer sign flip and subtracting (acc - (-p) == acc + p exactly in IEEE-754,
+// signed zeros included) keeps FMUL2 + FADD2.
+__device__ __forceinline__ f2_t f2_add_product(f2_t acc, f2_t p) {
+    const f2_t np = p ^ 0x8000000080000000ull;
+    f2_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(acc), "l"(np));
+    return d;
+}
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+    f2_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+
+// bf16x2 word -> two fp32 (exact).
+__device__ __forceinline__ f2_t bf16x2_to_f2(uint32_t w) {
+    return f2_pack(w << 16, w & 0xFFFF0000u);
+}
+
+// ---------------------------------------------------------------------------------
+// mbarrier + TMA (cp.async.bulk.tensor) wrappers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0,
+                                            int32_t c1, uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// ---------------------------------------------------------------------------------
+// Warp-wide argmax under better(): returns the winning (score, index) to all lanes.
+__device__ __forceinline__ void warp_best(float& s, uint32_t& i) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const float os = __shfl_xor_sync(0xFFFFFFFFu, s, off);
+        const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, i, off);
+        if (better(os, oi, s, i)) {
+            s = os;
+            i = oi;
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ float load_as_float(const T* p);
+template <>
+__device__ __forceinline__ float load_as_float<float>(const float* p) {
+    return *p;
+}
+template <>
+__device__ __forceinline__ float load_as_float<__nv_bfloat16>(const __nv_bfloat16* p) {
+    return __bfloat162float(*p);
+}
+
+}  // namespace reattn_dev

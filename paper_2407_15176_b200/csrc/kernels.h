@@ -1,0 +1,156 @@
+// Host-side launch interface of the sm_100a kernels (internal; the public boundary is
+// include/reattn_cuda.h).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace reattn_impl {
+
+enum DType { kF32 = 0, kBF16 = 1 };
+
+// Scope descriptor written on the device by the vote/span/scope kernel and read by the
+// attention kernels, so a whole attend_step runs without a host round trip.
+struct ScopeHeader {
+    uint32_t L;          // scope length L'
+    uint32_t n_spans;
+    uint32_t coverage;   // rows selected from the middle
+    uint32_t n_winners;
+    int32_t error;       // 0 ok, see kScopeErr*
+    uint32_t pad[3];
+};
+enum {
+    kScopeOk = 0,
+    kScopeErrWindow = 1,      // "scope exceeds pretrain window"
+    kScopeErrSpanRange = 2,   // "assemble_scope: span outside middle"
+    kScopeErrQueryLong = 3,   // "attend_step: query block longer than scope"
+    kScopeErrWinnerRange = 4, // "expand_spans: winner outside middle"
+    kScopeErrTooMany = 5,     // candidate count beyond the device vote capacity
+};
+
+// Inputs/outputs of the warp-level vote + spans + scope routine (select_small.cuh), used
+// standalone and fused into the K-scan's last CTA.
+struct SmallSelectIO {
+    uint32_t k_prime, span_m, middle_len;
+    int span_mode;
+    uint32_t g_end, l_start, total, window, n_q;
+    uint32_t* winners;
+    uint32_t* span_b;
+    uint32_t* span_e;
+    uint32_t* scope_src;
+    ScopeHeader* hdr;
+};
+constexpr uint32_t kSmallSelectMax = 32;
+
+// ---- K1: decode scan + top-k (selection.hpp:275-355) -------------------------------
+struct ScanArgs {
+    const float* q;        // [n_q][n_heads*d] pre-rotation queries
+    int n_q, n_heads, n_kv, d;
+    const void* keys;      // head 0, row 0 of a head-major [n_kv][head_stride][d] array
+    int dtype;
+    uint64_t head_stride;  // rows between heads
+    uint64_t row0;         // middle row 0 inside each head
+    uint32_t count;        // middle length
+    int k;
+    int lanes;             // kLanesUnfused / kLanesFma
+    uint32_t* idx_out;     // [n_kv][n_q][k]
+    float* score_out;
+    // fast path only: run vote + spans + scope in the last CTA (n_kv * min(k, count) <= 32)
+    int fuse_select = 0;
+    SmallSelectIO sel = {};
+};
+
+// Fast path: TMA-staged, one thread per key row, q in registers, register top-k.
+// Requires d == 128, n_q == 1, k <= 8.
+bool scan_fast_supported(const ScanArgs& a);
+size_t scan_fast_workspace(const ScanArgs& a, int num_sms);
+// `kmap` is a 2-D tiled tensor map over [n_kv*head_stride rows][d] with a 128-byte box
+// width and SWIZZLE_128B (built by make_key_tensor_map).
+cudaError_t launch_scan_fast(const ScanArgs& a, const CUtensorMap& kmap, void* workspace,
+                             int num_sms, cudaStream_t s);
+bool make_key_tensor_map(CUtensorMap* map, const void* base, int dtype, uint64_t d,
+                         uint64_t rows, int box_rows);
+int scan_fast_box_rows(int dtype);
+
+// Generic path: any d, n_q, k (k <= kGenericMaxK), streaming threshold buffer + bitonic
+// compaction in shared memory; one CTA per (query, kv head).
+constexpr int kGenericMaxK = 7936;
+cudaError_t launch_scan_generic(const ScanArgs& a, cudaStream_t s);
+
+// ---- K3: vote + spans + scope (selection.hpp:359-456, scope.hpp:248-289) ----------
+struct SelectArgs {
+    const uint32_t* cand_idx;  // n_lists lists of list_len valid entries, list stride
+    const float* cand_score;
+    uint32_t n_lists, list_len, list_stride;
+    uint32_t k_prime;
+    uint32_t span_m;
+    uint32_t middle_len;
+    int span_mode;
+    // scope build (skipped when build_scope == 0)
+    int build_scope;
+    uint32_t g_end, l_start, total, window, n_q;
+    // external winners / spans (bypass stages): used by the standalone APIs
+    const uint32_t* winners_in;  // if non-null: skip the vote, use these n_winners_in
+    uint32_t n_winners_in;
+    const uint32_t* span_b_in;   // if non-null: skip vote + expand, use these spans
+    const uint32_t* span_e_in;
+    uint32_t n_spans_in;
+    // outputs
+    uint32_t* winners;   // [k_prime]
+    uint32_t* rank_votes;  // optional [k_prime]: votes of each winner (tally API)
+    float* rank_score;     // optional [k_prime]: max score of each winner
+    uint32_t* span_b;    // [k_prime]
+    uint32_t* span_e;
+    uint32_t* scope_src; // [window]
+    ScopeHeader* hdr;
+};
+constexpr uint32_t kVoteMaxSmem = 8192;
+size_t select_smem_bytes(uint32_t n_cand, uint32_t k_prime);
+cudaError_t launch_select(const SelectArgs& a, cudaStream_t s);
+
+// ---- K4+K5: gather + RoPE + finite-scope attention (attend.hpp, engine.hpp:529-565)
+struct AttnArgs {
+    const float* q;          // query rows, q_row_stride floats apart; head h at +h*d
+    uint64_t q_row_stride;
+    int n_q, n_head, n_kv, group, d, dv;
+    const void* k_base;      // [n_kv][head_stride][d]
+    const void* v_base;      // [n_kv][head_stride][dv]
+    int dtype;
+    uint64_t head_stride;
+    const uint32_t* src;     // scope row -> cache row (nullptr: identity)
+    const ScopeHeader* hdr;  // L from the device header (nullptr: use L_host)
+    uint32_t L_host;
+    const float* rope_cos;   // [max_pos][d/2] (nullptr: no rotation)
+    const float* rope_sin;
+    int causal;              // 1: row i sees [0, boundary+i+1)
+    int boundary_is_tail;    // 1: boundary = L - n_q (attend_step), else boundary_host
+    uint32_t boundary_host;
+    double* part;            // workspace, see attend_workspace
+    float* out;              // [n_q][n_head*dv]
+    double* entropy;         // [n_q][n_head]
+};
+constexpr int kAttnSplit = 64;
+size_t attend_workspace(const AttnArgs& a, uint32_t L_max);
+cudaError_t launch_attend(const AttnArgs& a, uint32_t L_max, cudaStream_t s);
+int attend_kernel_count(const AttnArgs& a, uint32_t L_max);
+
+// ---- misc kernels ------------------------------------------------------------------
+// rows x (n_kv*d) fp32 (DenseMatrix layout) -> head-major [n_kv][head_stride][d] at row0.
+cudaError_t launch_cache_append(const float* src, void* dst, int dtype, uint64_t rows,
+                                uint64_t n_kv, uint64_t d, uint64_t head_stride, uint64_t row0,
+                                cudaStream_t s);
+// scope gather to fp32 [n_kv][L][d] (assemble_scope's copies, scope.hpp:274-287).
+cudaError_t launch_gather(const void* base, int dtype, uint64_t n_kv, uint64_t d,
+                          uint64_t head_stride, const uint32_t* src, uint32_t L, float* out,
+                          cudaStream_t s);
+cudaError_t launch_rope_rotate(float* rows, const uint32_t* pos, uint64_t n_rows, uint64_t d,
+                               const float* cos_t, const float* sin_t, cudaStream_t s);
+cudaError_t launch_synth_uniform(void* dst, int dtype, uint64_t n, uint64_t seed,
+                                 uint64_t offset, cudaStream_t s);
+// entropy stats reduction in the reference's order (engine.hpp:558-564): for h, for i.
+cudaError_t launch_entropy_stats(const double* entropy, int n_q, int n_head, double* out2,
+                                 cudaStream_t s);
+
+}  // namespace reattn_impl

@@ -1,0 +1,628 @@
+// K1 — position-agnostic q·Kᵀ scan fused with an exact running top-k.
+//
+// Restates reattn::fused_topk_scores (reference selection.hpp:275-355) on sm_100a:
+//   * group-mean query per KV head (selection.hpp:246-263): sequential fp32 adds, then
+//     multiply by float(1/group);
+//   * score = dot_f32 (dense_matrix.hpp:41-56): eight lanes over elements j, j+8, ...,
+//     then ((l0+l1)+(l2+l3))+((l4+l5)+(l6+l7)).  The lane update is emulated exactly in
+//     either of the two codegen variants the reference compiles to:
+//     unfused (round(a*b) then round(l+p)) or FMA — so scores are bit-identical;
+//   * exact top-k with ties to the lower index (selection.hpp:81-135), output sorted by
+//     (score desc, index asc).
+//
+// Fast path (decode, d=128, n_q=1, k<=8): a persistent grid, one CTA per SM.  A producer
+// warp streams 64 KB tiles of key rows with TMA (cp.async.bulk.tensor, SWIZZLE_128B) into
+// a 3-stage shared-memory ring; each consumer thread owns one key row per tile, holds the
+// group-mean query in registers as 64 packed fp32x2 pairs and evaluates the 8-lane dot
+// with FMUL2/FADD2 (or FFMA2), then keeps a register top-k (the common reject is one
+// compare against a register threshold, as selection.hpp:230-236).  Per-CTA top-k go to a
+// slot array; the last CTA to finish (atomic ticket) merges them deterministically.
+//
+// Generic path (any d / n_q / k): one CTA per (query, kv head) streaming the whole
+// middle, appending candidates above the running k-th key into a shared buffer and
+// compacting it with a bitonic sort — bounded scratch, exact, deterministic.
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "select_small.cuh"
+
+using namespace reattn_dev;
+
+namespace reattn_impl {
+
+namespace {
+
+template <typename KT>
+struct FastCfg {
+    static constexpr int D = 128;
+    static constexpr int ESZ = (int)sizeof(KT);
+    static constexpr int ROW_BYTES = D * ESZ;       // 256 (bf16) / 512 (fp32)
+    // key rows per stage = consumer threads.  bf16: 7 consumer warps + 1 producer warp = 8
+    // warps, i.e. 2 per SM sub-partition, which leaves ptxas 255 registers per thread for
+    // the 128-float query kept in registers (9 warps would cap it at 168 and spill).
+    static constexpr int ROWS = ESZ == 2 ? 224 : 128;
+    static constexpr int NBOX = ROW_BYTES / 128;    // 128-byte TMA boxes per row
+    static constexpr int BOX_ELEMS = 128 / ESZ;
+    static constexpr int STAGE_BYTES = ROWS * ROW_BYTES;
+    static constexpr int STAGES = 3;
+    static constexpr int CONSUMERS = ROWS;
+    static constexpr int CWARPS = CONSUMERS / 32;
+    static constexpr int THREADS = CONSUMERS + 32;  // + one TMA producer warp
+    static constexpr int KMAX = 8;
+    static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES +
+                                   2 * STAGES * sizeof(uint64_t) + D * sizeof(float) +
+                                   CWARPS * KMAX * (sizeof(float) + sizeof(uint32_t)) + 16;
+};
+
+struct FastArgs {
+    const float* q;
+    int n_heads, n_kv, group;
+    uint64_t head_stride, row0;
+    uint32_t count;
+    int k;
+    uint32_t tiles_per_head, total_tiles;
+    uint32_t* slot_idx;
+    float* slot_score;
+    unsigned int* ticket;
+    uint32_t* idx_out;
+    float* score_out;
+    int fuse_select;
+    SmallSelectIO sel;
+};
+
+template <int KMAX>
+__device__ __forceinline__ void topk_reset(float (&ts)[KMAX], uint32_t (&ti)[KMAX]) {
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        ts[j] = -INFINITY;
+        ti[j] = kNoIndex;
+    }
+}
+
+// Bubble (s, i) into the sorted list; full (score desc, index asc) comparator.
+template <int KMAX>
+__device__ __forceinline__ void topk_insert(float (&ts)[KMAX], uint32_t (&ti)[KMAX], int k,
+                                            float s, uint32_t i) {
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        if (j < k && better(s, i, ts[j], ti[j])) {
+            const float t = ts[j];
+            const uint32_t u = ti[j];
+            ts[j] = s;
+            ti[j] = i;
+            s = t;
+            i = u;
+        }
+    }
+}
+
+template <int KMAX>
+__device__ __forceinline__ float topk_threshold(const float (&ts)[KMAX], int k) {
+    float thr = ts[0];
+#pragma unroll
+    for (int j = 1; j < KMAX; ++j)
+        if (j == k - 1) thr = ts[j];
+    return thr;
+}
+
+template <int KMAX>
+__device__ __forceinline__ void topk_pop(float (&ts)[KMAX], uint32_t (&ti)[KMAX]) {
+#pragma unroll
+    for (int j = 0; j + 1 < KMAX; ++j) {
+        ts[j] = ts[j + 1];
+        ti[j] = ti[j + 1];
+    }
+    ts[KMAX - 1] = -INFINITY;
+    ti[KMAX - 1] = kNoIndex;
+}
+
+template <int LANES>
+__device__ __forceinline__ void lane_step(f2_t& acc, f2_t q, f2_t k) {
+    if (LANES == kLanesFma)
+        acc = f2_fma(q, k, acc);
+    else
+        acc = f2_add_product(acc, f2_mul(q, k));
+}
+
+__device__ __forceinline__ float lane_tree(f2_t a0, f2_t a1, f2_t a2, f2_t a3) {
+    const float s01 = __fadd_rn(f2_lo(a0), f2_hi(a0));
+    const float s23 = __fadd_rn(f2_lo(a1), f2_hi(a1));
+    const float s45 = __fadd_rn(f2_lo(a2), f2_hi(a2));
+    const float s67 = __fadd_rn(f2_lo(a3), f2_hi(a3));
+    return __fadd_rn(__fadd_rn(s01, s23), __fadd_rn(s45, s67));
+}
+
+template <typename KT, int LANES>
+__global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
+    scan_fast_kernel(const __grid_constant__ CUtensorMap kmap, const FastArgs a) {
+    using C = FastCfg<KT>;
+    constexpr int KMAX = C::KMAX;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* stages = smem;
+    uint64_t* full = (uint64_t*)(smem + (size_t)C::STAGES * C::STAGE_BYTES);
+    uint64_t* empty = full + C::STAGES;
+    float* s_mq = (float*)(empty + C::STAGES);
+    float* s_ws = s_mq + C::D;
+    uint32_t* s_wi = (uint32_t*)(s_ws + C::CWARPS * KMAX);
+    __shared__ int s_last;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const uint32_t G = gridDim.x, b = blockIdx.x;
+    const uint32_t t_begin = (uint32_t)((uint64_t)b * a.total_tiles / G);
+    const uint32_t t_end = (uint32_t)((uint64_t)(b + 1) * a.total_tiles / G);
+    const int k = a.k;
+
+    if (tid == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], C::CWARPS);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == C::CWARPS) {
+        // ===== TMA producer =====
+        if (lane == 0) {
+            prefetch_tensormap(&kmap);
+            const uint64_t pol = policy_evict_first();
+            uint32_t it = 0;
+            for (uint32_t t = t_begin; t < t_end; ++t, ++it) {
+                const int s = it % C::STAGES;
+                const uint32_t ph = (it / C::STAGES) & 1u;
+                if (it >= (uint32_t)C::STAGES) mbar_wait(&empty[s], ph ^ 1u);
+                const uint32_t kv = t / a.tiles_per_head, j = t % a.tiles_per_head;
+                const int32_t row =
+                    (int32_t)(kv * a.head_stride + a.row0 + (uint64_t)j * C::ROWS);
+                mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+#pragma unroll
+                for (int box = 0; box < C::NBOX; ++box)
+                    tma_load_2d(stages + (size_t)s * C::STAGE_BYTES + box * C::ROWS * 128, &kmap,
+                                box * C::BOX_ELEMS, row, &full[s], pol);
+            }
+        }
+    } else {
+        // ===== consumers: one key row per thread per tile =====
+        f2_t qv[C::D / 2];
+        float ts[KMAX];
+        uint32_t ti[KMAX];
+        float thr = -INFINITY;
+        topk_reset<KMAX>(ts, ti);
+        uint32_t cur_kv = kNoIndex;
+        const uint32_t sw = (uint32_t)tid & 7u;
+
+        auto flush = [&](uint32_t kv) {
+            // warp-level top-k of the warp's 32 lists, then warp 0 merges the warps
+            for (int r = 0; r < k; ++r) {
+                float bs = ts[0];
+                uint32_t bi = ti[0];
+                warp_best(bs, bi);
+                if (lane == 0) {
+                    s_ws[warp * KMAX + r] = bs;
+                    s_wi[warp * KMAX + r] = bi;
+                }
+                if (bi != kNoIndex && ti[0] == bi) topk_pop<KMAX>(ts, ti);
+            }
+            named_bar_sync(1, C::CONSUMERS);
+            if (warp == 0) {
+                float ls[2];
+                uint32_t li[2];
+                ls[0] = ls[1] = -INFINITY;
+                li[0] = li[1] = kNoIndex;
+                const int n = C::CWARPS * k;
+                for (int e = lane; e < n; e += 32) {
+                    const int w = e / k, r = e % k;
+                    float s = s_ws[w * KMAX + r];
+                    uint32_t i = s_wi[w * KMAX + r];
+                    if (better(s, i, ls[0], li[0])) {
+                        ls[1] = ls[0];
+                        li[1] = li[0];
+                        ls[0] = s;
+                        li[0] = i;
+                    } else if (better(s, i, ls[1], li[1])) {
+                        ls[1] = s;
+                        li[1] = i;
+                    }
+                }
+                for (int r = 0; r < k; ++r) {
+                    float bs = ls[0];
+                    uint32_t bi = li[0];
+                    warp_best(bs, bi);
+                    if (lane == 0) {
+                        const size_t slot = ((size_t)kv * G + b) * KMAX + r;
+                        a.slot_score[slot] = bs;
+                        a.slot_idx[slot] = bi;
+                    }
+                    if (bi != kNoIndex && li[0] == bi) {
+                        ls[0] = ls[1];
+                        li[0] = li[1];
+                        ls[1] = -INFINITY;
+                        li[1] = kNoIndex;
+                    }
+                }
+                __threadfence();
+            }
+            named_bar_sync(1, C::CONSUMERS);
+            topk_reset<KMAX>(ts, ti);
+            thr = -INFINITY;
+        };
+
+        uint32_t it = 0;
+        for (uint32_t t = t_begin; t < t_end; ++t, ++it) {
+            const uint32_t kv = t / a.tiles_per_head, j = t % a.tiles_per_head;
+            if (kv != cur_kv) {
+                if (cur_kv != kNoIndex) flush(cur_kv);
+                // group-mean query for this kv head (selection.hpp:250-258)
+                if (tid < C::D) {
+                    const float inv = __fdiv_rn(1.0f, (float)a.group);
+                    float acc = 0.0f;
+                    for (int g = 0; g < a.group; ++g)
+                        acc = __fadd_rn(acc, a.q[(size_t)(kv * a.group + g) * C::D + tid]);
+                    s_mq[tid] = __fmul_rn(acc, inv);
+                }
+                named_bar_sync(1, C::CONSUMERS);
+#pragma unroll
+                for (int p = 0; p < C::D / 2; ++p) qv[p] = f2_packf(s_mq[2 * p], s_mq[2 * p + 1]);
+                cur_kv = kv;
+            }
+            const int s = it % C::STAGES;
+            const uint32_t ph = (it / C::STAGES) & 1u;
+            mbar_wait(&full[s], ph);
+            const uint32_t row = j * C::ROWS + (uint32_t)tid;
+            if (row < a.count) {
+                const uint32_t sbase =
+                    smem_u32(stages + (size_t)s * C::STAGE_BYTES) + (uint32_t)tid * 128u;
+                f2_t a0 = f2_pack(0u, 0u), a1 = a0, a2 = a0, a3 = a0;
+#pragma unroll
+                for (int c = 0; c < C::D / 8; ++c) {
+                    f2_t k0, k1, k2, k3;
+                    if (C::ESZ == 2) {
+                        const int box = c >> 3, cb = c & 7;
+                        const uint4 w = lds128(sbase + box * C::ROWS * 128 + (((uint32_t)cb ^ sw) << 4));
+                        k0 = bf16x2_to_f2(w.x);
+                        k1 = bf16x2_to_f2(w.y);
+                        k2 = bf16x2_to_f2(w.z);
+                        k3 = bf16x2_to_f2(w.w);
+                    } else {
+                        const int box = c >> 2, u0 = (c & 3) * 2;
+                        const uint32_t bb = sbase + box * C::ROWS * 128;
+                        const uint4 w0 = lds128(bb + (((uint32_t)u0 ^ sw) << 4));
+                        const uint4 w1 = lds128(bb + (((uint32_t)(u0 + 1) ^ sw) << 4));
+                        k0 = f2_pack(w0.x, w0.y);
+                        k1 = f2_pack(w0.z, w0.w);
+                        k2 = f2_pack(w1.x, w1.y);
+                        k3 = f2_pack(w1.z, w1.w);
+                    }
+                    lane_step<LANES>(a0, qv[4 * c + 0], k0);
+                    lane_step<LANES>(a1, qv[4 * c + 1], k1);
+                    lane_step<LANES>(a2, qv[4 * c + 2], k2);
+                    lane_step<LANES>(a3, qv[4 * c + 3], k3);
+                }
+                const float score = lane_tree(a0, a1, a2, a3);
+                if (score > thr) {
+                    topk_insert<KMAX>(ts, ti, k, score, row);
+                    thr = topk_threshold<KMAX>(ts, k);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        if (cur_kv != kNoIndex) flush(cur_kv);
+    }
+
+    // ===== cross-CTA merge by the last CTA to finish =====
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        const unsigned int done = atomicAdd(a.ticket, 1u);
+        s_last = (done == G - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int nwarps = C::THREADS / 32;
+    for (int kv = warp; kv < a.n_kv; kv += nwarps) {
+        float ls[KMAX];
+        uint32_t li[KMAX];
+        topk_reset<KMAX>(ls, li);
+        // CTAs covering this head's tiles [h0, h1): CTA b starts at floor(b*T/G) (every CTA
+        // owns >= 1 tile since G <= T), so the first/last coverers follow directly.
+        const uint64_t T = a.total_tiles;
+        const uint64_t h0 = (uint64_t)kv * a.tiles_per_head, h1 = h0 + a.tiles_per_head;
+        const uint32_t b0 = (uint32_t)(((h0 + 1) * G + T - 1) / T - 1);
+        const uint32_t b1 = (uint32_t)((h1 * G + T - 1) / T - 1);
+        const int n = (int)(b1 - b0 + 1) * k;
+        for (int e = lane; e < n; e += 32) {
+            const size_t slot = ((size_t)kv * G + b0 + e / k) * KMAX + e % k;
+            const float s = __ldcg(a.slot_score + slot);
+            const uint32_t i = __ldcg(a.slot_idx + slot);
+            if (i != kNoIndex) topk_insert<KMAX>(ls, li, k, s, i);
+        }
+        for (int r = 0; r < k; ++r) {
+            float bs = ls[0];
+            uint32_t bi = li[0];
+            warp_best(bs, bi);
+            if (lane == 0) {
+                a.idx_out[(size_t)kv * k + r] = bi;
+                a.score_out[(size_t)kv * k + r] = bs;
+            }
+            if (bi != kNoIndex && li[0] == bi) topk_pop<KMAX>(ls, li);
+        }
+    }
+    if (tid == 0) *a.ticket = 0u;  // re-arm for the next launch (graph replay)
+    if (a.fuse_select) {
+        // vote + spans + scope on the merged candidates [kv][0..kk) (selection.hpp:359-456)
+        __shared__ SmallSelectSmem ssel;
+        __syncthreads();
+        const int kk = (int)min((uint32_t)k, a.count);
+        const int n = a.n_kv * kk;
+        uint32_t ci = 0;
+        float cs = 0.0f;
+        const bool valid = tid < n;
+        if (valid) {
+            ci = a.idx_out[(size_t)(tid / kk) * k + tid % kk];
+            cs = a.score_out[(size_t)(tid / kk) * k + tid % kk];
+        }
+        small_select_scope(a.sel, ci, cs, valid, ssel);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Generic exact path.
+struct GenArgs {
+    const float* q;
+    int n_q, n_heads, n_kv, d, group;
+    const void* keys;
+    uint64_t head_stride, row0;
+    uint32_t count;
+    int k;
+    int nbuf;  // power of two >= k + 512
+    uint32_t* idx_out;
+    float* score_out;
+};
+
+__device__ void bitonic_desc_u64(unsigned long long* buf, int n) {
+    for (int k2 = 2; k2 <= n; k2 <<= 1) {
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const unsigned long long x = buf[i], y = buf[ixj];
+                    const bool desc = (i & k2) == 0;
+                    if (desc ? (x < y) : (x > y)) {
+                        buf[i] = y;
+                        buf[ixj] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+template <typename KT, int LANES>
+__global__ void __launch_bounds__(256) scan_generic_kernel(const GenArgs a) {
+    extern __shared__ unsigned long long gsm[];
+    unsigned long long* buf = gsm;                  // [nbuf]
+    float* mq = (float*)(gsm + a.nbuf);             // [d]
+    __shared__ unsigned int s_nb;
+    const int qi = blockIdx.x, kv = blockIdx.y, tid = threadIdx.x;
+    const int d = a.d;
+    // group-mean query (selection.hpp:250-258)
+    const float inv = __fdiv_rn(1.0f, (float)a.group);
+    for (int c = tid; c < d; c += blockDim.x) {
+        float acc = 0.0f;
+        for (int g = 0; g < a.group; ++g)
+            acc = __fadd_rn(acc, a.q[(size_t)qi * a.n_heads * d + (size_t)(kv * a.group + g) * d + c]);
+        mq[c] = __fmul_rn(acc, inv);
+    }
+    if (tid == 0) s_nb = 0;
+    __syncthreads();
+
+    const KT* keys = (const KT*)a.keys + ((size_t)kv * a.head_stride + a.row0) * d;
+    uint32_t r = 0;                // valid sorted entries at buf[0, r)
+    unsigned long long thr = 0;    // key of the k-th best once r == k
+    const uint32_t kk = (uint32_t)a.k;
+    for (uint32_t base = 0; base < a.count; base += blockDim.x) {
+        const uint32_t row = base + tid;
+        if (row < a.count) {
+            const KT* kr = keys + (size_t)row * d;
+            float l[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            int j = 0;
+            for (; j + 8 <= d; j += 8) {
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const float kvv = load_as_float<KT>(kr + j + t);
+                    l[t] = (LANES == kLanesFma) ? __fmaf_rn(mq[j + t], kvv, l[t])
+                                                : __fadd_rn(l[t], __fmul_rn(mq[j + t], kvv));
+                }
+            }
+            for (; j < d; ++j) {
+                const float kvv = load_as_float<KT>(kr + j);
+                l[0] = (LANES == kLanesFma) ? __fmaf_rn(mq[j], kvv, l[0])
+                                            : __fadd_rn(l[0], __fmul_rn(mq[j], kvv));
+            }
+            const float s = __fadd_rn(__fadd_rn(__fadd_rn(l[0], l[1]), __fadd_rn(l[2], l[3])),
+                                      __fadd_rn(__fadd_rn(l[4], l[5]), __fadd_rn(l[6], l[7])));
+            const unsigned long long key = topk_key(s, row);
+            if (r < kk || key > thr) {
+                const unsigned int pos = atomicAdd(&s_nb, 1u);
+                buf[r + pos] = key;
+            }
+        }
+        __syncthreads();
+        const uint32_t nb = s_nb;
+        const bool last = base + blockDim.x >= a.count;
+        if (r + nb + blockDim.x > (uint32_t)a.nbuf || last) {
+            for (int i = r + nb + tid; i < a.nbuf; i += blockDim.x) buf[i] = 0ull;
+            __syncthreads();
+            bitonic_desc_u64(buf, a.nbuf);
+            r = min(kk, r + nb);
+            thr = (r == kk) ? buf[kk - 1] : 0ull;
+            if (tid == 0) s_nb = 0;
+        }
+        __syncthreads();
+    }
+    const size_t o = ((size_t)kv * a.n_q + qi) * a.k;
+    for (uint32_t j = tid; j < r; j += blockDim.x) {
+        a.idx_out[o + j] = key_index(buf[j]);
+        a.score_out[o + j] = key_score(buf[j]);
+    }
+}
+
+template <typename F>
+void set_smem_once(F* fn, size_t bytes) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------
+int scan_fast_box_rows(int dtype) {
+    return dtype == kBF16 ? FastCfg<__nv_bfloat16>::ROWS : FastCfg<float>::ROWS;
+}
+
+bool scan_fast_supported(const ScanArgs& a) {
+    return a.d == 128 && a.n_q == 1 && a.k >= 1 && a.k <= 8 && a.count > 0 &&
+           (a.dtype == kBF16 || a.dtype == kF32) &&
+           (uint64_t)a.n_kv * a.head_stride < (1ull << 31) && a.n_kv <= 65535;
+}
+
+static uint32_t fast_tiles_per_head(const ScanArgs& a) {
+    const uint32_t rows = (uint32_t)scan_fast_box_rows(a.dtype);
+    return (a.count + rows - 1) / rows;
+}
+
+size_t scan_fast_workspace(const ScanArgs& a, int num_sms) {
+    const size_t G = (size_t)std::max(1, num_sms);
+    // ticket (256 B aligned) + slots
+    return 256 + (size_t)a.n_kv * G * 8 * (sizeof(uint32_t) + sizeof(float));
+}
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                       const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                       const cuuint32_t*, CUtensorMapInterleave,
+                                       CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                       CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t encode_fn() {
+    static PFN_encodeTiled_t fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_encodeTiled_t)p;
+    });
+    return fn;
+}
+
+bool make_key_tensor_map(CUtensorMap* map, const void* base, int dtype, uint64_t d, uint64_t rows,
+                         int box_rows) {
+    PFN_encodeTiled_t enc = encode_fn();
+    if (!enc) return false;
+    const uint64_t esz = dtype == kBF16 ? 2 : 4;
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(d * esz)};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(map, dtype == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                               : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                           2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+cudaError_t launch_scan_fast(const ScanArgs& a, const CUtensorMap& kmap, void* workspace,
+                             int num_sms, cudaStream_t s) {
+    FastArgs f;
+    f.q = a.q;
+    f.n_heads = a.n_heads;
+    f.n_kv = a.n_kv;
+    f.group = a.n_heads / a.n_kv;
+    f.head_stride = a.head_stride;
+    f.row0 = a.row0;
+    f.count = a.count;
+    f.k = a.k;
+    f.tiles_per_head = fast_tiles_per_head(a);
+    f.total_tiles = f.tiles_per_head * (uint32_t)a.n_kv;
+    const int G = (int)std::min<uint32_t>((uint32_t)std::max(1, num_sms), f.total_tiles);
+    uint8_t* ws = (uint8_t*)workspace;
+    f.ticket = (unsigned int*)ws;
+    f.slot_idx = (uint32_t*)(ws + 256);
+    f.slot_score = (float*)(ws + 256 + (size_t)a.n_kv * num_sms * 8 * sizeof(uint32_t));
+    f.idx_out = a.idx_out;
+    f.score_out = a.score_out;
+    f.fuse_select = a.fuse_select;
+    f.sel = a.sel;
+    if (a.dtype == kBF16) {
+        using C = FastCfg<__nv_bfloat16>;
+        if (a.lanes == kLanesFma) {
+            static bool once = (set_smem_once(scan_fast_kernel<__nv_bfloat16, kLanesFma>, C::SMEM), true);
+            (void)once;
+            scan_fast_kernel<__nv_bfloat16, kLanesFma><<<G, C::THREADS, C::SMEM, s>>>(kmap, f);
+        } else {
+            static bool once = (set_smem_once(scan_fast_kernel<__nv_bfloat16, kLanesUnfused>, C::SMEM), true);
+            (void)once;
+            scan_fast_kernel<__nv_bfloat16, kLanesUnfused><<<G, C::THREADS, C::SMEM, s>>>(kmap, f);
+        }
+    } else {
+        using C = FastCfg<float>;
+        if (a.lanes == kLanesFma) {
+            static bool once = (set_smem_once(scan_fast_kernel<float, kLanesFma>, C::SMEM), true);
+            (void)once;
+            scan_fast_kernel<float, kLanesFma><<<G, C::THREADS, C::SMEM, s>>>(kmap, f);
+        } else {
+            static bool once = (set_smem_once(scan_fast_kernel<float, kLanesUnfused>, C::SMEM), true);
+            (void)once;
+            scan_fast_kernel<float, kLanesUnfused><<<G, C::THREADS, C::SMEM, s>>>(kmap, f);
+        }
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan_generic(const ScanArgs& a, cudaStream_t s) {
+    GenArgs g;
+    g.q = a.q;
+    g.n_q = a.n_q;
+    g.n_heads = a.n_heads;
+    g.n_kv = a.n_kv;
+    g.d = a.d;
+    g.group = a.n_heads / a.n_kv;
+    g.keys = a.keys;
+    g.head_stride = a.head_stride;
+    g.row0 = a.row0;
+    g.count = a.count;
+    g.k = a.k;
+    int nbuf = 512;
+    while (nbuf < a.k + 512) nbuf <<= 1;
+    g.nbuf = nbuf;
+    g.idx_out = a.idx_out;
+    g.score_out = a.score_out;
+    const size_t smem = (size_t)nbuf * sizeof(unsigned long long) + (size_t)a.d * sizeof(float);
+    dim3 grid(a.n_q, a.n_kv);
+#define GEN_LAUNCH(KT, L)                                                              \
+    do {                                                                               \
+        set_smem_once(scan_generic_kernel<KT, L>, smem);                               \
+        scan_generic_kernel<KT, L><<<grid, 256, smem, s>>>(g);                         \
+    } while (0)
+    if (a.dtype == kBF16) {
+        if (a.lanes == kLanesFma) GEN_LAUNCH(__nv_bfloat16, kLanesFma);
+        else GEN_LAUNCH(__nv_bfloat16, kLanesUnfused);
+    } else {
+        if (a.lanes == kLanesFma) GEN_LAUNCH(float, kLanesFma);
+        else GEN_LAUNCH(float, kLanesUnfused);
+    }
+#undef GEN_LAUNCH
+    return cudaGetLastError();
+}
+
+}  // namespace reattn_impl

@@ -1,0 +1,404 @@
+"""ctypes binding of libreattn_cuda.so (the C-ABI in include/reattn_cuda.h).
+
+This is the Python host mirror of the reference's hot-path interface
+(/root/reference/proj/include/reattn: fused_topk_scores, vote, expand_spans,
+assemble_scope, attend, attend_step).  Device memory and streams come from PyTorch
+(plumbing only); every computation runs in the sm_100a kernels of the library.  There is
+no CPU fallback: if the library is missing or no GPU is present, calls fail loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libreattn_cuda.so")
+HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "reattn_cuda.h")
+
+OK, EINVAL, ERANGE, ELOGIC, ECUDA, ERUNTIME = range(6)
+F32, BF16 = 0, 1
+SPAN_ALIGNED, SPAN_CENTERED = 0, 1
+MODE_FULL, MODE_WINDOW, MODE_REATTENTION = 0, 1, 2
+LANES_UNFUSED, LANES_FMA = 0, 1
+
+u64 = C.c_uint64
+vp = C.c_void_p
+
+
+class SelectionConfig(C.Structure):
+    """reattn::SelectionConfig (selection.hpp:127-152); defaults are the reference's."""
+
+    _fields_ = [("k", u64), ("k_prime", u64), ("span_m", u64), ("tile_size", u64),
+                ("l_global", u64), ("l_local", u64), ("l_chunk", u64), ("span_mode", C.c_int32),
+                ("reserved", C.c_int32)]
+
+    def __init__(self, k=4, k_prime=127, span_m=32, tile_size=2048, l_global=32, l_local=4096,
+                 l_chunk=512, span_mode=SPAN_ALIGNED):
+        super().__init__(k, k_prime, span_m, tile_size, l_global, l_local, l_chunk, span_mode, 0)
+
+    def budget(self) -> int:
+        return self.l_global + self.k_prime * self.span_m + self.l_local
+
+
+class StepStats(C.Structure):
+    _fields_ = [("max_position_used", u64), ("ood_positions", u64), ("coverage_total", C.c_int32),
+                ("reserved", C.c_int32), ("entropy_max", C.c_double), ("entropy_sum", C.c_double),
+                ("entropy_rows", u64), ("scope_len", u64), ("n_spans", u64), ("coverage", u64),
+                ("peak_scratch_bytes", u64)]
+
+
+class ReattnError(RuntimeError):
+    pass
+
+
+class InvalidArgument(ReattnError, ValueError):
+    """std::invalid_argument"""
+
+
+class OutOfRange(ReattnError, IndexError):
+    """std::out_of_range"""
+
+
+class LogicError(ReattnError):
+    """std::logic_error"""
+
+
+class CudaError(ReattnError):
+    pass
+
+
+_EXC = {EINVAL: InvalidArgument, ERANGE: OutOfRange, ELOGIC: LogicError, ECUDA: CudaError,
+        ERUNTIME: ReattnError}
+
+# (name, restype, argtypes) for every exported symbol; tests check this list against the
+# header so the binding and include/reattn_cuda.h cannot drift.
+SIGNATURES = [
+    ("reattn_version", C.c_char_p, []),
+    ("reattn_ctx_create", C.c_int, [C.c_int, C.POINTER(vp)]),
+    ("reattn_ctx_destroy", None, [vp]),
+    ("reattn_last_error", C.c_char_p, [vp]),
+    ("reattn_ctx_set_stream", C.c_int, [vp, vp]),
+    ("reattn_ctx_stream", vp, [vp]),
+    ("reattn_ctx_set_lanes", C.c_int, [vp, C.c_int]),
+    ("reattn_ctx_synchronize", C.c_int, [vp]),
+    ("reattn_ctx_num_sms", C.c_int, [vp]),
+    ("reattn_malloc", C.c_int, [vp, u64, C.POINTER(vp)]),
+    ("reattn_free", C.c_int, [vp, vp]),
+    ("reattn_memcpy_h2d", C.c_int, [vp, vp, vp, u64]),
+    ("reattn_memcpy_d2h", C.c_int, [vp, vp, vp, u64]),
+    ("reattn_cache_create", C.c_int, [vp, u64, u64, u64, u64, u64, C.c_int, C.POINTER(vp)]),
+    ("reattn_cache_destroy", None, [vp]),
+    ("reattn_cache_reserve", C.c_int, [vp, vp, u64]),
+    ("reattn_cache_append", C.c_int, [vp, vp, vp, vp, u64, C.c_int]),
+    ("reattn_cache_set_total", C.c_int, [vp, vp, u64]),
+    ("reattn_cache_info", C.c_int, [vp] + [C.POINTER(u64)] * 8 + [C.POINTER(C.c_int)]),
+    ("reattn_cache_keys", vp, [vp]),
+    ("reattn_cache_values", vp, [vp]),
+    ("reattn_rope_create", C.c_int, [vp, u64, C.c_double, u64, C.POINTER(vp)]),
+    ("reattn_rope_destroy", None, [vp]),
+    ("reattn_rope_tables_host", C.c_int, [vp, vp, vp]),
+    ("reattn_rope_rotate", C.c_int, [vp, vp, vp, vp, u64]),
+    ("reattn_fused_topk", C.c_int, [vp, vp, u64, u64, vp, C.c_int, u64, u64, u64, u64, u64, u64,
+                                    vp, vp, C.POINTER(u64), C.POINTER(u64)]),
+    ("reattn_vote", C.c_int, [vp, vp, vp, u64, u64, vp, C.POINTER(u64)]),
+    ("reattn_tally", C.c_int, [vp, vp, vp, u64, vp, vp, vp, C.POINTER(u64)]),
+    ("reattn_expand_spans", C.c_int, [vp, vp, u64, u64, u64, C.c_int, vp, vp, C.POINTER(u64)]),
+    ("reattn_assemble_scope", C.c_int, [vp, vp, vp, vp, u64, u64, vp, vp, vp, C.POINTER(u64)]),
+    ("reattn_attend", C.c_int, [vp, vp, u64, vp, vp, u64, u64, u64, C.c_int, u64, vp, vp]),
+    ("reattn_attend_step", C.c_int, [vp, vp, vp, vp, u64, u64, C.POINTER(SelectionConfig),
+                                     C.c_int, vp, C.POINTER(StepStats), vp, vp, vp]),
+    ("reattn_plan_create", C.c_int, [vp, vp, vp, u64, u64, C.POINTER(SelectionConfig), C.c_int,
+                                     C.POINTER(vp)]),
+    ("reattn_plan_destroy", None, [vp]),
+    ("reattn_plan_q", vp, [vp]),
+    ("reattn_plan_out", vp, [vp]),
+    ("reattn_plan_launch", C.c_int, [vp]),
+    ("reattn_plan_launch_scan", C.c_int, [vp]),
+    ("reattn_plan_run_host", C.c_int, [vp, vp, vp]),
+    ("reattn_plan_stats", C.c_int, [vp, C.POINTER(StepStats)]),
+    ("reattn_plan_info", C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
+    ("reattn_synth_uniform", C.c_int, [vp, vp, u64, C.c_int, u64, u64]),
+]
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Load libreattn_cuda.so.  Raises if it has not been built (no silent fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built; run __graft_entry__.build() "
+                          "(make -C paper_2407_15176_b200/csrc)")
+    lib = C.CDLL(path)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _ptr(t) -> int:
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+class Context:
+    """One device context (reattn_ctx): stream, lane arithmetic, scratch arena."""
+
+    def __init__(self, device: int = 0, stream=None, lanes: int = LANES_UNFUSED):
+        self.lib = load_library()
+        h = vp()
+        rc = self.lib.reattn_ctx_create(device, C.byref(h))
+        if rc != OK:
+            raise CudaError(f"reattn_ctx_create failed (rc={rc}); is a GPU visible?")
+        self.h = h
+        self.device = device
+        if stream is not None:
+            self.check(self.lib.reattn_ctx_set_stream(self.h, stream))
+        self.set_lanes(lanes)
+
+    def check(self, rc: int) -> None:
+        if rc != OK:
+            msg = self.lib.reattn_last_error(self.h).decode()
+            raise _EXC.get(rc, ReattnError)(msg)
+
+    def set_lanes(self, lanes: int) -> None:
+        self.check(self.lib.reattn_ctx_set_lanes(self.h, lanes))
+
+    @property
+    def stream(self) -> int:
+        return self.lib.reattn_ctx_stream(self.h)
+
+    def synchronize(self) -> None:
+        self.check(self.lib.reattn_ctx_synchronize(self.h))
+
+    def close(self) -> None:
+        if self.h:
+            self.lib.reattn_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- selection (device tensors) ----
+    def fused_topk(self, q, n_heads: int, keys, n_kv: int, head_stride: int, row0: int,
+                   count: int, d: int, k: int, idx_out, score_out, key_dtype: int) -> tuple:
+        n_out, scratch = u64(), u64()
+        self.check(self.lib.reattn_fused_topk(self.h, _ptr(q), q.shape[0], n_heads, _ptr(keys),
+                                              key_dtype, n_kv, head_stride, row0, count, d, k,
+                                              _ptr(idx_out), _ptr(score_out), C.byref(n_out),
+                                              C.byref(scratch)))
+        return n_out.value, scratch.value
+
+    def vote(self, idx, score, k_prime: int, winners_out) -> int:
+        n = u64()
+        self.check(self.lib.reattn_vote(self.h, _ptr(idx), _ptr(score), idx.numel(), k_prime,
+                                        _ptr(winners_out), C.byref(n)))
+        return n.value
+
+    def tally(self, idx, score, idx_out, votes_out, score_out) -> int:
+        n = u64()
+        self.check(self.lib.reattn_tally(self.h, _ptr(idx), _ptr(score), idx.numel(),
+                                         _ptr(idx_out), _ptr(votes_out), _ptr(score_out),
+                                         C.byref(n)))
+        return n.value
+
+    def expand_spans(self, winners, span_m: int, middle_len: int, mode: int, b_out, e_out) -> int:
+        n = u64()
+        self.check(self.lib.reattn_expand_spans(self.h, _ptr(winners), winners.numel(), span_m,
+                                                middle_len, mode, _ptr(b_out), _ptr(e_out),
+                                                C.byref(n)))
+        return n.value
+
+    def attend(self, q, k, v, boundary, out, entropy) -> None:
+        n_q, d = q.shape
+        L, dv = v.shape
+        self.check(self.lib.reattn_attend(self.h, _ptr(q), n_q, _ptr(k), _ptr(v), L, d, dv,
+                                          int(boundary is not None), boundary or 0, _ptr(out),
+                                          _ptr(entropy)))
+
+    def synth_uniform(self, t, seed: int, offset: int = 0) -> None:
+        import torch
+        dt = BF16 if t.dtype == torch.bfloat16 else F32
+        self.check(self.lib.reattn_synth_uniform(self.h, _ptr(t), t.numel(), dt, seed, offset))
+
+
+class Rope:
+    """reattn::RotaryTable (rope.hpp:317-366) with its tables resident on the device."""
+
+    def __init__(self, ctx: Context, head_dim: int, base: float, max_position: int):
+        self.ctx = ctx
+        h = vp()
+        ctx.check(ctx.lib.reattn_rope_create(ctx.h, head_dim, base, max_position, C.byref(h)))
+        self.h = h
+        self.head_dim, self.base, self.max_position = head_dim, base, max_position
+
+    def rotate(self, rows, positions) -> None:
+        import numpy as np
+        pos = np.ascontiguousarray(np.asarray(positions, dtype=np.uint64))
+        self.ctx.check(self.ctx.lib.reattn_rope_rotate(self.ctx.h, self.h, _ptr(rows),
+                                                       pos.ctypes.data, rows.shape[0]))
+
+    def tables(self):
+        import numpy as np
+        c = np.zeros((self.max_position, self.head_dim // 2), np.float32)
+        s = np.zeros_like(c)
+        self.ctx.check(self.ctx.lib.reattn_rope_tables_host(self.h, c.ctypes.data, s.ctypes.data))
+        return c, s
+
+    def __del__(self):
+        # dependents keep their Context alive; skip if it was closed explicitly
+        if getattr(self, "h", None) and self.ctx.h:
+            self.ctx.lib.reattn_rope_destroy(self.h)
+            self.h = None
+
+
+class Cache:
+    """Device SegmentedKvCache (kv_cache.hpp:38-118): head-major [n_kv][capacity][d]."""
+
+    def __init__(self, ctx: Context, n_kv: int, d: int, l_global: int, l_local_max: int,
+                 capacity: int, dtype: int = BF16):
+        self.ctx = ctx
+        h = vp()
+        ctx.check(ctx.lib.reattn_cache_create(ctx.h, n_kv, d, l_global, l_local_max, capacity,
+                                              dtype, C.byref(h)))
+        self.h = h
+        self.n_kv, self.d, self.l_global, self.l_local_max = n_kv, d, l_global, l_local_max
+        self.capacity, self.dtype = capacity, dtype
+
+    def append(self, keys, values) -> None:
+        """keys/values: torch [rows, n_kv*d] fp32 (device) or numpy fp32 (host)."""
+        on_dev = hasattr(keys, "data_ptr")
+        kp = keys.data_ptr() if on_dev else keys.ctypes.data
+        vpp = values.data_ptr() if on_dev else values.ctypes.data
+        self.ctx.check(self.ctx.lib.reattn_cache_append(self.ctx.h, self.h, kp, vpp,
+                                                        keys.shape[0], int(on_dev)))
+
+    def set_total(self, total: int) -> None:
+        self.ctx.check(self.ctx.lib.reattn_cache_set_total(self.ctx.h, self.h, total))
+
+    def info(self) -> dict:
+        vals = [u64() for _ in range(8)]
+        dt = C.c_int()
+        self.ctx.lib.reattn_cache_info(self.h, *[C.byref(v) for v in vals], C.byref(dt))
+        keys = ["n_kv", "d", "l_global", "l_local_max", "capacity", "total", "global_end",
+                "local_start"]
+        out = {k: v.value for k, v in zip(keys, vals)}
+        out["dtype"] = dt.value
+        return out
+
+    def keys_tensor(self):
+        return self._view(self.ctx.lib.reattn_cache_keys(self.h))
+
+    def values_tensor(self):
+        return self._view(self.ctx.lib.reattn_cache_values(self.h))
+
+    def _view(self, ptr):
+        import torch
+        dt = torch.bfloat16 if self.dtype == BF16 else torch.float32
+        n = self.n_kv * self.capacity * self.d
+        return _wrap_device(ptr, n, dt, self.ctx.device).view(self.n_kv, self.capacity, self.d)
+
+    def __del__(self):
+        # dependents keep their Context alive; skip if it was closed explicitly
+        if getattr(self, "h", None) and self.ctx.h:
+            self.ctx.lib.reattn_cache_destroy(self.h)
+            self.h = None
+
+
+def _wrap_device(ptr: int, numel: int, dtype, device: int):
+    """Zero-copy torch view of library-owned device memory (via __cuda_array_interface__)."""
+    import torch
+
+    class _CAI:
+        pass
+
+    typestr = {torch.float32: "<f4", torch.bfloat16: "<V2", torch.float64: "<f8",
+               torch.int32: "<i4"}[dtype]
+    holder = _CAI()
+    holder.__cuda_array_interface__ = {"shape": (numel,), "typestr": typestr if dtype != torch.bfloat16 else "<i2",
+                                       "data": (ptr, False), "version": 3}
+    t = torch.as_tensor(holder, device=f"cuda:{device}")
+    if dtype == torch.bfloat16:
+        t = t.view(torch.bfloat16)
+    return t
+
+
+@dataclass
+class StepResult:
+    out: object
+    stats: StepStats
+    spans: tuple
+    entropy: object
+
+
+def attend_step(ctx: Context, cache: Cache, rope: Rope, q, n_head: int, cfg: SelectionConfig,
+                mode: int = MODE_REATTENTION, out=None) -> StepResult:
+    """engine.hpp:501 attend_step on device tensors.  q: [n_q, n_head*d] fp32 (cuda)."""
+    import numpy as np
+    import torch
+    n_q = q.shape[0]
+    if out is None:
+        out = torch.empty_like(q)
+    st = StepStats()
+    kp = max(1, cfg.k_prime)
+    sb = np.zeros(kp, np.uint64)
+    se = np.zeros(kp, np.uint64)
+    ent = np.zeros(max(1, n_q * n_head), np.float64)
+    ctx.check(ctx.lib.reattn_attend_step(ctx.h, cache.h, rope.h, _ptr(q), n_q, n_head,
+                                         C.byref(cfg), mode, _ptr(out), C.byref(st),
+                                         sb.ctypes.data, se.ctypes.data, ent.ctypes.data))
+    n = st.n_spans
+    return StepResult(out, st, (sb[:n].copy(), se[:n].copy()), ent[: n_q * n_head].reshape(n_q, n_head))
+
+
+class Plan:
+    """One attend_step shape captured as a CUDA graph (reattn_plan_*)."""
+
+    def __init__(self, ctx: Context, cache: Cache, rope: Rope, n_q: int, n_head: int,
+                 cfg: SelectionConfig, mode: int = MODE_REATTENTION):
+        self.ctx, self.cache, self.rope = ctx, cache, rope
+        h = vp()
+        ctx.check(ctx.lib.reattn_plan_create(ctx.h, cache.h, rope.h, n_q, n_head, C.byref(cfg),
+                                             mode, C.byref(h)))
+        self.h = h
+        self.n_q, self.n_head = n_q, n_head
+        numel = n_q * n_head * cache.d
+        import torch
+        self.q = _wrap_device(ctx.lib.reattn_plan_q(h), numel, torch.float32, ctx.device).view(n_q, -1)
+        self.out = _wrap_device(ctx.lib.reattn_plan_out(h), numel, torch.float32, ctx.device).view(n_q, -1)
+
+    def launch(self) -> None:
+        self.ctx.check(self.ctx.lib.reattn_plan_launch(self.h))
+
+    def launch_scan(self) -> None:
+        self.ctx.check(self.ctx.lib.reattn_plan_launch_scan(self.h))
+
+    def run_host(self, q_host, out_host) -> None:
+        self.ctx.check(self.ctx.lib.reattn_plan_run_host(self.h, _ptr(q_host), _ptr(out_host)))
+
+    def stats(self) -> StepStats:
+        st = StepStats()
+        self.ctx.check(self.ctx.lib.reattn_plan_stats(self.h, C.byref(st)))
+        return st
+
+    def info(self) -> dict:
+        a, b, c = u64(), u64(), u64()
+        self.ctx.check(self.ctx.lib.reattn_plan_info(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"kernels_per_step": a.value, "scan_bytes": b.value, "scope_bytes_upper": c.value}
+
+    def __del__(self):
+        # dependents keep their Context alive; skip if it was closed explicitly
+        if getattr(self, "h", None) and self.ctx.h:
+            self.ctx.lib.reattn_plan_destroy(self.h)
+            self.h = None

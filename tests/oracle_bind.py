@@ -66,12 +66,14 @@ def oracle() -> C.CDLL:
         lib.oracle_expand_spans.argtypes = [u64p, sz, sz, sz, C.c_int, u64p, u64p, C.POINTER(sz)]
         lib.oracle_rope_table.argtypes = [sz, C.c_double, sz, f32p, f32p]
         lib.oracle_attend.argtypes = [f32p, sz, f32p, f32p, sz, sz, sz, C.c_int, sz, f32p, f64p]
+        lib.oracle_rotate_row.argtypes = [f32p, sz, f32p, f32p]
         lib.oracle_scope_indices.argtypes = [sz, sz, sz, u64p, u64p, sz, sz, u64p, C.POINTER(sz)]
         lib.oracle_attend_step.argtypes = [f32p, sz, sz, f32p, f32p, sz, sz, sz, sz,
                                            C.POINTER(SelectionConfig), f32p, f32p, sz, C.c_int,
                                            f32p, C.POINTER(StepStats), u64p, u64p]
         lib.oracle_set_lane_mode.argtypes = [C.c_int]
         lib.oracle_get_lane_mode.restype = C.c_int
+        lib.oracle_synth_uniform.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, f32p, C.c_int]
         lib.oracle_round_bf16.restype = C.c_float
         lib.oracle_round_bf16.argtypes = [C.c_float]
         _oracle = lib

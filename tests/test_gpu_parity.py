@@ -1,0 +1,343 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) vs the CPU oracle (oracle/).
+
+Bars (north_star): selected indices and fp32 scores bit-identical (eps = 0 — the kernels
+emulate the reference's exact lane arithmetic); attention outputs max-abs <= 1e-5 (we hold
+them to 1e-6, the reference's own attend-vs-long-double bar, test_numerics.cpp:295),
+entropies <= 1e-9.  Mirrors the reference's tests: test_selection.cpp, test_scope.cpp,
+test_numerics.cpp, test_engine.cpp, acceptance_test.cpp C01/C04/C05/C09.
+"""
+import numpy as np
+import pytest
+
+import oracle_bind as ob
+import synth
+
+torch = pytest.importorskip("torch")
+from paper_2407_15176_b200 import native as N  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+ATTN_TOL = 1e-6
+ENT_TOL = 1e-9
+
+
+def dev(x, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    return t if dtype is None else t.to(dtype)
+
+
+def gpu_topk(ctx, q, n_heads, keys_hm, k, dtype=N.F32, head_stride=None, row0=0, count=None):
+    """keys_hm: numpy [n_kv, rows, d] fp32 (bf16-representable when dtype == BF16)."""
+    n_kv, rows, d = keys_hm.shape
+    count = rows - row0 if count is None else count
+    kt = dev(keys_hm, torch.bfloat16 if dtype == N.BF16 else torch.float32)
+    qt = dev(q.astype(np.float32))
+    n_q = q.shape[0]
+    idx = torch.zeros(n_kv * n_q * k, dtype=torch.int32, device="cuda")
+    sc = torch.zeros(n_kv * n_q * k, dtype=torch.float32, device="cuda")
+    n_out, scratch = ctx.fused_topk(qt, n_heads, kt, n_kv, head_stride or rows, row0, count, d, k,
+                                    idx, sc, dtype)
+    i = idx.cpu().numpy().view(np.uint32).reshape(n_kv, n_q, k)[:, :, :n_out].astype(np.uint64)
+    s = sc.cpu().numpy().reshape(n_kv, n_q, k)[:, :, :n_out]
+    return i, s, scratch
+
+
+def oracle_topk(q, n_heads, keys_hm, k, lanes, row0=0, count=None):
+    n_kv, rows, d = keys_hm.shape
+    count = rows - row0 if count is None else count
+    heads = [np.ascontiguousarray(keys_hm[h, row0:row0 + count]) for h in range(n_kv)]
+    with ob.lane_mode(lanes):
+        return ob.topk(q, n_heads, heads, k)
+
+
+def assert_topk_equal(got, want, label=""):
+    gi, gs = got[0], got[1]
+    wi, ws = want
+    assert gi.shape == wi.shape, label
+    assert np.array_equal(gi, wi), f"{label}: index mismatch\n{gi}\n{wi}"
+    # bit-identical scores (a zero score may differ only in its sign: == treats them equal)
+    assert np.array_equal(gs, ws), f"{label}: scores differ\n{gs}\n{ws}"
+    nz = gs != 0
+    assert np.array_equal(gs[nz].view(np.uint32), ws[nz].view(np.uint32)), label
+
+
+# ---------------------------------------------------------------------------------------
+def test_synth_generator_matches_host(ctx):
+    for dt in (torch.float32, torch.bfloat16):
+        t = torch.empty(100003, dtype=dt, device="cuda")
+        ctx.synth_uniform(t, seed=77, offset=5)
+        want = synth.uniform(77, 100003, offset=5)
+        if dt == torch.bfloat16:
+            want = synth.bf16_round(want)
+        assert np.array_equal(t.float().cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("lanes", [N.LANES_UNFUSED, N.LANES_FMA])
+@pytest.mark.parametrize("dtype", [N.BF16, N.F32])
+def test_fast_scan_decode_geometry(ctx, lanes, dtype):
+    """K1 fast path: LLaMA-3.1-8B heads (32 q / 8 kv, d=128), n_q=1, k in 1..8, sizes that
+    straddle the 224/128-row TMA tiles and the per-CTA split."""
+    ctx.set_lanes(lanes)
+    try:
+        for count, k, seed in [(1, 4, 1), (3, 4, 2), (4, 4, 3), (5, 8, 4), (223, 4, 5), (224, 4, 6),
+                               (225, 1, 7), (4097, 8, 8), (28640, 4, 9), (126944, 4, 10)]:
+            n_kv, d, nh = 8, 128, 32
+            rows = count + 37
+            keys = synth.uniform(seed, n_kv * rows * d).reshape(n_kv, rows, d)
+            if dtype == N.BF16:
+                keys = synth.bf16_round(keys)
+            q = synth.uniform(seed + 1000, nh * d).reshape(1, nh * d)
+            got = gpu_topk(ctx, q, nh, keys, k, dtype, row0=32, count=count)
+            want = oracle_topk(q, nh, keys, k, lanes, row0=32, count=count)
+            assert_topk_equal(got, want, f"count={count} k={k}")
+    finally:
+        ctx.set_lanes(N.LANES_UNFUSED)
+
+
+@pytest.mark.parametrize("lanes", [N.LANES_UNFUSED, N.LANES_FMA])
+def test_generic_scan_matches_oracle(ctx, lanes):
+    """Generic path: test_selection.cpp:105-131 sizes x k (incl. large k), several d / n_q /
+    GQA groups, fp32 keys."""
+    ctx.set_lanes(lanes)
+    rng = np.random.default_rng(31)
+    try:
+        for count in [0, 1, 3, 4, 5, 127, 1000, 2047, 2048, 2049, 10000]:
+            for k in (1, 4, 8, 100):
+                n_kv = 1 + count % 2
+                nh = n_kv * (1 + (count + k) % 3)
+                d = [32, 16, 8, 24, 128][(count + k) % 5]
+                n_q = 1 + (count + k) % 5
+                keys = rng.uniform(-1, 1, (n_kv, count, d)).astype(np.float32)
+                q = rng.uniform(-1, 1, (n_q, nh * d)).astype(np.float32)
+                got = gpu_topk(ctx, q, nh, keys, k)
+                want = oracle_topk(q, nh, keys, k, lanes)
+                assert_topk_equal(got, want, f"count={count} k={k} d={d} n_q={n_q}")
+    finally:
+        ctx.set_lanes(N.LANES_UNFUSED)
+
+
+def test_topk_ties_keep_lower_index(ctx):
+    """test_selection.cpp:168-191 known answer: ten equal keys -> {0, 7, 15, 16}."""
+    d, L = 8, 64
+    data = np.zeros((1, L, d), np.float32)
+    for i in (0, 7, 15, 16, 17, 31, 32, 49, 62, 63):
+        data[0, i] = 0.5
+    q = np.ones((1, d), np.float32)
+    i, s, _ = gpu_topk(ctx, q, 1, data, 4)
+    assert list(i[0, 0]) == [0, 7, 15, 16]
+    # same on the fast path (d=128, bf16)
+    d = 128
+    data = np.zeros((8, 3000, d), np.float32)
+    for h in range(8):
+        for r in (0, 7, 15, 16, 17, 31, 32, 49, 62, 63, 1500, 2999):
+            data[h, r] = 0.5
+    q = np.ones((1, 32 * d), np.float32)
+    i, s, _ = gpu_topk(ctx, q, 32, data, 4, N.BF16)
+    assert all(list(i[h, 0]) == [0, 7, 15, 16] for h in range(8))
+
+
+def test_scratch_independent_of_middle_length(ctx):
+    """test_selection.cpp:210-231 / acceptance C06: device workspace is flat in middle len."""
+    scr = []
+    for count in (4096, 262144):
+        keys = synth.uniform(5, count * 32).reshape(1, count, 32)
+        q = synth.uniform(6, 4 * 32).reshape(4, 32)
+        scr.append(gpu_topk(ctx, q, 1, keys, 4)[2])
+    assert scr[0] == scr[1]
+
+
+def test_vote_and_tally_match_oracle(ctx):
+    """test_selection.cpp:233-298 (map oracle) via the reference-restating oracle."""
+    rng = np.random.default_rng(53)
+    for it in range(300):
+        n = int(rng.integers(1, 200))
+        idx = rng.integers(0, 50, n).astype(np.uint64)
+        score = (rng.integers(0, 1000, n) / 500.0 - 1.0).astype(np.float32)
+        kp = int(rng.integers(1, 25))
+        want = ob.vote(idx, score, kp)
+        w = torch.zeros(kp, dtype=torch.int32, device="cuda")
+        nw = ctx.vote(dev(idx.astype(np.int32)), dev(score), kp, w)
+        got = w.cpu().numpy()[:nw].astype(np.uint64)
+        assert np.array_equal(got, want), it
+    # known answers (test_selection.cpp:272-292)
+    for idx, sc, kp, want in [([9, 2, 7], [5.0, 3.0, 1.0], 2, [9, 2]),
+                              ([7, 3, 7, 5], [0.1, 9.0, 0.2, 0.05], 3, [7, 3, 5])]:
+        w = torch.zeros(kp, dtype=torch.int32, device="cuda")
+        nw = ctx.vote(dev(np.array(idx, np.int32)), dev(np.array(sc, np.float32)), kp, w)
+        assert list(w.cpu().numpy()[:nw]) == want
+
+
+def test_expand_spans_match_oracle(ctx):
+    rng = np.random.default_rng(59)
+    for it in range(200):
+        mode = it % 2
+        m = 1 + it % 64 if mode == 0 else 2 + it % 63
+        L = int(rng.integers(m, 100000))
+        wn = rng.integers(0, L, int(rng.integers(1, 128))).astype(np.uint64)
+        want = ob.expand_spans(wn, m, L, mode)
+        b = torch.zeros(len(wn), dtype=torch.int32, device="cuda")
+        e = torch.zeros_like(b)
+        ns = ctx.expand_spans(dev(wn.astype(np.int32)), m, L, mode, b, e)
+        assert np.array_equal(b.cpu().numpy()[:ns].astype(np.uint64), want[0]), it
+        assert np.array_equal(e.cpu().numpy()[:ns].astype(np.uint64), want[1]), it
+    # known answers (test_selection.cpp:325-337) and the range error (:373-376)
+    b = torch.zeros(2, dtype=torch.int32, device="cuda")
+    e = torch.zeros_like(b)
+    assert ctx.expand_spans(dev(np.array([5, 20], np.int32)), 32, 100, 0, b, e) == 1
+    assert (b[0].item(), e[0].item()) == (0, 32)
+    assert ctx.expand_spans(dev(np.array([98], np.int32)), 32, 100, 0, b, e) == 1
+    assert (b[0].item(), e[0].item()) == (96, 100)
+    with pytest.raises(N.OutOfRange, match="expand_spans: winner outside middle"):
+        ctx.expand_spans(dev(np.array([100], np.int32)), 32, 100, 0, b, e)
+
+
+def test_attend_matches_oracle(ctx):
+    """test_numerics.cpp:281-302: 1000-instance style fuzz (fewer here), f64 state."""
+    rng = np.random.default_rng(23)
+    for it in range(200):
+        n_q, L, d = int(rng.integers(1, 9)), int(rng.integers(1, 513)), int(rng.integers(4, 65)) & ~1
+        dv = d if it % 3 else max(2, d // 2)
+        q = rng.uniform(-1, 1, (n_q, d)).astype(np.float32)
+        k = rng.uniform(-1, 1, (L, d)).astype(np.float32)
+        v = rng.uniform(-1, 1, (L, dv)).astype(np.float32)
+        bd = L - n_q if (it % 2 == 0 and L >= n_q) else None
+        out = torch.zeros(n_q, dv, device="cuda")
+        ent = torch.zeros(n_q, dtype=torch.float64, device="cuda")
+        ctx.attend(dev(q), dev(k), dev(v), bd, out, ent)
+        wo, we = ob.attend(q, k, v, bd)
+        assert np.abs(out.cpu().numpy() - wo).max() <= ATTN_TOL, it
+        assert np.abs(ent.cpu().numpy() - we).max() <= ENT_TOL, it
+    with pytest.raises(N.InvalidArgument, match="empty key set"):
+        ctx.attend(dev(np.zeros((1, 8), np.float32)), dev(np.zeros((0, 8), np.float32)),
+                   dev(np.zeros((0, 8), np.float32)), None, out, ent)
+
+
+def test_rope_tables_and_rotation(ctx):
+    r = N.Rope(ctx, 128, 500000.0, 8192)
+    c, s = r.tables()
+    wc, ws = ob.rope_table(128, 500000.0, 8192)
+    assert np.array_equal(c, wc) and np.array_equal(s, ws)
+    rows = synth.uniform(3, 16 * 128).reshape(16, 128)
+    pos = np.array([0, 1, 5, 100, 4095, 8191] + list(range(10)), np.uint64)
+    t = dev(rows)
+    r.rotate(t, pos)
+    want = rows.copy()
+    for i in range(16):
+        row = want[i].copy()
+        ob.oracle().oracle_rotate_row(row, 128, wc[pos[i]].copy(), ws[pos[i]].copy())
+        want[i] = row
+    assert np.array_equal(t.cpu().numpy(), want)
+    with pytest.raises(N.OutOfRange, match="position out of pretrained range"):
+        r.rotate(t[:1], [8192])
+
+
+# ---------------------------------------------------------------------------------------
+def make_cache(ctx, n_kv, d, total, cfg, dtype, seed, extra=0):
+    """Device cache filled with synthetic rows; returns (cache, host fp32 K, host fp32 V)."""
+    cap = total + extra
+    cache = N.Cache(ctx, n_kv, d, cfg.l_global, cfg.l_local, cap, dtype)
+    kt, vt = cache.keys_tensor(), cache.values_tensor()
+    ctx.synth_uniform(kt, seed)
+    ctx.synth_uniform(vt, seed + 1)
+    cache.set_total(total)
+    return cache, kt.float().cpu().numpy(), vt.float().cpu().numpy()
+
+
+def step_vs_oracle(ctx, n_kv, nh, d, total, cfg, dtype, seed, window, base=500000.0, n_q=1,
+                   mode=N.MODE_REATTENTION):
+    cache, hk, hv = make_cache(ctx, n_kv, d, total, cfg, dtype, seed)
+    rope = N.Rope(ctx, d, base, window)
+    q = synth.uniform(seed + 7, n_q * nh * d).reshape(n_q, nh * d)
+    res = N.attend_step(ctx, cache, rope, dev(q), nh, cfg, mode)
+    ocfg = ob.SelectionConfig(cfg.k, cfg.k_prime, cfg.span_m, cfg.tile_size, cfg.l_global,
+                              cfg.l_local, cfg.l_chunk, cfg.span_mode)
+    out, st, spans = ob.attend_step(q, nh, hk, hv, total, ocfg, base, window, mode)
+    return res, out, st, spans
+
+
+@pytest.mark.parametrize("total", [100, 4128, 4200, 9000, 40000, 131072])
+def test_attend_step_llama_geometry_bf16(ctx, total):
+    """engine.hpp:501 attend_step at LLaMA-3.1-8B head geometry, bf16 cache, defaults."""
+    cfg = N.SelectionConfig()
+    res, out, st, spans = step_vs_oracle(ctx, 8, 32, 128, total, cfg, N.BF16, 11 + total, 8192)
+    assert res.stats.scope_len == st.scope_len
+    assert np.array_equal(res.spans[0], spans[0]) and np.array_equal(res.spans[1], spans[1])
+    assert np.abs(res.out.cpu().numpy() - out).max() <= ATTN_TOL
+    assert abs(res.stats.entropy_max - st.entropy_max) <= ENT_TOL
+    assert abs(res.stats.entropy_sum - st.entropy_sum) <= 32 * ENT_TOL
+    assert res.stats.max_position_used == st.max_position_used
+    assert bool(res.stats.coverage_total) == bool(st.coverage_total)
+
+
+@pytest.mark.parametrize("case", range(8))
+def test_attend_step_toy_geometries(ctx, case):
+    """test_engine.cpp toy_selection-like configs, fp32 caches, prefill-sized n_q, both span
+    modes and the window mode (k'=0 / AttentionMode::Window)."""
+    rng = np.random.default_rng(case)
+    cfg = N.SelectionConfig(k=4, k_prime=64, span_m=16, l_global=16, l_local=256, l_chunk=128)
+    cfg.span_mode = case % 2
+    if case == 5:
+        cfg.k_prime = 0
+    n_q = [1, 4, 128, 1, 32, 7, 40, 16][case]
+    total = [300, 1000, 2000, 5000, 777, 4200, 3000, 20000][case]
+    mode = N.MODE_WINDOW if case == 7 else N.MODE_REATTENTION
+    if case == 6:
+        cfg.k, cfg.k_prime = 100, 100
+    res, out, st, spans = step_vs_oracle(ctx, 2, 4, 16, total, cfg, N.F32, 100 + case, 2048,
+                                         base=10000.0, n_q=n_q, mode=mode)
+    assert res.stats.scope_len == st.scope_len
+    assert np.array_equal(res.spans[0], spans[0])
+    assert np.abs(res.out.cpu().numpy() - out).max() <= ATTN_TOL
+    assert abs(res.stats.entropy_max - st.entropy_max) <= ENT_TOL
+
+
+def test_attend_step_errors(ctx):
+    cfg = N.SelectionConfig(l_global=4, l_local=8, k_prime=2, span_m=4)
+    cache, _, _ = make_cache(ctx, 1, 4, 12, cfg, N.F32, 3)
+    rope = N.Rope(ctx, 4, 10000.0, 11)
+    q = dev(np.zeros((1, 4), np.float32))
+    with pytest.raises(N.InvalidArgument, match="scope exceeds pretrain window"):
+        N.attend_step(ctx, cache, rope, q, 1, cfg)
+    rope = N.Rope(ctx, 4, 10000.0, 64)
+    with pytest.raises(N.LogicError, match="query block longer than scope"):
+        N.attend_step(ctx, cache, rope, dev(np.zeros((13, 4), np.float32)), 1, cfg)
+    with pytest.raises(N.InvalidArgument, match="multiple of kv heads"):
+        cache2, _, _ = make_cache(ctx, 3, 4, 12, cfg, N.F32, 3)
+        N.attend_step(ctx, cache2, rope, dev(np.zeros((1, 16), np.float32)), 4, cfg)
+
+
+def test_plan_graph_replay_matches_step(ctx):
+    """The CUDA-graph plan replays exactly the synchronous attend_step (bitwise)."""
+    cfg = N.SelectionConfig()
+    cache, _, _ = make_cache(ctx, 8, 128, 60000, cfg, N.BF16, 21)
+    rope = N.Rope(ctx, 128, 500000.0, 8192)
+    plan = N.Plan(ctx, cache, rope, 1, 32, cfg)
+    for s in range(3):
+        q = dev(synth.uniform(300 + s, 32 * 128).reshape(1, -1))
+        ref = N.attend_step(ctx, cache, rope, q, 32, cfg)
+        plan.q.copy_(q)
+        torch.cuda.synchronize()
+        plan.launch()
+        st = plan.stats()
+        assert torch.equal(plan.out, ref.out), \
+            (s, (plan.out - ref.out).abs().max().item(), st.scope_len, ref.stats.scope_len)
+        assert st.scope_len == ref.stats.scope_len
+        qh = q.cpu().pin_memory()
+        oh = torch.empty_like(qh).pin_memory()
+        plan.run_host(qh, oh)
+        assert torch.equal(oh, ref.out.cpu())
+
+
+@pytest.mark.slow
+def test_fast_scan_1m_context(ctx):
+    """Full-size config 4 selection (1M ctx, middle 1,044,448 rows x 8 heads): bit-exact vs
+    the oracle."""
+    cfg = N.SelectionConfig()
+    total = 1 << 20
+    cache, hk, _ = make_cache(ctx, 8, 128, total, cfg, N.BF16, 41)
+    q = synth.uniform(42, 32 * 128).reshape(1, -1)
+    info = cache.info()
+    g, ls = info["global_end"], info["local_start"]
+    got = gpu_topk(ctx, q, 32, hk, 4, N.BF16, row0=g, count=ls - g)
+    want = oracle_topk(q, 32, hk, 4, N.LANES_UNFUSED, row0=g, count=ls - g)
+    assert_topk_equal(got, want, "1M")
