@@ -310,8 +310,22 @@ constexpr int kDecPart = kDecD + 4;  // partial row: m, A, B, pad, acc[128] (16-
 
 struct DecodeArgs {
     AttnArgs a;
-    int n_chunks;  // grid.x (upper bound from L_max)
+    int n_splits;        // grid.x (upper bound from L_max)
+    int chunks_per_cta;  // 32-row chunks per CTA
 };
+
+DecodeArgs plan_decode(const AttnArgs& a, uint32_t L_max, int num_sms) {
+    DecodeArgs D;
+    D.a = a;
+    const int chunks = std::max(1, (int)((L_max + kDecChunk - 1) / kDecChunk));
+    // about two CTAs per SM over all kv heads, at most 8 chunks (256 rows) per CTA
+    // one 32-row chunk per CTA keeps many small CTAs in flight (latency-bound phases);
+    // very long scopes fold several chunks into one CTA to bound the combine's fan-in
+    const int want = std::max(1, 16 * num_sms / std::max(1, a.n_kv));
+    D.chunks_per_cta = std::min(8, std::max(1, (chunks + want - 1) / want));
+    D.n_splits = (chunks + D.chunks_per_cta - 1) / D.chunks_per_cta;
+    return D;
+}
 
 template <typename KT>
 __device__ __forceinline__ void load8(const KT* p, float (&v)[8]);
@@ -334,53 +348,125 @@ __device__ __forceinline__ void load8<float>(const float* p, float (&v)[8]) {
 }
 
 constexpr size_t decode_smem_bytes() {
-    return (size_t)(8 * kDecD + 8 * kDecChunk + 32) * sizeof(double) +
+    return (size_t)(8 * kDecD + 8 * kDecChunk + 64) * sizeof(double) +
            (size_t)kDecChunk * kDecKSF * sizeof(float) + (size_t)kDecChunk * kDecD * sizeof(float);
 }
 
+// Raw 16-byte words of 8 consecutive elements (converted only when staged to smem, so a
+// prefetch never waits on its own loads).
 template <typename KT>
-__global__ void __launch_bounds__(kDecThreads) attend_decode_kernel(const DecodeArgs P) {
+struct Raw8 {
+    static constexpr int W = (int)sizeof(KT) / 2;  // uint4 words per 8 elements
+    uint4 w[W];
+    __device__ __forceinline__ void load(const KT* p) {
+#pragma unroll
+        for (int i = 0; i < W; ++i) w[i] = __ldg(reinterpret_cast<const uint4*>(p) + i);
+    }
+    __device__ __forceinline__ void to_float(float (&v)[8]) const {
+        if (W == 1) {
+            const uint32_t u[4] = {w[0].x, w[0].y, w[0].z, w[0].w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                v[2 * i] = __uint_as_float(u[i] << 16);
+                v[2 * i + 1] = __uint_as_float(u[i] & 0xFFFF0000u);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                v[4 * i + 0] = __uint_as_float(w[i].x);
+                v[4 * i + 1] = __uint_as_float(w[i].y);
+                v[4 * i + 2] = __uint_as_float(w[i].z);
+                v[4 * i + 3] = __uint_as_float(w[i].w);
+            }
+        }
+    }
+};
+
+// Register-staged gather of one 32-row chunk: scope-table lookups, 16-byte K/V loads and
+// the RoPE table rows for the chunk's compact positions.
+template <typename KT>
+struct ChunkRegs {
+    static constexpr int kIter = kDecChunk * (kDecD / 8) / kDecThreads;  // 4
+    Raw8<KT> kr[kIter], vr[kIter];
+    float4 c4[kIter], s4[kIter];
+
+    __device__ __forceinline__ void load(const AttnArgs& a, int kv, uint32_t k0, int nk) {
+        const int tid = threadIdx.x;
+        constexpr int half = kDecD / 2;
+        uint32_t cr[kIter];
+#pragma unroll
+        for (int i = 0; i < kIter; ++i) {
+            const int r = (tid + i * kDecThreads) >> 4;
+            cr[i] = r < nk ? (a.src ? __ldg(a.src + k0 + r) : k0 + r) : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < kIter; ++i) {
+            const int e = tid + i * kDecThreads, r = e >> 4, c8 = (e & 15) * 8;
+            if (r < nk) {
+                const size_t rowb = ((size_t)kv * a.head_stride + cr[i]) * kDecD + c8;
+                kr[i].load((const KT*)a.k_base + rowb);
+                vr[i].load((const KT*)a.v_base + rowb);
+                if (a.rope_cos) {
+                    c4[i] = __ldg(reinterpret_cast<const float4*>(a.rope_cos + (size_t)(k0 + r) * half + c8 / 2));
+                    s4[i] = __ldg(reinterpret_cast<const float4*>(a.rope_sin + (size_t)(k0 + r) * half + c8 / 2));
+                }
+            }
+        }
+    }
+    // rotate K at its compact position (rope.hpp:347-358, unfused fp32) and stage to smem
+    __device__ __forceinline__ void store(const AttnArgs& a, int nk, float* ks, float* vs) const {
+        const int tid = threadIdx.x;
+#pragma unroll
+        for (int i = 0; i < kIter; ++i) {
+            const int e = tid + i * kDecThreads, r = e >> 4, c8 = (e & 15) * 8;
+            if (r < nk) {
+                float kf[8], vf[8];
+                kr[i].to_float(kf);
+                vr[i].to_float(vf);
+                if (a.rope_cos) {
+                    const float cc[4] = {c4[i].x, c4[i].y, c4[i].z, c4[i].w};
+                    const float ss[4] = {s4[i].x, s4[i].y, s4[i].z, s4[i].w};
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const float x = kf[2 * t], y = kf[2 * t + 1];
+                        kf[2 * t] = __fsub_rn(__fmul_rn(x, cc[t]), __fmul_rn(y, ss[t]));
+                        kf[2 * t + 1] = __fadd_rn(__fmul_rn(x, ss[t]), __fmul_rn(y, cc[t]));
+                    }
+                }
+                float4* kd = reinterpret_cast<float4*>(ks + r * kDecKSF + c8);
+                kd[0] = make_float4(kf[0], kf[1], kf[2], kf[3]);
+                kd[1] = make_float4(kf[4], kf[5], kf[6], kf[7]);
+                float4* vd = reinterpret_cast<float4*>(vs + r * kDecD + c8);
+                vd[0] = make_float4(vf[0], vf[1], vf[2], vf[3]);
+                vd[1] = make_float4(vf[4], vf[5], vf[6], vf[7]);
+            }
+        }
+    }
+};
+
+// One CTA per (range of P.chunks_per_cta chunks of the scope, kv head): flash-decode with
+// an online (m, A, B, acc) state per q head; the next chunk's gather is issued into
+// registers before the current chunk is computed.
+template <typename KT, int G>
+__global__ void __launch_bounds__(kDecThreads, 5) attend_decode_kernel(const DecodeArgs P) {
     const AttnArgs& a = P.a;
     if (a.hdr && a.hdr->error != 0) return;
     const uint32_t L = scope_len(a);
-    const int chunk = blockIdx.x, kv = blockIdx.y;
-    const uint32_t k0 = (uint32_t)chunk * kDecChunk;
-    if (k0 >= L) return;
-    const int nk = (int)min((uint32_t)kDecChunk, L - k0);
-    const int G = a.group;
+    const int split = blockIdx.x, kv = blockIdx.y;
+    const uint32_t key_begin = (uint32_t)split * P.chunks_per_cta * kDecChunk;
+    if (key_begin >= L) return;
+    const uint32_t key_end = min(L, key_begin + (uint32_t)P.chunks_per_cta * kDecChunk);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     extern __shared__ __align__(16) double dsm[];
     double* qd = dsm;                              // [8][kDecD]
     double* lg = qd + 8 * kDecD;                   // [8][kDecChunk]
-    double* st = lg + 8 * kDecChunk;               // [8][3] (+pad)
-    float* ks = (float*)(st + 32);                 // [kDecChunk][kDecKSF]
+    double* st = lg + 8 * kDecChunk;               // [8][4]: m, A, B, rescale  (+pad)
+    float* ks = (float*)(st + 64);                 // [kDecChunk][kDecKSF]
     float* vs = ks + kDecChunk * kDecKSF;          // [kDecChunk][kDecD]
     constexpr int half = kDecD / 2;
 
-    // ---- gather K (RoPE at compact position k0+r) and V through the scope table;
-    //      all loads of the thread issued before any use ----
-    constexpr int kIter = kDecChunk * (kDecD / 8) / kDecThreads;  // 4
-    uint32_t cr[kIter];
-#pragma unroll
-    for (int i = 0; i < kIter; ++i) {
-        const int e = tid + i * kDecThreads, r = e >> 4;
-        cr[i] = r < nk ? (a.src ? __ldg(a.src + k0 + r) : k0 + r) : 0u;
-    }
-    float kf[kIter][8], vf[kIter][8];
-    float4 c4[kIter], s4[kIter];
-#pragma unroll
-    for (int i = 0; i < kIter; ++i) {
-        const int e = tid + i * kDecThreads, r = e >> 4, c8 = (e & 15) * 8;
-        if (r < nk) {
-            const size_t rowb = ((size_t)kv * a.head_stride + cr[i]) * kDecD + c8;
-            load8<KT>((const KT*)a.k_base + rowb, kf[i]);
-            load8<KT>((const KT*)a.v_base + rowb, vf[i]);
-            if (a.rope_cos) {
-                c4[i] = __ldg(reinterpret_cast<const float4*>(a.rope_cos + (size_t)(k0 + r) * half + c8 / 2));
-                s4[i] = __ldg(reinterpret_cast<const float4*>(a.rope_sin + (size_t)(k0 + r) * half + c8 / 2));
-            }
-        }
-    }
+    ChunkRegs<KT> cur;
+    cur.load(a, kv, key_begin, (int)min((uint32_t)kDecChunk, key_end - key_begin));
     // queries of the group, rotated at L'-1 (engine.hpp:546-551), kept as f64
     const uint32_t qpos = L - 1u;
     for (int e = tid; e < G * half; e += kDecThreads) {
@@ -397,121 +483,125 @@ __global__ void __launch_bounds__(kDecThreads) attend_decode_kernel(const Decode
         qd[g * kDecD + 2 * j] = (double)rx;
         qd[g * kDecD + 2 * j + 1] = (double)ry;
     }
-#pragma unroll
-    for (int i = 0; i < kIter; ++i) {
-        const int e = tid + i * kDecThreads, r = e >> 4, c8 = (e & 15) * 8;
-        if (r < nk) {
-            if (a.rope_cos) {
-                const float cc[4] = {c4[i].x, c4[i].y, c4[i].z, c4[i].w};
-                const float ss[4] = {s4[i].x, s4[i].y, s4[i].z, s4[i].w};
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const float x = kf[i][2 * t], y = kf[i][2 * t + 1];
-                    kf[i][2 * t] = __fsub_rn(__fmul_rn(x, cc[t]), __fmul_rn(y, ss[t]));
-                    kf[i][2 * t + 1] = __fadd_rn(__fmul_rn(x, ss[t]), __fmul_rn(y, cc[t]));
-                }
-            }
-            float4* kr = reinterpret_cast<float4*>(ks + r * kDecKSF + c8);
-            kr[0] = make_float4(kf[i][0], kf[i][1], kf[i][2], kf[i][3]);
-            kr[1] = make_float4(kf[i][4], kf[i][5], kf[i][6], kf[i][7]);
-            float4* vr = reinterpret_cast<float4*>(vs + r * kDecD + c8);
-            vr[0] = make_float4(vf[i][0], vf[i][1], vf[i][2], vf[i][3]);
-            vr[1] = make_float4(vf[i][4], vf[i][5], vf[i][6], vf[i][7]);
-        }
+    if (tid < 8) {
+        st[tid * 4 + 0] = -INFINITY;
+        st[tid * 4 + 1] = 0.0;
+        st[tid * 4 + 2] = 0.0;
+        st[tid * 4 + 3] = 1.0;
     }
+    cur.store(a, (int)min((uint32_t)kDecChunk, key_end - key_begin), ks, vs);
     __syncthreads();
-    // ---- logits (attend.hpp:430): thread (key j, lane pair p) accumulates lanes 2p, 2p+1
-    //      of dot_f64 for every head; the tree ((l0+l1)+(l2+l3))+((l4+l5)+(l6+l7)) is
-    //      finished across the 4 threads of the key with shuffles (exact order) ----
-    {
-        const double scale = 1.0 / sqrt((double)kDecD);
-        const int j = tid >> 2, p = tid & 3;
-        double acc[8][2];
+
+    const double scale = 1.0 / sqrt((double)kDecD);
+    double acc[G];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) acc[g][0] = acc[g][1] = 0.0;
-        if (j < nk) {
-            const float* kr = ks + j * kDecKSF + 2 * p;
+    for (int g = 0; g < G; ++g) acc[g] = 0.0;
+    for (uint32_t k0 = key_begin; k0 < key_end; k0 += kDecChunk) {
+        const int nk = (int)min((uint32_t)kDecChunk, key_end - k0);
+        const uint32_t k1 = k0 + kDecChunk;
+        const int nk1 = k1 < key_end ? (int)min((uint32_t)kDecChunk, key_end - k1) : 0;
+        ChunkRegs<KT> nxt;
+        if (nk1 > 0) nxt.load(a, kv, k1, nk1);  // in flight during this chunk's math
+        // ---- logits (attend.hpp:430): thread (key j, lane pair p) accumulates lanes 2p,
+        //      2p+1 of dot_f64 for every head; tree finished with two shuffles ----
+        {
+            const int j = tid >> 2, p = tid & 3;
+            double l2[G][2];
+#pragma unroll
+            for (int g = 0; g < G; ++g) l2[g][0] = l2[g][1] = 0.0;
+            if (j < nk) {
+                const float* kr = ks + j * kDecKSF + 2 * p;
 #pragma unroll 4
-            for (int c = 0; c < kDecD / 8; ++c) {
-                const float2 k2 = *reinterpret_cast<const float2*>(kr + 8 * c);
-                const double ka = (double)k2.x, kb = (double)k2.y;
+                for (int c = 0; c < kDecD / 8; ++c) {
+                    const float2 k2 = *reinterpret_cast<const float2*>(kr + 8 * c);
+                    const double ka = (double)k2.x, kb = (double)k2.y;
 #pragma unroll
-                for (int g = 0; g < 8; ++g) {
-                    if (g < G) {
+                    for (int g = 0; g < G; ++g) {
                         const double2 q2 =
                             *reinterpret_cast<const double2*>(qd + g * kDecD + 8 * c + 2 * p);
-                        acc[g][0] = fma(q2.x, ka, acc[g][0]);
-                        acc[g][1] = fma(q2.y, kb, acc[g][1]);
+                        l2[g][0] = fma(q2.x, ka, l2[g][0]);
+                        l2[g][1] = fma(q2.y, kb, l2[g][1]);
                     }
                 }
             }
-        }
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-            if (g < G) {
-                double s = acc[g][0] + acc[g][1];
+            for (int g = 0; g < G; ++g) {
+                double s = l2[g][0] + l2[g][1];
                 s = s + __shfl_xor_sync(0xFFFFFFFFu, s, 1);
                 s = s + __shfl_xor_sync(0xFFFFFFFFu, s, 2);
                 if (p == 0) lg[g * kDecChunk + j] = j < nk ? s * scale : -INFINITY;
             }
         }
-    }
-    __syncthreads();
-    // ---- per-head softmax statistics of this slice (one warp per head) ----
-    for (int g = warp; g < G; g += kDecThreads / 32) {
-        const double s = lane < nk ? lg[g * kDecChunk + lane] : -INFINITY;
-        double m = s;
+        __syncthreads();
+        // ---- online softmax update per head (attend.hpp:432-447), one warp per head ----
+        for (int g = warp; g < G; g += kDecThreads / 32) {
+            const double s = lane < nk ? lg[g * kDecChunk + lane] : -INFINITY;
+            double mc = s;
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xFFFFFFFFu, m, off));
-        const double w = lane < nk ? exp(s - m) : 0.0;
-        double A = w, B = lane < nk ? (s - m) * w : 0.0;
+            for (int off = 16; off > 0; off >>= 1) mc = fmax(mc, __shfl_xor_sync(0xFFFFFFFFu, mc, off));
+            const double m_old = st[g * 4 + 0];
+            const double m_new = fmax(m_old, mc);
+            const double w = lane < nk ? exp(s - m_new) : 0.0;
+            double sa = w, sb = lane < nk ? (s - m_new) * w : 0.0;
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            A += __shfl_xor_sync(0xFFFFFFFFu, A, off);
-            B += __shfl_xor_sync(0xFFFFFFFFu, B, off);
+            for (int off = 16; off > 0; off >>= 1) {
+                sa += __shfl_xor_sync(0xFFFFFFFFu, sa, off);
+                sb += __shfl_xor_sync(0xFFFFFFFFu, sb, off);
+            }
+            lg[g * kDecChunk + lane] = w;
+            if (lane == 0) {
+                const double A = st[g * 4 + 1], B = st[g * 4 + 2];
+                // empty running state (first chunk): no rescale term (avoids 0 * -inf)
+                const double r = A > 0.0 ? exp(m_old - m_new) : 0.0;
+                st[g * 4 + 0] = m_new;
+                st[g * 4 + 1] = A * r + sa;
+                st[g * 4 + 2] = (A > 0.0 ? r * (B + (m_old - m_new) * A) : 0.0) + sb;
+                st[g * 4 + 3] = r;
+            }
         }
-        lg[g * kDecChunk + lane] = w;
-        if (lane == 0) {
-            st[g * 3 + 0] = m;
-            st[g * 3 + 1] = A;
-            st[g * 3 + 2] = B;
+        __syncthreads();
+        // ---- values: thread c owns output column c for every head of the group ----
+        {
+            const int c = tid;
+#pragma unroll
+            for (int g = 0; g < G; ++g) acc[g] *= st[g * 4 + 3];
+            for (int j = 0; j < nk; ++j) {
+                const double v = (double)vs[j * kDecD + c];
+#pragma unroll
+                for (int g = 0; g < G; ++g) acc[g] = fma(lg[g * kDecChunk + j], v, acc[g]);
+            }
+        }
+        __syncthreads();
+        if (nk1 > 0) {
+            nxt.store(a, nk1, ks, vs);
+            __syncthreads();
         }
     }
-    __syncthreads();
-    // ---- values: thread c owns output column c for every head of the group ----
     const int c = tid;
-    double acc[8];
 #pragma unroll
-    for (int g = 0; g < 8; ++g) acc[g] = 0.0;
-    for (int j = 0; j < nk; ++j) {
-        const double v = (double)vs[j * kDecD + c];
-#pragma unroll
-        for (int g = 0; g < 8; ++g)
-            if (g < G) acc[g] = fma(lg[g * kDecChunk + j], v, acc[g]);
-    }
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-        if (g < G) {
-            double* p = a.part + (((size_t)chunk * a.n_kv + kv) * G + g) * kDecPart;
-            p[4 + c] = acc[g];
-            if (c < 3) p[c] = st[g * 3 + c];
-        }
+    for (int g = 0; g < G; ++g) {
+        double* p = a.part + (((size_t)split * a.n_kv + kv) * G + g) * kDecPart;
+        p[4 + c] = acc[g];
+        if (c < 3) p[c] = st[g * 4 + c];
     }
 }
 
-// Merge the slices of one q head: weights in parallel, then 8 warps each sum a strided
-// subset of slices (lanes own 4 columns, 16-byte loads), reduced in a fixed order.
+// Merge the key-range partials of one q head: grid (head, column quarter); weights in
+// parallel, then 8 warps each sum a strided subset of partials for 32 columns (one per
+// lane), reduced in a fixed order (deterministic).
 constexpr int kCombThreads = 256;
+constexpr int kCombCols = 32;
 __global__ void __launch_bounds__(kCombThreads) attend_decode_combine(const DecodeArgs P) {
     const AttnArgs& a = P.a;
     if (a.hdr && a.hdr->error != 0) return;
     const uint32_t L = scope_len(a);
-    const int h = blockIdx.x;
+    const int h = blockIdx.x, cb = blockIdx.y;
     const int kv = h / a.group, g = h % a.group;
-    const int ns = (int)((L + kDecChunk - 1) / kDecChunk);
+    const uint32_t keys_per = (uint32_t)P.chunks_per_cta * kDecChunk;
+    const int ns = (int)((L + keys_per - 1) / keys_per);
     constexpr int NW = kCombThreads / 32;
-    __shared__ double w_s[2048];
-    __shared__ double red[NW][kDecD];
+    __shared__ double w_s[1024];
+    __shared__ double red[NW][kCombCols];
     __shared__ double rs[NW][3];
     __shared__ double s_M, s_A;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -534,7 +624,7 @@ __global__ void __launch_bounds__(kCombThreads) attend_decode_combine(const Deco
     double A = 0.0, B = 0.0;
     for (int s = tid; s < ns; s += kCombThreads) {
         const double* p = prow(s);
-        const double w = exp(p[0] - M);
+        const double w = p[1] > 0.0 ? exp(p[0] - M) : 0.0;
         w_s[s] = w;
         A += p[1] * w;
         B += w * (p[2] + (p[0] - M) * p[1]);
@@ -556,27 +646,20 @@ __global__ void __launch_bounds__(kCombThreads) attend_decode_combine(const Deco
             Bt += rs[w][2];
         }
         s_A = At;
-        const double hh = log(At) - Bt / At;
-        a.entropy[h] = hh < 0.0 ? 0.0 : hh;
+        if (cb == 0) {
+            const double hh = log(At) - Bt / At;
+            a.entropy[h] = hh < 0.0 ? 0.0 : hh;
+        }
     }
-    // value rows: warp w sums slices w, w+NW, ...; lane owns columns 4*lane .. 4*lane+3
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int s = warp; s < ns; s += NW) {
-        const double2* p = reinterpret_cast<const double2*>(prow(s) + 4 + 4 * lane);
-        const double2 x = p[0], y = p[1];
-        const double w = w_s[s];
-        acc[0] = fma(x.x, w, acc[0]);
-        acc[1] = fma(x.y, w, acc[1]);
-        acc[2] = fma(y.x, w, acc[2]);
-        acc[3] = fma(y.y, w, acc[3]);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) red[warp][4 * lane + u] = acc[u];
+    const int col = cb * kCombCols + lane;
+    double acc = 0.0;
+    for (int s = warp; s < ns; s += NW) acc = fma(prow(s)[4 + col], w_s[s], acc);
+    red[warp][lane] = acc;
     __syncthreads();
-    if (tid < kDecD) {
+    if (tid < kCombCols) {
         double t = 0.0;
         for (int w = 0; w < NW; ++w) t += red[w][tid];
-        a.out[(size_t)h * kDecD + tid] = (float)(t / s_A);
+        a.out[(size_t)h * kDecD + cb * kCombCols + tid] = (float)(t / s_A);
     }
 }
 
@@ -624,8 +707,8 @@ int sm_count() {
 
 size_t attend_workspace(const AttnArgs& a, uint32_t L_max) {
     if (decode_eligible(a, L_max)) {
-        const size_t nc = (L_max + kDecChunk - 1) / kDecChunk;
-        return nc * a.n_kv * a.group * kDecPart * sizeof(double);
+        const DecodeArgs D = plan_decode(a, L_max, sm_count());
+        return (size_t)D.n_splits * a.n_kv * a.group * kDecPart * sizeof(double);
     }
     const AttnLaunch P = plan_attend(a, L_max, sm_count());
     if (P.direct) return 0;
@@ -639,21 +722,34 @@ int attend_kernel_count(const AttnArgs& a, uint32_t L_max) {
 
 cudaError_t launch_attend(const AttnArgs& a, uint32_t L_max, cudaStream_t s) {
     if (decode_eligible(a, L_max)) {
-        DecodeArgs D;
-        D.a = a;
-        D.n_chunks = (int)((L_max + kDecChunk - 1) / kDecChunk);
-        dim3 grid(D.n_chunks, a.n_kv);
+        const DecodeArgs D = plan_decode(a, L_max, sm_count());
+        dim3 grid(D.n_splits, a.n_kv);
         const size_t smem = decode_smem_bytes();
+#define DEC_LAUNCH(KT, GG)                                                                \
+    do {                                                                                  \
+        cudaFuncSetAttribute(attend_decode_kernel<KT, GG>,                                \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+        attend_decode_kernel<KT, GG><<<grid, kDecThreads, smem, s>>>(D);                  \
+    } while (0)
+#define DEC_DISPATCH(KT)                        \
+    switch (a.group) {                          \
+        case 1: DEC_LAUNCH(KT, 1); break;       \
+        case 2: DEC_LAUNCH(KT, 2); break;       \
+        case 3: DEC_LAUNCH(KT, 3); break;       \
+        case 4: DEC_LAUNCH(KT, 4); break;       \
+        case 5: DEC_LAUNCH(KT, 5); break;       \
+        case 6: DEC_LAUNCH(KT, 6); break;       \
+        case 7: DEC_LAUNCH(KT, 7); break;       \
+        default: DEC_LAUNCH(KT, 8); break;      \
+    }
         if (a.dtype == kBF16) {
-            cudaFuncSetAttribute(attend_decode_kernel<__nv_bfloat16>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attend_decode_kernel<__nv_bfloat16><<<grid, kDecThreads, smem, s>>>(D);
+            DEC_DISPATCH(__nv_bfloat16);
         } else {
-            cudaFuncSetAttribute(attend_decode_kernel<float>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attend_decode_kernel<float><<<grid, kDecThreads, smem, s>>>(D);
+            DEC_DISPATCH(float);
         }
-        attend_decode_combine<<<a.n_head, kCombThreads, 0, s>>>(D);
+#undef DEC_DISPATCH
+#undef DEC_LAUNCH
+        attend_decode_combine<<<dim3(a.n_head, kDecD / kCombCols), kCombThreads, 0, s>>>(D);
         return cudaGetLastError();
     }
     const AttnLaunch P = plan_attend(a, L_max, sm_count());

@@ -190,7 +190,9 @@ int plan_step(reattn_ctx* ctx, const reattn_cache* cache, const reattn_rope* rop
     P.select = mode == REATTN_MODE_REATTENTION && cfg->k_prime > 0 && P.middle > 0;
     P.kk = std::min<uint64_t>(cfg->k, P.middle);
     const uint64_t local = P.total - P.l_start;
-    uint64_t sel_rows = P.select ? std::min<uint64_t>(P.middle, cfg->k_prime * cfg->span_m) : 0;
+    // at most min(k', #candidates) winners, each expanding to <= span_m rows
+    const uint64_t max_winners = std::min<uint64_t>(cfg->k_prime, P.n_kv * n_q * P.kk);
+    uint64_t sel_rows = P.select ? std::min<uint64_t>(P.middle, max_winners * cfg->span_m) : 0;
     P.L_upper = (uint32_t)std::min<uint64_t>(P.window, P.g_end + sel_rows + local);
     if (P.total >= (1ull << 32) || P.window >= (1ull << 31))
         return set_err(ctx, REATTN_EINVAL, "attend_step: cache too long for 32-bit indices");
