@@ -8,8 +8,8 @@
  *
  * Each entry point replaces one reference function of
  * /root/reference/proj/include/reattn/ (cited per declaration).  The reference has no FFI
- * of its own: its boundary is the header-only C++ API, which include/reattn/*.hpp
- * re-creates on top of this ABI.
+ * of its own: its boundary is the header-only C++ API, which the headers under
+ * include/reattn/ re-create on top of this ABI.
  *
  * Device pointers ("_dev") are CUDA global memory of the context's device; all work is
  * enqueued on the context's stream.  Functions documented "synchronous" return after the

@@ -1,0 +1,429 @@
+// The reference's own hot-path unit tests (proj/tests/test_selection.cpp, test_scope.cpp,
+// test_numerics.cpp, acceptance_test.cpp C01/C04/C09), ported onto the drop-in headers
+// (include/reattn/*.hpp -> C-ABI -> sm_100a kernels).  Oracles: the reference tests' own
+// independent oracles where they are self-contained, and the C restatement in oracle/
+// (TEST INFRASTRUCTURE ONLY, linked here as the checker).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <map>
+#include <random>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../oracle/reattn_oracle.h"
+#include "reattn/reattn.hpp"
+
+using namespace reattn;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(cond, ...)                                                      \
+    do {                                                                      \
+        ++g_checks;                                                           \
+        if (!(cond)) {                                                        \
+            ++g_fail;                                                         \
+            std::printf("FAIL %s:%d: %s ", __FILE__, __LINE__, #cond);         \
+            std::printf(__VA_ARGS__);                                         \
+            std::printf("\n");                                                \
+        }                                                                     \
+    } while (0)
+template <typename E, typename F>
+static bool throws(F&& f, const char* msg = nullptr) {
+    try {
+        f();
+    } catch (const E& e) {
+        return !msg || std::string(e.what()).find(msg) != std::string::npos;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+static DenseMatrix random_rows(std::size_t r, std::size_t c, std::mt19937& rng) {
+    std::uniform_real_distribution<float> dist(-1.0f, 1.0f);
+    DenseMatrix m(r, c);
+    for (float& v : m.values) v = dist(rng);
+    return m;
+}
+
+// oracle top-k for host views
+static PerHeadTopk oracle_topk(const DenseMatrix& q, std::size_t n_heads,
+                               const std::vector<std::vector<float>>& heads, std::size_t count,
+                               std::size_t d, std::size_t k) {
+    const std::size_t n_kv = heads.size(), n_q = q.rows;
+    std::vector<const float*> ptrs;
+    for (auto& h : heads) ptrs.push_back(h.data());
+    std::vector<uint64_t> idx(std::max<std::size_t>(1, n_kv * n_q * k));
+    std::vector<float> sc(idx.size());
+    size_t n_out = 0;
+    oracle_topk(q.values.data(), n_q, n_heads, ptrs.data(), n_kv, count, d, d, k, idx.data(),
+                sc.data(), &n_out);
+    PerHeadTopk out(n_kv, std::vector<std::vector<TopkEntry>>(n_q));
+    for (std::size_t kv = 0; kv < n_kv; ++kv)
+        for (std::size_t qq = 0; qq < n_q; ++qq)
+            for (std::size_t j = 0; j < n_out; ++j)
+                out[kv][qq].push_back(TopkEntry{idx[(kv * n_q + qq) * k + j], sc[(kv * n_q + qq) * k + j]});
+    return out;
+}
+
+static void test_fused_topk() {
+    // test_selection.cpp:105-131
+    std::mt19937 rng(31);
+    const std::size_t d = 32;
+    for (std::size_t len : {0u, 1u, 3u, 4u, 5u, 127u, 1000u, 2047u, 2048u, 2049u, 10000u})
+        for (std::size_t tile : {16u, 100u, 2048u})
+            for (std::size_t k : {1u, 4u, 8u}) {
+                const std::size_t n_kv = 1 + len % 2, n_heads = n_kv * 2, n_q = 1 + (len + tile) % 5;
+                std::vector<std::vector<float>> heads(n_kv, std::vector<float>(len * d));
+                std::uniform_real_distribution<float> dist(-1.0f, 1.0f);
+                for (auto& h : heads)
+                    for (float& v : h) v = dist(rng);
+                std::vector<KeySegmentView> views;
+                for (auto& h : heads) views.push_back(KeySegmentView{h.data(), len, d});
+                const DenseMatrix q = random_rows(n_q, n_heads * d, rng);
+                SelectionConfig cfg;
+                cfg.k = k;
+                cfg.tile_size = tile;
+                const PerHeadTopk got = fused_topk_scores(q, n_heads, views, cfg);
+                const PerHeadTopk want = oracle_topk(q, n_heads, heads, len, d, k);
+                bool eq = got.size() == want.size();
+                for (std::size_t kv = 0; eq && kv < got.size(); ++kv)
+                    for (std::size_t qq = 0; eq && qq < got[kv].size(); ++qq) {
+                        eq = got[kv][qq].size() == want[kv][qq].size();
+                        for (std::size_t i = 0; eq && i < got[kv][qq].size(); ++i)
+                            eq = got[kv][qq][i].index == want[kv][qq][i].index &&
+                                 got[kv][qq][i].score == want[kv][qq][i].score;
+                    }
+                CHECK(eq, "fused vs oracle len=%zu tile=%zu k=%zu", len, tile, k);
+            }
+    // :168-191 ties keep the lower index
+    const std::size_t dd = 8, L = 64;
+    std::vector<float> data(L * dd, 0.0f);
+    for (std::size_t i : {0u, 7u, 15u, 16u, 17u, 31u, 32u, 49u, 62u, 63u})
+        for (std::size_t c = 0; c < dd; ++c) data[i * dd + c] = 0.5f;
+    KeySegmentView view{data.data(), L, dd};
+    DenseMatrix q(1, dd);
+    for (std::size_t c = 0; c < dd; ++c) q.at(0, c) = 1.0f;
+    SelectionConfig cfg;
+    const PerHeadTopk got = fused_topk_scores(q, 1, std::span<const KeySegmentView>(&view, 1), cfg);
+    CHECK(got[0][0].size() == 4 && got[0][0][0].index == 0 && got[0][0][1].index == 7 &&
+              got[0][0][2].index == 15 && got[0][0][3].index == 16, "ties");
+    // :210-231 scratch independent of the middle length
+    std::size_t peaks[2];
+    for (int i = 0; i < 2; ++i) {
+        const std::size_t len = i ? 262144 : 4096;
+        std::vector<float> h(len * 32);
+        std::uniform_real_distribution<float> dist(-1.0f, 1.0f);
+        for (float& v : h) v = dist(rng);
+        KeySegmentView v{h.data(), len, 32};
+        ScratchMeter m;
+        fused_topk_scores(random_rows(4, 32, rng), 1, std::span<const KeySegmentView>(&v, 1), cfg, &m);
+        peaks[i] = m.peak;
+    }
+    CHECK(peaks[0] == peaks[1] && peaks[0] > 0, "scratch %zu vs %zu", peaks[0], peaks[1]);
+    // :401-407 head mismatch throws
+    std::vector<std::vector<float>> mid(3, std::vector<float>(10 * 8, 0.f));
+    std::vector<KeySegmentView> mv;
+    for (auto& h : mid) mv.push_back(KeySegmentView{h.data(), 10, 8});
+    CHECK(throws<std::invalid_argument>([&] { fused_topk_scores(random_rows(1, 32, rng), 4, mv, cfg); }),
+          "head mismatch");
+}
+
+static void test_vote_spans() {
+    // test_selection.cpp:233-270 map oracle
+    std::mt19937 rng(53);
+    std::uniform_int_distribution<std::size_t> idx(0, 49);
+    std::uniform_real_distribution<float> score(-1.0f, 1.0f);
+    for (int iter = 0; iter < 200; ++iter) {
+        PerHeadTopk per_head(8, std::vector<std::vector<TopkEntry>>(4));
+        std::map<std::size_t, std::pair<std::size_t, float>> tally;
+        for (auto& head : per_head)
+            for (auto& query : head) {
+                std::set<std::size_t> seen;
+                for (int j = 0; j < 4; ++j) {
+                    std::size_t i = idx(rng);
+                    while (seen.count(i)) i = idx(rng);
+                    seen.insert(i);
+                    const float s = score(rng);
+                    query.push_back(TopkEntry{i, s});
+                    auto it = tally.find(i);
+                    if (it == tally.end())
+                        tally[i] = {1, s};
+                    else {
+                        it->second.first += 1;
+                        it->second.second = std::max(it->second.second, s);
+                    }
+                }
+            }
+        std::vector<std::pair<std::size_t, std::pair<std::size_t, float>>> ranked(tally.begin(), tally.end());
+        std::sort(ranked.begin(), ranked.end(), [](const auto& a, const auto& b) {
+            if (a.second.first != b.second.first) return a.second.first > b.second.first;
+            if (a.second.second != b.second.second) return a.second.second > b.second.second;
+            return a.first < b.first;
+        });
+        const std::size_t k_prime = 1 + iter % 20;
+        const auto got = vote(per_head, k_prime);
+        bool ok = got.size() == std::min(k_prime, ranked.size());
+        for (std::size_t i = 0; ok && i < got.size(); ++i) ok = got[i] == ranked[i].first;
+        CHECK(ok, "vote iter %d", iter);
+        if (iter == 0) {
+            const auto t = tally_candidates(per_head);
+            bool tok = t.size() == ranked.size();
+            for (std::size_t i = 0; tok && i < t.size(); ++i)
+                tok = t[i].middle_index == ranked[i].first && t[i].votes == ranked[i].second.first &&
+                      t[i].score == ranked[i].second.second;
+            CHECK(tok, "tally");
+        }
+    }
+    {  // :281-292 agreement outranks score
+        PerHeadTopk ph(1, std::vector<std::vector<TopkEntry>>(2));
+        ph[0][0] = {TopkEntry{7, 0.1f}, TopkEntry{3, 9.0f}};
+        ph[0][1] = {TopkEntry{7, 0.2f}, TopkEntry{5, 0.05f}};
+        const auto w = vote(ph, 3);
+        CHECK(w.size() == 3 && w[0] == 7 && w[1] == 3 && w[2] == 5, "agreement");
+        CHECK(vote(ph, 0).empty(), "k'=0");
+    }
+    // :300-323 aligned blocks from the set oracle; :339-371 centered vs interval oracle
+    for (int iter = 0; iter < 100; ++iter) {
+        const std::size_t m = 1 + iter % 64;
+        const std::size_t len = 1 + std::uniform_int_distribution<std::size_t>(0, 100000)(rng);
+        std::vector<std::size_t> winners(120);
+        std::uniform_int_distribution<std::size_t> pick(0, len - 1);
+        for (auto& w : winners) w = pick(rng);
+        const SpanSet got = expand_spans(winners, m, len);
+        std::set<std::size_t> blocks;
+        for (std::size_t w : winners) blocks.insert(w / m);
+        bool ok = got.spans.size() == blocks.size();
+        std::size_t i = 0;
+        for (std::size_t b : blocks) {
+            if (!ok) break;
+            ok = got.spans[i].begin == b * m && got.spans[i].end == std::min(b * m + m, len);
+            ++i;
+        }
+        CHECK(ok, "aligned iter %d", iter);
+        const std::size_t mc = 2 + iter % 63;
+        const std::size_t lc = mc + std::uniform_int_distribution<std::size_t>(0, 5000)(rng);
+        std::vector<std::size_t> wc(40);
+        std::uniform_int_distribution<std::size_t> pc(0, lc - 1);
+        for (auto& w : wc) w = pc(rng);
+        const SpanSet gc = expand_spans(wc, mc, lc, SpanMode::Centered);
+        std::vector<uint64_t> w64(wc.begin(), wc.end()), ob(wc.size()), oe(wc.size());
+        size_t on = 0;
+        oracle_expand_spans(w64.data(), w64.size(), mc, lc, ORACLE_SPAN_CENTERED, ob.data(), oe.data(), &on);
+        bool okc = gc.spans.size() == on;
+        for (std::size_t j = 0; okc && j < on; ++j) okc = gc.spans[j].begin == ob[j] && gc.spans[j].end == oe[j];
+        CHECK(okc, "centered iter %d", iter);
+    }
+    CHECK(expand_spans(std::vector<std::size_t>{5, 20}, 32, 100).spans == (std::vector<Span>{{0, 32}}), "5,20");
+    CHECK(expand_spans(std::vector<std::size_t>{98}, 32, 100).spans == (std::vector<Span>{{96, 100}}), "98");
+    CHECK(throws<std::out_of_range>([] { expand_spans(std::vector<std::size_t>{100}, 32, 100); },
+                                    "expand_spans: winner outside middle"), "winner range");
+    CHECK(expand_spans(std::vector<std::size_t>{}, 32, 100).empty(), "empty");
+}
+
+static void check_scope(const AttentionScope& scope, const SegmentedKvCache& cache, const SpanSet& spans,
+                        const char* label) {
+    const auto segs = cache.views();
+    std::vector<std::size_t> want;
+    for (std::size_t i = segs.global.begin; i < segs.global.end; ++i) want.push_back(i);
+    for (const Span& s : spans.spans)
+        for (std::size_t i = s.begin; i < s.end; ++i) want.push_back(segs.middle.begin + i);
+    for (std::size_t i = segs.local.begin; i < segs.local.end; ++i) want.push_back(i);
+    bool ok = scope.length == want.size() && scope.source_indices == want;
+    for (std::size_t kv = 0; ok && kv < cache.n_kv_heads(); ++kv)
+        for (std::size_t r = 0; ok && r < scope.length; ++r)
+            ok = std::equal(scope.key_row(kv, r), scope.key_row(kv, r) + cache.d_head(), cache.key(kv, want[r])) &&
+                 std::equal(scope.value_row(kv, r), scope.value_row(kv, r) + cache.d_head(), cache.value(kv, want[r]));
+    CHECK(ok, "%s", label);
+}
+
+static void test_scope() {
+    // test_scope.cpp:53-132
+    std::mt19937 rng(71);
+    for (int iter = 0; iter < 30; ++iter) {
+        const std::size_t g = std::uniform_int_distribution<std::size_t>(0, 40)(rng);
+        const std::size_t loc = std::uniform_int_distribution<std::size_t>(1, 64)(rng);
+        const std::size_t total = std::uniform_int_distribution<std::size_t>(1, 2000)(rng);
+        SegmentedKvCache cache(2, 8, g, loc);
+        cache.append(random_rows(total, 16, rng), random_rows(total, 16, rng));
+        SpanSet spans;
+        if (cache.middle_len() > 0) {
+            std::vector<std::size_t> winners(8);
+            std::uniform_int_distribution<std::size_t> pick(0, cache.middle_len() - 1);
+            for (auto& w : winners) w = pick(rng);
+            spans = expand_spans(winners, 16, cache.middle_len());
+        }
+        check_scope(assemble_scope(cache, spans, 1 << 20), cache, spans, "gather oracle");
+    }
+    {
+        SegmentedKvCache cache(1, 4, 4, 8);
+        cache.append(random_rows(50, 4, rng), random_rows(50, 4, rng));
+        const AttentionScope s = assemble_window_scope(cache, 4096);
+        CHECK(s.length == 12 && s.source_indices[0] == 0 && s.source_indices[4] == 42, "window");
+    }
+    {
+        SegmentedKvCache cache(1, 4, 4, 8);
+        cache.append(random_rows(12, 4, rng), random_rows(12, 4, rng));
+        CHECK(throws<std::invalid_argument>([&] { assemble_scope(cache, SpanSet{}, 11); },
+                                            "scope exceeds pretrain window"), "overflow");
+        CHECK(assemble_scope(cache, SpanSet{}, 12).length == 12, "fits");
+    }
+    {
+        SegmentedKvCache cache(1, 4, 4, 8);
+        cache.append(random_rows(20, 4, rng), random_rows(20, 4, rng));
+        SpanSet spans;
+        spans.spans.push_back(Span{4, 9});
+        CHECK(throws<std::out_of_range>([&] { assemble_scope(cache, spans, 4096); }), "span range");
+    }
+    {  // C01: the budget fills the window exactly
+        SegmentedKvCache cache(1, 2, 32, 4096);
+        cache.append(random_rows(9000, 2, rng), random_rows(9000, 2, rng));
+        std::vector<std::size_t> winners;
+        for (std::size_t b = 0; b < 127; ++b) winners.push_back(b * 32);
+        const SpanSet spans = expand_spans(winners, 32, cache.middle_len());
+        CHECK(spans.coverage() == 127u * 32u, "coverage");
+        const AttentionScope s = assemble_scope(cache, spans, 8192);
+        CHECK(s.length == 8192 && s.length == SelectionConfig{}.budget(), "budget 8192");
+        check_scope(s, cache, spans, "budget gather");
+    }
+}
+
+static void test_rope_attend() {
+    std::mt19937 rng(3);
+    {  // test_numerics.cpp:150-237
+        const RotaryTable t(8, 10000.0, 16);
+        const DenseMatrix m = random_rows(4, 8, rng);
+        const std::vector<std::size_t> pos(4, 0);
+        CHECK(rope_rotate(m, pos, t).values == m.values, "pos 0 identity");
+        const RotaryTable t2(2, 10000.0, 64);
+        for (std::size_t p : {1u, 5u, 63u}) {
+            DenseMatrix v(1, 2);
+            v.at(0, 0) = 1.0f;
+            const std::vector<std::size_t> pp{p};
+            const DenseMatrix r = rope_rotate(v, pp, t2);
+            CHECK(std::abs(r.at(0, 0) - std::cos(double(p))) < 1e-6 && std::abs(r.at(0, 1) - std::sin(double(p))) < 1e-6,
+                  "angle %zu", p);
+        }
+        const RotaryTable t3(8, 10000.0, 100);
+        DenseMatrix z(1, 8);
+        CHECK(throws<std::out_of_range>([&] { t3.rotate_row(z.row(0), 100); }, "position out of pretrained range"),
+              "ood");
+        CHECK(throws<std::invalid_argument>([] { RotaryTable(7, 10000.0, 16); }), "odd dim");
+        CHECK(throws<std::invalid_argument>([] { RotaryTable(8, -1.0, 16); }), "base");
+        CHECK(throws<std::invalid_argument>([] { RotaryTable(8, 10000.0, 0); }), "max pos");
+        // table bytes equal the oracle restatement (rope.hpp:325-337)
+        const RotaryTable t4(128, 500000.0, 8192);
+        std::vector<float> oc(8192 * 64), os(8192 * 64);
+        oracle_rope_table(128, 500000.0, 8192, oc.data(), os.data());
+        CHECK(std::equal(oc.begin(), oc.end(), t4.cos_row(0)) && std::equal(os.begin(), os.end(), t4.sin_row(0)),
+              "table");
+    }
+    {  // :281-320 attend vs oracle, causal boundary, single key, empty set
+        std::uniform_int_distribution<std::size_t> nq(1, 8), len(1, 512), dim(4, 64);
+        for (int iter = 0; iter < 200; ++iter) {
+            const std::size_t n_q = nq(rng), L = len(rng), d = dim(rng) & ~1ull;
+            const DenseMatrix q = random_rows(n_q, d, rng), k = random_rows(L, d, rng), v = random_rows(L, d, rng);
+            std::optional<std::size_t> b;
+            if (iter % 2 == 0 && L >= n_q) b = L - n_q;
+            const AttendResult got = attend(q, k, v, b);
+            std::vector<float> out(n_q * d);
+            std::vector<double> ent(n_q);
+            oracle_attend(q.values.data(), n_q, k.values.data(), v.values.data(), L, d, d, b.has_value(),
+                          b.value_or(0), out.data(), ent.data());
+            double md = 0, me = 0;
+            for (std::size_t i = 0; i < out.size(); ++i) md = std::max(md, std::abs(double(out[i]) - got.output.values[i]));
+            for (std::size_t i = 0; i < n_q; ++i) me = std::max(me, std::abs(ent[i] - got.row_entropy[i]));
+            CHECK(md <= 1e-6 && me <= 1e-9, "attend iter %d md=%g me=%g", iter, md, me);
+        }
+        DenseMatrix q(2, 4), k(3, 4), v(3, 4);
+        for (std::size_t c = 0; c < 4; ++c) {
+            q.at(0, c) = q.at(1, c) = 1.0f;
+            k.at(2, c) = 100.0f;
+            v.at(0, c) = 5.0f;
+            v.at(1, c) = 9.0f;
+            v.at(2, c) = -50.0f;
+        }
+        const AttendResult r = attend(q, k, v, 0);
+        CHECK(r.output.at(0, 0) == 5.0f && std::abs(r.output.at(1, 0) - 7.0f) < 1e-6, "causal boundary");
+        DenseMatrix e(0, 8);
+        CHECK(throws<std::invalid_argument>([&] { attend(DenseMatrix(1, 8), e, e); }, "empty key set"), "empty");
+    }
+}
+
+static void test_attend_step() {
+    // engine.hpp attend_step vs the oracle restatement, toy + LLaMA geometries, both modes
+    std::mt19937 rng(7);
+    struct Case { std::size_t n_kv, nh, d, total, n_q, window; SelectionConfig cfg; AttentionMode mode; };
+    std::vector<Case> cases;
+    SelectionConfig toy;
+    toy.l_global = 16; toy.l_local = 256; toy.l_chunk = 128; toy.span_m = 16; toy.k = 4; toy.k_prime = 64;
+    cases.push_back({2, 4, 16, 2000, 1, 2048, toy, AttentionMode::ReAttention});
+    cases.push_back({2, 4, 16, 3000, 64, 2048, toy, AttentionMode::ReAttention});
+    SelectionConfig cen = toy;
+    cen.span_mode = SpanMode::Centered;
+    cases.push_back({2, 4, 16, 5000, 8, 2048, cen, AttentionMode::ReAttention});
+    cases.push_back({2, 4, 16, 900, 32, 2048, toy, AttentionMode::Window});
+    cases.push_back({8, 32, 128, 12000, 1, 8192, SelectionConfig{}, AttentionMode::ReAttention});
+    for (const Case& c : cases) {
+        SegmentedKvCache cache(c.n_kv, c.d, c.cfg.l_global, c.cfg.l_local);
+        const DenseMatrix K = random_rows(c.total, c.n_kv * c.d, rng), V = random_rows(c.total, c.n_kv * c.d, rng);
+        cache.append(K, V);
+        const RotaryTable rope(c.d, 10000.0, c.window);
+        const DenseMatrix q = random_rows(c.n_q, c.nh * c.d, rng);
+        RunStats st;
+        SpanSet spans;
+        const DenseMatrix out = attend_step(q, c.nh, cache, c.cfg, rope, c.mode, &st, nullptr, &spans);
+        // oracle on the head-major copy
+        std::vector<float> hk(c.n_kv * c.total * c.d), hv(hk.size());
+        for (std::size_t h = 0; h < c.n_kv; ++h)
+            for (std::size_t r = 0; r < c.total; ++r)
+                for (std::size_t e = 0; e < c.d; ++e) {
+                    hk[(h * c.total + r) * c.d + e] = K.at(r, h * c.d + e);
+                    hv[(h * c.total + r) * c.d + e] = V.at(r, h * c.d + e);
+                }
+        std::vector<float> oc(c.window * c.d / 2), os(oc.size()), oout(c.n_q * c.nh * c.d);
+        oracle_rope_table(c.d, 10000.0, c.window, oc.data(), os.data());
+        oracle_selection_config ocfg{c.cfg.k, c.cfg.k_prime, c.cfg.span_m, c.cfg.tile_size, c.cfg.l_global,
+                                     c.cfg.l_local, c.cfg.l_chunk, c.cfg.span_mode == SpanMode::Aligned ? 0 : 1};
+        oracle_step_stats ost{};
+        ost.coverage_total = 1;
+        std::vector<uint64_t> sb(c.cfg.k_prime + 1), se(c.cfg.k_prime + 1);
+        const int rc = oracle_attend_step(q.values.data(), c.n_q, c.nh, hk.data(), hv.data(), c.n_kv, c.d, c.total,
+                                          c.total, &ocfg, oc.data(), os.data(), c.window, (int)c.mode, oout.data(),
+                                          &ost, sb.data(), se.data());
+        double md = 0;
+        for (std::size_t i = 0; i < oout.size(); ++i) md = std::max(md, std::abs(double(oout[i]) - out.values[i]));
+        bool spans_eq = spans.spans.size() == ost.n_spans;
+        for (std::size_t i = 0; spans_eq && i < ost.n_spans; ++i)
+            spans_eq = spans.spans[i].begin == sb[i] && spans.spans[i].end == se[i];
+        CHECK(rc == 0 && md <= 1e-6 && spans_eq && st.scope_len_max == ost.scope_len &&
+                  std::abs(st.entropy_max - ost.entropy_max) <= 1e-9 && st.coverage_total == (bool)ost.coverage_total,
+              "attend_step total=%zu n_q=%zu md=%g L=%zu/%zu", c.total, c.n_q, md, st.scope_len_max, ost.scope_len);
+    }
+    {  // errors: engine.hpp:509-511, scope.hpp:262-263, engine.hpp:527
+        SelectionConfig cfg;
+        cfg.l_global = 4; cfg.l_local = 8; cfg.k_prime = 2; cfg.span_m = 4;
+        SegmentedKvCache cache(1, 4, 4, 8);
+        cache.append(random_rows(12, 4, rng), random_rows(12, 4, rng));
+        CHECK(throws<std::invalid_argument>([&] { attend_step(DenseMatrix(1, 4), 1, cache, cfg, RotaryTable(4, 1e4, 11),
+                                                              AttentionMode::ReAttention); },
+                                            "scope exceeds pretrain window"), "window");
+        CHECK(throws<std::logic_error>([&] { attend_step(DenseMatrix(13, 4), 1, cache, cfg, RotaryTable(4, 1e4, 64),
+                                                         AttentionMode::ReAttention); },
+                                       "query block longer than scope"), "query long");
+        CHECK(throws<std::invalid_argument>([&] { attend_step(DenseMatrix(1, 10), 3, cache, cfg, RotaryTable(4, 1e4, 64),
+                                                              AttentionMode::ReAttention); },
+                                            "query width"), "width");
+    }
+}
+
+int main() {
+    test_fused_topk();
+    test_vote_spans();
+    test_scope();
+    test_rope_attend();
+    test_attend_step();
+    std::printf("%d checks, %d failures\n", g_checks, g_fail);
+    return g_fail ? 1 : 0;
+}
