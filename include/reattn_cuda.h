@@ -186,6 +186,39 @@ int reattn_plan_stats(reattn_plan* plan, reattn_step_stats* stats);
 int reattn_plan_info(const reattn_plan* plan, uint64_t* kernels_per_step,
                      uint64_t* scan_bytes, uint64_t* scope_bytes);
 
+/* ---- sequence-sharded decode ---------------------------------------- */
+/* Rank `rank` of `world` holds [global | its middle shard | local] in `local_cache` (same
+ * l_global / l_local as the unsharded cache; the shard is the local cache's middle).  The
+ * middle of the GLOBAL cache (`global_total` rows) is split at multiples of span_m:
+ * shard r = [floor(r*M/world/m)*m, floor((r+1)*M/world/m)*m) (last shard ends at M).
+ * A step is four asynchronous stages on the context stream with two all-gathers between
+ * them, done by the caller's collective library (NCCL):
+ *   scan -> all_gather(cand) -> select -> attend -> all_gather(part) -> combine.
+ * Every rank ends with the full output. */
+typedef struct reattn_shard_plan reattn_shard_plan;
+int reattn_shard_plan_create(reattn_ctx* ctx, const reattn_cache* local_cache,
+                             const reattn_rope* rope, uint64_t n_head,
+                             const reattn_selection_config* cfg, uint64_t global_total,
+                             int world, int rank, reattn_shard_plan** out);
+void reattn_shard_plan_destroy(reattn_shard_plan* plan);
+/* shard boundaries in middle coordinates (rank r: [begin, begin + len)) */
+int reattn_shard_range(uint64_t middle_len, uint64_t span_m, int world, int rank,
+                       uint64_t* begin, uint64_t* len);
+float* reattn_shard_plan_q(const reattn_shard_plan* plan);    /* [1][n_head*d] */
+float* reattn_shard_plan_out(const reattn_shard_plan* plan);  /* [1][n_head*d] */
+/* device buffers for the two all-gathers: this rank's send block and the world-sized
+ * receive buffer (rank r's block at recv + r * bytes) */
+int reattn_shard_buffers(const reattn_shard_plan* plan, void** cand_send, void** cand_recv,
+                         uint64_t* cand_bytes, void** part_send, void** part_recv,
+                         uint64_t* part_bytes);
+int reattn_shard_scan(reattn_shard_plan* plan);     /* local K scan -> cand_send */
+int reattn_shard_select(reattn_shard_plan* plan);   /* cand_recv -> vote/spans/scopes */
+int reattn_shard_attend(reattn_shard_plan* plan);   /* owned scope rows -> part_send */
+int reattn_shard_combine(reattn_shard_plan* plan);  /* part_recv -> out */
+/* synchronise; header errors surface here */
+int reattn_shard_stats(reattn_shard_plan* plan, reattn_step_stats* stats, uint64_t* span_b_host,
+                       uint64_t* span_e_host);
+
 /* ---- synthetic inputs (tests and benchmarks; not on the hot path) ---------------- */
 /* dst[i] = splitmix64(seed, offset+i) mapped to [-1, 1) (24 significant bits), stored as
  * fp32 or bf16 (round to nearest even). */

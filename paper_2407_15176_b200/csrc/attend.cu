@@ -312,6 +312,7 @@ struct DecodeArgs {
     AttnArgs a;
     int n_splits;        // grid.x (upper bound from L_max)
     int chunks_per_cta;  // 32-row chunks per CTA
+    int n_src;           // combine: partial sets laid out [n_src][n_splits] (sharded: ranks)
 };
 
 DecodeArgs plan_decode(const AttnArgs& a, uint32_t L_max, int num_sms) {
@@ -324,6 +325,7 @@ DecodeArgs plan_decode(const AttnArgs& a, uint32_t L_max, int num_sms) {
     const int want = std::max(1, 16 * num_sms / std::max(1, a.n_kv));
     D.chunks_per_cta = std::min(8, std::max(1, (chunks + want - 1) / want));
     D.n_splits = (chunks + D.chunks_per_cta - 1) / D.chunks_per_cta;
+    D.n_src = 1;
     return D;
 }
 
@@ -349,7 +351,8 @@ __device__ __forceinline__ void load8<float>(const float* p, float (&v)[8]) {
 
 constexpr size_t decode_smem_bytes() {
     return (size_t)(8 * kDecD + 8 * kDecChunk + 64) * sizeof(double) +
-           (size_t)kDecChunk * kDecKSF * sizeof(float) + (size_t)kDecChunk * kDecD * sizeof(float);
+           (size_t)kDecChunk * kDecKSF * sizeof(float) + (size_t)kDecChunk * kDecD * sizeof(float) +
+           kDecChunk;
 }
 
 // Raw 16-byte words of 8 consecutive elements (converted only when staged to smem, so a
@@ -389,6 +392,7 @@ struct ChunkRegs {
     static constexpr int kIter = kDecChunk * (kDecD / 8) / kDecThreads;  // 4
     Raw8<KT> kr[kIter], vr[kIter];
     float4 c4[kIter], s4[kIter];
+    bool own[kIter];
 
     __device__ __forceinline__ void load(const AttnArgs& a, int kv, uint32_t k0, int nk) {
         const int tid = threadIdx.x;
@@ -397,12 +401,13 @@ struct ChunkRegs {
 #pragma unroll
         for (int i = 0; i < kIter; ++i) {
             const int r = (tid + i * kDecThreads) >> 4;
-            cr[i] = r < nk ? (a.src ? __ldg(a.src + k0 + r) : k0 + r) : 0u;
+            cr[i] = r < nk ? (a.src ? __ldg(a.src + k0 + r) : k0 + r) : reattn_dev::kNoIndex;
+            own[i] = cr[i] != reattn_dev::kNoIndex;  // sharded scopes mask rows owned elsewhere
         }
 #pragma unroll
         for (int i = 0; i < kIter; ++i) {
             const int e = tid + i * kDecThreads, r = e >> 4, c8 = (e & 15) * 8;
-            if (r < nk) {
+            if (own[i]) {
                 const size_t rowb = ((size_t)kv * a.head_stride + cr[i]) * kDecD + c8;
                 kr[i].load((const KT*)a.k_base + rowb);
                 vr[i].load((const KT*)a.v_base + rowb);
@@ -414,12 +419,20 @@ struct ChunkRegs {
         }
     }
     // rotate K at its compact position (rope.hpp:347-358, unfused fp32) and stage to smem
-    __device__ __forceinline__ void store(const AttnArgs& a, int nk, float* ks, float* vs) const {
+    __device__ __forceinline__ void store(const AttnArgs& a, int nk, float* ks, float* vs,
+                                          uint8_t* rowok) const {
         const int tid = threadIdx.x;
 #pragma unroll
         for (int i = 0; i < kIter; ++i) {
             const int e = tid + i * kDecThreads, r = e >> 4, c8 = (e & 15) * 8;
-            if (r < nk) {
+            if (r < nk && (e & 15) == 0) rowok[r] = own[i] ? 1 : 0;
+            if (r < nk && !own[i]) {  // masked row: zeros keep 0 * v finite in the PV loop
+                float4* kd = reinterpret_cast<float4*>(ks + r * kDecKSF + c8);
+                kd[0] = kd[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                float4* vd = reinterpret_cast<float4*>(vs + r * kDecD + c8);
+                vd[0] = vd[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            if (r < nk && own[i]) {
                 float kf[8], vf[8];
                 kr[i].to_float(kf);
                 vr[i].to_float(vf);
@@ -463,6 +476,7 @@ __global__ void __launch_bounds__(kDecThreads, 5) attend_decode_kernel(const Dec
     double* st = lg + 8 * kDecChunk;               // [8][4]: m, A, B, rescale  (+pad)
     float* ks = (float*)(st + 64);                 // [kDecChunk][kDecKSF]
     float* vs = ks + kDecChunk * kDecKSF;          // [kDecChunk][kDecD]
+    uint8_t* rowok = (uint8_t*)(vs + kDecChunk * kDecD);  // [kDecChunk] row attended here
     constexpr int half = kDecD / 2;
 
     ChunkRegs<KT> cur;
@@ -489,7 +503,7 @@ __global__ void __launch_bounds__(kDecThreads, 5) attend_decode_kernel(const Dec
         st[tid * 4 + 2] = 0.0;
         st[tid * 4 + 3] = 1.0;
     }
-    cur.store(a, (int)min((uint32_t)kDecChunk, key_end - key_begin), ks, vs);
+    cur.store(a, (int)min((uint32_t)kDecChunk, key_end - key_begin), ks, vs, rowok);
     __syncthreads();
 
     const double scale = 1.0 / sqrt((double)kDecD);
@@ -529,7 +543,7 @@ __global__ void __launch_bounds__(kDecThreads, 5) attend_decode_kernel(const Dec
                 double s = l2[g][0] + l2[g][1];
                 s = s + __shfl_xor_sync(0xFFFFFFFFu, s, 1);
                 s = s + __shfl_xor_sync(0xFFFFFFFFu, s, 2);
-                if (p == 0) lg[g * kDecChunk + j] = j < nk ? s * scale : -INFINITY;
+                if (p == 0) lg[g * kDecChunk + j] = (j < nk && rowok[j]) ? s * scale : -INFINITY;
             }
         }
         __syncthreads();
@@ -541,8 +555,9 @@ __global__ void __launch_bounds__(kDecThreads, 5) attend_decode_kernel(const Dec
             for (int off = 16; off > 0; off >>= 1) mc = fmax(mc, __shfl_xor_sync(0xFFFFFFFFu, mc, off));
             const double m_old = st[g * 4 + 0];
             const double m_new = fmax(m_old, mc);
-            const double w = lane < nk ? exp(s - m_new) : 0.0;
-            double sa = w, sb = lane < nk ? (s - m_new) * w : 0.0;
+            const bool live = lane < nk && s != -INFINITY;  // masked / padded keys drop out
+            const double w = live ? exp(s - m_new) : 0.0;
+            double sa = w, sb = live ? (s - m_new) * w : 0.0;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
                 sa += __shfl_xor_sync(0xFFFFFFFFu, sa, off);
@@ -573,7 +588,7 @@ __global__ void __launch_bounds__(kDecThreads, 5) attend_decode_kernel(const Dec
         }
         __syncthreads();
         if (nk1 > 0) {
-            nxt.store(a, nk1, ks, vs);
+            nxt.store(a, nk1, ks, vs, rowok);
             __syncthreads();
         }
     }
@@ -590,6 +605,7 @@ __global__ void __launch_bounds__(kDecThreads, 5) attend_decode_kernel(const Dec
 // parallel, then 8 warps each sum a strided subset of partials for 32 columns (one per
 // lane), reduced in a fixed order (deterministic).
 constexpr int kCombThreads = 256;
+constexpr int kCombMaxParts = 2048;  // sources x key ranges per head
 constexpr int kCombCols = 32;
 __global__ void __launch_bounds__(kCombThreads) attend_decode_combine(const DecodeArgs P) {
     const AttnArgs& a = P.a;
@@ -598,15 +614,18 @@ __global__ void __launch_bounds__(kCombThreads) attend_decode_combine(const Deco
     const int h = blockIdx.x, cb = blockIdx.y;
     const int kv = h / a.group, g = h % a.group;
     const uint32_t keys_per = (uint32_t)P.chunks_per_cta * kDecChunk;
-    const int ns = (int)((L + keys_per - 1) / keys_per);
+    int ns = (int)((L + keys_per - 1) / keys_per);
     constexpr int NW = kCombThreads / 32;
-    __shared__ double w_s[1024];
+    __shared__ double w_s[kCombMaxParts];
     __shared__ double red[NW][kCombCols];
     __shared__ double rs[NW][3];
     __shared__ double s_M, s_A;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ns_src = ns;
+    ns = ns * P.n_src;  // every source (rank) contributes the same split layout
     auto prow = [&](int s) {
-        return a.part + (((size_t)s * a.n_kv + kv) * a.group + g) * kDecPart;
+        const size_t split = (size_t)(s / ns_src) * P.n_splits + s % ns_src;
+        return a.part + ((split * a.n_kv + kv) * a.group + g) * kDecPart;
     };
     double m = -INFINITY;
     for (int s = tid; s < ns; s += kCombThreads) m = fmax(m, prow(s)[0]);
@@ -624,10 +643,13 @@ __global__ void __launch_bounds__(kCombThreads) attend_decode_combine(const Deco
     double A = 0.0, B = 0.0;
     for (int s = tid; s < ns; s += kCombThreads) {
         const double* p = prow(s);
+        // empty partials (fully masked ranges, A == 0) contribute nothing (no 0 * -inf)
         const double w = p[1] > 0.0 ? exp(p[0] - M) : 0.0;
         w_s[s] = w;
-        A += p[1] * w;
-        B += w * (p[2] + (p[0] - M) * p[1]);
+        if (p[1] > 0.0) {
+            A += p[1] * w;
+            B += w * (p[2] + (p[0] - M) * p[1]);
+        }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -765,6 +787,59 @@ cudaError_t launch_attend(const AttnArgs& a, uint32_t L_max, cudaStream_t s) {
         attend_split_kernel<float><<<grid, kAttnThreads, smem, s>>>(P);
     }
     if (!P.direct) attend_combine_kernel<<<a.n_q * a.n_head, 128, 0, s>>>(P);
+    return cudaGetLastError();
+}
+
+}  // namespace reattn_impl
+
+// ---- sharded decode: the two halves of the decode attention, exposed separately so the
+// partial states of all ranks can be all-gathered between them ---------------------------
+namespace reattn_impl {
+
+bool attend_decode_supported(const AttnArgs& a, uint32_t L_max) { return decode_eligible(a, L_max); }
+
+size_t attend_decode_partial_bytes(const AttnArgs& a, uint32_t L_max) {
+    const DecodeArgs D = plan_decode(a, L_max, sm_count());
+    return (size_t)D.n_splits * a.n_kv * a.group * kDecPart * sizeof(double);
+}
+
+cudaError_t launch_attend_decode_partials(const AttnArgs& a, uint32_t L_max, cudaStream_t s) {
+    const DecodeArgs D = plan_decode(a, L_max, sm_count());
+    dim3 grid(D.n_splits, a.n_kv);
+    const size_t smem = decode_smem_bytes();
+#define DEC_LAUNCH(KT, GG)                                                                \
+    do {                                                                                  \
+        cudaFuncSetAttribute(attend_decode_kernel<KT, GG>,                                \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+        attend_decode_kernel<KT, GG><<<grid, kDecThreads, smem, s>>>(D);                  \
+    } while (0)
+#define DEC_DISPATCH(KT)                        \
+    switch (a.group) {                          \
+        case 1: DEC_LAUNCH(KT, 1); break;       \
+        case 2: DEC_LAUNCH(KT, 2); break;       \
+        case 3: DEC_LAUNCH(KT, 3); break;       \
+        case 4: DEC_LAUNCH(KT, 4); break;       \
+        case 5: DEC_LAUNCH(KT, 5); break;       \
+        case 6: DEC_LAUNCH(KT, 6); break;       \
+        case 7: DEC_LAUNCH(KT, 7); break;       \
+        default: DEC_LAUNCH(KT, 8); break;      \
+    }
+    if (a.dtype == kBF16) {
+        DEC_DISPATCH(__nv_bfloat16);
+    } else {
+        DEC_DISPATCH(float);
+    }
+#undef DEC_DISPATCH
+#undef DEC_LAUNCH
+    return cudaGetLastError();
+}
+
+cudaError_t launch_attend_decode_combine(const AttnArgs& a, uint32_t L_max, int n_src,
+                                         cudaStream_t s) {
+    DecodeArgs D = plan_decode(a, L_max, sm_count());
+    D.n_src = n_src;
+    if ((size_t)n_src * D.n_splits > (size_t)kCombMaxParts) return cudaErrorInvalidValue;
+    attend_decode_combine<<<dim3(a.n_head, kDecD / kCombCols), kCombThreads, 0, s>>>(D);
     return cudaGetLastError();
 }
 

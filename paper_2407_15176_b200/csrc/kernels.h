@@ -135,6 +135,28 @@ constexpr int kAttnSplit = 64;
 size_t attend_workspace(const AttnArgs& a, uint32_t L_max);
 cudaError_t launch_attend(const AttnArgs& a, uint32_t L_max, cudaStream_t s);
 int attend_kernel_count(const AttnArgs& a, uint32_t L_max);
+// sharded decode halves (n_q == 1, d == 128): partial states, then the multi-source combine
+bool attend_decode_supported(const AttnArgs& a, uint32_t L_max);
+size_t attend_decode_partial_bytes(const AttnArgs& a, uint32_t L_max);  // per source
+cudaError_t launch_attend_decode_partials(const AttnArgs& a, uint32_t L_max, cudaStream_t s);
+cudaError_t launch_attend_decode_combine(const AttnArgs& a, uint32_t L_max, int n_src,
+                                         cudaStream_t s);
+
+// ---- sharded decode: merge gathered candidates, vote/spans/scope, local ownership ------
+struct ShardSelectArgs {
+    // source s, list l, rank j at [s * src_stride + l * k + j]; indices are shard-local
+    // middle indices (kNoIndex = empty slot)
+    const uint32_t* cand_idx;
+    const float* cand_score;
+    size_t src_stride;
+    int n_src, n_lists, k, kk;  // kk = min(k, global middle length)
+    uint32_t src_offset[64];    // shard_begin of each source rank
+    SmallSelectIO sel;          // global geometry; sel.scope_src receives the GLOBAL table
+    int rank;
+    uint32_t shard_begin, shard_len;
+    uint32_t* local_src;        // [L'] local cache row, or kNoIndex when owned elsewhere
+};
+cudaError_t launch_shard_merge_select(const ShardSelectArgs& a, cudaStream_t s);
 
 // ---- misc kernels ------------------------------------------------------------------
 // rows x (n_kv*d) fp32 (DenseMatrix layout) -> head-major [n_kv][head_stride][d] at row0.

@@ -119,6 +119,19 @@ SIGNATURES = [
     ("reattn_plan_stats", C.c_int, [vp, C.POINTER(StepStats)]),
     ("reattn_plan_info", C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
     ("reattn_synth_uniform", C.c_int, [vp, vp, u64, C.c_int, u64, u64]),
+    ("reattn_shard_plan_create", C.c_int, [vp, vp, vp, u64, C.POINTER(SelectionConfig), u64,
+                                           C.c_int, C.c_int, C.POINTER(vp)]),
+    ("reattn_shard_plan_destroy", None, [vp]),
+    ("reattn_shard_range", C.c_int, [u64, u64, C.c_int, C.c_int, C.POINTER(u64), C.POINTER(u64)]),
+    ("reattn_shard_plan_q", vp, [vp]),
+    ("reattn_shard_plan_out", vp, [vp]),
+    ("reattn_shard_buffers", C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(u64),
+                                       C.POINTER(vp), C.POINTER(vp), C.POINTER(u64)]),
+    ("reattn_shard_scan", C.c_int, [vp]),
+    ("reattn_shard_select", C.c_int, [vp]),
+    ("reattn_shard_attend", C.c_int, [vp]),
+    ("reattn_shard_combine", C.c_int, [vp]),
+    ("reattn_shard_stats", C.c_int, [vp, C.POINTER(StepStats), vp, vp]),
 ]
 
 _lib = None
