@@ -36,6 +36,9 @@ struct StepPlan {
     ScopeHeader* hdr = nullptr;
     double* part = nullptr;
     double* entropy = nullptr;
+    bool large_vote = false;  // > kVoteMaxSmem candidates: device radix-sort vote
+    size_t vote_ws_bytes = 0;
+    void* vote_ws = nullptr;
     size_t part_bytes = 0;
     size_t scratch_bytes = 0;
     uint64_t kernels = 0;
@@ -72,9 +75,10 @@ int plan_step(reattn_ctx* ctx, const reattn_cache* cache, const reattn_rope* rop
         return set_err(ctx, REATTN_EINVAL, "attend_step: cache too long for 32-bit indices");
     if (P.select) {
         const uint64_t n_cand = P.n_kv * n_q * P.kk;
-        if (n_cand > kVoteMaxSmem)
-            return set_err(ctx, REATTN_ERUNTIME,
-                           "vote: candidate count exceeds device capacity (8192)");
+        if (n_cand >= (1ull << 31))
+            return set_err(ctx, REATTN_ERUNTIME, "vote: candidate count exceeds 2^31");
+        P.large_vote = n_cand > kVoteMaxSmem;
+        P.vote_ws_bytes = P.large_vote ? vote_large_workspace((uint32_t)n_cand) : 0;
         ScanArgs& a = P.scan.a;
         a.q = q_dev;
         a.n_q = (int)n_q;
@@ -140,6 +144,7 @@ void carve_step(StepPlan& P, const reattn_cache* cache, const reattn_rope* rope,
     P.part_bytes = attend_workspace(a, std::max<uint32_t>(1, P.L_upper));
     P.part = c.take<double>(P.part_bytes / sizeof(double) + 1);
     P.entropy = c.take<double>(std::max<uint64_t>(1, P.n_q * P.n_head));
+    P.vote_ws = c.take<uint8_t>(P.vote_ws_bytes);
     P.scratch_bytes = c.off;
 }
 
@@ -200,7 +205,10 @@ int enqueue_step(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache, const 
         if (rc) return rc;
         ++P.kernels;
     }
-    if (!fused) {
+    if (!fused && P.large_vote) {
+        CU(ctx, launch_vote_large(sa, P.vote_ws, s));
+        P.kernels += 8;
+    } else if (!fused) {
         CU(ctx, launch_select(sa, s));
         ++P.kernels;
     }
@@ -557,9 +565,9 @@ int reattn_vote(reattn_ctx* ctx, const uint32_t* idx_dev, const float* score_dev
                 uint64_t k_prime, uint32_t* winners_dev, uint64_t* n_winners) {
     *n_winners = 0;
     if (k_prime == 0 || n == 0) return REATTN_OK;
-    if (n > kVoteMaxSmem)
-        return set_err(ctx, REATTN_ERUNTIME, "vote: candidate count exceeds device capacity (8192)");
-    int rc = ensure_arena(ctx, 4096);
+    if (n >= (1ull << 31)) return set_err(ctx, REATTN_ERUNTIME, "vote: candidate count exceeds 2^31");
+    const bool large = n > kVoteMaxSmem;
+    int rc = ensure_arena(ctx, 4096 + (large ? vote_large_workspace((uint32_t)n) : 0));
     if (rc) return rc;
     SelectArgs sa;
     std::memset(&sa, 0, sizeof(sa));
@@ -571,7 +579,10 @@ int reattn_vote(reattn_ctx* ctx, const uint32_t* idx_dev, const float* score_dev
     sa.k_prime = (uint32_t)std::min<uint64_t>(k_prime, n);
     sa.winners = winners_dev;
     sa.hdr = (ScopeHeader*)ctx->arena;
-    CU(ctx, launch_select(sa, ctx->stream));
+    if (large)
+        CU(ctx, launch_vote_large(sa, (uint8_t*)ctx->arena + 4096, ctx->stream));
+    else
+        CU(ctx, launch_select(sa, ctx->stream));
     ScopeHeader h;
     CU(ctx, cudaMemcpyAsync(&h, sa.hdr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
@@ -585,9 +596,9 @@ int reattn_tally(reattn_ctx* ctx, const uint32_t* idx_dev, const float* score_de
                  uint32_t* idx_out, uint32_t* votes_out, float* score_out, uint64_t* n_unique) {
     *n_unique = 0;
     if (n == 0) return REATTN_OK;
-    if (n > kVoteMaxSmem)
-        return set_err(ctx, REATTN_ERUNTIME, "vote: candidate count exceeds device capacity (8192)");
-    int rc = ensure_arena(ctx, 4096);
+    if (n >= (1ull << 31)) return set_err(ctx, REATTN_ERUNTIME, "vote: candidate count exceeds 2^31");
+    const bool large = n > kVoteMaxSmem;
+    int rc = ensure_arena(ctx, 4096 + (large ? vote_large_workspace((uint32_t)n) : 0));
     if (rc) return rc;
     SelectArgs sa;
     std::memset(&sa, 0, sizeof(sa));
@@ -601,7 +612,10 @@ int reattn_tally(reattn_ctx* ctx, const uint32_t* idx_dev, const float* score_de
     sa.rank_votes = votes_out;
     sa.rank_score = score_out;
     sa.hdr = (ScopeHeader*)ctx->arena;
-    CU(ctx, launch_select(sa, ctx->stream));
+    if (large)
+        CU(ctx, launch_vote_large(sa, (uint8_t*)ctx->arena + 4096, ctx->stream));
+    else
+        CU(ctx, launch_select(sa, ctx->stream));
     ScopeHeader h;
     CU(ctx, cudaMemcpyAsync(&h, sa.hdr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));

@@ -94,6 +94,7 @@ struct SelectArgs {
     // external winners / spans (bypass stages): used by the standalone APIs
     const uint32_t* winners_in;  // if non-null: skip the vote, use these n_winners_in
     uint32_t n_winners_in;
+    const uint32_t* n_winners_dev;  // if non-null: the winner count, read on the device
     const uint32_t* span_b_in;   // if non-null: skip vote + expand, use these spans
     const uint32_t* span_e_in;
     uint32_t n_spans_in;
@@ -109,6 +110,9 @@ struct SelectArgs {
 constexpr uint32_t kVoteMaxSmem = 8192;
 size_t select_smem_bytes(uint32_t n_cand, uint32_t k_prime);
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t s);
+// > kVoteMaxSmem candidates: device-wide radix-sort vote (vote_large.cu), then spans+scope
+size_t vote_large_workspace(uint32_t n_cand);
+cudaError_t launch_vote_large(const SelectArgs& a, void* workspace, cudaStream_t s);
 
 // ---- K4+K5: gather + RoPE + finite-scope attention (attend.hpp, engine.hpp:529-565)
 struct AttnArgs {

@@ -211,8 +211,10 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectArgs a)
         if (tid == 0) s_nw = nw;
         __syncthreads();
     } else if (have_winners) {
-        for (uint32_t j = tid; j < a.n_winners_in; j += blockDim.x) winners[j] = a.winners_in[j];
-        if (tid == 0) s_nw = a.n_winners_in;
+        const uint32_t nwin = a.n_winners_dev ? *a.n_winners_dev : a.n_winners_in;
+        if (winners != a.winners_in)
+            for (uint32_t j = tid; j < nwin; j += blockDim.x) winners[j] = a.winners_in[j];
+        if (tid == 0) s_nw = nwin;
         __syncthreads();
     }
 

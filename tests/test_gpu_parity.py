@@ -341,3 +341,26 @@ def test_fast_scan_1m_context(ctx):
     got = gpu_topk(ctx, q, 32, hk, 4, N.BF16, row0=g, count=ls - g)
     want = oracle_topk(q, 32, hk, 4, N.LANES_UNFUSED, row0=g, count=ls - g)
     assert_topk_equal(got, want, "1M")
+
+
+def test_vote_large_candidate_sets(ctx):
+    """> 8192 candidates (prefill): device radix-sort vote vs the oracle."""
+    rng = np.random.default_rng(7)
+    for n, span, kp in ((8193, 3000, 127), (20000, 500, 64), (131072, 100000, 127),
+                        (131072, 200, 512)):
+        idx = rng.integers(0, span, n).astype(np.uint64)
+        score = (rng.integers(0, 4000, n) / 2000.0 - 1.0).astype(np.float32)
+        want = ob.vote(idx, score, kp)
+        w = torch.zeros(kp, dtype=torch.int32, device="cuda")
+        nw = ctx.vote(dev(idx.astype(np.int32)), dev(score), kp, w)
+        assert np.array_equal(w.cpu().numpy()[:nw].astype(np.uint64), want), n
+
+
+def test_attend_step_prefill_chunk_large_vote(ctx):
+    """test_engine.cpp-style k = k' = 100 prefill chunk: 2 x 100 x 100 = 20,000 candidates."""
+    cfg = N.SelectionConfig(k=100, k_prime=100, span_m=16, l_global=16, l_local=256, l_chunk=128)
+    res, out, st, spans = step_vs_oracle(ctx, 2, 4, 16, 3000, cfg, N.F32, 600, 2048,
+                                         base=10000.0, n_q=100)
+    assert res.stats.scope_len == st.scope_len
+    assert np.array_equal(res.spans[0], spans[0])
+    assert np.abs(res.out.cpu().numpy() - out).max() <= ATTN_TOL
