@@ -49,6 +49,10 @@ typedef enum { REATTN_MODE_FULL = 0, REATTN_MODE_WINDOW = 1, REATTN_MODE_REATTEN
 /* Lane arithmetic of the fp32 score dot (dense_matrix.hpp:41-56); the reference compiles
  * `l += a*b` either unfused or as an FMA depending on compiler/ISA/d. */
 typedef enum { REATTN_LANES_UNFUSED = 0, REATTN_LANES_FMA = 1 } reattn_lanes;
+/* Prefill (n_q > 1) score scan: EXACT = CUDA-core path bit-identical to the reference
+ * (default); TENSOR = tcgen05 bf16 hi+lo GEMM with TMEM accumulators (selected indices
+ * equal up to the north_star ε-tie rule). */
+typedef enum { REATTN_PREFILL_EXACT = 0, REATTN_PREFILL_TENSOR = 1 } reattn_prefill_mode;
 
 /* selection.hpp:127-152 SelectionConfig (tile_size only bounds the reference's CPU scratch;
  * it never changes results and is ignored here). */
@@ -81,6 +85,7 @@ const char* reattn_last_error(const reattn_ctx* ctx);
 int reattn_ctx_set_stream(reattn_ctx* ctx, void* cuda_stream);
 void* reattn_ctx_stream(const reattn_ctx* ctx);
 int reattn_ctx_set_lanes(reattn_ctx* ctx, int lanes);
+int reattn_ctx_set_prefill(reattn_ctx* ctx, int prefill_mode);
 int reattn_ctx_synchronize(reattn_ctx* ctx);
 int reattn_ctx_num_sms(const reattn_ctx* ctx);
 /* device memory helpers for callers without their own allocator (the C++ shim) */

@@ -319,11 +319,16 @@ DecodeArgs plan_decode(const AttnArgs& a, uint32_t L_max, int num_sms) {
     DecodeArgs D;
     D.a = a;
     const int chunks = std::max(1, (int)((L_max + kDecChunk - 1) / kDecChunk));
-    // about two CTAs per SM over all kv heads, at most 8 chunks (256 rows) per CTA
     // one 32-row chunk per CTA keeps many small CTAs in flight (latency-bound phases);
-    // very long scopes fold several chunks into one CTA to bound the combine's fan-in
+    // very long scopes fold several chunks into one CTA to bound the combine's fan-in.
+    // REATTN_DEC_CPC overrides (tuning experiments).
     const int want = std::max(1, 16 * num_sms / std::max(1, a.n_kv));
     D.chunks_per_cta = std::min(8, std::max(1, (chunks + want - 1) / want));
+    static const int cpc_env = [] {
+        const char* e = std::getenv("REATTN_DEC_CPC");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (cpc_env > 0) D.chunks_per_cta = std::min(64, cpc_env);
     D.n_splits = (chunks + D.chunks_per_cta - 1) / D.chunks_per_cta;
     D.n_src = 1;
     return D;

@@ -314,6 +314,12 @@ int reattn_ctx_set_lanes(reattn_ctx* ctx, int lanes) {
     ctx->lanes = lanes;
     return REATTN_OK;
 }
+int reattn_ctx_set_prefill(reattn_ctx* ctx, int mode) {
+    if (mode != REATTN_PREFILL_EXACT && mode != REATTN_PREFILL_TENSOR)
+        return set_err(ctx, REATTN_EINVAL, "unknown prefill mode");
+    ctx->prefill = mode;
+    return REATTN_OK;
+}
 int reattn_ctx_synchronize(reattn_ctx* ctx) {
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     return REATTN_OK;
@@ -550,7 +556,8 @@ int reattn_fused_topk(reattn_ctx* ctx, const float* q_dev, uint64_t n_q, uint64_
     int rc = plan_scan(ctx, sp);
     if (rc) return rc;
     // fixed workspace: independent of `count` (the scratch contract, test_selection.cpp:228)
-    const size_t ws_fixed = scan_fast_workspace(a, ctx->num_sms);
+    // fixed workspace: independent of `count` (the scratch contract, test_selection.cpp:228)
+    const size_t ws_fixed = std::max(scan_fast_workspace(a, ctx->num_sms), sp.ws_bytes);
     if (scratch_bytes) *scratch_bytes = ws_fixed + n_q * n_kv * k * 8;
     if (count == 0 || n_q == 0) return REATTN_OK;
     rc = ensure_arena(ctx, ws_fixed + 256);

@@ -17,6 +17,7 @@ struct reattn_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int lanes = REATTN_LANES_UNFUSED;
+    int prefill = REATTN_PREFILL_EXACT;  // REATTN_PREFILL_TENSOR: tcgen05 scan for n_q > 1
     int num_sms = 148;
     std::string err;
     void* arena = nullptr;  // scratch for synchronous calls
@@ -110,11 +111,21 @@ inline int status_from_scope(reattn_ctx* ctx, int32_t e) {
 struct ScanPlan {
     ScanArgs a;
     bool fast = false;
+    bool tc = false;  // prefill on tcgen05 (opt-in, ε-tie parity)
     CUtensorMap map;
     size_t ws_bytes = 0;
 };
 
 inline int plan_scan(reattn_ctx* ctx, ScanPlan& sp) {
+    sp.tc = false;
+    if (ctx->prefill == REATTN_PREFILL_TENSOR && sp.a.n_q > 1 && prefill_tc_supported(sp.a) &&
+        make_key_tensor_map(&sp.map, sp.a.keys, sp.a.dtype, sp.a.d,
+                            (uint64_t)sp.a.n_kv * sp.a.head_stride, prefill_tc_key_box_rows())) {
+        sp.tc = true;
+        sp.fast = false;
+        sp.ws_bytes = prefill_tc_workspace(sp.a);
+        return REATTN_OK;
+    }
     sp.fast = scan_fast_supported(sp.a);
     sp.ws_bytes = 0;
     if (sp.fast) {
@@ -134,6 +145,10 @@ inline int plan_scan(reattn_ctx* ctx, ScanPlan& sp) {
 // entry points share the context arena, so they clear the ticket first (zero_ticket).
 inline int enqueue_scan(reattn_ctx* ctx, const ScanPlan& sp, void* ws, cudaStream_t s,
                         bool zero_ticket) {
+    if (sp.tc) {
+        CU(ctx, launch_prefill_tc(sp.a, sp.map, ws, s));
+        return REATTN_OK;
+    }
     if (sp.fast && zero_ticket) CU(ctx, cudaMemsetAsync(ws, 0, 256, s));
     if (sp.fast)
         CU(ctx, launch_scan_fast(sp.a, sp.map, ws, ctx->num_sms, s));

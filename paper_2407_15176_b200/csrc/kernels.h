@@ -74,6 +74,14 @@ bool make_key_tensor_map(CUtensorMap* map, const void* base, int dtype, uint64_t
                          uint64_t rows, int box_rows);
 int scan_fast_box_rows(int dtype);
 
+// Prefill path on tcgen05 (prefill_tc.cu): bf16 hi+lo split of the group-mean query, fp32
+// TMEM accumulation, fused register top-k.  d == 128, bf16 keys, k <= 8.  ε-tie parity.
+bool prefill_tc_supported(const ScanArgs& a);
+size_t prefill_tc_workspace(const ScanArgs& a);
+int prefill_tc_key_box_rows();
+cudaError_t launch_prefill_tc(const ScanArgs& a, const CUtensorMap& kmap, void* workspace,
+                              cudaStream_t s);
+
 // Generic path: any d, n_q, k (k <= kGenericMaxK), streaming threshold buffer + bitonic
 // compaction in shared memory; one CTA per (query, kv head).
 constexpr int kGenericMaxK = 7936;

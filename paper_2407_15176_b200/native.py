@@ -21,6 +21,7 @@ F32, BF16 = 0, 1
 SPAN_ALIGNED, SPAN_CENTERED = 0, 1
 MODE_FULL, MODE_WINDOW, MODE_REATTENTION = 0, 1, 2
 LANES_UNFUSED, LANES_FMA = 0, 1
+PREFILL_EXACT, PREFILL_TENSOR = 0, 1
 
 u64 = C.c_uint64
 vp = C.c_void_p
@@ -81,6 +82,7 @@ SIGNATURES = [
     ("reattn_ctx_set_stream", C.c_int, [vp, vp]),
     ("reattn_ctx_stream", vp, [vp]),
     ("reattn_ctx_set_lanes", C.c_int, [vp, C.c_int]),
+    ("reattn_ctx_set_prefill", C.c_int, [vp, C.c_int]),
     ("reattn_ctx_synchronize", C.c_int, [vp]),
     ("reattn_ctx_num_sms", C.c_int, [vp]),
     ("reattn_malloc", C.c_int, [vp, u64, C.POINTER(vp)]),
@@ -184,6 +186,10 @@ class Context:
 
     def set_lanes(self, lanes: int) -> None:
         self.check(self.lib.reattn_ctx_set_lanes(self.h, lanes))
+
+    def set_prefill(self, mode: int) -> None:
+        """PREFILL_EXACT (CUDA cores, bit-exact) or PREFILL_TENSOR (tcgen05, ε-tie)."""
+        self.check(self.lib.reattn_ctx_set_prefill(self.h, mode))
 
     @property
     def stream(self) -> int:
