@@ -40,6 +40,9 @@ struct StepPlan {
     size_t vote_ws_bytes = 0;
     void* vote_ws = nullptr;
     size_t part_bytes = 0;
+    bool attn_tc = false;     // prefill attention on tcgen05 (ctx prefill mode TENSOR)
+    size_t attn_tc_bytes = 0;
+    void* attn_tc_ws = nullptr;
     size_t scratch_bytes = 0;
     uint64_t kernels = 0;
 };
@@ -95,6 +98,8 @@ int plan_step(reattn_ctx* ctx, const reattn_cache* cache, const reattn_rope* rop
         int rc = plan_scan(ctx, P.scan);
         if (rc) return rc;
     }
+    P.attn_tc = (ctx->prefill & REATTN_PREFILL_TENSOR_ATTN) && n_q > 1 && cache->d == 128 &&
+                cache->dtype == kBF16;
     (void)out_dev;
     return REATTN_OK;
 }
@@ -143,6 +148,9 @@ void carve_step(StepPlan& P, const reattn_cache* cache, const reattn_rope* rope,
     AttnArgs a = step_attn_args(P, cache, rope, nullptr, nullptr);
     P.part_bytes = attend_workspace(a, std::max<uint32_t>(1, P.L_upper));
     P.part = c.take<double>(P.part_bytes / sizeof(double) + 1);
+    P.attn_tc = P.attn_tc && attend_tc_supported(a);
+    P.attn_tc_bytes = P.attn_tc ? attend_tc_workspace(a, std::max<uint32_t>(1, P.L_upper)) : 0;
+    P.attn_tc_ws = c.take<uint8_t>(P.attn_tc_bytes);
     P.entropy = c.take<double>(std::max<uint64_t>(1, P.n_q * P.n_head));
     P.vote_ws = c.take<uint8_t>(P.vote_ws_bytes);
     P.scratch_bytes = c.off;
@@ -214,8 +222,13 @@ int enqueue_step(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache, const 
     }
     if (P.n_q > 0) {
         AttnArgs a = step_attn_args(P, cache, rope, q_dev, out_dev);
-        CU(ctx, launch_attend(a, std::max<uint32_t>(1, P.L_upper), s));
-        P.kernels += attend_kernel_count(a, std::max<uint32_t>(1, P.L_upper));
+        if (P.attn_tc) {
+            CU(ctx, launch_attend_tc(a, std::max<uint32_t>(1, P.L_upper), P.attn_tc_ws, s));
+            P.kernels += 2;
+        } else {
+            CU(ctx, launch_attend(a, std::max<uint32_t>(1, P.L_upper), s));
+            P.kernels += attend_kernel_count(a, std::max<uint32_t>(1, P.L_upper));
+        }
     }
     return REATTN_OK;
 }
@@ -315,7 +328,7 @@ int reattn_ctx_set_lanes(reattn_ctx* ctx, int lanes) {
     return REATTN_OK;
 }
 int reattn_ctx_set_prefill(reattn_ctx* ctx, int mode) {
-    if (mode != REATTN_PREFILL_EXACT && mode != REATTN_PREFILL_TENSOR)
+    if (mode < REATTN_PREFILL_EXACT || mode > REATTN_PREFILL_TENSOR)
         return set_err(ctx, REATTN_EINVAL, "unknown prefill mode");
     ctx->prefill = mode;
     return REATTN_OK;

@@ -17,7 +17,7 @@ struct reattn_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int lanes = REATTN_LANES_UNFUSED;
-    int prefill = REATTN_PREFILL_EXACT;  // REATTN_PREFILL_TENSOR: tcgen05 scan for n_q > 1
+    int prefill = REATTN_PREFILL_EXACT;  // reattn_prefill_mode bits (tcgen05 scan / attention)
     int num_sms = 148;
     std::string err;
     void* arena = nullptr;  // scratch for synchronous calls
@@ -118,7 +118,7 @@ struct ScanPlan {
 
 inline int plan_scan(reattn_ctx* ctx, ScanPlan& sp) {
     sp.tc = false;
-    if (ctx->prefill == REATTN_PREFILL_TENSOR && sp.a.n_q > 1 && prefill_tc_supported(sp.a) &&
+    if ((ctx->prefill & REATTN_PREFILL_TENSOR_SCAN) && sp.a.n_q > 1 && prefill_tc_supported(sp.a) &&
         make_key_tensor_map(&sp.map, sp.a.keys, sp.a.dtype, sp.a.d,
                             (uint64_t)sp.a.n_kv * sp.a.head_stride, prefill_tc_key_box_rows())) {
         sp.tc = true;

@@ -147,6 +147,11 @@ constexpr int kAttnSplit = 64;
 size_t attend_workspace(const AttnArgs& a, uint32_t L_max);
 cudaError_t launch_attend(const AttnArgs& a, uint32_t L_max, cudaStream_t s);
 int attend_kernel_count(const AttnArgs& a, uint32_t L_max);
+// prefill attention on tcgen05 (attend_tc.cu): d == dv == 128, bf16 cache; bf16 hi+lo split
+// operands, fp32 TMEM accumulation (bf16 tolerance).  ws: attend_tc_workspace bytes.
+bool attend_tc_supported(const AttnArgs& a);
+size_t attend_tc_workspace(const AttnArgs& a, uint32_t L_max);
+cudaError_t launch_attend_tc(const AttnArgs& a, uint32_t L_max, void* ws, cudaStream_t s);
 // sharded decode halves (n_q == 1, d == 128): partial states, then the multi-source combine
 bool attend_decode_supported(const AttnArgs& a, uint32_t L_max);
 size_t attend_decode_partial_bytes(const AttnArgs& a, uint32_t L_max);  // per source
