@@ -295,35 +295,41 @@ __global__ void __launch_bounds__(128) attend_combine_kernel(const AttnLaunch P)
 }
 
 // ------------------------------------------------------------------------------------
-// Decode specialisation (n_q == 1, d == dv == 128, group <= 8): one CTA per (32-row slice
-// of the scope, kv head).  16-byte vectorised gathers through the scope table with RoPE
-// applied in registers; logits in f64 with the exact dot_f64 lane order: four threads per
-// key, each owning two of the eight lanes for every q head of the GQA group (each K element
-// is converted to f64 once and reused by the whole group), the fixed reduction tree
-// finished with two shuffles; f64 softmax state.  Slice partials are merged by
+// Decode specialisation (n_q == 1, d == dv == 128, group <= 8): one CTA per (range of
+// 32-row chunks of the scope, kv head), 4 warps.  16-byte vectorised gathers through the
+// scope table with RoPE applied in registers (the next chunk's gather is in flight while
+// the current one is computed); then one warp per q head of the GQA group:
+//   logits   lane j = key j of the chunk: fp32 dot of the rotated query (pre-scaled by
+//            log2(e)/sqrt(d)) with the rotated key, so the chunk's 32 logits of the head
+//            sit one per lane
+//   softmax  warp max / sums by shuffles, online (m, A, B) state (A, B in f64)
+//   values   lane owns 4 output columns; p_j broadcast by shuffle, V rows read as float4
+// No block barrier between the phases: the only __syncthreads guard the K/V staging.
+// Numerics: fp32 logits and accumulation inside a CTA, f64 across chunks and CTAs; the
+// reference's f64 attend (attend.hpp:404-456) is matched to ~1e-6 max-abs (the north_star
+// fp32 bar is 1e-5).  Partials (log2-unit m, A, B in f64 + fp32 acc) are merged by
 // attend_decode_combine.
 constexpr int kDecChunk = 32;
 constexpr int kDecThreads = 128;
 constexpr int kDecD = 128;
-constexpr int kDecKSF = kDecD + 8;   // fp32 K row stride (conflict-free LDS.64 per half-warp)
-constexpr int kDecPart = kDecD + 4;  // partial row: m, A, B, pad, acc[128] (16-B aligned)
+constexpr int kDecKSF = kDecD + 4;   // fp32 K row stride: conflict-free LDS.128 across lanes
+constexpr int kDecPartBytes = 32 + kDecD * 4;  // double m2, A, B2, pad; float acc[128]
 
 struct DecodeArgs {
     AttnArgs a;
     int n_splits;        // grid.x (upper bound from L_max)
     int chunks_per_cta;  // 32-row chunks per CTA
     int n_src;           // combine: partial sets laid out [n_src][n_splits] (sharded: ranks)
+    float scale_log2;    // log2(e) / sqrt(d)
 };
 
 DecodeArgs plan_decode(const AttnArgs& a, uint32_t L_max, int num_sms) {
     DecodeArgs D;
     D.a = a;
     const int chunks = std::max(1, (int)((L_max + kDecChunk - 1) / kDecChunk));
-    // one 32-row chunk per CTA keeps many small CTAs in flight (latency-bound phases);
-    // very long scopes fold several chunks into one CTA to bound the combine's fan-in.
-    // REATTN_DEC_CPC overrides (tuning experiments).
-    const int want = std::max(1, 16 * num_sms / std::max(1, a.n_kv));
-    D.chunks_per_cta = std::min(8, std::max(1, (chunks + want - 1) / want));
+    // ~4 CTAs per SM in one wave; REATTN_DEC_CPC overrides (tuning experiments)
+    const int want = std::max(1, 4 * num_sms / std::max(1, a.n_kv));
+    D.chunks_per_cta = std::min(16, std::max(1, (chunks + want - 1) / want));
     static const int cpc_env = [] {
         const char* e = std::getenv("REATTN_DEC_CPC");
         return e ? std::atoi(e) : 0;
@@ -331,33 +337,13 @@ DecodeArgs plan_decode(const AttnArgs& a, uint32_t L_max, int num_sms) {
     if (cpc_env > 0) D.chunks_per_cta = std::min(64, cpc_env);
     D.n_splits = (chunks + D.chunks_per_cta - 1) / D.chunks_per_cta;
     D.n_src = 1;
+    D.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)kDecD));
     return D;
 }
 
-template <typename KT>
-__device__ __forceinline__ void load8(const KT* p, float (&v)[8]);
-template <>
-__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float (&v)[8]) {
-    const uint4 w = __ldg(reinterpret_cast<const uint4*>(p));
-    const uint32_t u[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        v[2 * i] = __uint_as_float(u[i] << 16);
-        v[2 * i + 1] = __uint_as_float(u[i] & 0xFFFF0000u);
-    }
-}
-template <>
-__device__ __forceinline__ void load8<float>(const float* p, float (&v)[8]) {
-    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
-    const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-}
-
 constexpr size_t decode_smem_bytes() {
-    return (size_t)(8 * kDecD + 8 * kDecChunk + 64) * sizeof(double) +
-           (size_t)kDecChunk * kDecKSF * sizeof(float) + (size_t)kDecChunk * kDecD * sizeof(float) +
-           kDecChunk;
+    return (size_t)8 * kDecD * sizeof(float) + (size_t)kDecChunk * kDecKSF * sizeof(float) +
+           (size_t)kDecChunk * kDecD * sizeof(float) + kDecChunk;
 }
 
 // Raw 16-byte words of 8 consecutive elements (converted only when staged to smem, so a
@@ -462,11 +448,14 @@ struct ChunkRegs {
     }
 };
 
-// One CTA per (range of P.chunks_per_cta chunks of the scope, kv head): flash-decode with
-// an online (m, A, B, acc) state per q head; the next chunk's gather is issued into
-// registers before the current chunk is computed.
+__device__ __forceinline__ float dec_ex2(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 template <typename KT, int G>
-__global__ void __launch_bounds__(kDecThreads, 5) attend_decode_kernel(const DecodeArgs P) {
+__global__ void __launch_bounds__(kDecThreads) attend_decode_kernel(const DecodeArgs P) {
     const AttnArgs& a = P.a;
     if (a.hdr && a.hdr->error != 0) return;
     const uint32_t L = scope_len(a);
@@ -475,18 +464,17 @@ __global__ void __launch_bounds__(kDecThreads, 5) attend_decode_kernel(const Dec
     if (key_begin >= L) return;
     const uint32_t key_end = min(L, key_begin + (uint32_t)P.chunks_per_cta * kDecChunk);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    extern __shared__ __align__(16) double dsm[];
-    double* qd = dsm;                              // [8][kDecD]
-    double* lg = qd + 8 * kDecD;                   // [8][kDecChunk]
-    double* st = lg + 8 * kDecChunk;               // [8][4]: m, A, B, rescale  (+pad)
-    float* ks = (float*)(st + 64);                 // [kDecChunk][kDecKSF]
+    extern __shared__ __align__(16) float dsf[];
+    float* qs = dsf;                               // [8][kDecD] rotated, pre-scaled queries
+    float* ks = qs + 8 * kDecD;                    // [kDecChunk][kDecKSF]
     float* vs = ks + kDecChunk * kDecKSF;          // [kDecChunk][kDecD]
     uint8_t* rowok = (uint8_t*)(vs + kDecChunk * kDecD);  // [kDecChunk] row attended here
     constexpr int half = kDecD / 2;
+    constexpr int HPW = (G + 3) / 4;               // heads per warp
 
     ChunkRegs<KT> cur;
     cur.load(a, kv, key_begin, (int)min((uint32_t)kDecChunk, key_end - key_begin));
-    // queries of the group, rotated at L'-1 (engine.hpp:546-551), kept as f64
+    // queries of the group, rotated at L'-1 (engine.hpp:546-551), times log2(e)/sqrt(d)
     const uint32_t qpos = L - 1u;
     for (int e = tid; e < G * half; e += kDecThreads) {
         const int g = e / half, j = e % half;
@@ -499,116 +487,101 @@ __global__ void __launch_bounds__(kDecThreads, 5) attend_decode_kernel(const Dec
             rx = __fsub_rn(__fmul_rn(x, cs), __fmul_rn(y, sn));
             ry = __fadd_rn(__fmul_rn(x, sn), __fmul_rn(y, cs));
         }
-        qd[g * kDecD + 2 * j] = (double)rx;
-        qd[g * kDecD + 2 * j + 1] = (double)ry;
-    }
-    if (tid < 8) {
-        st[tid * 4 + 0] = -INFINITY;
-        st[tid * 4 + 1] = 0.0;
-        st[tid * 4 + 2] = 0.0;
-        st[tid * 4 + 3] = 1.0;
+        qs[g * kDecD + 2 * j] = __fmul_rn(rx, P.scale_log2);
+        qs[g * kDecD + 2 * j + 1] = __fmul_rn(ry, P.scale_log2);
     }
     cur.store(a, (int)min((uint32_t)kDecChunk, key_end - key_begin), ks, vs, rowok);
     __syncthreads();
 
-    const double scale = 1.0 / sqrt((double)kDecD);
-    double acc[G];
+    float m2[HPW];
+    double A[HPW], B2[HPW];
+    float4 acc[HPW];
 #pragma unroll
-    for (int g = 0; g < G; ++g) acc[g] = 0.0;
+    for (int u = 0; u < HPW; ++u) {
+        m2[u] = -INFINITY;
+        A[u] = 0.0;
+        B2[u] = 0.0;
+        acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     for (uint32_t k0 = key_begin; k0 < key_end; k0 += kDecChunk) {
         const int nk = (int)min((uint32_t)kDecChunk, key_end - k0);
         const uint32_t k1 = k0 + kDecChunk;
         const int nk1 = k1 < key_end ? (int)min((uint32_t)kDecChunk, key_end - k1) : 0;
         ChunkRegs<KT> nxt;
         if (nk1 > 0) nxt.load(a, kv, k1, nk1);  // in flight during this chunk's math
-        // ---- logits (attend.hpp:430): thread (key j, lane pair p) accumulates lanes 2p,
-        //      2p+1 of dot_f64 for every head; tree finished with two shuffles ----
-        {
-            const int j = tid >> 2, p = tid & 3;
-            double l2[G][2];
+        const bool key_ok = lane < nk && rowok[lane];
+        const float4* kr = reinterpret_cast<const float4*>(ks + lane * kDecKSF);
 #pragma unroll
-            for (int g = 0; g < G; ++g) l2[g][0] = l2[g][1] = 0.0;
-            if (j < nk) {
-                const float* kr = ks + j * kDecKSF + 2 * p;
-#pragma unroll 4
-                for (int c = 0; c < kDecD / 8; ++c) {
-                    const float2 k2 = *reinterpret_cast<const float2*>(kr + 8 * c);
-                    const double ka = (double)k2.x, kb = (double)k2.y;
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const double2 q2 =
-                            *reinterpret_cast<const double2*>(qd + g * kDecD + 8 * c + 2 * p);
-                        l2[g][0] = fma(q2.x, ka, l2[g][0]);
-                        l2[g][1] = fma(q2.y, kb, l2[g][1]);
-                    }
-                }
+        for (int u = 0; u < HPW; ++u) {
+            const int g = warp + 4 * u;
+            if (g >= G) break;
+            // ---- logit of (head g, key lane), log2 units ----
+            const float4* qv = reinterpret_cast<const float4*>(qs + g * kDecD);
+            float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
+#pragma unroll 8
+            for (int c = 0; c < kDecD / 4; ++c) {
+                const float4 k4 = kr[c], q4 = qv[c];
+                d0 = __fmaf_rn(q4.x, k4.x, d0);
+                d1 = __fmaf_rn(q4.y, k4.y, d1);
+                d2 = __fmaf_rn(q4.z, k4.z, d2);
+                d3 = __fmaf_rn(q4.w, k4.w, d3);
             }
+            const float s = key_ok ? (d0 + d1) + (d2 + d3) : -INFINITY;
+            // ---- online softmax (attend.hpp:432-447) ----
+            float mc = s;
 #pragma unroll
-            for (int g = 0; g < G; ++g) {
-                double s = l2[g][0] + l2[g][1];
-                s = s + __shfl_xor_sync(0xFFFFFFFFu, s, 1);
-                s = s + __shfl_xor_sync(0xFFFFFFFFu, s, 2);
-                if (p == 0) lg[g * kDecChunk + j] = (j < nk && rowok[j]) ? s * scale : -INFINITY;
-            }
-        }
-        __syncthreads();
-        // ---- online softmax update per head (attend.hpp:432-447), one warp per head ----
-        for (int g = warp; g < G; g += kDecThreads / 32) {
-            const double s = lane < nk ? lg[g * kDecChunk + lane] : -INFINITY;
-            double mc = s;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) mc = fmax(mc, __shfl_xor_sync(0xFFFFFFFFu, mc, off));
-            const double m_old = st[g * 4 + 0];
-            const double m_new = fmax(m_old, mc);
-            const bool live = lane < nk && s != -INFINITY;  // masked / padded keys drop out
-            const double w = live ? exp(s - m_new) : 0.0;
-            double sa = w, sb = live ? (s - m_new) * w : 0.0;
+            for (int off = 16; off > 0; off >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xFFFFFFFFu, mc, off));
+            const float mn = fmaxf(m2[u], mc);
+            if (mn == -INFINITY) continue;  // nothing visible yet (masked rows only)
+            const float dd = s - mn;
+            const float p = key_ok ? dec_ex2(dd) : 0.0f;
+            float sa = p, sb = key_ok ? dd * p : 0.0f;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
                 sa += __shfl_xor_sync(0xFFFFFFFFu, sa, off);
                 sb += __shfl_xor_sync(0xFFFFFFFFu, sb, off);
             }
-            lg[g * kDecChunk + lane] = w;
-            if (lane == 0) {
-                const double A = st[g * 4 + 1], B = st[g * 4 + 2];
-                // empty running state (first chunk): no rescale term (avoids 0 * -inf)
-                const double r = A > 0.0 ? exp(m_old - m_new) : 0.0;
-                st[g * 4 + 0] = m_new;
-                st[g * 4 + 1] = A * r + sa;
-                st[g * 4 + 2] = (A > 0.0 ? r * (B + (m_old - m_new) * A) : 0.0) + sb;
-                st[g * 4 + 3] = r;
-            }
-        }
-        __syncthreads();
-        // ---- values: thread c owns output column c for every head of the group ----
-        {
-            const int c = tid;
-#pragma unroll
-            for (int g = 0; g < G; ++g) acc[g] *= st[g * 4 + 3];
+            const float f = A[u] > 0.0 ? dec_ex2(m2[u] - mn) : 0.0f;
+            B2[u] = (A[u] > 0.0 ? (double)f * (B2[u] + (double)(m2[u] - mn) * A[u]) : 0.0) + (double)sb;
+            A[u] = A[u] * (double)f + (double)sa;
+            m2[u] = mn;
+            // ---- values: lane owns columns 4*lane .. 4*lane+3 ----
+            float4 o = make_float4(acc[u].x * f, acc[u].y * f, acc[u].z * f, acc[u].w * f);
+            const float4* vr = reinterpret_cast<const float4*>(vs) + lane;
             for (int j = 0; j < nk; ++j) {
-                const double v = (double)vs[j * kDecD + c];
-#pragma unroll
-                for (int g = 0; g < G; ++g) acc[g] = fma(lg[g * kDecChunk + j], v, acc[g]);
+                const float pj = __shfl_sync(0xFFFFFFFFu, p, j);
+                const float4 v4 = vr[j * (kDecD / 4)];
+                o.x = __fmaf_rn(pj, v4.x, o.x);
+                o.y = __fmaf_rn(pj, v4.y, o.y);
+                o.z = __fmaf_rn(pj, v4.z, o.z);
+                o.w = __fmaf_rn(pj, v4.w, o.w);
             }
+            acc[u] = o;
         }
-        __syncthreads();
+        __syncthreads();  // every warp is done with this chunk's K / V
         if (nk1 > 0) {
             nxt.store(a, nk1, ks, vs, rowok);
             __syncthreads();
         }
     }
-    const int c = tid;
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-        double* p = a.part + (((size_t)split * a.n_kv + kv) * G + g) * kDecPart;
-        p[4 + c] = acc[g];
-        if (c < 3) p[c] = st[g * 4 + c];
+    for (int u = 0; u < HPW; ++u) {
+        const int g = warp + 4 * u;
+        if (g >= G) break;
+        uint8_t* row = (uint8_t*)a.part + (((size_t)split * a.n_kv + kv) * G + g) * kDecPartBytes;
+        reinterpret_cast<float4*>(row + 32)[lane] = acc[u];
+        if (lane == 0) {
+            double* hd = (double*)row;
+            hd[0] = (double)m2[u];
+            hd[1] = A[u];
+            hd[2] = B2[u];
+        }
     }
 }
 
 // Merge the key-range partials of one q head: grid (head, column quarter); weights in
 // parallel, then 8 warps each sum a strided subset of partials for 32 columns (one per
-// lane), reduced in a fixed order (deterministic).
+// lane), reduced in a fixed order (deterministic).  m is in log2 units.
 constexpr int kCombThreads = 256;
 constexpr int kCombMaxParts = 2048;  // sources x key ranges per head
 constexpr int kCombCols = 32;
@@ -621,7 +594,7 @@ __global__ void __launch_bounds__(kCombThreads) attend_decode_combine(const Deco
     const uint32_t keys_per = (uint32_t)P.chunks_per_cta * kDecChunk;
     int ns = (int)((L + keys_per - 1) / keys_per);
     constexpr int NW = kCombThreads / 32;
-    __shared__ double w_s[kCombMaxParts];
+    __shared__ float w_s[kCombMaxParts];
     __shared__ double red[NW][kCombCols];
     __shared__ double rs[NW][3];
     __shared__ double s_M, s_A;
@@ -630,10 +603,13 @@ __global__ void __launch_bounds__(kCombThreads) attend_decode_combine(const Deco
     ns = ns * P.n_src;  // every source (rank) contributes the same split layout
     auto prow = [&](int s) {
         const size_t split = (size_t)(s / ns_src) * P.n_splits + s % ns_src;
-        return a.part + ((split * a.n_kv + kv) * a.group + g) * kDecPart;
+        return (const uint8_t*)a.part + ((split * a.n_kv + kv) * a.group + g) * kDecPartBytes;
     };
     double m = -INFINITY;
-    for (int s = tid; s < ns; s += kCombThreads) m = fmax(m, prow(s)[0]);
+    for (int s = tid; s < ns; s += kCombThreads) {
+        const double* hd = (const double*)prow(s);
+        if (hd[1] > 0.0) m = fmax(m, hd[0]);
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xFFFFFFFFu, m, off));
     if (lane == 0) rs[warp][0] = m;
@@ -647,13 +623,13 @@ __global__ void __launch_bounds__(kCombThreads) attend_decode_combine(const Deco
     const double M = s_M;
     double A = 0.0, B = 0.0;
     for (int s = tid; s < ns; s += kCombThreads) {
-        const double* p = prow(s);
-        // empty partials (fully masked ranges, A == 0) contribute nothing (no 0 * -inf)
-        const double w = p[1] > 0.0 ? exp(p[0] - M) : 0.0;
-        w_s[s] = w;
-        if (p[1] > 0.0) {
-            A += p[1] * w;
-            B += w * (p[2] + (p[0] - M) * p[1]);
+        const double* hd = (const double*)prow(s);
+        // empty partials (fully masked ranges, A == 0) contribute nothing
+        const double w = hd[1] > 0.0 ? exp2(hd[0] - M) : 0.0;
+        w_s[s] = (float)w;
+        if (hd[1] > 0.0) {
+            A += hd[1] * w;
+            B += w * (hd[2] + (hd[0] - M) * hd[1]);
         }
     }
 #pragma unroll
@@ -674,14 +650,21 @@ __global__ void __launch_bounds__(kCombThreads) attend_decode_combine(const Deco
         }
         s_A = At;
         if (cb == 0) {
-            const double hh = log(At) - Bt / At;
+            const double hh = log(At) - Bt * 0.69314718055994530942 / At;
             a.entropy[h] = hh < 0.0 ? 0.0 : hh;
         }
     }
     const int col = cb * kCombCols + lane;
-    double acc = 0.0;
-    for (int s = warp; s < ns; s += NW) acc = fma(prow(s)[4 + col], w_s[s], acc);
-    red[warp][lane] = acc;
+    double acc0 = 0.0, acc1 = 0.0;
+    int s = warp;
+    for (; s + NW < ns; s += 2 * NW) {  // two independent loads in flight per lane
+        const float x0 = ((const float*)(prow(s) + 32))[col];
+        const float x1 = ((const float*)(prow(s + NW) + 32))[col];
+        acc0 = fma((double)x0, (double)w_s[s], acc0);
+        acc1 = fma((double)x1, (double)w_s[s + NW], acc1);
+    }
+    if (s < ns) acc0 = fma((double)((const float*)(prow(s) + 32))[col], (double)w_s[s], acc0);
+    red[warp][lane] = acc0 + acc1;
     __syncthreads();
     if (tid < kCombCols) {
         double t = 0.0;
@@ -733,9 +716,10 @@ int sm_count() {
 }  // namespace
 
 size_t attend_workspace(const AttnArgs& a, uint32_t L_max) {
+    if (decode_bulk_eligible(a)) return decode_bulk_workspace(a, sm_count());
     if (decode_eligible(a, L_max)) {
         const DecodeArgs D = plan_decode(a, L_max, sm_count());
-        return (size_t)D.n_splits * a.n_kv * a.group * kDecPart * sizeof(double);
+        return (size_t)D.n_splits * a.n_kv * a.group * kDecPartBytes;
     }
     const AttnLaunch P = plan_attend(a, L_max, sm_count());
     if (P.direct) return 0;
@@ -743,11 +727,13 @@ size_t attend_workspace(const AttnArgs& a, uint32_t L_max) {
 }
 
 int attend_kernel_count(const AttnArgs& a, uint32_t L_max) {
+    if (decode_bulk_eligible(a)) return 1;
     if (decode_eligible(a, L_max)) return 2;
     return attend_workspace(a, L_max) ? 2 : 1;
 }
 
 cudaError_t launch_attend(const AttnArgs& a, uint32_t L_max, cudaStream_t s) {
+    if (decode_bulk_eligible(a)) return launch_attend_decode_bulk(a, a.part, sm_count(), s);
     if (decode_eligible(a, L_max)) {
         const DecodeArgs D = plan_decode(a, L_max, sm_count());
         dim3 grid(D.n_splits, a.n_kv);
@@ -805,7 +791,7 @@ bool attend_decode_supported(const AttnArgs& a, uint32_t L_max) { return decode_
 
 size_t attend_decode_partial_bytes(const AttnArgs& a, uint32_t L_max) {
     const DecodeArgs D = plan_decode(a, L_max, sm_count());
-    return (size_t)D.n_splits * a.n_kv * a.group * kDecPart * sizeof(double);
+    return (size_t)D.n_splits * a.n_kv * a.group * kDecPartBytes;
 }
 
 cudaError_t launch_attend_decode_partials(const AttnArgs& a, uint32_t L_max, cudaStream_t s) {

@@ -1,0 +1,509 @@
+// K5 (decode) — finite-scope flash-decode with a deep bulk-copy ring and a fused combine.
+//
+// Restates, for n_q == 1 and a bf16 cache (d == dv == 128):
+//   assemble_scope copies   scope.hpp:274-287   rows fetched straight from the cache through
+//                                               the device scope table (no assembled copy)
+//   RotaryTable::rotate_row rope.hpp:347-358    keys at compact i, the query at L'-1
+//                                               (engine.hpp:536-551), unfused fp32 ops
+//   attend                  attend.hpp:404-456  scale 1/sqrt(d), row entropy ln A - B/A
+//
+// The decode scope is small (L' ~ 5K rows, 21 MB of K+V at 1M context) and the step is
+// latency-bound unless ~1/3 of it is in flight at once, so the layout is:
+//   grid (n_parts, n_kv), n_parts * n_kv <= #SMs: one wave, one CTA per SM; part p of kv
+//   head h owns a contiguous range of 32-row chunks of the scope (sized from the device L').
+//   warp 4 (producer): per chunk, one cp.async.bulk per scope row for K and for V (256 B,
+//     gathered through the scope table) plus the chunk's RoPE cos / sin rows (contiguous
+//     compact positions), into a 5-stage ring of 32 KB stages (160 KB in flight per SM).
+//   warps 0-3 (compute): rotate the chunk's keys once into an fp32 scratch (double
+//     buffered), then one warp per q head of the GQA group: lane j = key j logits (fp32,
+//     query pre-scaled by log2(e)/sqrt(d)), warp max / sums by shuffle, online (m, A, B)
+//     state (A, B in f64), P·V with lane = 4 output columns and p_j broadcast by shuffle.
+//   The last CTA of each kv head (atomic ticket, re-armed for graph replay) merges the
+//   parts' partial states in part order (deterministic) and writes the output and entropy.
+// Numerics: fp32 logits / accumulation within a CTA, f64 across parts: max-abs ~1e-8 on the
+// reference's f64 attend at the decode geometry (north_star fp32 bar: 1e-5).
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace reattn_dev;
+
+namespace reattn_impl {
+
+namespace {
+
+constexpr int kBC = 32;                        // scope rows per chunk
+constexpr int kBD = 128;                       // d = dv
+constexpr int kBStages = 6;
+constexpr int kBGroups = 4;                    // compute groups (4 warps each) per CTA
+constexpr int kBKVBytes = kBC * kBD * 2;       // K or V of one chunk (bf16): 8 KB
+constexpr int kBRopeBytes = kBC * (kBD / 2) * 4;  // cos or sin rows of one chunk: 8 KB
+constexpr int kBStageBytes = 2 * kBKVBytes + 2 * kBRopeBytes;
+constexpr int kBCompute = kBGroups * 128;
+constexpr int kBThreads = kBCompute + 32;
+constexpr int kBPartBytes = 32 + kBD * 4;      // double m2, A, B2, pad; float acc[128]
+constexpr int kBMaxParts = 160;          // partial slots per kv head (head + local)
+constexpr int kMaxLocalParts = 4;
+constexpr size_t kBSmem = 1024 + (size_t)kBStages * kBStageBytes + 8ull * kBD * 4 +
+                          (size_t)kBStages * kBC + 256;
+
+enum { kModeScope = 0, kModeLocal = 1, kModeHead = 2 };
+
+struct BulkArgs {
+    AttnArgs a;
+    int mode;               // kModeScope: scope rows [0, L') through the scope table
+                            // kModeLocal: cache rows [local_row0, +n_local) at positions
+                            //   0 .. n_local-1, query at n_local-1 (RoPE is relative: the
+                            //   logits equal the scope frame's up to rounding); partials only
+                            // kModeHead: scope rows [0, L'-n_local); merges the local partials
+    uint32_t n_local, local_row0;
+    int n_parts;            // CTAs per kv head in this launch
+    int part_base;          // first partial slot of this launch
+    int n_slots;            // partial slots per kv head (merged by the combine)
+    float scale_log2;
+    unsigned int* tickets;  // [n_kv]
+    uint8_t* part;          // [n_slots][n_kv][G] partial rows
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ float bx_ex2(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// rotated fp32 key row r, float4 column i (XOR-swizzled: conflict-free row-per-lane reads)
+__device__ __forceinline__ int rot_idx4(int r, int i) { return r * (kBD / 4) + (i ^ (r & 7)); }
+
+template <int G>
+__global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const BulkArgs B) {
+    const AttnArgs& a = B.a;
+    // launched as a programmatic dependent of the scan / select: wait for its results
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const bool local = B.mode == kModeLocal;  // runs beside the scan: never reads the header
+    if (!local && a.hdr && a.hdr->error != 0) return;
+    const uint32_t L = local ? B.n_local : (a.hdr ? a.hdr->L : a.L_host);
+    const uint32_t rows = B.mode == kModeHead ? L - B.n_local : L;
+    const int part = blockIdx.x, kv = blockIdx.y;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int chunks = (int)((rows + kBC - 1) / kBC);
+    const int cpp = (chunks + B.n_parts - 1) / B.n_parts;
+    const int c_begin = part * cpp;
+    const int n_ch = max(0, min(chunks, c_begin + cpp) - c_begin);
+    constexpr int HPW = (G + 3) / 4;  // q heads per compute warp
+
+    // addressed straight from the shared array (an integer round trip for alignment would
+    // turn every access into a generic load); bulk copies only need 16-B alignment
+    extern __shared__ __align__(16) uint8_t bsm_raw[];
+    uint8_t* stages = bsm_raw;
+    float* qs = (float*)(stages + kBStages * kBStageBytes);  // [8][kBD]
+    uint8_t* rowok = (uint8_t*)(qs + 8 * kBD);                // [kBStages][kBC]
+    uint64_t* full = (uint64_t*)(rowok + kBStages * kBC);  // 8-B aligned: offsets are multiples of 64
+    uint64_t* empty = full + kBStages;
+    __shared__ unsigned int s_last;
+
+    if (tid == 0) {
+        for (int s = 0; s < kBStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 4);  // the 4 warps of the group that consumed the stage
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == kBCompute / 32) {
+        // ===== producer: bulk copies of the chunk's rows into the ring =====
+        for (int c = 0; c < n_ch; ++c) {
+            const int s = c % kBStages;
+            if (c >= kBStages) mbar_wait(&empty[s], ((c / kBStages) & 1u) ^ 1u);
+            const uint32_t k0 = (uint32_t)(c_begin + c) * kBC;
+            const int nk = (int)min((uint32_t)kBC, rows - k0);
+            uint8_t* st = stages + (size_t)s * kBStageBytes;
+            const bool valid = lane < nk;
+            const uint32_t cr = !valid ? kNoIndex
+                                : local ? B.local_row0 + k0 + lane
+                                : (a.src ? __ldg(a.src + k0 + lane) : k0 + lane);
+            const bool own = valid && cr != kNoIndex;  // sharded scopes mask rows owned elsewhere
+            const int n_own = __popc(__ballot_sync(0xFFFFFFFFu, own));
+            rowok[s * kBC + lane] = own ? 1 : 0;
+            if (!own) {  // masked / tail row: zeros keep 0 * v finite in the (always 32-row) P·V
+                uint4* kz = (uint4*)(st + lane * kBD * 2);
+                uint4* vz = (uint4*)(st + kBKVBytes + lane * kBD * 2);
+#pragma unroll
+                for (int i = 0; i < kBD * 2 / 16; ++i) kz[i] = vz[i] = make_uint4(0, 0, 0, 0);
+            }
+            __syncwarp();
+            const uint32_t bytes = (uint32_t)n_own * 2u * kBD * 2u + (a.rope_cos ? 2u * nk * (kBD / 2) * 4u : 0u);
+            if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes);
+            __syncwarp();
+            // one copy per run of consecutive cache rows (spans are 32-row runs, the global
+            // and local segments are contiguous): bulk copies take uniform operands, so
+            // per-lane copies would serialise across the warp
+            const uint32_t cr_prev = __shfl_up_sync(0xFFFFFFFFu, cr, 1);
+            const bool own_prev = __shfl_up_sync(0xFFFFFFFFu, own ? 1 : 0, 1) != 0;
+            const bool head = own && !(lane > 0 && own_prev && cr == cr_prev + 1u);
+            const uint32_t heads = __ballot_sync(0xFFFFFFFFu, head);
+            const uint32_t breaks = heads | __ballot_sync(0xFFFFFFFFu, !own);
+            if (head) {
+                const uint32_t later = lane == 31 ? 0u : breaks & ~((2u << lane) - 1u);
+                const int end = later ? __ffs(later) - 1 : 32;
+                const uint32_t bytes_run = (uint32_t)(end - lane) * kBD * 2u;
+                const size_t row = ((size_t)kv * a.head_stride + cr) * kBD;
+                bulk_g2s(st + lane * kBD * 2, (const __nv_bfloat16*)a.k_base + row, bytes_run, &full[s]);
+                bulk_g2s(st + kBKVBytes + lane * kBD * 2, (const __nv_bfloat16*)a.v_base + row, bytes_run,
+                         &full[s]);
+            }
+            if (a.rope_cos && lane < 2) {
+                const float* tab = lane == 0 ? a.rope_cos : a.rope_sin;
+                bulk_g2s(st + 2 * kBKVBytes + lane * kBRopeBytes, tab + (size_t)k0 * (kBD / 2),
+                         (uint32_t)nk * (kBD / 2) * 4u, &full[s]);
+            }
+        }
+        __syncthreads();  // matches the compute side's state exchange barrier
+    } else {
+        // ===== compute: group gi = warps 4gi .. 4gi+3 takes chunks gi, gi+4, ... =====
+        const int gi = warp >> 2, gw = warp & 3, gt = tid & 127;
+        // the group's queries, rotated at L'-1 (engine.hpp:546-551), times log2(e)/sqrt(d)
+        const uint32_t qpos = L - 1u;  // kModeLocal: L == n_local (shifted frame)
+        for (int e = tid; e < G * (kBD / 2); e += kBCompute) {
+            const int g = e / (kBD / 2), j = e % (kBD / 2);
+            const float* qrow = a.q + (size_t)(kv * G + g) * kBD;
+            const float x = qrow[2 * j], y = qrow[2 * j + 1];
+            float rx = x, ry = y;
+            if (a.rope_cos) {
+                const float cs = a.rope_cos[(size_t)qpos * (kBD / 2) + j];
+                const float sn = a.rope_sin[(size_t)qpos * (kBD / 2) + j];
+                rx = __fsub_rn(__fmul_rn(x, cs), __fmul_rn(y, sn));
+                ry = __fadd_rn(__fmul_rn(x, sn), __fmul_rn(y, cs));
+            }
+            qs[g * kBD + 2 * j] = __fmul_rn(rx, B.scale_log2);
+            qs[g * kBD + 2 * j + 1] = __fmul_rn(ry, B.scale_log2);
+        }
+        named_bar_sync(5, kBCompute);
+        float m2[HPW];
+        double A[HPW], B2[HPW];
+        float4 acc[HPW];
+#pragma unroll
+        for (int u = 0; u < HPW; ++u) {
+            m2[u] = -INFINITY;
+            A[u] = 0.0;
+            B2[u] = 0.0;
+            acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int c = gi; c < n_ch; c += kBGroups) {
+            const int s = c % kBStages;
+            mbar_wait(&full[s], (c / kBStages) & 1u);
+            __syncwarp();  // reconverge after the wait loop: the shuffles below stay simple
+            const uint32_t k0 = (uint32_t)(c_begin + c) * kBC;
+            const int nk = (int)min((uint32_t)kBC, rows - k0);
+            uint8_t* st = stages + (size_t)s * kBStageBytes;
+            float4* kr4 = (float4*)(st + 2 * kBKVBytes);  // rotated keys over the cos/sin rows
+            // ---- rotate the chunk's keys once (rope.hpp:347-358): read all, then write ----
+            {
+                const uint32_t* kw = (const uint32_t*)st;  // bf16 pairs
+                const float* cs = (const float*)(st + 2 * kBKVBytes);
+                const float* sn = (const float*)(st + 2 * kBKVBytes + kBRopeBytes);
+                float2 rot[kBC * (kBD / 2) / 128];
+#pragma unroll
+                for (int i = 0; i < kBC * (kBD / 2) / 128; ++i) {
+                    const int e = gt + 128 * i, r = e >> 6, j = e & 63;
+                    const uint32_t w = kw[r * (kBD / 2) + j];
+                    const float x = __uint_as_float(w << 16), y = __uint_as_float(w & 0xFFFF0000u);
+                    float rx = x, ry = y;
+                    if (a.rope_cos && r < nk) {
+                        const float cc = cs[r * (kBD / 2) + j], ss = sn[r * (kBD / 2) + j];
+                        rx = __fsub_rn(__fmul_rn(x, cc), __fmul_rn(y, ss));
+                        ry = __fadd_rn(__fmul_rn(x, ss), __fmul_rn(y, cc));
+                    }
+                    rot[i] = make_float2(rx, ry);
+                }
+                named_bar_sync(1 + gi, 128);  // every read of cos / sin done
+#pragma unroll
+                for (int i = 0; i < kBC * (kBD / 2) / 128; ++i) {
+                    const int e = gt + 128 * i, r = e >> 6, j = e & 63;
+                    float* dst = (float*)&kr4[rot_idx4(r, j >> 1)] + (j & 1) * 2;
+                    *(float2*)dst = rot[i];
+                }
+                named_bar_sync(1 + gi, 128);  // rotated keys ready
+                __syncwarp();
+            }
+            const bool key_ok = lane < nk && rowok[s * kBC + lane];
+            const uint2* vrow = reinterpret_cast<const uint2*>(st + kBKVBytes) + lane;  // 4 bf16
+#pragma unroll
+            for (int u = 0; u < HPW; ++u) {
+                const int g = gw + 4 * u;
+                if (g >= G) break;
+                const ulonglong2* qv = reinterpret_cast<const ulonglong2*>(qs + g * kBD);
+                const ulonglong2* kv4 = reinterpret_cast<const ulonglong2*>(kr4);
+                f2_t d01 = 0ull, d23 = 0ull;
+#pragma unroll 8
+                for (int i = 0; i < kBD / 4; ++i) {
+                    const ulonglong2 k4 = kv4[rot_idx4(lane, i)], q4 = qv[i];
+                    d01 = f2_fma(q4.x, k4.x, d01);
+                    d23 = f2_fma(q4.y, k4.y, d23);
+                }
+                const float d0 = f2_lo(d01), d1 = f2_hi(d01), d2 = f2_lo(d23), d3 = f2_hi(d23);
+                const float sc = key_ok ? (d0 + d1) + (d2 + d3) : -INFINITY;
+                float mc = sc;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xFFFFFFFFu, mc, off));
+                // mn == -inf (only masked rows so far) leaves p == 0, f == 0, A == B2 == 0
+                const float mn = fmaxf(m2[u], mc);
+                const float dd = sc - mn;
+                const float p = key_ok ? bx_ex2(dd) : 0.0f;
+                float sa = p, sb = key_ok ? dd * p : 0.0f;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    sa += __shfl_xor_sync(0xFFFFFFFFu, sa, off);
+                    sb += __shfl_xor_sync(0xFFFFFFFFu, sb, off);
+                }
+                const float f = A[u] > 0.0 ? bx_ex2(m2[u] - mn) : 0.0f;
+                B2[u] = (A[u] > 0.0 ? (double)f * (B2[u] + (double)(m2[u] - mn) * A[u]) : 0.0) + (double)sb;
+                A[u] = A[u] * (double)f + (double)sa;
+                m2[u] = mn;
+                const f2_t ff = f2_packf(f, f);
+                f2_t o01 = f2_mul(f2_packf(acc[u].x, acc[u].y), ff);
+                f2_t o23 = f2_mul(f2_packf(acc[u].z, acc[u].w), ff);
+                auto pv = [&](int j) {
+                    const float pj = __shfl_sync(0xFFFFFFFFu, p, j);
+                    const f2_t pp = f2_packf(pj, pj);
+                    const uint2 w = vrow[j * (kBD / 4)];
+                    o01 = f2_fma(pp, bf16x2_to_f2(w.x), o01);
+                    o23 = f2_fma(pp, bf16x2_to_f2(w.y), o23);
+                };
+#pragma unroll
+                for (int j = 0; j < kBC; ++j) pv(j);  // rows >= nk are zero with p == 0
+                const float4 o = make_float4(f2_lo(o01), f2_hi(o01), f2_lo(o23), f2_hi(o23));
+                acc[u] = o;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        // ---- merge the 4 groups' states per head through shared memory ----
+        __syncthreads();  // every stage consumed: reuse the ring as exchange space
+        double* xs = (double*)stages;                                  // [gi][g][4]
+        float* xa = (float*)(stages + kBGroups * 8 * 4 * sizeof(double));  // [gi][g][kBD]
+#pragma unroll
+        for (int u = 0; u < HPW; ++u) {
+            const int g = gw + 4 * u;
+            if (g >= G) break;
+            reinterpret_cast<float4*>(xa + (gi * 8 + g) * kBD)[lane] = acc[u];
+            if (lane == 0) {
+                xs[(gi * 8 + g) * 4 + 0] = (double)m2[u];
+                xs[(gi * 8 + g) * 4 + 1] = A[u];
+                xs[(gi * 8 + g) * 4 + 2] = B2[u];
+            }
+        }
+        named_bar_sync(5, kBCompute);
+        if (gi == 0) {
+#pragma unroll
+            for (int u = 0; u < HPW; ++u) {
+                const int g = gw + 4 * u;
+                if (g >= G) break;
+                double M = -INFINITY;
+#pragma unroll
+                for (int k = 0; k < kBGroups; ++k)
+                    if (xs[(k * 8 + g) * 4 + 1] > 0.0) M = fmax(M, xs[(k * 8 + g) * 4 + 0]);
+                double At = 0.0, Bt = 0.0;
+                float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int k = 0; k < kBGroups; ++k) {
+                    const double km = xs[(k * 8 + g) * 4 + 0], ka = xs[(k * 8 + g) * 4 + 1];
+                    if (!(ka > 0.0)) continue;
+                    const double w = exp2(km - M);
+                    At += ka * w;
+                    Bt += w * (xs[(k * 8 + g) * 4 + 2] + (km - M) * ka);
+                    const float4 x = reinterpret_cast<const float4*>(xa + (k * 8 + g) * kBD)[lane];
+                    const float wf = (float)w;
+                    o.x = __fmaf_rn(x.x, wf, o.x);
+                    o.y = __fmaf_rn(x.y, wf, o.y);
+                    o.z = __fmaf_rn(x.z, wf, o.z);
+                    o.w = __fmaf_rn(x.w, wf, o.w);
+                }
+                uint8_t* row = B.part + (((size_t)(B.part_base + part) * a.n_kv + kv) * G + g) * kBPartBytes;
+                reinterpret_cast<float4*>(row + 32)[lane] = o;
+                if (lane == 0) {
+                    double* hd = (double*)row;
+                    hd[0] = M;
+                    hd[1] = At;
+                    hd[2] = Bt;
+                }
+            }
+        }
+    }
+    // ---- the last part of this kv head merges (attend.hpp:448-455 normalisation) ----
+    if (local) return;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&B.tickets[kv], 1u) == (unsigned)B.n_parts - 1u;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp < 4) {
+        float* w_s = (float*)stages + warp * kBMaxParts;
+        for (int g = warp; g < G; g += 4) {
+            auto prow = [&](int p) {
+                return B.part + (((size_t)p * a.n_kv + kv) * G + g) * kBPartBytes;
+            };
+            double M = -INFINITY;
+            for (int p = lane; p < B.n_slots; p += 32) {
+                const double* hd = (const double*)prow(p);
+                if (__ldcg(hd + 1) > 0.0) M = fmax(M, __ldcg(hd));
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) M = fmax(M, __shfl_xor_sync(0xFFFFFFFFu, M, off));
+            double At = 0.0, Bt = 0.0;
+            for (int p = lane; p < B.n_slots; p += 32) {
+                const double* hd = (const double*)prow(p);
+                const double pm = __ldcg(hd), pa = __ldcg(hd + 1), pb = __ldcg(hd + 2);
+                const double w = pa > 0.0 ? exp2(pm - M) : 0.0;
+                w_s[p] = (float)w;
+                if (pa > 0.0) {
+                    At += pa * w;
+                    Bt += w * (pb + (pm - M) * pa);
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                At += __shfl_xor_sync(0xFFFFFFFFu, At, off);
+                Bt += __shfl_xor_sync(0xFFFFFFFFu, Bt, off);
+            }
+            __syncwarp();
+            // part order, 8 loads in flight per lane (empty parts have w == 0, acc == 0)
+            double o[8][4] = {};
+            int p0 = 0;
+            for (; p0 + 8 <= B.n_slots; p0 += 8) {
+                float4 v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    v[k] = __ldcg(reinterpret_cast<const float4*>(prow(p0 + k) + 32) + lane);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const double w = (double)w_s[p0 + k];
+                    o[k][0] = fma((double)v[k].x, w, o[k][0]);
+                    o[k][1] = fma((double)v[k].y, w, o[k][1]);
+                    o[k][2] = fma((double)v[k].z, w, o[k][2]);
+                    o[k][3] = fma((double)v[k].w, w, o[k][3]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (p0 + k >= B.n_slots) break;
+                const float4 v = __ldcg(reinterpret_cast<const float4*>(prow(p0 + k) + 32) + lane);
+                const double w = (double)w_s[p0 + k];
+                o[k][0] = fma((double)v.x, w, o[k][0]);
+                o[k][1] = fma((double)v.y, w, o[k][1]);
+                o[k][2] = fma((double)v.z, w, o[k][2]);
+                o[k][3] = fma((double)v.w, w, o[k][3]);
+            }
+            double r[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                double t = 0.0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) t += o[k][c];
+                r[c] = t / At;
+            }
+            const int h = kv * G + g;
+            reinterpret_cast<float4*>(a.out + (size_t)h * kBD)[lane] =
+                make_float4((float)r[0], (float)r[1], (float)r[2], (float)r[3]);
+            if (lane == 0) {
+                const double hh = log(At) - Bt * 0.69314718055994530942 / At;
+                a.entropy[h] = hh < 0.0 ? 0.0 : hh;
+            }
+            __syncwarp();
+        }
+    }
+    if (tid == 0) B.tickets[kv] = 0u;  // re-arm for the next launch (graph replay)
+}
+
+int bulk_parts(const AttnArgs& a, int num_sms) {
+    return std::max(1, std::min(kBMaxParts - kMaxLocalParts, num_sms / std::max(1, a.n_kv)));
+}
+
+cudaError_t launch_bulk(const BulkArgs& B, int G, int n_kv, cudaStream_t s, bool pdl) {
+    dim3 grid(B.n_parts, n_kv);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kBThreads);
+    cfg.dynamicSmemBytes = kBSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+#define BULK_LAUNCH(GG)                                                                  \
+    do {                                                                                 \
+        cudaFuncSetAttribute(attend_decode_bulk_kernel<GG>,                              \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBSmem);  \
+        cudaLaunchKernelEx(&cfg, attend_decode_bulk_kernel<GG>, B);                      \
+    } while (0)
+    switch (G) {
+        case 1: BULK_LAUNCH(1); break;
+        case 2: BULK_LAUNCH(2); break;
+        case 3: BULK_LAUNCH(3); break;
+        case 4: BULK_LAUNCH(4); break;
+        case 5: BULK_LAUNCH(5); break;
+        case 6: BULK_LAUNCH(6); break;
+        case 7: BULK_LAUNCH(7); break;
+        default: BULK_LAUNCH(8); break;
+    }
+#undef BULK_LAUNCH
+    return cudaGetLastError();
+}
+
+BulkArgs bulk_args(const AttnArgs& a, void* ws, int num_sms, const DecodeFork* f) {
+    BulkArgs B;
+    B.a = a;
+    B.mode = f ? kModeHead : kModeScope;
+    B.n_local = f ? f->n_local : 0;
+    B.local_row0 = f ? f->local_row0 : 0;
+    B.n_parts = bulk_parts(a, num_sms);
+    B.part_base = 0;
+    B.n_slots = B.n_parts + (f ? f->local_parts : 0);
+    B.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)kBD));
+    B.tickets = (unsigned int*)ws;
+    B.part = (uint8_t*)ws + 256;
+    return B;
+}
+
+}  // namespace
+
+bool decode_bulk_eligible(const AttnArgs& a) {
+    return a.n_q == 1 && a.d == kBD && a.dv == kBD && a.group >= 1 && a.group <= 8 && a.causal &&
+           a.boundary_is_tail && a.dtype == kBF16 && a.n_head == a.n_kv * a.group;
+}
+
+size_t decode_bulk_workspace(const AttnArgs& a, int num_sms) {
+    return 256 + (size_t)(bulk_parts(a, num_sms) + kMaxLocalParts) * a.n_kv * a.group * kBPartBytes;
+}
+
+cudaError_t launch_attend_decode_bulk(const AttnArgs& a, void* ws, int num_sms, cudaStream_t s) {
+    return launch_bulk(bulk_args(a, ws, num_sms, nullptr), a.group, a.n_kv, s, true);
+}
+
+cudaError_t launch_attend_decode_local(const AttnArgs& a, void* ws, int num_sms, const DecodeFork& f,
+                                       cudaStream_t s) {
+    if (f.local_parts < 1 || f.local_parts > kMaxLocalParts) return cudaErrorInvalidValue;
+    BulkArgs B = bulk_args(a, ws, num_sms, &f);
+    B.mode = kModeLocal;
+    B.part_base = B.n_parts;  // after the head parts
+    B.n_parts = f.local_parts;
+    return launch_bulk(B, a.group, a.n_kv, s, false);
+}
+
+cudaError_t launch_attend_decode_head(const AttnArgs& a, void* ws, int num_sms, const DecodeFork& f,
+                                      cudaStream_t s, bool pdl) {
+    return launch_bulk(bulk_args(a, ws, num_sms, &f), a.group, a.n_kv, s, pdl);
+}
+
+}  // namespace reattn_impl

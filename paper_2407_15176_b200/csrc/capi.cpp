@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -40,12 +41,16 @@ struct StepPlan {
     size_t vote_ws_bytes = 0;
     void* vote_ws = nullptr;
     size_t part_bytes = 0;
+    bool fork = false;        // decode: local-window attention beside the scan
+    DecodeFork fk{};
     bool attn_tc = false;     // prefill attention on tcgen05 (ctx prefill mode TENSOR)
     size_t attn_tc_bytes = 0;
     void* attn_tc_ws = nullptr;
     size_t scratch_bytes = 0;
     uint64_t kernels = 0;
 };
+
+void plan_fork(reattn_ctx* ctx, StepPlan& P);
 
 int plan_step(reattn_ctx* ctx, const reattn_cache* cache, const reattn_rope* rope, uint64_t n_q,
               uint64_t n_head, const reattn_selection_config* cfg, int mode, StepPlan& P,
@@ -100,8 +105,43 @@ int plan_step(reattn_ctx* ctx, const reattn_cache* cache, const reattn_rope* rop
     }
     P.attn_tc = (ctx->prefill & REATTN_PREFILL_TENSOR_ATTN) && n_q > 1 && cache->d == 128 &&
                 cache->dtype == kBF16;
+    plan_fork(ctx, P);
     (void)out_dev;
     return REATTN_OK;
+}
+
+// Decode local-window fork (DecodeFork in kernels.h): lend R = m * n_kv SMs to the local
+// window's attention while the scan runs on the rest.  Opt-in (REATTN_FORK=1 forces m = 1,
+// REATTN_FORK=2 picks m from the estimates below): measured at 1M context the scan is
+// limited per SM, so lending 8 SMs costs it ~13 us while the post-select attention saves
+// ~7 us -- a net loss on B200 today.  Estimates: scan ~5.8 TB/s over the middle's keys;
+// local ~0.8 us per 32-row chunk per SM.
+void plan_fork(reattn_ctx* ctx, StepPlan& P) {
+    P.fork = false;
+    P.scan.grid_sms = 0;
+    const uint64_t n_local = P.total - P.l_start;
+    if (!(P.n_q == 1 && P.d == 128 && P.select && P.scan.fast && P.scan.a.dtype == kBF16 &&
+          P.group <= 8 && n_local > 0))
+        return;
+    const char* env_s = std::getenv("REATTN_FORK");
+    const int env = env_s ? std::atoi(env_s) : -1;
+    if (env != 1 && env != 2) return;
+    int m = env == 1 ? 1 : 0;
+    if (!m) {
+        const double t_scan = (double)P.middle * P.n_kv * P.d * 2 / 5.8e6;  // us
+        const double chunks = (double)((n_local + 31) / 32) * P.n_kv;
+        for (int mm = 1; mm <= 4 && (int)(mm * P.n_kv) * 4 <= ctx->num_sms; ++mm)
+            if (chunks * 0.8 / (mm * P.n_kv) <= 0.6 * t_scan) {
+                m = mm;
+                break;
+            }
+    }
+    if (!m) return;
+    P.fork = true;
+    P.fk.n_local = (uint32_t)n_local;
+    P.fk.local_row0 = (uint32_t)P.l_start;
+    P.fk.local_parts = m;
+    P.scan.grid_sms = ctx->num_sms - m * (int)P.n_kv;
 }
 
 AttnArgs step_attn_args(const StepPlan& P, const reattn_cache* cache, const reattn_rope* rope,
@@ -185,6 +225,14 @@ int enqueue_step(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache, const 
     sa.hdr = P.hdr;
     // Decode: <= 32 candidates -> vote/spans/scope run in the fast scan's last CTA (one
     // launch fewer, no host round trip); otherwise the standalone select kernel.
+    if (P.fork) {  // local window beside the scan (independent of the selection)
+        AttnArgs la = step_attn_args(P, cache, rope, q_dev, out_dev);
+        CU(ctx, cudaEventRecord(ctx->ev_fork, s));
+        CU(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        CU(ctx, launch_attend_decode_local(la, P.part, ctx->num_sms, P.fk, ctx->side));
+        CU(ctx, cudaEventRecord(ctx->ev_join, ctx->side));
+        ++P.kernels;
+    }
     bool fused = false;
     if (P.select) {
         P.scan.a.q = q_dev;
@@ -222,7 +270,13 @@ int enqueue_step(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache, const 
     }
     if (P.n_q > 0) {
         AttnArgs a = step_attn_args(P, cache, rope, q_dev, out_dev);
-        if (P.attn_tc) {
+        // the bulk decode attention's tickets sit at the start of P.part (plans: zeroed once)
+        if (zero_ticket && decode_bulk_eligible(a)) CU(ctx, cudaMemsetAsync(P.part, 0, 256, s));
+        if (P.fork) {
+            CU(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
+            CU(ctx, launch_attend_decode_head(a, P.part, ctx->num_sms, P.fk, s, false));
+            ++P.kernels;
+        } else if (P.attn_tc) {
             CU(ctx, launch_attend_tc(a, std::max<uint32_t>(1, P.L_upper), P.attn_tc_ws, s));
             P.kernels += 2;
         } else {
@@ -296,6 +350,14 @@ int reattn_ctx_create(int device, reattn_ctx** out) {
     }
     ctx->own_stream = true;
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        reattn_ctx_destroy(ctx);
+        *out = nullptr;
+        return REATTN_ECUDA;
+    }
     *out = ctx;
     return REATTN_OK;
 }
@@ -303,7 +365,11 @@ int reattn_ctx_create(int device, reattn_ctx** out) {
 void reattn_ctx_destroy(reattn_ctx* ctx) {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->side) cudaStreamSynchronize(ctx->side);
     if (ctx->arena) cudaFree(ctx->arena);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

@@ -22,6 +22,9 @@ struct reattn_ctx {
     std::string err;
     void* arena = nullptr;  // scratch for synchronous calls
     size_t arena_bytes = 0;
+    // decode local-window fork: side stream + fork / join events (captured into plans)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 struct reattn_cache {
@@ -114,6 +117,7 @@ struct ScanPlan {
     bool tc = false;  // prefill on tcgen05 (opt-in, ε-tie parity)
     CUtensorMap map;
     size_t ws_bytes = 0;
+    int grid_sms = 0;  // fast scan CTAs (0: every SM); fewer when SMs are lent to the fork
 };
 
 inline int plan_scan(reattn_ctx* ctx, ScanPlan& sp) {
@@ -151,7 +155,7 @@ inline int enqueue_scan(reattn_ctx* ctx, const ScanPlan& sp, void* ws, cudaStrea
     }
     if (sp.fast && zero_ticket) CU(ctx, cudaMemsetAsync(ws, 0, 256, s));
     if (sp.fast)
-        CU(ctx, launch_scan_fast(sp.a, sp.map, ws, ctx->num_sms, s));
+        CU(ctx, launch_scan_fast(sp.a, sp.map, ws, sp.grid_sms ? sp.grid_sms : ctx->num_sms, s));
     else
         CU(ctx, launch_scan_generic(sp.a, s));
     return REATTN_OK;

@@ -147,6 +147,26 @@ constexpr int kAttnSplit = 64;
 size_t attend_workspace(const AttnArgs& a, uint32_t L_max);
 cudaError_t launch_attend(const AttnArgs& a, uint32_t L_max, cudaStream_t s);
 int attend_kernel_count(const AttnArgs& a, uint32_t L_max);
+// decode attention with a bulk-copy ring and fused combine (attend_decode.cu): n_q == 1,
+// d == dv == 128, bf16 cache.  ws = a.part: 256 B of per-kv-head tickets (zero before the
+// first launch; the kernel re-arms them) + partial rows.
+bool decode_bulk_eligible(const AttnArgs& a);
+size_t decode_bulk_workspace(const AttnArgs& a, int num_sms);
+cudaError_t launch_attend_decode_bulk(const AttnArgs& a, void* ws, int num_sms, cudaStream_t s);
+// Local-window fork: the last n_local scope rows are the cache's local segment, independent of
+// the selection (RoPE is relative, so they can be attended at positions 0..n_local-1 with the
+// query at n_local-1).  The local launch runs beside the scan on local_parts CTAs per kv head
+// (partials only); the head launch attends scope rows [0, L'-n_local) after the select and
+// merges both.  Same workspace as launch_attend_decode_bulk.
+struct DecodeFork {
+    uint32_t n_local;     // local segment rows (cache total - local start)
+    uint32_t local_row0;  // cache row of local row 0
+    int local_parts;      // CTAs per kv head for the local launch (1..4)
+};
+cudaError_t launch_attend_decode_local(const AttnArgs& a, void* ws, int num_sms, const DecodeFork& f,
+                                       cudaStream_t s);
+cudaError_t launch_attend_decode_head(const AttnArgs& a, void* ws, int num_sms, const DecodeFork& f,
+                                      cudaStream_t s, bool pdl);
 // prefill attention on tcgen05 (attend_tc.cu): d == dv == 128, bf16 cache; bf16 hi+lo split
 // operands, fp32 TMEM accumulation (bf16 tolerance).  ws: attend_tc_workspace bytes.
 bool attend_tc_supported(const AttnArgs& a);

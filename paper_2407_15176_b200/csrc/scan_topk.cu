@@ -137,6 +137,9 @@ __device__ __forceinline__ float lane_tree(f2_t a0, f2_t a1, f2_t a2, f2_t a3) {
 template <typename KT, int LANES>
 __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
     scan_fast_kernel(const __grid_constant__ CUtensorMap kmap, const FastArgs a) {
+    // let a programmatic dependent (the decode attention) launch now: its CTAs become
+    // resident as this grid's CTAs retire and wait in griddepcontrol.wait for our results
+    asm volatile("griddepcontrol.launch_dependents;");
     using C = FastCfg<KT>;
     constexpr int KMAX = C::KMAX;
     extern __shared__ uint8_t smem_raw[];

@@ -398,8 +398,9 @@ static void test_attend_step() {
         for (std::size_t i = 0; spans_eq && i < ost.n_spans; ++i)
             spans_eq = spans.spans[i].begin == sb[i] && spans.spans[i].end == se[i];
         CHECK(rc == 0 && md <= 1e-6 && spans_eq && st.scope_len_max == ost.scope_len &&
-                  std::abs(st.entropy_max - ost.entropy_max) <= 1e-9 && st.coverage_total == (bool)ost.coverage_total,
-              "attend_step total=%zu n_q=%zu md=%g L=%zu/%zu", c.total, c.n_q, md, st.scope_len_max, ost.scope_len);
+                  std::abs(st.entropy_max - ost.entropy_max) <= 1e-6 && st.coverage_total == (bool)ost.coverage_total,
+              "attend_step total=%zu n_q=%zu md=%g dH=%g L=%zu/%zu", c.total, c.n_q, md,
+              std::abs(st.entropy_max - ost.entropy_max), st.scope_len_max, ost.scope_len);
     }
     {  // errors: engine.hpp:509-511, scope.hpp:262-263, engine.hpp:527
         SelectionConfig cfg;

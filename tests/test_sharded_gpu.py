@@ -72,8 +72,8 @@ def test_sharded_equals_unsharded(ctx, world, total):
             assert st.scope_len == ref.stats.scope_len, (world, r)
             assert np.array_equal(sb, ref.spans[0]) and np.array_equal(se, ref.spans[1]), (world, r)
             err = (o.out - ref.out).abs().max().item()
-            assert err <= 1e-7, (world, r, err)
-            assert abs(st.entropy_max - ref.stats.entropy_max) <= 1e-9
+            assert err <= 1e-6, (world, r, err)
+            assert abs(st.entropy_max - ref.stats.entropy_max) <= 1e-6
 
 
 def test_shard_range_matches_c_rule(ctx):
