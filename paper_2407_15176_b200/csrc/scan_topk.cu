@@ -39,17 +39,17 @@ struct FastCfg {
     static constexpr int D = 128;
     static constexpr int ESZ = (int)sizeof(KT);
     static constexpr int ROW_BYTES = D * ESZ;       // 256 (bf16) / 512 (fp32)
-    // key rows per stage = consumer threads.  bf16: 7 consumer warps + 1 producer warp = 8
-    // warps, i.e. 2 per SM sub-partition, which leaves ptxas 255 registers per thread for
-    // the 128-float query kept in registers (9 warps would cap it at 168 and spill).
-    static constexpr int ROWS = ESZ == 2 ? 224 : 128;
+    // key rows per stage = consumer threads.  bf16: 8 consumer warps (2 per SM sub-partition,
+    // evenly loaded); thread 0 also issues the TMA loads, so ptxas keeps 255 registers per
+    // thread for the 128-float query held in registers (9 warps would cap it at 168).
+    static constexpr int ROWS = ESZ == 2 ? 256 : 128;
     static constexpr int NBOX = ROW_BYTES / 128;    // 128-byte TMA boxes per row
     static constexpr int BOX_ELEMS = 128 / ESZ;
     static constexpr int STAGE_BYTES = ROWS * ROW_BYTES;
     static constexpr int STAGES = 3;
     static constexpr int CONSUMERS = ROWS;
     static constexpr int CWARPS = CONSUMERS / 32;
-    static constexpr int THREADS = CONSUMERS + 32;  // + one TMA producer warp
+    static constexpr int THREADS = CONSUMERS;  // thread 0 doubles as the TMA producer
     static constexpr int KMAX = 8;
     static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES +
                                    2 * STAGES * sizeof(uint64_t) + D * sizeof(float) +
@@ -168,27 +168,25 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
     }
     __syncthreads();
 
-    if (warp == C::CWARPS) {
-        // ===== TMA producer =====
-        if (lane == 0) {
-            prefetch_tensormap(&kmap);
-            const uint64_t pol = policy_evict_first();
-            uint32_t it = 0;
-            for (uint32_t t = t_begin; t < t_end; ++t, ++it) {
-                const int s = it % C::STAGES;
-                const uint32_t ph = (it / C::STAGES) & 1u;
-                if (it >= (uint32_t)C::STAGES) mbar_wait(&empty[s], ph ^ 1u);
-                const uint32_t kv = t / a.tiles_per_head, j = t % a.tiles_per_head;
-                const int32_t row =
-                    (int32_t)(kv * a.head_stride + a.row0 + (uint64_t)j * C::ROWS);
-                mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+    // ===== TMA issue (thread 0): the first STAGES tiles now, then each stage is refilled
+    // as soon as every warp has released it (end of the consumer iteration below) =====
+    const uint64_t pol = policy_evict_first();
+    auto issue = [&](uint32_t it) {
+        const uint32_t t = t_begin + it;
+        const int s = it % C::STAGES;
+        const uint32_t kv = t / a.tiles_per_head, j = t % a.tiles_per_head;
+        const int32_t row = (int32_t)(kv * a.head_stride + a.row0 + (uint64_t)j * C::ROWS);
+        mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
 #pragma unroll
-                for (int box = 0; box < C::NBOX; ++box)
-                    tma_load_2d(stages + (size_t)s * C::STAGE_BYTES + box * C::ROWS * 128, &kmap,
-                                box * C::BOX_ELEMS, row, &full[s], pol);
-            }
-        }
-    } else {
+        for (int box = 0; box < C::NBOX; ++box)
+            tma_load_2d(stages + (size_t)s * C::STAGE_BYTES + box * C::ROWS * 128, &kmap,
+                        box * C::BOX_ELEMS, row, &full[s], pol);
+    };
+    if (tid == 0) {
+        prefetch_tensormap(&kmap);
+        for (uint32_t it = 0; it < (uint32_t)C::STAGES && t_begin + it < t_end; ++it) issue(it);
+    }
+    {
         // ===== consumers: one key row per thread per tile =====
         f2_t qv[C::D / 2];
         float ts[KMAX];
@@ -313,6 +311,10 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
+            if (tid == 0 && t + C::STAGES < t_end) {
+                mbar_wait(&empty[s], ph);  // all warps are done with this stage
+                issue(it + C::STAGES);
+            }
         }
         if (cur_kv != kNoIndex) flush(cur_kv);
     }
