@@ -123,7 +123,12 @@ __device__ __forceinline__ void lane_step(f2_t& acc, f2_t q, f2_t k) {
     if (LANES == kLanesFma)
         acc = f2_fma(q, k, acc);
     else
-        acc = f2_add_product(acc, f2_mul(q, k));
+        // unfused lane: round(q*k), then round(acc + .).  The product comes from an FFMA2 with
+        // a +0 addend -- ptxas cannot contract an FMA into the following add (it does contract
+        // mul.rn.f32x2 + add.rn.f32x2, even with --fmad=false).  RN(q*k + 0) == RN(q*k) except
+        // for an exact -0 product, which becomes +0; the accumulator starts at +0 and sums of
+        // floats never round to -0, so acc + (+0) == acc + (-0) and the lanes stay bit-exact.
+        acc = f2_add(acc, f2_fma(q, k, 0ull));
 }
 
 __device__ __forceinline__ float lane_tree(f2_t a0, f2_t a1, f2_t a2, f2_t a3) {

@@ -13,7 +13,7 @@ import os
 from dataclasses import dataclass
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libreattn_cuda.so")
+LIB_PATH = os.environ.get("REATTN_LIB", os.path.join(PKG_DIR, "libreattn_cuda.so"))
 HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "reattn_cuda.h")
 
 OK, EINVAL, ERANGE, ELOGIC, ECUDA, ERUNTIME = range(6)
