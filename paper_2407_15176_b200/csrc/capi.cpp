@@ -111,11 +111,10 @@ int plan_step(reattn_ctx* ctx, const reattn_cache* cache, const reattn_rope* rop
 }
 
 // Decode local-window fork (DecodeFork in kernels.h): lend R = m * n_kv SMs to the local
-// window's attention while the scan runs on the rest.  Opt-in (REATTN_FORK=1 forces m = 1,
-// REATTN_FORK=2 picks m from the estimates below): measured at 1M context the scan is
-// limited per SM, so lending 8 SMs costs it ~13 us while the post-select attention saves
-// ~7 us -- a net loss on B200 today.  Estimates: scan ~5.8 TB/s over the middle's keys;
-// local ~0.8 us per 32-row chunk per SM.
+// window's attention while the scan runs on the rest, when the local work fits well inside
+// the scan (estimates: scan ~5.8 TB/s over the middle's keys; local ~0.8 us per 32-row chunk
+// per SM, measured).  At 1M context on B200 it costs the scan ~3 us and saves ~7 us of
+// post-select attention.  REATTN_FORK=0 disables it, REATTN_FORK=1 forces m = 1.
 void plan_fork(reattn_ctx* ctx, StepPlan& P) {
     P.fork = false;
     P.scan.grid_sms = 0;
@@ -125,13 +124,13 @@ void plan_fork(reattn_ctx* ctx, StepPlan& P) {
         return;
     const char* env_s = std::getenv("REATTN_FORK");
     const int env = env_s ? std::atoi(env_s) : -1;
-    if (env != 1 && env != 2) return;
+    if (env == 0) return;
     int m = env == 1 ? 1 : 0;
     if (!m) {
         const double t_scan = (double)P.middle * P.n_kv * P.d * 2 / 5.8e6;  // us
         const double chunks = (double)((n_local + 31) / 32) * P.n_kv;
-        for (int mm = 1; mm <= 4 && (int)(mm * P.n_kv) * 4 <= ctx->num_sms; ++mm)
-            if (chunks * 0.8 / (mm * P.n_kv) <= 0.6 * t_scan) {
+        for (int mm = 1; mm <= 2 && (int)(mm * P.n_kv) * 8 <= ctx->num_sms; ++mm)
+            if (chunks * 0.8 / (mm * P.n_kv) <= 0.5 * t_scan) {
                 m = mm;
                 break;
             }
