@@ -38,6 +38,16 @@ ROPE_BASE = 500000.0
 WINDOW = 8192
 
 
+def load_traffic() -> dict | None:
+    """dram read+write bytes per scan launch from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_decode_1m.json")) as f:
+            p = json.load(f)
+        return {"bytes": int(p["traffic_bytes"]), "source": p["source"]}
+    except Exception:
+        return None
+
+
 def load_peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -308,7 +318,9 @@ def run_ours(args) -> None:
         "step_frac_of_hbm": step_bytes / (ms_per_step * 1e-3) / 1e9 / peaks["hbm_gbs"],
         "roofline": {"bound": "hbm", "kernel": "scan_fast_kernel (K1)", "achieved": achieved,
                      "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                     "traffic": None, "bytes_per_launch": scan_bytes,
+                     "traffic": (load_traffic() or {}).get("bytes"),
+                     "traffic_source": (load_traffic() or {}).get("source"),
+                     "bytes_per_launch": scan_bytes,
                      "launch_us": scan_ms * 1000.0, "peak_source": peaks["source"],
                      "peak_note": "peak is the measured copy (read+write) bandwidth; the scan "
                                   "only reads, so frac can exceed 1",
