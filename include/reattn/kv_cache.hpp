@@ -7,6 +7,10 @@
 
 #include <algorithm>
 #include <cstddef>
+#include <cstdint>
+#include <cstring>
+#include <span>
+#include <string>
 #include <memory>
 #include <stdexcept>
 #include <utility>
@@ -131,7 +135,48 @@ public:
     }
     const reattn_cache* device() const { return dev_.get(); }
 
+    // Adopt a device cache created by the C-ABI (snapshot load); with host_shadow the rows
+    // are read back once for the reference's host accessors (bf16 widened exactly).
+    static SegmentedKvCache adopt(reattn_cache* c, bool host_shadow = true) {
+        std::uint64_t n_kv = 0, d = 0, g = 0, loc = 0, cap = 0, total = 0;
+        int dt = 0;
+        reattn_cache_info(c, &n_kv, &d, &g, &loc, &cap, &total, nullptr, nullptr, &dt);
+        SegmentedKvCache out(c, n_kv, d, g, loc, host_shadow);
+        out.total_ = total;
+        if (host_shadow && total) {
+            const std::size_t esz = dt == REATTN_BF16 ? 2 : 4;
+            std::vector<std::uint8_t> raw(total * d * esz);
+            for (int part = 0; part < 2; ++part) {
+                const auto* base = static_cast<const std::uint8_t*>(part ? reattn_cache_values(c)
+                                                                         : reattn_cache_keys(c));
+                for (std::size_t h = 0; h < n_kv; ++h) {
+                    gpu::check(reattn_memcpy_d2h(gpu::context(), raw.data(), base + h * cap * d * esz,
+                                                 raw.size()));
+                    auto& dst = part ? out.values_[h] : out.keys_[h];
+                    dst.resize(total * d);
+                    for (std::size_t e = 0; e < total * d; ++e) {
+                        if (esz == 4) {
+                            std::memcpy(&dst[e], raw.data() + 4 * e, 4);
+                        } else {
+                            std::uint16_t b;
+                            std::memcpy(&b, raw.data() + 2 * e, 2);
+                            const std::uint32_t w = std::uint32_t(b) << 16;
+                            std::memcpy(&dst[e], &w, 4);
+                        }
+                    }
+                }
+            }
+        }
+        return out;
+    }
+
 private:
+    SegmentedKvCache(reattn_cache* c, std::size_t n_kv, std::size_t d, std::size_t g,
+                     std::size_t loc, bool host_shadow)
+        : n_kv_(n_kv), d_(d), g_(g), local_(loc), shadow_(host_shadow), keys_(n_kv),
+          values_(n_kv) {
+        dev_.reset(c);
+    }
     void need_shadow() const {
         if (!shadow_)
             throw std::logic_error("SegmentedKvCache: host accessors need host_shadow = true");
@@ -144,5 +189,34 @@ private:
     std::vector<std::vector<float>> keys_, values_;
     std::unique_ptr<reattn_cache, Del> dev_;
 };
+
+// RKVC snapshot container (reference kv_cache.hpp:121-209): magic "RKVC", u32 version,
+// u32 n_layers / n_kv_heads / d_head, per layer u64 {total, l_global, l_local_max} and raw
+// f32 key and value payloads, head-major.  Same signatures, messages and exception types;
+// the payloads stream straight between the file and device storage.
+inline void write_cache_snapshot(const std::string& path, std::span<const SegmentedKvCache> layers) {
+    std::vector<const reattn_cache*> dev;
+    for (const auto& l : layers) dev.push_back(l.device());
+    gpu::check(reattn_snapshot_write(gpu::context(), path.c_str(), dev.data(),
+                                     static_cast<std::uint32_t>(dev.size())));
+}
+
+inline std::vector<SegmentedKvCache> read_cache_snapshot(
+    const std::string& path, SegmentedKvCache::Storage storage = SegmentedKvCache::Storage::F32,
+    bool host_shadow = true) {
+    reattn_snapshot* s = nullptr;
+    gpu::check(reattn_snapshot_open(gpu::context(), path.c_str(), &s));
+    std::unique_ptr<reattn_snapshot, void (*)(reattn_snapshot*)> guard(s, reattn_snapshot_close);
+    std::uint32_t n_layers = 0;
+    reattn_snapshot_info(s, &n_layers, nullptr, nullptr);
+    std::vector<SegmentedKvCache> layers;
+    layers.reserve(n_layers);
+    for (std::uint32_t l = 0; l < n_layers; ++l) {
+        reattn_cache* c = nullptr;
+        gpu::check(reattn_snapshot_load_layer(gpu::context(), s, l, static_cast<int>(storage), 0, &c));
+        layers.push_back(SegmentedKvCache::adopt(c, host_shadow));
+    }
+    return layers;
+}
 
 }  // namespace reattn

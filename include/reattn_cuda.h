@@ -120,6 +120,24 @@ int reattn_cache_info(const reattn_cache* cache, uint64_t* n_kv, uint64_t* d, ui
 void* reattn_cache_keys(const reattn_cache* cache);
 void* reattn_cache_values(const reattn_cache* cache);
 
+/* ---- RKVC cache snapshots: kv_cache.hpp:121-209 write/read_cache_snapshot ---------- */
+/* open: parses and validates the whole file in the reference's read order (messages and
+ * error kinds as read_cache_snapshot: runtime_error -> ERUNTIME, the SegmentedKvCache
+ * constructor's invalid_argument -> EINVAL).  load_layer: a new device cache of `dtype`
+ * (bf16 storage rounds the f32 payload) with capacity max(capacity, total).  write: the
+ * layers' rows as f32, head-major; bf16 caches are widened exactly. */
+typedef struct reattn_snapshot reattn_snapshot;
+int reattn_snapshot_open(reattn_ctx* ctx, const char* path, reattn_snapshot** out);
+int reattn_snapshot_info(const reattn_snapshot* snap, uint32_t* n_layers, uint32_t* n_kv,
+                         uint32_t* d_head);
+int reattn_snapshot_layer_info(const reattn_snapshot* snap, uint32_t layer, uint64_t* total,
+                               uint64_t* l_global, uint64_t* l_local_max);
+int reattn_snapshot_load_layer(reattn_ctx* ctx, reattn_snapshot* snap, uint32_t layer, int dtype,
+                               uint64_t capacity, reattn_cache** out);
+void reattn_snapshot_close(reattn_snapshot* snap);
+int reattn_snapshot_write(reattn_ctx* ctx, const char* path, const reattn_cache* const* layers,
+                          uint32_t n_layers);
+
 /* ---- rotary table: rope.hpp:317-366 RotaryTable ----------------------------------- */
 int reattn_rope_create(reattn_ctx* ctx, uint64_t head_dim, double base, uint64_t max_position,
                        reattn_rope** out);

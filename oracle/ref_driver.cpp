@@ -10,11 +10,13 @@
 #include <memory>
 #include <optional>
 #include <stdexcept>
+#include <span>
 #include <string>
 #include <vector>
 
 #include "reattn/attend.hpp"
 #include "reattn/engine.hpp"
+#include "reattn/kv_cache.hpp"
 #include "reattn/rope.hpp"
 #include "reattn/scope.hpp"
 #include "reattn/selection.hpp"
@@ -205,6 +207,39 @@ void* ref_cache_create(std::size_t n_kv, std::size_t d, std::size_t l_global,
 }
 
 void ref_cache_destroy(void* p) { delete static_cast<RefCache*>(p); }
+
+// kv_cache.hpp:143-166 write_cache_snapshot over caches built by ref_cache_create.
+int ref_snapshot_write(const char* path, void* const* caches, std::size_t n) {
+    REF_TRY({
+        std::vector<SegmentedKvCache> layers;
+        for (std::size_t i = 0; i < n; ++i) layers.push_back(static_cast<RefCache*>(caches[i])->cache);
+        write_cache_snapshot(path, std::span<const SegmentedKvCache>(layers));
+    })
+}
+
+// kv_cache.hpp:168-209 read_cache_snapshot: the layer count, and for `layer` its geometry
+// (n_kv, d, total, l_global, l_local_max) and head-major payloads when they fit `cap` floats.
+int ref_snapshot_read(const char* path, std::size_t layer, std::size_t* n_layers, uint64_t* info5,
+                      float* keys, float* values, std::size_t cap) {
+    REF_TRY({
+        const auto layers = read_cache_snapshot(path);
+        *n_layers = layers.size();
+        if (layer < layers.size()) {
+            const auto& c = layers[layer];
+            info5[0] = c.n_kv_heads();
+            info5[1] = c.d_head();
+            info5[2] = c.total();
+            info5[3] = c.l_global();
+            info5[4] = c.l_local_max();
+            const std::size_t per = c.total() * c.d_head();
+            if (keys && values && per * c.n_kv_heads() <= cap && c.total())
+                for (std::size_t h = 0; h < c.n_kv_heads(); ++h) {
+                    std::memcpy(keys + h * per, c.key(h, 0), per * sizeof(float));
+                    std::memcpy(values + h * per, c.value(h, 0), per * sizeof(float));
+                }
+        }
+    })
+}
 
 struct RefStats {
     std::size_t max_position_used, ood_positions;

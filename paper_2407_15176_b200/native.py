@@ -94,6 +94,12 @@ SIGNATURES = [
     ("reattn_cache_reserve", C.c_int, [vp, vp, u64]),
     ("reattn_cache_append", C.c_int, [vp, vp, vp, vp, u64, C.c_int]),
     ("reattn_cache_set_total", C.c_int, [vp, vp, u64]),
+    ("reattn_snapshot_open", C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
+    ("reattn_snapshot_info", C.c_int, [vp] + [C.POINTER(C.c_uint32)] * 3),
+    ("reattn_snapshot_layer_info", C.c_int, [vp, C.c_uint32] + [C.POINTER(u64)] * 3),
+    ("reattn_snapshot_load_layer", C.c_int, [vp, vp, C.c_uint32, C.c_int, u64, C.POINTER(vp)]),
+    ("reattn_snapshot_close", None, [vp]),
+    ("reattn_snapshot_write", C.c_int, [vp, C.c_char_p, C.POINTER(vp), C.c_uint32]),
     ("reattn_cache_info", C.c_int, [vp] + [C.POINTER(u64)] * 8 + [C.POINTER(C.c_int)]),
     ("reattn_cache_keys", vp, [vp]),
     ("reattn_cache_values", vp, [vp]),
@@ -253,6 +259,48 @@ class Context:
         self.check(self.lib.reattn_synth_uniform(self.h, _ptr(t), t.numel(), dt, seed, offset))
 
 
+class Snapshot:
+    """RKVC cache snapshot (kv_cache.hpp:121-209) read into device caches."""
+
+    def __init__(self, ctx: Context, path: str):
+        self.ctx = ctx
+        h = vp()
+        ctx.check(ctx.lib.reattn_snapshot_open(ctx.h, os.fsencode(path), C.byref(h)))
+        self.h = h
+        a, b, c = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        ctx.lib.reattn_snapshot_info(h, C.byref(a), C.byref(b), C.byref(c))
+        self.n_layers, self.n_kv, self.d = a.value, b.value, c.value
+
+    def layer_info(self, layer: int) -> dict:
+        t, g, l = u64(), u64(), u64()
+        self.ctx.check(self.ctx.lib.reattn_snapshot_layer_info(self.h, layer, C.byref(t),
+                                                               C.byref(g), C.byref(l)))
+        return {"total": t.value, "l_global": g.value, "l_local_max": l.value}
+
+    def load_layer(self, layer: int, dtype: int = F32, capacity: int = 0) -> "Cache":
+        h = vp()
+        self.ctx.check(self.ctx.lib.reattn_snapshot_load_layer(self.ctx.h, self.h, layer, dtype,
+                                                               capacity, C.byref(h)))
+        return Cache._adopt(self.ctx, h)
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.ctx.lib.reattn_snapshot_close(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def write_snapshot(ctx: Context, path: str, caches) -> None:
+    """write_cache_snapshot (kv_cache.hpp:143-166) from device caches."""
+    arr = (vp * max(1, len(caches)))(*[c.h for c in caches])
+    ctx.check(ctx.lib.reattn_snapshot_write(ctx.h, os.fsencode(path), arr, len(caches)))
+
+
 class Rope:
     """reattn::RotaryTable (rope.hpp:317-366) with its tables resident on the device."""
 
@@ -295,6 +343,15 @@ class Cache:
         self.h = h
         self.n_kv, self.d, self.l_global, self.l_local_max = n_kv, d, l_global, l_local_max
         self.capacity, self.dtype = capacity, dtype
+
+    @classmethod
+    def _adopt(cls, ctx: Context, h) -> "Cache":
+        self = cls.__new__(cls)
+        self.ctx, self.h = ctx, h
+        i = self.info()
+        self.n_kv, self.d, self.l_global, self.l_local_max = i["n_kv"], i["d"], i["l_global"], i["l_local_max"]
+        self.capacity, self.dtype = i["capacity"], i["dtype"]
+        return self
 
     def append(self, keys, values) -> None:
         """keys/values: torch [rows, n_kv*d] fp32 (device) or numpy fp32 (host)."""

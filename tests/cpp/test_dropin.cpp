@@ -419,7 +419,57 @@ static void test_attend_step() {
     }
 }
 
+// kv_cache.hpp:121-209 snapshot round trip through the drop-in API, plus the reference's
+// failure messages (runtime_error / invalid_argument) for corrupt files.
+static void test_snapshot() {
+    std::mt19937 rng(91);
+    std::vector<SegmentedKvCache> layers;
+    const std::size_t totals[3] = {70, 0, 5};
+    for (std::size_t t : totals) {
+        SegmentedKvCache c(2, 16, 4, 32);
+        if (t) c.append(random_rows(t, 32, rng), random_rows(t, 32, rng));
+        layers.push_back(std::move(c));
+    }
+    const std::string path = "/tmp/reattn_dropin_snapshot.rkvc";
+    write_cache_snapshot(path, std::span<const SegmentedKvCache>(layers));
+    for (auto storage : {SegmentedKvCache::Storage::F32, SegmentedKvCache::Storage::BF16}) {
+        auto back = read_cache_snapshot(path, storage);
+        bool ok = back.size() == 3;
+        for (std::size_t l = 0; ok && l < 3; ++l) {
+            ok = back[l].total() == layers[l].total() && back[l].l_global() == 4 &&
+                 back[l].l_local_max() == 32 && back[l].n_kv_heads() == 2 && back[l].d_head() == 16;
+            for (std::size_t h = 0; ok && h < 2; ++h)
+                for (std::size_t e = 0; ok && e < layers[l].total() * 16; ++e) {
+                    const float want = layers[l].key(h, 0)[e], wv = layers[l].value(h, 0)[e];
+                    const float gk = back[l].key(h, 0)[e], gv = back[l].value(h, 0)[e];
+                    if (storage == SegmentedKvCache::Storage::F32)
+                        ok = gk == want && gv == wv;
+                    else
+                        ok = gk == oracle_round_bf16(want) && gv == oracle_round_bf16(wv);
+                }
+        }
+        CHECK(ok, "snapshot round trip storage=%d", (int)storage);
+    }
+    {
+        FILE* f = std::fopen(path.c_str(), "wb");
+        std::fwrite("RKVX", 1, 4, f);
+        std::fclose(f);
+        CHECK(throws<std::runtime_error>([&] { read_cache_snapshot(path); },
+                                         "not a cache snapshot (bad magic)"),
+              "snapshot bad magic");
+        CHECK(throws<std::runtime_error>([&] { read_cache_snapshot("/tmp/no/such.rkvc"); },
+                                         "cannot open /tmp/no/such.rkvc"),
+              "snapshot missing file");
+        CHECK(throws<std::invalid_argument>(
+                  [&] { write_cache_snapshot(path, std::span<const SegmentedKvCache>()); },
+                  "cache snapshot: no layers"),
+              "snapshot no layers");
+    }
+    std::remove(path.c_str());
+}
+
 int main() {
+    test_snapshot();
     test_fused_topk();
     test_vote_spans();
     test_scope();

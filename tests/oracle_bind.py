@@ -154,6 +154,8 @@ def ref() -> C.CDLL | None:
                                         C.c_int, C.c_double, sz, C.c_int, f32p,
                                         C.POINTER(StepStats), u64p, u64p]
         lib.ref_fma_selfcheck.argtypes = [sz, sz, C.POINTER(sz), C.POINTER(sz)]
+        lib.ref_snapshot_write.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), sz]
+        lib.ref_snapshot_read.argtypes = [C.c_char_p, sz, C.POINTER(sz), u64p, f32p, f32p, sz]
         _ref = lib
     return _ref
 
