@@ -42,13 +42,13 @@ constexpr int kBRopeBytes = kBC * (kBD / 2) * 4;  // cos or sin rows of one chun
 constexpr int kBStageBytes = 2 * kBKVBytes + 2 * kBRopeBytes;
 constexpr int kBCompute = kBGroups * 128;
 constexpr int kBThreads = kBCompute + 32;
-constexpr int kBPartBytes = 32 + kBD * 4;      // double m2, A, B2, pad; float acc[128]
+constexpr int kBPartBytes = kDecodePartBytes;  // double m2, A, B2, pad; float acc[128]
 constexpr int kBMaxParts = 160;          // partial slots per kv head (head + local)
 constexpr int kMaxLocalParts = 4;
 constexpr size_t kBSmem = 1024 + (size_t)kBStages * kBStageBytes + 8ull * kBD * 4 +
                           (size_t)kBStages * kBC + 256;
 
-enum { kModeScope = 0, kModeLocal = 1, kModeHead = 2 };
+enum { kModeScope = 0, kModeLocal = 1, kModeHead = 2, kModeRanges = 3 };
 
 struct BulkArgs {
     AttnArgs a;
@@ -57,7 +57,11 @@ struct BulkArgs {
                             //   0 .. n_local-1, query at n_local-1 (RoPE is relative: the
                             //   logits equal the scope frame's up to rounding); partials only
                             // kModeHead: scope rows [0, L'-n_local); merges the local partials
+                            // kModeRanges: the scope rows of a ShardRanges (sharded decode);
+                            //   the merged state goes to `merged` as partial rows
     uint32_t n_local, local_row0;
+    const uint32_t* ranges;  // kModeRanges: device ShardRanges
+    uint8_t* merged;         // non-null: write merged partial rows [n_head] instead of out
     int n_parts;            // CTAs per kv head in this launch
     int part_base;          // first partial slot of this launch
     int n_slots;            // partial slots per kv head (merged by the combine)
@@ -94,7 +98,35 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
     const uint32_t rows = B.mode == kModeHead ? L - B.n_local : L;
     const int part = blockIdx.x, kv = blockIdx.y;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int chunks = (int)((rows + kBC - 1) / kBC);
+    ShardRanges R;
+    R.n = 0;
+    int chunks;
+    if (B.mode == kModeRanges) {
+        R = *(const ShardRanges*)B.ranges;
+        chunks = 0;
+        for (uint32_t i = 0; i < R.n; ++i) chunks += (int)((R.end[i] - R.begin[i] + kBC - 1) / kBC);
+    } else {
+        chunks = (int)((rows + kBC - 1) / kBC);
+    }
+    // chunk -> first scope row and row count (kModeRanges: chunks never straddle ranges)
+    auto geom = [&](int cg, uint32_t& k0, int& nk) {
+        if (B.mode != kModeRanges) {
+            k0 = (uint32_t)cg * kBC;
+            nk = (int)min((uint32_t)kBC, rows - k0);
+            return;
+        }
+        for (uint32_t i = 0; i < R.n; ++i) {
+            const int cc = (int)((R.end[i] - R.begin[i] + kBC - 1) / kBC);
+            if (cg < cc) {
+                k0 = R.begin[i] + (uint32_t)cg * kBC;
+                nk = (int)min((uint32_t)kBC, R.end[i] - k0);
+                return;
+            }
+            cg -= cc;
+        }
+        k0 = 0;
+        nk = 0;
+    };
     const int cpp = (chunks + B.n_parts - 1) / B.n_parts;
     const int c_begin = part * cpp;
     const int n_ch = max(0, min(chunks, c_begin + cpp) - c_begin);
@@ -124,8 +156,9 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
         for (int c = 0; c < n_ch; ++c) {
             const int s = c % kBStages;
             if (c >= kBStages) mbar_wait(&empty[s], ((c / kBStages) & 1u) ^ 1u);
-            const uint32_t k0 = (uint32_t)(c_begin + c) * kBC;
-            const int nk = (int)min((uint32_t)kBC, rows - k0);
+            uint32_t k0;
+            int nk;
+            geom(c_begin + c, k0, nk);
             uint8_t* st = stages + (size_t)s * kBStageBytes;
             const bool valid = lane < nk;
             const uint32_t cr = !valid ? kNoIndex
@@ -202,8 +235,9 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
             const int s = c % kBStages;
             mbar_wait(&full[s], (c / kBStages) & 1u);
             __syncwarp();  // reconverge after the wait loop: the shuffles below stay simple
-            const uint32_t k0 = (uint32_t)(c_begin + c) * kBC;
-            const int nk = (int)min((uint32_t)kBC, rows - k0);
+            uint32_t k0;
+            int nk;
+            geom(c_begin + c, k0, nk);
             uint8_t* st = stages + (size_t)s * kBStageBytes;
             float4* kr4 = (float4*)(st + 2 * kBKVBytes);  // rotated keys over the cos/sin rows
             // ---- rotate the chunk's keys once (rope.hpp:347-358): read all, then write ----
@@ -413,11 +447,26 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
                 r[c] = t / At;
             }
             const int h = kv * G + g;
-            reinterpret_cast<float4*>(a.out + (size_t)h * kBD)[lane] =
-                make_float4((float)r[0], (float)r[1], (float)r[2], (float)r[3]);
-            if (lane == 0) {
-                const double hh = log(At) - Bt * 0.69314718055994530942 / At;
-                a.entropy[h] = hh < 0.0 ? 0.0 : hh;
+            if (B.merged) {  // one partial row per q head (sharded decode: combined across ranks)
+                uint8_t* row = B.merged + (size_t)h * kBPartBytes;
+                double un[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) un[c] = r[c] * At;  // back to un-normalised sums
+                reinterpret_cast<float4*>(row + 32)[lane] =
+                    make_float4((float)un[0], (float)un[1], (float)un[2], (float)un[3]);
+                if (lane == 0) {
+                    double* hd = (double*)row;
+                    hd[0] = M;
+                    hd[1] = At;
+                    hd[2] = Bt;
+                }
+            } else {
+                reinterpret_cast<float4*>(a.out + (size_t)h * kBD)[lane] =
+                    make_float4((float)r[0], (float)r[1], (float)r[2], (float)r[3]);
+                if (lane == 0) {
+                    const double hh = log(At) - Bt * 0.69314718055994530942 / At;
+                    a.entropy[h] = hh < 0.0 ? 0.0 : hh;
+                }
             }
             __syncwarp();
         }
@@ -467,6 +516,8 @@ BulkArgs bulk_args(const AttnArgs& a, void* ws, int num_sms, const DecodeFork* f
     B.mode = f ? kModeHead : kModeScope;
     B.n_local = f ? f->n_local : 0;
     B.local_row0 = f ? f->local_row0 : 0;
+    B.ranges = nullptr;
+    B.merged = nullptr;
     B.n_parts = bulk_parts(a, num_sms);
     B.part_base = 0;
     B.n_slots = B.n_parts + (f ? f->local_parts : 0);
@@ -504,6 +555,55 @@ cudaError_t launch_attend_decode_local(const AttnArgs& a, void* ws, int num_sms,
 cudaError_t launch_attend_decode_head(const AttnArgs& a, void* ws, int num_sms, const DecodeFork& f,
                                       cudaStream_t s, bool pdl) {
     return launch_bulk(bulk_args(a, ws, num_sms, &f), a.group, a.n_kv, s, pdl);
+}
+
+cudaError_t launch_attend_decode_ranges(const AttnArgs& a, void* ws, int num_sms,
+                                        const uint32_t* ranges, uint8_t* merged, cudaStream_t s) {
+    BulkArgs B = bulk_args(a, ws, num_sms, nullptr);
+    B.mode = kModeRanges;
+    B.ranges = ranges;
+    B.merged = merged;
+    return launch_bulk(B, a.group, a.n_kv, s, false);
+}
+
+namespace {
+// merge the ranks' partial rows of one q head (fixed source order): lane = 4 columns
+__global__ void __launch_bounds__(32) combine_sources_kernel(const AttnArgs a, const uint8_t* parts,
+                                                            int n_src, size_t stride) {
+    if (a.hdr && a.hdr->error != 0) return;
+    const int h = blockIdx.x, lane = threadIdx.x;
+    double M = -INFINITY;
+    for (int s = 0; s < n_src; ++s) {
+        const double* hd = (const double*)(parts + s * stride + (size_t)h * kBPartBytes);
+        if (hd[1] > 0.0) M = fmax(M, hd[0]);
+    }
+    double At = 0.0, Bt = 0.0, o[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int s = 0; s < n_src; ++s) {
+        const uint8_t* row = parts + s * stride + (size_t)h * kBPartBytes;
+        const double* hd = (const double*)row;
+        if (!(hd[1] > 0.0)) continue;
+        const double w = exp2(hd[0] - M);
+        At += hd[1] * w;
+        Bt += w * (hd[2] + (hd[0] - M) * hd[1]);
+        const float4 v = reinterpret_cast<const float4*>(row + 32)[lane];
+        o[0] = fma((double)v.x, w, o[0]);
+        o[1] = fma((double)v.y, w, o[1]);
+        o[2] = fma((double)v.z, w, o[2]);
+        o[3] = fma((double)v.w, w, o[3]);
+    }
+    reinterpret_cast<float4*>(a.out + (size_t)h * kBD)[lane] =
+        make_float4((float)(o[0] / At), (float)(o[1] / At), (float)(o[2] / At), (float)(o[3] / At));
+    if (lane == 0) {
+        const double hh = log(At) - Bt * 0.69314718055994530942 / At;
+        a.entropy[h] = hh < 0.0 ? 0.0 : hh;
+    }
+}
+}  // namespace
+
+cudaError_t launch_decode_combine_sources(const AttnArgs& a, const uint8_t* parts, int n_src,
+                                          size_t src_stride, cudaStream_t s) {
+    combine_sources_kernel<<<a.n_head, 32, 0, s>>>(a, parts, n_src, src_stride);
+    return cudaGetLastError();
 }
 
 }  // namespace reattn_impl

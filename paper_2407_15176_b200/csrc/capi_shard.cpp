@@ -33,8 +33,10 @@ struct reattn_shard_plan {
     uint32_t* scope_global = nullptr;
     uint32_t* scope_local = nullptr;
     ScopeHeader* hdr = nullptr;
-    double* part_send = nullptr;
-    double* part_recv = nullptr;
+    uint32_t* ranges = nullptr;   // ShardRanges of this rank (written by the select)
+    void* bulk_ws = nullptr;      // decode attention workspace (tickets + per-part partials)
+    double* part_send = nullptr;  // this rank's merged partial rows [n_head]
+    double* part_recv = nullptr;  // all ranks' [world][n_head]
     size_t part_bytes = 0;
     double* entropy = nullptr;
 };
@@ -89,8 +91,10 @@ void carve(reattn_shard_plan* p, Carver& c) {
     p->scope_global = c.take<uint32_t>(p->L_upper);
     p->scope_local = c.take<uint32_t>(p->L_upper);
     p->hdr = c.take<ScopeHeader>(1);
+    p->ranges = c.take<uint32_t>(sizeof(ShardRanges) / 4);
     AttnArgs a = shard_attn_args(p);
-    p->part_bytes = align_up(attend_decode_partial_bytes(a, p->L_upper), 256);
+    p->bulk_ws = c.take<uint8_t>(decode_bulk_workspace(a, p->ctx->num_sms));
+    p->part_bytes = align_up(p->n_head * kDecodePartBytes, 256);
     p->part_send = c.take<double>(p->part_bytes / 8);
     p->part_recv = c.take<double>(p->part_bytes / 8 * p->world);
     p->entropy = c.take<double>(p->n_head);
@@ -119,8 +123,8 @@ int reattn_shard_plan_create(reattn_ctx* ctx, const reattn_cache* cache, const r
         return set_err(ctx, REATTN_EINVAL, "shard plan: world must be 1..64 and rank < world");
     if (n_head % cache->n_kv != 0)
         return set_err(ctx, REATTN_EINVAL, "attend_step: n_head must be a multiple of kv heads");
-    if (rope->head_dim != cache->d || cache->d != 128)
-        return set_err(ctx, REATTN_EINVAL, "shard plan: decode path needs d_head == 128");
+    if (rope->head_dim != cache->d || cache->d != 128 || cache->dtype != REATTN_BF16)
+        return set_err(ctx, REATTN_EINVAL, "shard plan: decode path needs d_head == 128 and a bf16 cache");
     if (cfg->k == 0 || cfg->k > 8 || cfg->span_m == 0 || cfg->k_prime == 0)
         return set_err(ctx, REATTN_EINVAL, "shard plan: needs 1 <= k <= 8, span_m >= 1, k' >= 1");
     auto* p = new reattn_shard_plan();
@@ -261,6 +265,8 @@ int reattn_shard_select(reattn_shard_plan* p) {
     io.scope_src = p->scope_global;
     io.hdr = p->hdr;
     s.rank = p->rank;
+    s.world = p->world;
+    s.ranges = p->ranges;
     s.shard_begin = (uint32_t)p->shard_begin[p->rank];
     s.shard_len = (uint32_t)p->shard_len;
     s.local_src = p->scope_local;
@@ -268,16 +274,19 @@ int reattn_shard_select(reattn_shard_plan* p) {
     return REATTN_OK;
 }
 
+// this rank's scope rows (ShardRanges) -> one merged partial row per q head in part_send
 int reattn_shard_attend(reattn_shard_plan* p) {
     AttnArgs a = shard_attn_args(p);
-    CU(p->ctx, launch_attend_decode_partials(a, p->L_upper, p->ctx->stream));
+    CU(p->ctx, launch_attend_decode_ranges(a, p->bulk_ws, p->ctx->num_sms, p->ranges,
+                                           (uint8_t*)p->part_send, p->ctx->stream));
     return REATTN_OK;
 }
 
+// the all-gathered [world][n_head] partial rows -> output + entropy (fixed rank order)
 int reattn_shard_combine(reattn_shard_plan* p) {
     AttnArgs a = shard_attn_args(p);
-    a.part = p->part_recv;
-    CU(p->ctx, launch_attend_decode_combine(a, p->L_upper, p->world, p->ctx->stream));
+    CU(p->ctx, launch_decode_combine_sources(a, (const uint8_t*)p->part_recv, p->world,
+                                             p->part_bytes, p->ctx->stream));
     return REATTN_OK;
 }
 

@@ -189,11 +189,30 @@ struct ShardSelectArgs {
     int n_src, n_lists, k, kk;  // kk = min(k, global middle length)
     uint32_t src_offset[64];    // shard_begin of each source rank
     SmallSelectIO sel;          // global geometry; sel.scope_src receives the GLOBAL table
-    int rank;
+    int rank, world;
     uint32_t shard_begin, shard_len;
-    uint32_t* local_src;        // [L'] local cache row, or kNoIndex when owned elsewhere
+    uint32_t* local_src;        // [L'] local cache row, or kNoIndex (a middle row held elsewhere)
+    uint32_t* ranges;           // ShardRanges: the scope rows this rank attends
 };
 cudaError_t launch_shard_merge_select(const ShardSelectArgs& a, cudaStream_t s);
+// Scope rows (index ranges [begin, end) in scope order) attended by one rank of a sharded
+// decode step: rank 0 the global rows, every rank its own span rows and a 32-row aligned
+// 1/world slice of the local window.  Written on the device by the shard select.
+struct ShardRanges {
+    uint32_t n;
+    uint32_t begin[3], end[3];
+};
+// Sharded decode attention: the bulk decode kernel over the rank's ShardRanges; the parts of
+// each kv head are merged on the device into ONE partial row per q head at `merged`
+// ([n_head] rows of kDecodePartBytes: f64 m (log2), A, B, pad; fp32 acc[128]).  ws as
+// decode_bulk_workspace.
+constexpr int kDecodePartBytes = 32 + 128 * 4;
+cudaError_t launch_attend_decode_ranges(const AttnArgs& a, void* ws, int num_sms,
+                                        const uint32_t* ranges, uint8_t* merged, cudaStream_t s);
+// Final merge of n_src ranks' merged partial rows (rank s at parts + s * src_stride bytes,
+// [n_head] rows each) -> out + entropy.
+cudaError_t launch_decode_combine_sources(const AttnArgs& a, const uint8_t* parts, int n_src,
+                                          size_t src_stride, cudaStream_t s);
 
 // ---- misc kernels ------------------------------------------------------------------
 // rows x (n_kv*d) fp32 (DenseMatrix layout) -> head-major [n_kv][head_stride][d] at row0.

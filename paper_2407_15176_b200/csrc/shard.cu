@@ -7,8 +7,11 @@
 // under (score desc, index asc) is the exact global top-k (selection.hpp:81-135 ordering),
 // so after an all-gather every rank merges identically and continues with the reference's
 // vote / expand_spans / assemble_scope (selection.hpp:359-456, scope.hpp:248-272).
-// Replicated rows (global, local) are attended by rank 0 only; a middle row by its owner;
-// everything else is masked (kNoIndex) so partial attention states can be combined.
+// The scope table is translated to this rank's local cache rows (replicated global and local
+// rows exist on every rank; a middle row only at its owner), and the rank's share of the
+// attention is written as ShardRanges: rank 0 the global rows, every rank the span rows of
+// its own shard (contiguous in scope order) and a 32-row aligned 1/world slice of the local
+// window -- every scope row is attended by exactly one rank, and the work is balanced.
 #include "common.cuh"
 #include "kernels.h"
 #include "select_small.cuh"
@@ -84,23 +87,57 @@ __global__ void __launch_bounds__(kMergeThreads) shard_merge_select_kernel(const
     const bool valid = tid < n && m_idx[tid < n ? tid : 0] != kNoIndex;
     small_select_scope(a.sel, valid ? m_idx[tid] : 0u, valid ? m_score[tid] : 0.0f, valid, ssel);
     __syncthreads();
-    // ---- translate to this rank's local rows (kNoIndex = not owned here) ----
+    // ---- translate to this rank's local rows; find the rank's span rows ----
+    __shared__ uint32_t s_mb, s_me;
+    if (tid == 0) {
+        s_mb = 0xFFFFFFFFu;
+        s_me = 0;
+    }
+    __syncthreads();
     if (ssel.err != 0) return;
     const uint32_t L = ssel.L;
     for (uint32_t r = tid; r < L; r += blockDim.x) {
         const uint32_t s = a.sel.scope_src[r];
         uint32_t local;
         if (s < a.sel.g_end) {
-            local = a.rank == 0 ? s : kNoIndex;
+            local = s;
         } else if (s >= a.sel.l_start) {
-            local = a.rank == 0 ? a.sel.g_end + a.shard_len + (s - a.sel.l_start) : kNoIndex;
+            local = a.sel.g_end + a.shard_len + (s - a.sel.l_start);
         } else {
             const uint32_t m = s - a.sel.g_end;
-            local = (m >= a.shard_begin && m < a.shard_begin + a.shard_len)
-                        ? a.sel.g_end + (m - a.shard_begin)
-                        : kNoIndex;
+            const bool mine = m >= a.shard_begin && m < a.shard_begin + a.shard_len;
+            local = mine ? a.sel.g_end + (m - a.shard_begin) : kNoIndex;
+            if (mine) {
+                atomicMin(&s_mb, r);
+                atomicMax(&s_me, r + 1);
+            }
         }
         a.local_src[r] = local;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const uint32_t n_local = a.sel.total - a.sel.l_start;
+        const uint32_t lb = L - n_local;
+        auto cut = [&](int r) {  // 32-row aligned split of the local window
+            return (uint32_t)(((uint64_t)r * n_local / (uint32_t)a.world) / 32u * 32u);
+        };
+        const uint32_t c0 = a.rank == 0 ? 0u : cut(a.rank);
+        const uint32_t c1 = a.rank + 1 == a.world ? n_local : cut(a.rank + 1);
+        ShardRanges R;
+        R.n = 0;
+        if (a.rank == 0 && a.sel.g_end > 0) {
+            R.begin[R.n] = 0;
+            R.end[R.n++] = a.sel.g_end;
+        }
+        if (s_mb < s_me) {
+            R.begin[R.n] = s_mb;
+            R.end[R.n++] = s_me;
+        }
+        if (c1 > c0) {
+            R.begin[R.n] = lb + c0;
+            R.end[R.n++] = lb + c1;
+        }
+        *(ShardRanges*)a.ranges = R;
     }
 }
 

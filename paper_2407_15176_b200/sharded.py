@@ -101,20 +101,47 @@ class NativeOps:
 
 
 class ShardedDecodeStep:
-    """One rank's sequence-sharded decode step.  All ranks call step() collectively."""
+    """One rank's sequence-sharded decode step.  All ranks call step() collectively.
+
+    capture() records the whole step -- K scan, candidate all-gather (NCCL), merge + vote +
+    spans + scope, attention over this rank's scope rows, partial-state all-gather (NCCL),
+    combine -- as ONE CUDA graph on the context stream (NCCL collectives are captured like
+    kernels), so a step costs one graph launch instead of six host launches."""
 
     def __init__(self, ops, group=None):
         self.ops = ops
         self.group = group
+        self.graph = None
 
-    def step(self, q):
+    def _body(self):
         import torch.distributed as dist
         o = self.ops
-        o.q.copy_(q)
         o.scan()
         dist.all_gather_into_tensor(o.cand_recv, o.cand_send, group=self.group)
         o.select()
         o.attend()
         dist.all_gather_into_tensor(o.part_recv, o.part_send, group=self.group)
         o.combine()
+
+    def step(self, q):
+        o = self.ops
+        o.q.copy_(q)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._body()
         return o.out
+
+    def capture(self):
+        """Capture the step for the query buffer ops.q (call collectively on every rank, on
+        the stream the context launches on)."""
+        import torch
+        s = torch.cuda.current_stream()
+        self._body()  # warm-up outside capture: communicator and kernel attribute set-up
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self._body()
+        torch.cuda.synchronize()
+        self.graph = g
+        return self

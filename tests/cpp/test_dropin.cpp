@@ -446,7 +446,13 @@ static void test_snapshot() {
                         ok = gk == want && gv == wv;
                     else
                         ok = gk == oracle_round_bf16(want) && gv == oracle_round_bf16(wv);
+                    if (!ok)
+                        std::printf("snapshot mismatch layer %zu head %zu elem %zu: key %g/%g value %g/%g\n",
+                                    l, h, e, gk, want, gv, wv);
                 }
+            if (!ok && l < back.size())
+                std::printf("snapshot layer %zu: total %zu/%zu g %zu local %zu\n", l, back[l].total(),
+                            layers[l].total(), back[l].l_global(), back[l].l_local_max());
         }
         CHECK(ok, "snapshot round trip storage=%d", (int)storage);
     }

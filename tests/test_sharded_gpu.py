@@ -1,7 +1,7 @@
 """Sequence-sharded decode on one GPU: W ranks' device stages run one after another in one
 process (no kernel waits on another rank), the two all-gathers replaced by device copies.
-The result must equal the unsharded attend_step: same spans and L', outputs within 1e-7
-(only the order of the f64 partial merge differs)."""
+The result must equal the unsharded attend_step: same spans and L', outputs within 1e-6
+(the ranks attend disjoint scope rows with fp32 logits; only the merge order differs)."""
 import numpy as np
 import pytest
 
