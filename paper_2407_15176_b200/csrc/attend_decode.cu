@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
     if (warp < 4) {
         float* w_s = (float*)stages + warp * kBMaxParts;
         for (int g = warp; g < G; g += 4) {
+            __syncwarp();  // converged: plain SHFLs (see scan_topk.cu flush)
             auto prow = [&](int p) {
                 return B.part + (((size_t)p * a.n_kv + kv) * G + g) * kBPartBytes;
             };

@@ -3,7 +3,9 @@
 // Same contract as select_kernel (select.cu), restating selection.hpp:359-456 and
 // scope.hpp:248-289, but every ranking is an all-pairs count over shuffles in one warp
 // (32x32 compares) instead of block-wide bitonic sorts, so it costs a few hundred cycles.
-// Used by the select kernel's small path and fused into the K-scan's last CTA.
+// Used by the select kernel's small path and fused into the K-scan's last CTA.  The 32-way
+// shuffle loops are unrolled so their shuffles pipeline (rolled, each iteration waited on
+// its own shuffle latency: ~10 us in the scan's tail).
 #pragma once
 
 #include "common.cuh"
@@ -26,6 +28,9 @@ __device__ __forceinline__ void small_select_scope(const SmallSelectIO& io, uint
     using namespace reattn_dev;
     const int tid = threadIdx.x;
     if (tid < 32) {
+        // warp 0 is converged here: lets the compiler emit plain SHFLs instead of the
+        // collective fallback it needs for shuffles in a possibly divergent region
+        __syncwarp();
         const int i = tid;
         const uint32_t FULL = 0xFFFFFFFFu;
         const bool valid = c_valid && io.k_prime > 0;

@@ -87,10 +87,30 @@ def main():
             torch.cuda.synchronize()
             for o in ops:
                 stages["combine"].append(timed(o.combine, stream, flush))
+            # each rank's whole step as one CUDA graph, the two all-gathers replaced by
+            # device copies from the buffers gathered above (what NCCL would deliver)
+            cand_all, part_all = cand.clone(), part.clone()
+            graph_us = []
+            for o in ops:
+                def body(o=o):
+                    o.scan()
+                    o.cand_recv.copy_(cand_all)
+                    o.select()
+                    o.attend()
+                    o.part_recv.copy_(part_all)
+                    o.combine()
+                body()
+                torch.cuda.synchronize()
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, stream=stream):
+                    body()
+                graph_us.append(timed(gr.replay, stream, flush))
+                del gr
+            stages["graph_step"] = graph_us
             mx = {k: round(max(v), 1) for k, v in stages.items()}
             line = {"world": world, "ctx": total, "per_stage_max_over_ranks_us": mx,
                     "per_rank_us": {k: [round(x, 1) for x in v] for k, v in stages.items()},
-                    "device_sum_us": round(sum(mx.values()), 1),
+                    "device_sum_us": round(sum(v for k, v in mx.items() if k != "graph_step"), 1),
                     "exchange_bytes_per_rank": [int(ops[0].cand_send.numel() * ops[0].cand_send.element_size()),
                                                 int(ops[0].part_send.numel() * ops[0].part_send.element_size())],
                     "note": "one GPU, ranks timed one at a time; excludes the two NCCL all-gathers"}
