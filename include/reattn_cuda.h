@@ -216,6 +216,25 @@ int reattn_plan_stats(reattn_plan* plan, reattn_step_stats* stats);
 int reattn_plan_info(const reattn_plan* plan, uint64_t* kernels_per_step,
                      uint64_t* scan_bytes, uint64_t* scope_bytes);
 
+/* ---- batched decode (one graph over n_seq sequences with their own caches) ----------- */
+/* Batch > 1 is a reference non-goal; each sequence's result is exactly its own
+ * attend_step (engine.hpp:501, n_q = 1).  bf16 decode with a middle: the scans run back to
+ * back while sequence b's attention runs beside scan b+1 on `side_sms` spare SMs.
+ * q / out: [n_seq][n_head * d] fp32 on the device. */
+typedef struct reattn_batch_plan reattn_batch_plan;
+int reattn_batch_plan_create(reattn_ctx* ctx, const reattn_cache* const* caches, uint32_t n_seq,
+                             const reattn_rope* rope, uint64_t n_head,
+                             const reattn_selection_config* cfg, int mode,
+                             reattn_batch_plan** out);
+void reattn_batch_plan_destroy(reattn_batch_plan* plan);
+float* reattn_batch_plan_q(const reattn_batch_plan* plan);
+float* reattn_batch_plan_out(const reattn_batch_plan* plan);
+int reattn_batch_plan_launch(reattn_batch_plan* plan);
+int reattn_batch_plan_run_host(reattn_batch_plan* plan, const float* q_host, float* out_host);
+int reattn_batch_plan_stats(reattn_batch_plan* plan, uint32_t seq, reattn_step_stats* stats);
+int reattn_batch_plan_info(const reattn_batch_plan* plan, uint64_t* kernels_per_step,
+                           uint64_t* scan_bytes, int* side_sms);
+
 /* ---- sequence-sharded decode ---------------------------------------- */
 /* Rank `rank` of `world` holds [global | its middle shard | local] in `local_cache` (same
  * l_global / l_local as the unsharded cache; the shard is the local cache's middle).  The

@@ -8,18 +8,22 @@
 //   attend                  attend.hpp:404-456  scale 1/sqrt(d), row entropy ln A - B/A
 //
 // The decode scope is small (L' ~ 5K rows, 21 MB of K+V at 1M context) and the step is
-// latency-bound unless ~1/3 of it is in flight at once, so the layout is:
-//   grid (n_parts, n_kv), n_parts * n_kv <= #SMs: one wave, one CTA per SM; part p of kv
-//   head h owns a contiguous range of 32-row chunks of the scope (sized from the device L').
-//   warp 4 (producer): per chunk, one cp.async.bulk per scope row for K and for V (256 B,
-//     gathered through the scope table) plus the chunk's RoPE cos / sin rows (contiguous
-//     compact positions), into a 5-stage ring of 32 KB stages (160 KB in flight per SM).
-//   warps 0-3 (compute): rotate the chunk's keys once into an fp32 scratch (double
-//     buffered), then one warp per q head of the GQA group: lane j = key j logits (fp32,
-//     query pre-scaled by log2(e)/sqrt(d)), warp max / sums by shuffle, online (m, A, B)
-//     state (A, B in f64), P·V with lane = 4 output columns and p_j broadcast by shuffle.
-//   The last CTA of each kv head (atomic ticket, re-armed for graph replay) merges the
-//   parts' partial states in part order (deterministic) and writes the output and entropy.
+// latency-bound unless a large part of it is in flight at once, so the layout is:
+//   grid (n_parts, n_kv), one CTA per SM (197 KB smem); part p of kv head h owns a
+//   contiguous range of 32-row chunks of its rows (sized from the device L').
+//   warp 16 (producer): per chunk, one cp.async.bulk per run of consecutive cache rows for K
+//     and for V (gathered through the scope table) plus the chunk's RoPE cos / sin rows, into
+//     a 6-stage ring of 32 KB stages.
+//   warps 0-15 (compute): 4 groups of 4 warps take chunks round-robin; a group rotates the
+//     chunk's keys once into fp32 over the stage's cos/sin area (XOR-swizzled), then one warp
+//     per q head: lane j = key j logits (fp32, query pre-scaled by log2(e)/sqrt(d)), warp
+//     max / sums by shuffle, online (m, A, B) state (A, B in f64), P·V with lane = 4 output
+//     columns and p_j broadcast by shuffle.  The groups merge through shared memory.
+//   The last CTA of each kv head (atomic ticket, re-armed for graph replay) merges the parts'
+//   partial states in part order (deterministic) and writes the output and entropy, or one
+//   merged partial row per head (sharded decode).
+// Modes: the whole scope, the local window beside the scan (decode fork), the rows after it,
+// or a rank's ShardRanges (see BulkArgs).
 // Numerics: fp32 logits / accumulation within a CTA, f64 across parts: max-abs ~1e-8 on the
 // reference's f64 attend at the decode geometry (north_star fp32 bar: 1e-5).
 #include <algorithm>
@@ -37,6 +41,8 @@ constexpr int kBC = 32;                        // scope rows per chunk
 constexpr int kBD = 128;                       // d = dv
 constexpr int kBStages = 6;
 constexpr int kBGroups = 4;                    // compute groups (4 warps each) per CTA
+// chunks c and c - 2*kBStages must belong to the same group (see the consumer's stage wait)
+static_assert((2 * kBStages) % kBGroups == 0, "stage ring / group interleave");
 constexpr int kBKVBytes = kBC * kBD * 2;       // K or V of one chunk (bf16): 8 KB
 constexpr int kBRopeBytes = kBC * (kBD / 2) * 4;  // cos or sin rows of one chunk: 8 KB
 constexpr int kBStageBytes = 2 * kBKVBytes + 2 * kBRopeBytes;
@@ -233,6 +239,12 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
         }
         for (int c = gi; c < n_ch; c += kBGroups) {
             const int s = c % kBStages;
+            // Stage s holds chunks c-6, c, c+6 ... consumed by DIFFERENT groups, so a parity
+            // wait on full[s] alone could be satisfied by chunk c-6's completed phase while
+            // chunk c is not loaded yet.  Wait for chunk c-6's release first (unambiguous:
+            // chunk c-12 belongs to this group and is consumed); after it, full[s] is at most
+            // one phase ahead of what we wait for.
+            if (c >= kBStages) mbar_wait(&empty[s], ((c / kBStages) - 1) & 1u);
             mbar_wait(&full[s], (c / kBStages) & 1u);
             __syncwarp();  // reconverge after the wait loop: the shuffles below stay simple
             uint32_t k0;
@@ -541,6 +553,11 @@ size_t decode_bulk_workspace(const AttnArgs& a, int num_sms) {
 
 cudaError_t launch_attend_decode_bulk(const AttnArgs& a, void* ws, int num_sms, cudaStream_t s) {
     return launch_bulk(bulk_args(a, ws, num_sms, nullptr), a.group, a.n_kv, s, true);
+}
+
+cudaError_t launch_attend_decode_bulk_ex(const AttnArgs& a, void* ws, int num_sms, cudaStream_t s,
+                                         bool pdl) {
+    return launch_bulk(bulk_args(a, ws, num_sms, nullptr), a.group, a.n_kv, s, pdl);
 }
 
 cudaError_t launch_attend_decode_local(const AttnArgs& a, void* ws, int num_sms, const DecodeFork& f,

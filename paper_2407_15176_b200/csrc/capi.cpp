@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -195,8 +196,11 @@ void carve_step(StepPlan& P, const reattn_cache* cache, const reattn_rope* rope,
     P.scratch_bytes = c.off;
 }
 
-int enqueue_step(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache, const reattn_rope* rope,
-                 const float* q_dev, float* out_dev, cudaStream_t s, bool zero_ticket) {
+// The selection half of a step: the local-window fork (when planned), K1 (+ fused K3) or the
+// standalone select / large vote.  Leaves the scope header and table on the device.
+int enqueue_select_part(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache,
+                        const reattn_rope* rope, const float* q_dev, float* out_dev, cudaStream_t s,
+                        bool zero_ticket) {
     P.kernels = 0;
     SelectArgs sa;
     std::memset(&sa, 0, sizeof(sa));
@@ -267,8 +271,22 @@ int enqueue_step(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache, const 
         CU(ctx, launch_select(sa, s));
         ++P.kernels;
     }
+    return REATTN_OK;
+}
+
+// The attention half on stream `s`.  attn_sms < num_sms (batch pipelines): the decode
+// attention runs on that many SMs beside another sequence's scan, without PDL.
+int enqueue_attn_part(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache,
+                      const reattn_rope* rope, const float* q_dev, float* out_dev, cudaStream_t s,
+                      bool zero_ticket, int attn_sms) {
     if (P.n_q > 0) {
         AttnArgs a = step_attn_args(P, cache, rope, q_dev, out_dev);
+        if (attn_sms > 0 && attn_sms < ctx->num_sms && decode_bulk_eligible(a) && !P.fork) {
+            if (zero_ticket) CU(ctx, cudaMemsetAsync(P.part, 0, 256, s));
+            CU(ctx, launch_attend_decode_bulk_ex(a, P.part, attn_sms, s, false));
+            ++P.kernels;
+            return REATTN_OK;
+        }
         // the bulk decode attention's tickets sit at the start of P.part (plans: zeroed once)
         if (zero_ticket && decode_bulk_eligible(a)) CU(ctx, cudaMemsetAsync(P.part, 0, 256, s));
         if (P.fork) {
@@ -284,6 +302,13 @@ int enqueue_step(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache, const 
         }
     }
     return REATTN_OK;
+}
+
+int enqueue_step(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache, const reattn_rope* rope,
+                 const float* q_dev, float* out_dev, cudaStream_t s, bool zero_ticket) {
+    int rc = enqueue_select_part(ctx, P, cache, rope, q_dev, out_dev, s, zero_ticket);
+    if (rc) return rc;
+    return enqueue_attn_part(ctx, P, cache, rope, q_dev, out_dev, s, zero_ticket, 0);
 }
 
 int finish_step_stats(reattn_ctx* ctx, const StepPlan& P, const ScopeHeader& h,
@@ -959,6 +984,186 @@ int reattn_synth_uniform(reattn_ctx* ctx, void* dst, uint64_t n, int dtype, uint
     if (n == 0) return REATTN_OK;
     CU(ctx, launch_synth_uniform(dst, dtype, n, seed, offset, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+
+// ---- batched decode: one graph over n_seq independent sequences (own caches) ---------------
+// The decode scan is HBM-bound and sequences share no bytes, so batching cannot save
+// traffic; it hides latency instead.  Pipelined (bf16 decode): the scans run back to back on
+// num_sms - R SMs while sequence b's attention runs on the R spare SMs beside scan b+1 (side
+// stream, event per sequence); only the last sequence's attention runs on the whole GPU.
+struct reattn_batch_plan {
+    reattn_ctx* ctx = nullptr;
+    const reattn_rope* rope = nullptr;
+    std::vector<const reattn_cache*> caches;
+    std::vector<StepPlan> P;
+    uint64_t n_head = 0, d = 0;
+    void* mem = nullptr;
+    float* q = nullptr;
+    float* out = nullptr;
+    bool pipelined = false;
+    int side_sms = 0;
+    cudaStream_t side = nullptr;
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t ev_done = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t kernels = 0;
+    ~reattn_batch_plan() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        for (auto e : ev) cudaEventDestroy(e);
+        if (ev_done) cudaEventDestroy(ev_done);
+        if (side) cudaStreamDestroy(side);
+        if (mem) cudaFree(mem);
+    }
+};
+
+int reattn_batch_plan_create(reattn_ctx* ctx, const reattn_cache* const* caches, uint32_t n_seq,
+                             const reattn_rope* rope, uint64_t n_head,
+                             const reattn_selection_config* cfg, int mode,
+                             reattn_batch_plan** out) {
+    *out = nullptr;
+    if (n_seq == 0 || !caches) return set_err(ctx, REATTN_EINVAL, "batch plan: no sequences");
+    auto bp = std::make_unique<reattn_batch_plan>();
+    bp->ctx = ctx;
+    bp->rope = rope;
+    bp->caches.assign(caches, caches + n_seq);
+    bp->P.resize(n_seq);
+    bp->n_head = n_head;
+    bp->d = caches[0]->d;
+    bool pipe = n_seq > 1;
+    double t_scan = 0.0, t_attn = 0.0;
+    for (uint32_t b = 0; b < n_seq; ++b) {
+        if (caches[b]->d != bp->d)
+            return set_err(ctx, REATTN_EINVAL, "batch plan: every cache needs the same d_head");
+        int rc = plan_step(ctx, caches[b], rope, 1, n_head, cfg, mode, bp->P[b], nullptr, nullptr);
+        if (rc) return rc;
+        StepPlan& P = bp->P[b];
+        P.fork = false;
+        P.scan.grid_sms = 0;
+        pipe = pipe && P.select && P.scan.fast && P.d == 128 && caches[b]->dtype == kBF16 &&
+               P.group <= 8;
+        t_scan = std::max(t_scan, (double)P.middle * P.n_kv * P.d * 2 / 5.8e6);
+        t_attn = std::max(t_attn, (double)((P.L_upper + 31) / 32) * P.n_kv * 0.8);  // us x SM
+    }
+    if (pipe) {
+        const uint64_t n_kv = bp->P[0].n_kv;
+        int m = 1;
+        while (m < 4 && (int)(m * n_kv) * 8 <= ctx->num_sms && t_attn / (m * n_kv) > 0.8 * t_scan) ++m;
+        bp->side_sms = (int)(m * n_kv);
+        for (auto& P : bp->P) P.scan.grid_sms = ctx->num_sms - bp->side_sms;
+    }
+    bp->pipelined = pipe;
+    const uint64_t row = n_head * bp->d;
+    Carver sizer{nullptr, 0, 0};
+    sizer.take<float>(n_seq * row);
+    sizer.take<float>(n_seq * row);
+    for (uint32_t b = 0; b < n_seq; ++b) carve_step(bp->P[b], caches[b], rope, sizer);
+    cudaError_t e = cudaMalloc(&bp->mem, sizer.off + 256);
+    if (e == cudaSuccess) e = cudaMemset(bp->mem, 0, sizer.off + 256);
+    if (e != cudaSuccess)
+        return set_err(ctx, REATTN_ECUDA, std::string("batch plan allocation: ") + cudaGetErrorString(e));
+    Carver c{(uint8_t*)bp->mem, 0, sizer.off + 256};
+    bp->q = c.take<float>(n_seq * row);
+    bp->out = c.take<float>(n_seq * row);
+    for (uint32_t b = 0; b < n_seq; ++b) carve_step(bp->P[b], caches[b], rope, c);
+    CU(ctx, cudaStreamCreateWithFlags(&bp->side, cudaStreamNonBlocking));
+    bp->ev.resize(n_seq, nullptr);
+    for (auto& ev : bp->ev) CU(ctx, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CU(ctx, cudaEventCreateWithFlags(&bp->ev_done, cudaEventDisableTiming));
+    // capture
+    cudaStream_t cs;
+    CU(ctx, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CU(ctx, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    int rc = REATTN_OK;
+    for (uint32_t b = 0; b < n_seq && !rc; ++b) {
+        StepPlan& P = bp->P[b];
+        const float* qb = bp->q + b * row;
+        float* ob = bp->out + b * row;
+        if (!pipe) {
+            rc = enqueue_step(ctx, P, caches[b], rope, qb, ob, cs, false);
+            bp->kernels += P.kernels;
+            continue;
+        }
+        rc = enqueue_select_part(ctx, P, caches[b], rope, qb, ob, cs, false);
+        if (rc) break;
+        if (b + 1 < n_seq) {  // this sequence's attention beside the next scan
+            if (cudaEventRecord(bp->ev[b], cs) != cudaSuccess ||
+                cudaStreamWaitEvent(bp->side, bp->ev[b], 0) != cudaSuccess) {
+                rc = set_err(ctx, REATTN_ECUDA, "batch plan: event capture failed");
+                break;
+            }
+            rc = enqueue_attn_part(ctx, P, caches[b], rope, qb, ob, bp->side, false, bp->side_sms);
+        } else {
+            rc = enqueue_attn_part(ctx, P, caches[b], rope, qb, ob, cs, false, 0);
+        }
+        bp->kernels += P.kernels;
+    }
+    if (!rc && pipe) {
+        if (cudaEventRecord(bp->ev_done, bp->side) != cudaSuccess ||
+            cudaStreamWaitEvent(cs, bp->ev_done, 0) != cudaSuccess)
+            rc = set_err(ctx, REATTN_ECUDA, "batch plan: event capture failed");
+    }
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+    cudaStreamDestroy(cs);
+    if (rc || ce != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        return rc ? rc : set_err(ctx, REATTN_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    }
+    bp->graph = g;
+    e = cudaGraphInstantiate(&bp->exec, g, 0);
+    if (e != cudaSuccess)
+        return set_err(ctx, REATTN_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    *out = bp.release();
+    return REATTN_OK;
+}
+
+void reattn_batch_plan_destroy(reattn_batch_plan* p) {
+    if (!p) return;
+    cudaDeviceSynchronize();
+    delete p;
+}
+
+float* reattn_batch_plan_q(const reattn_batch_plan* p) { return p->q; }
+float* reattn_batch_plan_out(const reattn_batch_plan* p) { return p->out; }
+
+int reattn_batch_plan_launch(reattn_batch_plan* p) {
+    CU(p->ctx, cudaGraphLaunch(p->exec, p->ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_batch_plan_run_host(reattn_batch_plan* p, const float* q_host, float* out_host) {
+    const size_t bytes = p->P.size() * p->n_head * p->d * sizeof(float);
+    reattn_ctx* ctx = p->ctx;
+    CU(ctx, cudaMemcpyAsync(p->q, q_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    CU(ctx, cudaGraphLaunch(p->exec, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(out_host, p->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_batch_plan_stats(reattn_batch_plan* p, uint32_t seq, reattn_step_stats* st) {
+    if (seq >= p->P.size()) return set_err(p->ctx, REATTN_ERANGE, "batch plan: sequence out of range");
+    reattn_ctx* ctx = p->ctx;
+    ScopeHeader h;
+    CU(ctx, cudaMemcpyAsync(&h, p->P[seq].hdr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return finish_step_stats(ctx, p->P[seq], h, st, nullptr);
+}
+
+int reattn_batch_plan_info(const reattn_batch_plan* p, uint64_t* kernels, uint64_t* scan_bytes,
+                           int* side_sms) {
+    uint64_t bytes = 0;
+    for (size_t b = 0; b < p->P.size(); ++b) {
+        const uint64_t esz = p->caches[b]->dtype == REATTN_BF16 ? 2 : 4;
+        if (p->P[b].select) bytes += p->P[b].n_kv * p->P[b].middle * p->P[b].d * esz;
+    }
+    if (kernels) *kernels = p->kernels;
+    if (scan_bytes) *scan_bytes = bytes;
+    if (side_sms) *side_sms = p->pipelined ? p->side_sms : 0;
     return REATTN_OK;
 }
 

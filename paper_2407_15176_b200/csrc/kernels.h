@@ -153,6 +153,9 @@ int attend_kernel_count(const AttnArgs& a, uint32_t L_max);
 bool decode_bulk_eligible(const AttnArgs& a);
 size_t decode_bulk_workspace(const AttnArgs& a, int num_sms);
 cudaError_t launch_attend_decode_bulk(const AttnArgs& a, void* ws, int num_sms, cudaStream_t s);
+// same on `num_sms` SMs' worth of CTAs, with or without programmatic dependent launch
+cudaError_t launch_attend_decode_bulk_ex(const AttnArgs& a, void* ws, int num_sms, cudaStream_t s,
+                                         bool pdl);
 // Local-window fork: the last n_local scope rows are the cache's local segment, independent of
 // the selection (RoPE is relative, so they can be attended at positions 0..n_local-1 with the
 // query at n_local-1).  The local launch runs beside the scan on local_parts CTAs per kv head

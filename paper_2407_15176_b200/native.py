@@ -126,6 +126,15 @@ SIGNATURES = [
     ("reattn_plan_run_host", C.c_int, [vp, vp, vp]),
     ("reattn_plan_stats", C.c_int, [vp, C.POINTER(StepStats)]),
     ("reattn_plan_info", C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
+    ("reattn_batch_plan_create", C.c_int, [vp, C.POINTER(vp), C.c_uint32, vp, u64, vp, C.c_int,
+                                           C.POINTER(vp)]),
+    ("reattn_batch_plan_destroy", None, [vp]),
+    ("reattn_batch_plan_q", vp, [vp]),
+    ("reattn_batch_plan_out", vp, [vp]),
+    ("reattn_batch_plan_launch", C.c_int, [vp]),
+    ("reattn_batch_plan_run_host", C.c_int, [vp, vp, vp]),
+    ("reattn_batch_plan_stats", C.c_int, [vp, C.c_uint32, vp]),
+    ("reattn_batch_plan_info", C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(C.c_int)]),
     ("reattn_synth_uniform", C.c_int, [vp, vp, u64, C.c_int, u64, u64]),
     ("reattn_shard_plan_create", C.c_int, [vp, vp, vp, u64, C.POINTER(SelectionConfig), u64,
                                            C.c_int, C.c_int, C.POINTER(vp)]),
@@ -478,4 +487,46 @@ class Plan:
         # dependents keep their Context alive; skip if it was closed explicitly
         if getattr(self, "h", None) and self.ctx.h:
             self.ctx.lib.reattn_plan_destroy(self.h)
+            self.h = None
+
+
+class BatchPlan:
+    """Batched decode: one CUDA graph over n_seq sequences, each with its own cache
+    (reattn_batch_plan_*).  q / out: [n_seq, n_head*d] fp32 device tensors."""
+
+    def __init__(self, ctx: Context, caches, rope: Rope, n_head: int, cfg: SelectionConfig,
+                 mode: int = MODE_REATTENTION):
+        import torch
+        self.ctx, self.caches, self.rope = ctx, list(caches), rope
+        arr = (vp * len(self.caches))(*[c.h for c in self.caches])
+        h = vp()
+        ctx.check(ctx.lib.reattn_batch_plan_create(ctx.h, arr, len(self.caches), rope.h, n_head,
+                                                   C.byref(cfg), mode, C.byref(h)))
+        self.h = h
+        n, d = len(self.caches), self.caches[0].d
+        numel = n * n_head * d
+        self.q = _wrap_device(ctx.lib.reattn_batch_plan_q(h), numel, torch.float32,
+                              ctx.device).view(n, -1)
+        self.out = _wrap_device(ctx.lib.reattn_batch_plan_out(h), numel, torch.float32,
+                                ctx.device).view(n, -1)
+
+    def launch(self) -> None:
+        self.ctx.check(self.ctx.lib.reattn_batch_plan_launch(self.h))
+
+    def run_host(self, q_host, out_host) -> None:
+        self.ctx.check(self.ctx.lib.reattn_batch_plan_run_host(self.h, _ptr(q_host), _ptr(out_host)))
+
+    def stats(self, seq: int) -> StepStats:
+        st = StepStats()
+        self.ctx.check(self.ctx.lib.reattn_batch_plan_stats(self.h, seq, C.byref(st)))
+        return st
+
+    def info(self) -> dict:
+        a, b, c = u64(), u64(), C.c_int()
+        self.ctx.check(self.ctx.lib.reattn_batch_plan_info(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"kernels_per_step": a.value, "scan_bytes": b.value, "side_sms": c.value}
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.ctx.h:
+            self.ctx.lib.reattn_batch_plan_destroy(self.h)
             self.h = None

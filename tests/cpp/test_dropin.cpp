@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <unistd.h>
+
 #include "../../oracle/reattn_oracle.h"
 #include "reattn/reattn.hpp"
 
@@ -430,7 +432,7 @@ static void test_snapshot() {
         if (t) c.append(random_rows(t, 32, rng), random_rows(t, 32, rng));
         layers.push_back(std::move(c));
     }
-    const std::string path = "/tmp/reattn_dropin_snapshot.rkvc";
+    const std::string path = "/tmp/reattn_dropin_snapshot_" + std::to_string(::getpid()) + ".rkvc";
     write_cache_snapshot(path, std::span<const SegmentedKvCache>(layers));
     for (auto storage : {SegmentedKvCache::Storage::F32, SegmentedKvCache::Storage::BF16}) {
         auto back = read_cache_snapshot(path, storage);
