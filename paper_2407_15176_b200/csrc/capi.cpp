@@ -1041,14 +1041,16 @@ int reattn_batch_plan_create(reattn_ctx* ctx, const reattn_cache* const* caches,
         int rc = plan_step(ctx, caches[b], rope, 1, n_head, cfg, mode, bp->P[b], nullptr, nullptr);
         if (rc) return rc;
         StepPlan& P = bp->P[b];
-        P.fork = false;
-        P.scan.grid_sms = 0;
         pipe = pipe && P.select && P.scan.fast && P.d == 128 && caches[b]->dtype == kBF16 &&
                P.group <= 8;
         t_scan = std::max(t_scan, (double)P.middle * P.n_kv * P.d * 2 / 5.8e6);
         t_attn = std::max(t_attn, (double)((P.L_upper + 31) / 32) * P.n_kv * 0.8);  // us x SM
     }
-    if (pipe) {
+    if (pipe) {  // the pipeline replaces the per-sequence local-window fork
+        for (auto& P : bp->P) {
+            P.fork = false;
+            P.scan.grid_sms = 0;
+        }
         const uint64_t n_kv = bp->P[0].n_kv;
         int m = 1;
         while (m < 4 && (int)(m * n_kv) * 8 <= ctx->num_sms && t_attn / (m * n_kv) > 0.8 * t_scan) ++m;
