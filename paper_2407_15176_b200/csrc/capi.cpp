@@ -366,7 +366,9 @@ int reattn_ctx_create(int device, reattn_ctx** out) {
     auto* ctx = new reattn_ctx();
     ctx->device = device;
     cudaError_t e = cudaSetDevice(device);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    // a BLOCKING stream: work the caller issues on the legacy default stream (e.g. torch's
+    // default-stream uploads, cudaMemcpy) is ordered with this context's kernels
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamDefault);
     if (e != cudaSuccess) {
         delete ctx;
         *out = nullptr;
@@ -589,6 +591,9 @@ int reattn_rope_create(reattn_ctx* ctx, uint64_t head_dim, double base, uint64_t
     if (e == cudaSuccess) e = cudaMalloc(&r->sin_d, bytes);
     if (e == cudaSuccess) e = cudaMemcpy(r->cos_d, r->cos_h.data(), bytes, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(r->sin_d, r->sin_h.data(), bytes, cudaMemcpyHostToDevice);
+    // a pageable-source cudaMemcpy may return before its DMA lands: complete it before any
+    // stream (ordered with the legacy stream or not) can read the tables
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         cudaFree(r->cos_d);
         cudaFree(r->sin_d);
@@ -897,6 +902,7 @@ int reattn_plan_create(reattn_ctx* ctx, const reattn_cache* cache, const reattn_
     carve_step(p->P, cache, rope, sizer);
     cudaError_t e = cudaMalloc(&p->mem, sizer.off + 256);
     if (e == cudaSuccess) e = cudaMemset(p->mem, 0, sizer.off + 256);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();  // zeroed before any stream replays
     if (e != cudaSuccess) {
         delete p;
         return set_err(ctx, REATTN_ECUDA, std::string("plan allocation: ") + cudaGetErrorString(e));
@@ -1065,6 +1071,7 @@ int reattn_batch_plan_create(reattn_ctx* ctx, const reattn_cache* const* caches,
     for (uint32_t b = 0; b < n_seq; ++b) carve_step(bp->P[b], caches[b], rope, sizer);
     cudaError_t e = cudaMalloc(&bp->mem, sizer.off + 256);
     if (e == cudaSuccess) e = cudaMemset(bp->mem, 0, sizer.off + 256);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();  // zeroed before any stream replays
     if (e != cudaSuccess)
         return set_err(ctx, REATTN_ECUDA, std::string("batch plan allocation: ") + cudaGetErrorString(e));
     Carver c{(uint8_t*)bp->mem, 0, sizer.off + 256};

@@ -89,7 +89,9 @@ inline int ensure_arena(reattn_ctx* ctx, size_t bytes) {
     ctx->arena_bytes = 0;
     const size_t nb = align_up(bytes + bytes / 4, 1 << 20);
     CU(ctx, cudaMalloc(&ctx->arena, nb));
-    CU(ctx, cudaMemset(ctx->arena, 0, nb));
+    // zero in stream order: a legacy-stream cudaMemset is not ordered with this stream and
+    // could land after the caller's first copy into the arena
+    CU(ctx, cudaMemsetAsync(ctx->arena, 0, nb, ctx->stream));
     ctx->arena_bytes = nb;
     return REATTN_OK;
 }

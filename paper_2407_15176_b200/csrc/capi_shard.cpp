@@ -192,6 +192,7 @@ int reattn_shard_plan_create(reattn_ctx* ctx, const reattn_cache* cache, const r
     carve(p, sizer);
     cudaError_t e = cudaMalloc(&p->mem, sizer.off + 256);
     if (e == cudaSuccess) e = cudaMemset(p->mem, 0, sizer.off + 256);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();  // zeroed before any stream replays
     if (e != cudaSuccess) {
         delete p;
         return set_err(ctx, REATTN_ECUDA, std::string("shard plan allocation: ") + cudaGetErrorString(e));

@@ -187,6 +187,7 @@ int reattn_snapshot_write(reattn_ctx* ctx, const char* path, const reattn_cache*
                           uint32_t n_layers) {
     const std::string p = path ? path : "";
     if (n_layers == 0 || !layers) return set_err(ctx, REATTN_EINVAL, "cache snapshot: no layers");
+    CU(ctx, cudaStreamSynchronize(ctx->stream));  // rows appended on the context stream
     FILE* f = std::fopen(p.c_str(), "wb");
     if (!f) return set_err(ctx, REATTN_ERUNTIME, "cannot open " + p + " for writing");
     std::unique_ptr<FILE, int (*)(FILE*)> fg(f, std::fclose);

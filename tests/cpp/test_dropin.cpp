@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
+#include <cstdlib>
 #include <map>
 #include <random>
 #include <set>
@@ -476,7 +478,23 @@ static void test_snapshot() {
     std::remove(path.c_str());
 }
 
+// REATTN_TEST_GARBAGE=1: fill (and free) most device memory with 0xFF bytes first, so later
+// allocations start from garbage -- surfaces reads of memory a test never wrote.
+static void fill_device_garbage() {
+    std::vector<unsigned char> host(64u << 20, 0xFF);
+    std::vector<void*> blocks;
+    for (int i = 0; i < 24; ++i) {
+        void* p = nullptr;
+        if (reattn_malloc(gpu::context(), 4ull << 30, &p) != REATTN_OK) break;
+        for (std::size_t o = 0; o < (4ull << 30); o += host.size())
+            reattn_memcpy_h2d(gpu::context(), (char*)p + o, host.data(), host.size());
+        blocks.push_back(p);
+    }
+    for (void* p : blocks) reattn_free(gpu::context(), p);
+}
+
 int main() {
+    if (std::getenv("REATTN_TEST_GARBAGE")) fill_device_garbage();
     test_snapshot();
     test_fused_topk();
     test_vote_spans();

@@ -29,3 +29,17 @@ def test_dropin_reference_unit_tests_on_gpu():
     print(r.stdout[-4000:])
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " 0 failures" in r.stdout
+
+
+@pytest.mark.gpu
+def test_dropin_on_garbage_device_memory():
+    """Same program after filling (and freeing) most device memory with 0xFF bytes: every
+    buffer must be written before it is read and every copy ordered with the kernels that
+    consume it (this run exposed a legacy-stream memset racing the context stream)."""
+    _build()
+    env = dict(os.environ, REATTN_TEST_GARBAGE="1")
+    r = subprocess.run([os.path.join(CPP, "test_dropin")], capture_output=True, text=True,
+                       timeout=600, env=env)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " 0 failures" in r.stdout
