@@ -74,8 +74,9 @@ bool make_key_tensor_map(CUtensorMap* map, const void* base, int dtype, uint64_t
                          uint64_t rows, int box_rows);
 int scan_fast_box_rows(int dtype);
 
-// Prefill path on tcgen05 (prefill_tc.cu): bf16 hi+lo split of the group-mean query, fp32
-// TMEM accumulation, fused register top-k.  d == 128, bf16 keys, k <= 8.  ε-tie parity.
+// Prefill path on tcgen05 (prefill_tc.cu): one bf16 score GEMM of the group-mean query with
+// a bounded error, streaming approximate top-(k+4) lists, exact dot_f32 re-scoring of the
+// keys inside the error window.  d == 128, bf16 keys, k <= 8.  Bit-exact with the reference.
 bool prefill_tc_supported(const ScanArgs& a);
 size_t prefill_tc_workspace(const ScanArgs& a);
 int prefill_tc_key_box_rows();

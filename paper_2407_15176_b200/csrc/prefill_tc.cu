@@ -1,26 +1,39 @@
-// K2 — prefill score scan on the 5th-gen tensor cores (tcgen05 + TMEM), fused top-k.
+// K2 — prefill score scan on the 5th-gen tensor cores (tcgen05 + TMEM), fused exact top-k.
 //
-// Same contract as fused_topk_scores (reference selection.hpp:275-355) for a prefill
-// chunk (n_q up to l_chunk = 4096 queries): per (kv head, query) the top-k of
-// mq · k over the middle, ties to the lower index.  The score GEMM
-//     S[q, j] = mq[q, :] · K[j, :]      (128 queries x 256 keys per MMA tile, d = 128)
-// runs on tcgen05.mma (kind::f16, bf16 operands, fp32 accumulators in TMEM).  mq is the
-// exact fp32 group mean (selection.hpp:250-258) split into bf16 hi + lo (16 significant
-// bits); S = hi·K + lo·K accumulates both in the same TMEM tile.  Scores therefore carry
-// an error <= (2^-16 + 2·d·2^-24)·Σ|mq_i k_i| against the reference's fp32 dot: index
-// parity is the north_star ε-tie rule, not bit equality (the exact CUDA-core path stays
-// the default; this path is opt-in, reattn_ctx_set_prefill).
+// Same contract as fused_topk_scores (reference selection.hpp:275-355) for a prefill chunk
+// (n_q up to l_chunk = 4096 queries): per (kv head, query) the top-k of mq · k over the
+// middle, ties to the lower index -- with the reference's own fp32 scores, bit for bit.
+//
+//   1. S_hi[q, j] = hi(mq)[q, :] · K[j, :] on tcgen05.mma (kind::f16: bf16 operands, fp32
+//      accumulators in TMEM; 128 queries x 128 keys per tile, d = 128), ONE pass.  mq is the
+//      exact fp32 group mean (selection.hpp:250-258), hi(mq) its bf16 rounding.
+//   2. Error bound per query row: |dot_f32(mq, k_j) - S_hi[j]| < delta :=
+//      (||mq - hi(mq)||_1 + 2^-12 ||mq||_1) * max|k|.  The first term is the exact rounding
+//      residual of the operand; 2^-12 covers both fp32 accumulations (the reference's 8-lane
+//      dot: <= ~20 * 2^-24, the tensor core's 128-term sum: assumed <= 2^-13) with margin.
+//   3. Epilogue (streaming): each (row, column half) keeps the top L = KT + 4 keys by S_hi
+//      and admits a key only if S_hi > (its KT-th best S_hi) - 2 delta.  A key that is
+//      admitted but falls off the list raises `dropped` (the largest S_hi ever dropped).
+//   4. prefill_exact_merge_kernel (one warp per (kv head, query)): T = k-th best S_hi over all
+//      key-range parts; every key of the exact top-k has S_hi > T - 2 delta (the k keys
+//      with S_hi >= T score exactly >= T - delta).  Listed keys in that window are re-scored
+//      with the reference's own dot_f32 (dense_matrix.hpp:41-56: 8 lanes over elements
+//      j, j+8, ..., fixed tree; unfused or FMA lanes) -- about k + epsilon dots per query --
+//      and a part whose `dropped` reaches the window (near-ties: more than L - KT keys
+//      within 2 delta) is re-scanned exactly.  Selected indices and scores are therefore
+//      identical to the reference (tests/test_prefill_tc.py compares bitwise) while the
+//      tensor cores run the score GEMM once and the streaming epilogue does no exact math.
 //
 // Warp roles (320 threads, 1 CTA/SM):
-//   warp 0  TMA producer: the CTA's Q hi/lo tile once, then K tiles (2-stage ring, 64 KB)
-//   warp 1  TMEM allocator (512 columns = 2 accumulators of 256) + single-thread MMA issue
-//   warps 2-9  epilogue, two warps per TMEM lane quarter (one per 128-column half):
-//           2 x tcgen05.ld 32x32b.x64, release the accumulator, then 16 group maxes decide
-//           which 8-column groups enter the register top-k of the thread's query row.
+//   warp 0  TMA producer: the CTA's Q hi tile once, then K tiles (4-stage ring of 32 KB)
+//   warp 1  TMEM allocator (512 columns = 4 accumulators of 128) + single-thread MMA issue;
+//           the MMA commit releases both the accumulator's producer slot and the K stage
+//   warps 2-9  epilogue, two warps per TMEM lane quarter (one per 64-column half): one
+//           tcgen05.ld 32x32b.x64, release the accumulator, 8 group maxes against the
+//           admission limit, rare per-column list inserts.
 //
-// Grid: (query tile, kv head, key split).  256 query tiles on 148 SMs is 1.73 waves, so the
-// key range of each query tile is cut into `splits` contiguous parts chosen to fill whole
-// waves; each part writes a partial top-k list and prefill_merge_kernel reduces them.
+// Grid: (query tile, kv head, key split): the key range of each query tile is cut into
+// `splits` contiguous parts chosen to fill whole waves; the exact merge reduces them.
 #include <algorithm>
 
 #include "common.cuh"
@@ -34,37 +47,44 @@ namespace reattn_impl {
 namespace {
 
 constexpr int kPM = 128;  // queries per CTA = UMMA M
-constexpr int kPN = 256;  // keys per tile = UMMA N
+constexpr int kPN = 128;  // keys per tile = UMMA N
 constexpr int kPD = 128;  // head dim
-constexpr int kPStages = 2;
-constexpr int kPQBytes = kPM * kPD * 2;  // one of hi / lo: 32 KB
-constexpr int kPKBytes = kPN * kPD * 2;  // one K stage: 64 KB
-constexpr int kPThreads = 320;  // producer, MMA, 8 epilogue warps
-constexpr int kPKMax = 8;
-constexpr size_t kPSmem = 1024 + 2 * kPQBytes + kPStages * kPKBytes + 128 + 2 * kPM * kPKMax * 4 + 256 * 32;
+constexpr int kPStages = 4;
+constexpr int kPAcc = 4;  // TMEM accumulators of kPN columns
+constexpr int kPQBytes = kPM * kPD * 2;  // hi(mq) tile: 32 KB
+constexpr int kPKBytes = kPN * kPD * 2;  // one K stage: 32 KB
+constexpr int kPThreads = 320;           // producer, MMA, 8 epilogue warps
+constexpr int kPKMax = 8;                // largest k
+constexpr int kPExtra = 4;               // list slots beyond KT (near-tie margin)
+constexpr int kPL = 16;                  // part-list stride (>= kPKMax + kPExtra)
+constexpr int kPMaxSplits = 8;
+constexpr float kPAccumCoef = 0.000244140625f;  // 2^-12
+constexpr size_t kPSmem = 1024 + kPQBytes + kPStages * kPKBytes + 256 + kPM * (kPL * 8 + 4) + 2 * kPM * 4;
 
 struct PrefillArgs {
     int n_q, n_qpad, n_kv, k;
     uint32_t count;
     uint64_t head_stride, row0;
-    int tiles;             // key tiles of the whole middle
-    int splits;            // key-range parts per query tile (gridDim.z)
-    uint32_t* idx_out;     // splits == 1: final [n_kv][n_q][k]
-    float* score_out;
-    uint32_t* part_idx;    // splits > 1: [splits][n_kv][n_qpad][kPKMax]
-    float* part_score;
+    int tiles;              // key tiles of the whole middle
+    int splits;             // key-range parts per query tile (gridDim.z)
+    const float* dl;        // [n_kv][n_qpad] delta / max|k|
+    const unsigned* kmax;   // [n_kv] max |k| over the middle (float bits)
+    unsigned* board;        // [n_kv][n_qpad] best published KT-th S_hi (ordered bits, 0 = none)
+    uint32_t* part_idx;     // [splits][n_kv][n_qpad][kPL], sorted by better(), kNoIndex-padded
+    float* part_score;      // S_hi of those keys
+    float* part_dropped;    // [splits][n_kv][n_qpad]
 };
 
 constexpr uint32_t prefill_idesc() { return idesc_bf16_f32<kPM, kPN>(); }
 
-// Insert (cs, ci) into the descending list ts/ti, given cs > ts[KT-1].  One thread sees its
+// Insert (cs, ci) into the descending list ts/ti, given cs > ts[N-1].  One thread sees its
 // candidates in increasing key order, so an equal score never displaces an entry and
 // better() reduces to a strict >.  All compares use the original list: branch-free shift.
-template <int KT>
-__device__ __forceinline__ void insert_in_order(float (&ts)[KT], uint32_t (&ti)[KT], float cs,
+template <int N>
+__device__ __forceinline__ void insert_in_order(float (&ts)[N], uint32_t (&ti)[N], float cs,
                                                 uint32_t ci) {
 #pragma unroll
-    for (int j = KT - 1; j >= 0; --j) {
+    for (int j = N - 1; j >= 0; --j) {
         const bool here = cs > ts[j];
         const bool above = j > 0 && cs > ts[j > 0 ? j - 1 : 0];
         if (here) {
@@ -74,43 +94,69 @@ __device__ __forceinline__ void insert_in_order(float (&ts)[KT], uint32_t (&ti)[
     }
 }
 
+// float <-> unsigned with the same order (for atomicMax); 0 encodes "nothing published"
+__device__ __forceinline__ unsigned ord_enc(float f) {
+    const unsigned b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float ord_dec(unsigned u) {
+    if (u == 0u) return -INFINITY;
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+// KT-th largest of 8 values (KT <= 8): a lower bound of the KT-th largest of the 64 columns
+// they are the group maxima of
+template <int KT>
+__device__ __forceinline__ float kth_of_8(const float (&g)[8]) {
+    float h[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) h[j] = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        float v = g[c];
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+            const float hi_ = fmaxf(h[j], v);
+            v = fminf(h[j], v);
+            h[j] = hi_;
+        }
+    }
+    return h[KT - 1];
+}
+
 template <int KT>
 __global__ void __launch_bounds__(kPThreads, 1)
     prefill_scan_tc_kernel(const __grid_constant__ CUtensorMap qhi_map,
-                           const __grid_constant__ CUtensorMap qlo_map,
                            const __grid_constant__ CUtensorMap k_map, const PrefillArgs a) {
+    constexpr int L = KT + kPExtra;
     extern __shared__ uint8_t psm_raw[];
     uint8_t* sm = (uint8_t*)(((uintptr_t)psm_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* s_qhi = sm;
-    uint8_t* s_qlo = sm + kPQBytes;
-    uint8_t* s_k = sm + 2 * kPQBytes;
+    uint8_t* s_k = sm + kPQBytes;
     uint64_t* bars = (uint64_t*)(s_k + kPStages * kPKBytes);
     uint64_t* q_full = bars;
     uint64_t* full = bars + 1;
     uint64_t* empty = full + kPStages;
     uint64_t* tfull = empty + kPStages;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* s_tmem = (uint32_t*)(tempty + 2);
-    uint8_t* aux = (uint8_t*)bars + 128;  // half-merge lists, then the group staging area
+    uint64_t* tempty = tfull + kPAcc;
+    uint32_t* s_tmem = (uint32_t*)(tempty + kPAcc);
+    uint8_t* aux = (uint8_t*)bars + 256;  // half-merge lists
+    float* s_thr = (float*)(aux + kPM * (kPL * 8 + 4));  // [2][128] KT-th best S_hi per half
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int qtile = blockIdx.x, kv = blockIdx.y, split = blockIdx.z;
     const int t_first = (int)((int64_t)split * a.tiles / a.splits);
     const int n_tiles = (int)((int64_t)(split + 1) * a.tiles / a.splits) - t_first;
 
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(s_tmem)),
-                     "r"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
+    if (warp == 1) tmem_alloc(s_tmem, 512);
+    for (int i = tid; i < 2 * kPM; i += kPThreads) s_thr[i] = -INFINITY;
     if (tid == 0) {
         mbar_init(q_full, 1);
         for (int s = 0; s < kPStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], 1);  // MMA commit: the stage has been read
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kPAcc; ++b) {
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 256);
         }
@@ -124,16 +170,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
     if (warp == 0) {
         if (lane == 0) {  // ===== TMA producer =====
             prefetch_tensormap(&qhi_map);
-            prefetch_tensormap(&qlo_map);
             prefetch_tensormap(&k_map);
             const uint64_t pol = policy_evict_first();
             const uint64_t keep = policy_evict_last();  // K tiles: re-read by every query tile
             const int32_t qrow = (int32_t)(kv * a.n_qpad + qtile * kPM);
-            mbar_arrive_expect_tx(q_full, 2 * kPQBytes);
+            mbar_arrive_expect_tx(q_full, kPQBytes);
             tma_load_2d(s_qhi, &qhi_map, 0, qrow, q_full, pol);
             tma_load_2d(s_qhi + kPQBytes / 2, &qhi_map, 64, qrow, q_full, pol);
-            tma_load_2d(s_qlo, &qlo_map, 0, qrow, q_full, pol);
-            tma_load_2d(s_qlo + kPQBytes / 2, &qlo_map, 64, qrow, q_full, pol);
             for (int t = 0; t < n_tiles; ++t) {
                 const int s = t % kPStages;
                 const uint32_t ph = (t / kPStages) & 1u;
@@ -147,223 +190,410 @@ __global__ void __launch_bounds__(kPThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ===== MMA issuer =====
+        if (lane == 0) {  // ===== MMA issuer: S_hi = hi(mq) · K^T, one pass =====
             const uint32_t idesc = prefill_idesc();
             mbar_wait(q_full, 0);
             tc_fence_after();
-            const uint32_t qhi = smem_u32(s_qhi), qlo = smem_u32(s_qlo);
+            const uint32_t qhi = smem_u32(s_qhi);
             for (int t = 0; t < n_tiles; ++t) {
                 const int s = t % kPStages;
                 const uint32_t ph = (t / kPStages) & 1u;
-                const int b = t & 1;
-                const uint32_t bph = (t >> 1) & 1u;
-                if (t >= 2) mbar_wait(&tempty[b], bph ^ 1u);
+                const int b = t % kPAcc;
+                const uint32_t bph = (t / kPAcc) & 1u;
+                if (t >= kPAcc) mbar_wait(&tempty[b], bph ^ 1u);
                 mbar_wait(&full[s], ph);
                 tc_fence_after();
                 const uint32_t kbase = smem_u32(s_k + (size_t)s * kPKBytes);
                 const uint32_t d_tmem = tmem + (uint32_t)(b * kPN);
-                uint32_t acc = 0;
 #pragma unroll
-                for (int hl = 0; hl < 2; ++hl) {
-                    const uint32_t qb = hl ? qlo : qhi;
+                for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
-                    for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-                        for (int ks = 0; ks < 4; ++ks) {
-                            const uint64_t ad = umma_desc_sw128(qb + kb * (kPQBytes / 2) + ks * 32);
-                            const uint64_t bd = umma_desc_sw128(kbase + kb * (kPKBytes / 2) + ks * 32);
-                            mma_bf16_ss(d_tmem, ad, bd, idesc, acc);
-                            acc = 1;
-                        }
-                }
-                mma_commit(&empty[s]);  // smem stage free once these MMAs retire
+                    for (int ks = 0; ks < 4; ++ks) {
+                        const uint64_t ad = umma_desc_sw128(qhi + kb * (kPQBytes / 2) + ks * 32);
+                        const uint64_t bd = umma_desc_sw128(kbase + kb * (kPKBytes / 2) + ks * 32);
+                        mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | ks) ? 1u : 0u);
+                    }
+                mma_commit(&empty[s]);  // K stage consumed
                 mma_commit(&tfull[b]);  // accumulator ready for the epilogue
             }
         }
     } else {
         // ===== epilogue: 8 warps, two per TMEM lane quarter; the thread owning lane r owns
-        // query row r of the tile for one half (128 columns) of every key tile =====
+        // query row r of the tile for one half (64 columns) of every key tile =====
         const int ew = warp - 2;          // 0..7
         const int quarter = warp & 3;     // TMEM lane quarter this warp may access
-        const int half = ew >> 2;         // column half of the 256-key tile
+        const int half = ew >> 2;         // column half of the 128-key tile
         const int row = quarter * 32 + lane;
-        const int query = qtile * kPM + row;
-        const int e = ew * 32 + lane;
-        float ts[KT];
-        uint32_t ti[KT];
+        const size_t qrow = (size_t)kv * a.n_qpad + (size_t)qtile * kPM + row;
+        const float d2 = 2.0f * a.dl[qrow] * __uint_as_float(a.kmax[kv]);  // 2 delta
+        float as[L];
+        uint32_t ai[L];
 #pragma unroll
-        for (int j = 0; j < KT; ++j) {
-            ts[j] = -INFINITY;
-            ti[j] = kNoIndex;
+        for (int j = 0; j < L; ++j) {
+            as[j] = -INFINITY;
+            ai[j] = kNoIndex;
         }
-        float4* stage = (float4*)(aux + 2 * kPM * kPKMax * 4);  // [2][256] float4: one group
+        float dropped = -INFINITY;
+        // Threshold board: every part of this row publishes its KT-th best S_hi (KT keys score
+        // at least that, so it bounds the row's k-th best from below) and admits nothing at or
+        // below the best published value - 2 delta.  Parts of later waves start near the final
+        // threshold instead of paying k ln(n/k) admissions from -inf.
+        unsigned* board = a.board + qrow;
+        float tb = ord_dec(*(volatile unsigned*)board);
         for (int t = 0; t < n_tiles; ++t) {
-            const int b = t & 1;
-            const uint32_t bph = (t >> 1) & 1u;
+            if ((t & 31) == 31) {
+                if (as[KT - 1] > -INFINITY) atomicMax(board, ord_enc(as[KT - 1]));
+                tb = ord_dec(*(volatile unsigned*)board);
+            }
+            const int b = t % kPAcc;
+            const uint32_t bph = (t / kPAcc) & 1u;
             mbar_wait(&tfull[b], bph);
             tc_fence_after();
-            const uint32_t col = (uint32_t)(b * kPN + half * (kPN / 2));
-            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + col;
-            uint32_t r[128];
-            TMEM_LD_X64(taddr, r);  // both loads in flight before the single wait
-            TMEM_LD_X64(taddr + 64, (r + 64));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            tc_fence_before();
-            mbar_arrive(&tempty[b]);  // accumulator copied out: the MMA warp may reuse it
-            const uint32_t key0 = (uint32_t)(t_first + t) * kPN + half * (kPN / 2);
-            if (key0 + 128 > a.count) {  // tail tile: keys past the middle never qualify
+            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * kPN + half * 64);
+            uint32_t r[64];
+            TMEM_LD_X64(taddr, r);
+            tmem_wait_ld();
+            const uint32_t key0 = (uint32_t)(t_first + t) * kPN + half * 64;
+            if (key0 + 64 > a.count) {  // tail tile: keys past the middle never qualify
 #pragma unroll
-                for (int c = 0; c < 128; ++c)
+                for (int c = 0; c < 64; ++c)
                     if (key0 + c >= a.count) r[c] = __float_as_uint(-INFINITY);
             }
-            // common path: 16 group maxes (8 columns each), one 16-bit qualifying mask.  A warp
-            // enters the insert path whenever ANY lane qualifies (~32k/t of tiles), so the
-            // insert path touches only the qualifying groups: the group is staged through
-            // shared memory by predicated stores (registers cannot be indexed dynamically).
-            const float thr = ts[KT - 1];
-            uint32_t gmask = 0;
+            float gx[8];
 #pragma unroll
-            for (int g = 0; g < 16; ++g) {
+            for (int g = 0; g < 8; ++g) {
                 float m = __uint_as_float(r[8 * g]);
 #pragma unroll
                 for (int u = 1; u < 8; ++u) m = fmaxf(m, __uint_as_float(r[8 * g + u]));
-                gmask |= (m > thr ? 1u : 0u) << g;
+                gx[g] = m;
             }
-            while (gmask) {
-                const int g = __ffs(gmask) - 1;
-                gmask &= gmask - 1;
+            // admission limit: (KT-th best S_hi so far) - 2 delta.  Before the list holds KT
+            // keys, the KT-th largest group max of this tile bounds the KT-th best from below;
+            // those keys are not listed yet, so one ulp lower keeps an exact tie (delta == 0)
+            // with them admissible
+            // The other column half's KT-th best is a lower bound of the row's k-th best
+            // too (any subset's is): a key at or below it - 2 delta is outside the merge's
+            // window (prefill_exact_merge_kernel).  Its keys are not ordered before ours, so
+            // one ulp lower again.  Read racily: every value ever stored is a valid bound.
+            const float other = ((volatile float*)s_thr)[(half ^ 1) * kPM + row];
+            float lim = fmaxf(as[KT - 1] - d2, nextafterf(fmaxf(other, tb) - d2, -INFINITY));
+            if (as[KT - 1] == -INFINITY)
+                lim = fmaxf(lim, nextafterf(kth_of_8<KT>(gx) - d2, -INFINITY));
+            uint32_t gm = 0;  // this row's groups holding an admissible column
 #pragma unroll
-                for (int gg = 0; gg < 16; ++gg)
-                    if (gg == g) {
-                        stage[e] = make_float4(__uint_as_float(r[8 * gg]), __uint_as_float(r[8 * gg + 1]),
-                                               __uint_as_float(r[8 * gg + 2]), __uint_as_float(r[8 * gg + 3]));
-                        stage[256 + e] =
-                            make_float4(__uint_as_float(r[8 * gg + 4]), __uint_as_float(r[8 * gg + 5]),
-                                        __uint_as_float(r[8 * gg + 6]), __uint_as_float(r[8 * gg + 7]));
+            for (int g = 0; g < 8; ++g) gm |= (gx[g] > lim ? 1u : 0u) << g;
+            // rare path, rolled: the warp walks the union of its rows' groups and re-reads
+            // each group's 8 columns from TMEM (warp-uniform address, one row per lane)
+            uint32_t ug = __reduce_or_sync(0xFFFFFFFFu, gm);
+            while (ug) {
+                const int g = __ffs(ug) - 1;
+                ug &= ug - 1u;
+                uint32_t v8[8];
+                tmem_ld8(taddr + (uint32_t)(8 * g), v8);
+                if ((gm >> g) & 1u) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const float v = __uint_as_float(v8[u]);
+                        if (v > lim && key0 + (uint32_t)(8 * g + u) < a.count) {
+                            if (v > as[L - 1]) {
+                                dropped = fmaxf(dropped, as[L - 1]);
+                                insert_in_order<L>(as, ai, v, key0 + (uint32_t)(8 * g + u));
+                            } else {
+                                dropped = fmaxf(dropped, v);
+                            }
+                        }
                     }
-                const float4 v0 = stage[e], v1 = stage[256 + e];
-                const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (v[u] > ts[KT - 1]) insert_in_order<KT>(ts, ti, v[u], key0 + 8 * g + u);
+                }
             }
+            s_thr[half * kPM + row] = as[KT - 1];
+            tc_fence_before();
+            mbar_arrive(&tempty[b]);  // accumulator no longer read: the MMA warp may reuse it
         }
-        // merge the two column halves of each row (disjoint key sets; full order)
-        float* m_s = (float*)aux;                           // [128][kPKMax] scores
-        uint32_t* m_i = (uint32_t*)(aux + kPM * kPKMax * 4);  // [128][kPKMax] indices
-        if (half == 1)
+        // merge the two column halves of each row (disjoint key sets): top L under better(),
+        // anything pushed off the end raises `dropped`
+        float* m_s = (float*)aux;                               // [128][L] scores
+        uint32_t* m_i = (uint32_t*)(aux + kPM * kPL * 4);       // [128][L] indices
+        float* m_d = (float*)(aux + kPM * kPL * 8);             // [128] dropped
+        if (half == 1) {
 #pragma unroll
-            for (int j = 0; j < KT; ++j) {
-                m_s[row * kPKMax + j] = ts[j];
-                m_i[row * kPKMax + j] = ti[j];
+            for (int j = 0; j < L; ++j) {
+                m_s[row * kPL + j] = as[j];
+                m_i[row * kPL + j] = ai[j];
             }
+            m_d[row] = dropped;
+        }
         named_bar_sync(1, 256);
         if (half == 0) {
+            dropped = fmaxf(dropped, m_d[row]);
 #pragma unroll
-            for (int jj = 0; jj < KT; ++jj) {
-                float cs = m_s[row * kPKMax + jj];
-                uint32_t ci = m_i[row * kPKMax + jj];
+            for (int jj = 0; jj < L; ++jj) {
+                float cs = m_s[row * kPL + jj];
+                uint32_t ci = m_i[row * kPL + jj];
+                if (ci == kNoIndex) continue;
 #pragma unroll
-                for (int j = 0; j < KT; ++j) {
-                    if (better(cs, ci, ts[j], ti[j])) {
-                        const float tt = ts[j];
-                        const uint32_t uu = ti[j];
-                        ts[j] = cs;
-                        ti[j] = ci;
+                for (int j = 0; j < L; ++j) {
+                    if (better(cs, ci, as[j], ai[j])) {
+                        const float tt = as[j];
+                        const uint32_t uu = ai[j];
+                        as[j] = cs;
+                        ai[j] = ci;
                         cs = tt;
                         ci = uu;
                     }
                 }
+                if (ci != kNoIndex) dropped = fmaxf(dropped, cs);
             }
-            const int k = a.k;
-            if (a.splits > 1) {
-                const size_t o = (((size_t)split * a.n_kv + kv) * a.n_qpad + query) * kPKMax;
+            const size_t prow = ((size_t)split * a.n_kv + kv) * a.n_qpad + (size_t)qtile * kPM + row;
+            uint32_t* pi = a.part_idx + prow * kPL;
+            float* ps = a.part_score + prow * kPL;
 #pragma unroll
-                for (int j = 0; j < KT; ++j)
-                    if (j < k) {
-                        a.part_idx[o + j] = ti[j];
-                        a.part_score[o + j] = ts[j];
-                    }
-            } else if (query < a.n_q) {
-                const size_t o = ((size_t)kv * a.n_q + query) * k;
-#pragma unroll
-                for (int j = 0; j < KT; ++j)
-                    if (j < k) {
-                        a.idx_out[o + j] = ti[j];
-                        a.score_out[o + j] = ts[j];
-                    }
+            for (int j = 0; j < kPL; ++j) {
+                pi[j] = j < L ? ai[j] : kNoIndex;
+                ps[j] = j < L ? as[j] : -INFINITY;
             }
+            a.part_dropped[prow] = dropped;
+            if (as[KT - 1] > -INFINITY) atomicMax(board, ord_enc(as[KT - 1]));
         }
     }
+    tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+        tmem_dealloc(tmem, 512);
     }
 }
 
-// group-mean query (selection.hpp:250-258, exact fp32) split into bf16 hi + lo
+// group-mean query (selection.hpp:250-258, exact fp32): the fp32 row, its bf16 rounding (the
+// MMA operand) and delta / max|k| = ||mq - hi||_1 + 2^-12 ||mq||_1 per row (one warp per row)
 __global__ void prefill_prep_kernel(const float* q, int n_q, int n_heads, int n_kv, int n_qpad,
-                                    __nv_bfloat16* hi, __nv_bfloat16* lo) {
+                                    __nv_bfloat16* hi, float* mq, float* dl) {
     const int group = n_heads / n_kv;
     const float inv = __fdiv_rn(1.0f, (float)group);
-    const size_t n = (size_t)n_kv * n_qpad * kPD;
-    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n;
-         e += (size_t)gridDim.x * blockDim.x) {
-        const int c = (int)(e % kPD);
-        const size_t rq = e / kPD;
+    const int lane = threadIdx.x & 31;
+    const size_t rows = (size_t)n_kv * n_qpad;
+    for (size_t rq = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) / 32; rq < rows;
+         rq += (size_t)gridDim.x * blockDim.x / 32) {
         const int qi = (int)(rq % n_qpad), kv = (int)(rq / n_qpad);
-        float m = 0.0f;
-        if (qi < n_q) {
-            float acc = 0.0f;
-            for (int g = 0; g < group; ++g)
-                acc = __fadd_rn(acc, q[(size_t)qi * n_heads * kPD + (size_t)(kv * group + g) * kPD + c]);
-            m = __fmul_rn(acc, inv);
+        float s1 = 0.0f, se = 0.0f;
+        for (int c = lane; c < kPD; c += 32) {
+            float m = 0.0f;
+            if (qi < n_q) {
+                float acc = 0.0f;
+                for (int g = 0; g < group; ++g)
+                    acc = __fadd_rn(acc, q[(size_t)qi * n_heads * kPD + (size_t)(kv * group + g) * kPD + c]);
+                m = __fmul_rn(acc, inv);
+            }
+            const __nv_bfloat16 h = __float2bfloat16_rn(m);
+            mq[rq * kPD + c] = m;
+            hi[rq * kPD + c] = h;
+            s1 += fabsf(m);
+            se += fabsf(m - __bfloat162float(h));  // exact: m and h share the exponent range
         }
-        const __nv_bfloat16 h = __float2bfloat16_rn(m);
-        hi[e] = h;
-        lo[e] = __float2bfloat16_rn(__fsub_rn(m, __bfloat162float(h)));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, off);
+            se += __shfl_xor_sync(0xFFFFFFFFu, se, off);
+        }
+        // 1.001: the rounding of these sums themselves
+        if (lane == 0) dl[rq] = (se + kPAccumCoef * s1) * 1.001f;
     }
 }
 
-// reduce the per-split partial lists of each (kv head, query): disjoint key ranges, so the
-// union's top-k under better() is the top-k of the whole middle
-__global__ void prefill_merge_kernel(const uint32_t* part_idx, const float* part_score, int splits,
-                                     int n_kv, int n_q, int n_qpad, int k, uint32_t* idx_out,
-                                     float* score_out) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= n_kv * n_q) return;
-    const int kv = e / n_q, query = e % n_q;
+// max |k| over the middle rows of each kv head (float bits: non-negative floats order as
+// unsigned integers); out must be zeroed before the launch
+__global__ void prefill_kmax_kernel(const __nv_bfloat16* keys, uint64_t head_stride, uint64_t row0,
+                                    uint32_t count, int n_kv, unsigned* out) {
+    const int kv = blockIdx.y;
+    const uint4* base = reinterpret_cast<const uint4*>(keys + ((size_t)kv * head_stride + row0) * kPD);
+    const size_t n = (size_t)count * kPD / 8;
+    uint32_t mx = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const uint4 w = __ldg(base + i);
+        const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            mx = max(mx, (u[j] << 16) & 0x7FFFFFFFu);           // |low bf16| as float bits
+            mx = max(mx, u[j] & 0x7FFF0000u);                    // |high bf16|
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, off));
+    if ((threadIdx.x & 31) == 0) atomicMax(out + kv, mx);
+}
+
+struct PrefillMergeArgs {
+    const uint32_t* part_idx;
+    const float* part_score;
+    const float* part_dropped;
+    int splits, tiles, n_kv, n_q, n_qpad, k;
+    uint32_t count;
+    const __nv_bfloat16* keys;
+    uint64_t head_stride, row0;
+    const float* mq;
+    const float* dl;
+    const unsigned* kmax;
+    uint32_t* idx_out;
+    float* score_out;
+};
+
+// Insert (cs, ci) into the top-k list under better() (any arrival order).
+__device__ __forceinline__ void insert_better(float (&ts)[kPKMax], uint32_t (&ti)[kPKMax], int k,
+                                              float cs, uint32_t ci) {
+#pragma unroll
+    for (int j = 0; j < kPKMax; ++j) {
+        if (j < k && better(cs, ci, ts[j], ti[j])) {
+            const float tt = ts[j];
+            const uint32_t uu = ti[j];
+            ts[j] = cs;
+            ti[j] = ci;
+            cs = tt;
+            ci = uu;
+        }
+    }
+}
+
+// Exact dot_f32 (dense_matrix.hpp:41-56) of this lane's query with key `key`, 8 lanes per
+// key: lane t of the group accumulates the reference's lane t (elements t, t+8, ..., in
+// order) and the fixed tree ((l0+l1)+(l2+l3))+((l4+l5)+(l6+l7)) is three xor-shuffle adds
+// (IEEE addition commutes: every lane of the group ends with the same bits).
+template <int LANES>
+__device__ __forceinline__ float exact_dot8(const float (&qv)[16], const __nv_bfloat16* krow,
+                                            bool live, int t) {
+    float l = 0.0f;
+    if (live) {
+        float kf[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) kf[c] = __bfloat162float(krow[t + 8 * c]);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            if (LANES == kLanesFma)
+                l = __fmaf_rn(qv[c], kf[c], l);
+            else
+                l = __fadd_rn(l, __fmul_rn(qv[c], kf[c]));
+        }
+    }
+    float s = __fadd_rn(l, __shfl_xor_sync(0xFFFFFFFFu, l, 1));
+    s = __fadd_rn(s, __shfl_xor_sync(0xFFFFFFFFu, s, 2));
+    s = __fadd_rn(s, __shfl_xor_sync(0xFFFFFFFFu, s, 4));
+    return s;
+}
+
+// One warp per (kv head, query): T = k-th best S_hi over the parts' lists, exact re-scoring
+// of the listed keys with S_hi >= T - 2 delta, exact re-scan of any part whose dropped S_hi
+// reaches that window, exact top-k of the union (every lane holds the same list).
+template <int LANES>
+__global__ void __launch_bounds__(256) prefill_exact_merge_kernel(const PrefillMergeArgs m) {
+    __shared__ float s_sc[8][kPMaxSplits * kPL];
+    __shared__ uint32_t s_ix[8][kPMaxSplits * kPL];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int e = blockIdx.x * 8 + wib;
+    if (e >= m.n_kv * m.n_q) return;  // warp-uniform
+    const int kv = e / m.n_q, query = e % m.n_q;
+    const size_t qrow = (size_t)kv * m.n_qpad + query;
+    const int n = m.splits * kPL;
+    float* sc = s_sc[wib];
+    uint32_t* ix = s_ix[wib];
+    for (int i = lane; i < n; i += 32) {
+        const size_t o = (((size_t)(i / kPL) * m.n_kv + kv) * m.n_qpad + query) * kPL + (i % kPL);
+        const uint32_t id = m.part_idx[o];
+        ix[i] = id;
+        sc[i] = id == kNoIndex ? -INFINITY : m.part_score[o];
+    }
+    __syncwarp();
+    // T: k rounds of "best list head" across the (sorted) part lists, lane s owns part s
+    int pos = 0;
+    float T = -INFINITY;
+    for (int r = 0; r < m.k; ++r) {
+        float bs = -INFINITY;
+        uint32_t bi = kNoIndex;
+        if (lane < m.splits && pos < kPL) {
+            bs = sc[lane * kPL + pos];
+            bi = ix[lane * kPL + pos];
+        }
+        int bl = lane;
+#pragma unroll
+        for (int off = 1; off < kPMaxSplits; off <<= 1) {
+            const float os = __shfl_xor_sync(0xFFFFFFFFu, bs, off);
+            const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, bi, off);
+            const int ol = __shfl_xor_sync(0xFFFFFFFFu, bl, off);
+            if (oi != kNoIndex && (bi == kNoIndex || better(os, oi, bs, bi))) {
+                bs = os;
+                bi = oi;
+                bl = ol;
+            }
+        }
+        bs = __shfl_sync(0xFFFFFFFFu, bs, 0);
+        bi = __shfl_sync(0xFFFFFFFFu, bi, 0);
+        bl = __shfl_sync(0xFFFFFFFFu, bl, 0);
+        if (bi == kNoIndex) {  // fewer than k listed keys: every listed key is a candidate
+            T = -INFINITY;
+            break;
+        }
+        T = bs;
+        if (lane == bl) ++pos;
+    }
+    const float w = T - 2.0f * m.dl[qrow] * __uint_as_float(m.kmax[kv]);
+    uint32_t rescan = 0;  // parts to re-scan exactly
+    for (int s = 0; s < m.splits; ++s) {
+        const float d = m.part_dropped[(((size_t)s * m.n_kv + kv) * m.n_qpad + query)];
+        if (d > -INFINITY && d >= w) rescan |= 1u << s;
+    }
+    // compact the candidates (listed, S_hi >= w, part not re-scanned) to the front of ix
+    int nc = 0;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+        const int i = i0 + lane;
+        const bool c = i < n && ix[i] != kNoIndex && sc[i] >= w && !((rescan >> (i / kPL)) & 1u);
+        const uint32_t id = i < n ? ix[i] : kNoIndex;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, c);
+        __syncwarp();
+        if (c) ix[nc + __popc(bal & ((1u << lane) - 1u))] = id;
+        nc += __popc(bal);
+        __syncwarp();
+    }
+    const int t = lane & 7, j = lane >> 3;
+    float qv[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) qv[c] = m.mq[qrow * kPD + t + 8 * c];
+    const __nv_bfloat16* kbase = m.keys + ((size_t)kv * m.head_stride + m.row0) * kPD;
     float ts[kPKMax];
     uint32_t ti[kPKMax];
 #pragma unroll
-    for (int j = 0; j < kPKMax; ++j) {
-        ts[j] = -INFINITY;
-        ti[j] = kNoIndex;
+    for (int q = 0; q < kPKMax; ++q) {
+        ts[q] = -INFINITY;
+        ti[q] = kNoIndex;
     }
-    for (int s = 0; s < splits; ++s) {
-        const size_t o = (((size_t)s * n_kv + kv) * n_qpad + query) * kPKMax;
-        for (int jj = 0; jj < k; ++jj) {
-            float cs = part_score[o + jj];
-            uint32_t ci = part_idx[o + jj];
-            if (ci == kNoIndex) break;
+    auto consume = [&](uint32_t key, bool live) {
+        const float v = exact_dot8<LANES>(qv, kbase + (size_t)key * kPD, live, t);
 #pragma unroll
-            for (int j = 0; j < kPKMax; ++j) {
-                if (j < k && better(cs, ci, ts[j], ti[j])) {
-                    const float tt = ts[j];
-                    const uint32_t uu = ti[j];
-                    ts[j] = cs;
-                    ti[j] = ci;
-                    cs = tt;
-                    ci = uu;
-                }
-            }
+        for (int jj = 0; jj < 4; ++jj) {
+            const float vj = __shfl_sync(0xFFFFFFFFu, v, 8 * jj);
+            const uint32_t kj = __shfl_sync(0xFFFFFFFFu, key, 8 * jj);
+            const bool lj = __shfl_sync(0xFFFFFFFFu, live, 8 * jj);
+            if (lj) insert_better(ts, ti, m.k, vj, kj);
+        }
+    };
+    for (int p = 0; p < nc; p += 4) {
+        const bool live = p + j < nc;
+        consume(live ? ix[p + j] : 0u, live);
+    }
+    for (int s = 0; s < m.splits; ++s) {
+        if (!((rescan >> s) & 1u)) continue;
+        const uint32_t lo = (uint32_t)((int64_t)s * m.tiles / m.splits) * kPN;
+        const uint32_t hi = min(m.count, (uint32_t)((int64_t)(s + 1) * m.tiles / m.splits) * kPN);
+        for (uint32_t b0 = lo; b0 < hi; b0 += 4) {
+            const bool live = b0 + j < hi;
+            consume(live ? b0 + j : 0u, live);
         }
     }
-    const size_t o = ((size_t)kv * n_q + query) * k;
-    for (int j = 0; j < k; ++j) {
-        idx_out[o + j] = ti[j];
-        score_out[o + j] = ts[j];
+    if (lane == 0) {
+        const size_t o = ((size_t)kv * m.n_q + query) * m.k;
+#pragma unroll
+        for (int q = 0; q < kPKMax; ++q)
+            if (q < m.k) {
+                m.idx_out[o + q] = ti[q];
+                m.score_out[o + q] = ts[q];
+            }
     }
 }
 
@@ -379,12 +609,12 @@ int num_sms() {
 }
 
 // key-range parts per query tile: the fewest whose CTA count fills whole waves within 2%
-// (1 CTA per SM), keeping >= 32 key tiles per part so the pipeline fill stays amortised
+// (1 CTA per SM), keeping >= 64 key tiles per part so the pipeline fill stays amortised
 int choose_splits(int ctas, int tiles) {
     const int sms = num_sms();
     int best = 1;
     double best_eff = 0.0;
-    for (int s = 1; s <= 8 && (s == 1 || tiles / s >= 32); ++s) {
+    for (int s = 1; s <= kPMaxSplits && (s == 1 || tiles / s >= 64); ++s) {
         const long units = (long)ctas * s;
         const double eff = (double)units / ((units + sms - 1) / sms * sms);
         if (eff > best_eff + 0.02) {
@@ -397,16 +627,24 @@ int choose_splits(int ctas, int tiles) {
 
 struct PrefillGeom {
     int n_qpad, tiles, splits;
-    size_t q_bytes, part_bytes;
+    size_t hi_bytes, mq_bytes, dl_bytes, kmax_bytes, board_bytes, list_bytes, dropped_bytes;
 };
+
+size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
 PrefillGeom prefill_geom(const ScanArgs& a) {
     PrefillGeom g;
     g.n_qpad = (a.n_q + kPM - 1) / kPM * kPM;
     g.tiles = (int)((a.count + kPN - 1) / kPN);
     g.splits = choose_splits(g.n_qpad / kPM * a.n_kv, g.tiles);
-    g.q_bytes = 2 * (size_t)a.n_kv * g.n_qpad * kPD * sizeof(__nv_bfloat16);
-    g.part_bytes = g.splits > 1 ? (size_t)g.splits * a.n_kv * g.n_qpad * kPKMax * 8 : 0;
+    const size_t rows = (size_t)a.n_kv * g.n_qpad;
+    g.hi_bytes = al256(rows * kPD * sizeof(__nv_bfloat16));
+    g.mq_bytes = al256(rows * kPD * sizeof(float));
+    g.dl_bytes = al256(rows * sizeof(float));
+    g.kmax_bytes = al256((size_t)a.n_kv * sizeof(unsigned));
+    g.board_bytes = al256(rows * sizeof(unsigned));
+    g.list_bytes = al256((size_t)g.splits * rows * kPL * 4);  // one of indices / scores
+    g.dropped_bytes = al256((size_t)g.splits * rows * 4);
     return g;
 }
 
@@ -418,21 +656,40 @@ bool prefill_tc_supported(const ScanArgs& a) {
 
 size_t prefill_tc_workspace(const ScanArgs& a) {
     const PrefillGeom g = prefill_geom(a);
-    return g.q_bytes + g.part_bytes + 1024;
+    return g.hi_bytes + g.mq_bytes + g.dl_bytes + g.kmax_bytes + g.board_bytes + 2 * g.list_bytes + g.dropped_bytes + 1024;
 }
 
 cudaError_t launch_prefill_tc(const ScanArgs& a, const CUtensorMap& kmap, void* ws,
                               cudaStream_t s) {
     const PrefillGeom g = prefill_geom(a);
     const int n_qpad = g.n_qpad;
-    __nv_bfloat16* hi = (__nv_bfloat16*)ws;
-    __nv_bfloat16* lo = hi + (size_t)a.n_kv * n_qpad * kPD;
-    const size_t n = (size_t)a.n_kv * n_qpad * kPD;
-    prefill_prep_kernel<<<(int)std::min<size_t>(148 * 16, (n + 255) / 256), 256, 0, s>>>(
-        a.q, a.n_q, a.n_heads, a.n_kv, n_qpad, hi, lo);
-    CUtensorMap qh, ql;
-    if (!make_key_tensor_map(&qh, hi, kBF16, kPD, (uint64_t)a.n_kv * n_qpad, kPM) ||
-        !make_key_tensor_map(&ql, lo, kBF16, kPD, (uint64_t)a.n_kv * n_qpad, kPM))
+    uint8_t* w = (uint8_t*)ws;
+    __nv_bfloat16* hi = (__nv_bfloat16*)w;
+    w += g.hi_bytes;
+    float* mq = (float*)w;
+    w += g.mq_bytes;
+    float* dl = (float*)w;
+    w += g.dl_bytes;
+    unsigned* kmax = (unsigned*)w;
+    w += g.kmax_bytes;
+    unsigned* board = (unsigned*)w;
+    w += g.board_bytes;
+    uint32_t* part_idx = (uint32_t*)w;
+    w += g.list_bytes;
+    float* part_score = (float*)w;
+    w += g.list_bytes;
+    float* part_dropped = (float*)w;
+    const size_t rows = (size_t)a.n_kv * n_qpad;
+    prefill_prep_kernel<<<(int)std::min<size_t>(148 * 16, (rows * 32 + 255) / 256), 256, 0, s>>>(
+        a.q, a.n_q, a.n_heads, a.n_kv, n_qpad, hi, mq, dl);
+    cudaError_t e = cudaMemsetAsync(kmax, 0, (size_t)a.n_kv * sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(board, 0, rows * sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    prefill_kmax_kernel<<<dim3(std::max(1, num_sms() * 4 / std::max(1, a.n_kv)), a.n_kv), 256, 0, s>>>(
+        (const __nv_bfloat16*)a.keys, a.head_stride, a.row0, a.count, a.n_kv, kmax);
+    CUtensorMap qh;
+    if (!make_key_tensor_map(&qh, hi, kBF16, kPD, (uint64_t)a.n_kv * n_qpad, kPM))
         return cudaErrorInvalidValue;
     PrefillArgs p;
     p.n_q = a.n_q;
@@ -444,15 +701,16 @@ cudaError_t launch_prefill_tc(const ScanArgs& a, const CUtensorMap& kmap, void* 
     p.row0 = a.row0;
     p.tiles = g.tiles;
     p.splits = g.splits;
-    p.idx_out = a.idx_out;
-    p.score_out = a.score_out;
-    uint8_t* part = (uint8_t*)ws + (g.q_bytes + 255) / 256 * 256;
-    p.part_idx = (uint32_t*)part;
-    p.part_score = (float*)(part + g.part_bytes / 2);
+    p.dl = dl;
+    p.kmax = kmax;
+    p.board = board;
+    p.part_idx = part_idx;
+    p.part_score = part_score;
+    p.part_dropped = part_dropped;
     dim3 grid(n_qpad / kPM, a.n_kv, g.splits);
     auto launch = [&](auto kernel) {
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmem);
-        kernel<<<grid, kPThreads, kPSmem, s>>>(qh, ql, kmap, p);
+        kernel<<<grid, kPThreads, kPSmem, s>>>(qh, kmap, p);
     };
     if (a.k <= 1)
         launch(prefill_scan_tc_kernel<1>);
@@ -462,12 +720,30 @@ cudaError_t launch_prefill_tc(const ScanArgs& a, const CUtensorMap& kmap, void* 
         launch(prefill_scan_tc_kernel<4>);
     else
         launch(prefill_scan_tc_kernel<8>);
-    if (g.splits > 1) {
-        const int n = a.n_kv * a.n_q;
-        prefill_merge_kernel<<<(n + 127) / 128, 128, 0, s>>>(p.part_idx, p.part_score, g.splits,
-                                                             a.n_kv, a.n_q, n_qpad, a.k,
-                                                             a.idx_out, a.score_out);
-    }
+    PrefillMergeArgs mg;
+    mg.part_idx = part_idx;
+    mg.part_score = part_score;
+    mg.part_dropped = part_dropped;
+    mg.splits = g.splits;
+    mg.tiles = g.tiles;
+    mg.n_kv = a.n_kv;
+    mg.n_q = a.n_q;
+    mg.n_qpad = n_qpad;
+    mg.k = a.k;
+    mg.count = a.count;
+    mg.keys = (const __nv_bfloat16*)a.keys;
+    mg.head_stride = a.head_stride;
+    mg.row0 = a.row0;
+    mg.mq = mq;
+    mg.dl = dl;
+    mg.kmax = kmax;
+    mg.idx_out = a.idx_out;
+    mg.score_out = a.score_out;
+    const int nw = a.n_kv * a.n_q;
+    if (a.lanes == kLanesFma)
+        prefill_exact_merge_kernel<kLanesFma><<<(nw + 7) / 8, 256, 0, s>>>(mg);
+    else
+        prefill_exact_merge_kernel<kLanesUnfused><<<(nw + 7) / 8, 256, 0, s>>>(mg);
     return cudaGetLastError();
 }
 
