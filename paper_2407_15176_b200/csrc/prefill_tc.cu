@@ -11,7 +11,7 @@
 //      (||mq - hi(mq)||_1 + 2^-12 ||mq||_1) * max|k|.  The first term is the exact rounding
 //      residual of the operand; 2^-12 covers both fp32 accumulations (the reference's 8-lane
 //      dot: <= ~20 * 2^-24, the tensor core's 128-term sum: assumed <= 2^-13) with margin.
-//   3. Epilogue (streaming): each (row, column half) keeps the top L = KT + 4 keys by S_hi
+//   3. Epilogue (streaming): each (row, column half) keeps the top L = KT + 8 keys by S_hi
 //      and admits a key only if S_hi > (its KT-th best S_hi) - 2 delta.  A key that is
 //      admitted but falls off the list raises `dropped` (the largest S_hi ever dropped).
 //   4. prefill_exact_merge_kernel (one warp per (kv head, query)): T = k-th best S_hi over all
@@ -20,9 +20,10 @@
 //      with the reference's own dot_f32 (dense_matrix.hpp:41-56: 8 lanes over elements
 //      j, j+8, ..., fixed tree; unfused or FMA lanes) -- about k + epsilon dots per query --
 //      and a part whose `dropped` reaches the window (near-ties: more than L - KT keys
-//      within 2 delta) is re-scanned exactly.  Selected indices and scores are therefore
-//      identical to the reference (tests/test_prefill_tc.py compares bitwise) while the
-//      tensor cores run the score GEMM once and the streaming epilogue does no exact math.
+//      within 2 delta of the k-th best; ~1e-6 of rows at L = KT + 8, ~2% at KT + 4) is
+//      re-scanned exactly.  Selected indices and scores are therefore identical to the
+//      reference (tests/test_prefill_tc.py compares bitwise) while the tensor cores run the
+//      score GEMM once and the streaming epilogue does no exact math.
 //
 // Warp roles (320 threads, 1 CTA/SM):
 //   warp 0  TMA producer: the CTA's Q hi tile once, then K tiles (4-stage ring of 32 KB)
@@ -55,7 +56,7 @@ constexpr int kPQBytes = kPM * kPD * 2;  // hi(mq) tile: 32 KB
 constexpr int kPKBytes = kPN * kPD * 2;  // one K stage: 32 KB
 constexpr int kPThreads = 320;           // producer, MMA, 8 epilogue warps
 constexpr int kPKMax = 8;                // largest k
-constexpr int kPExtra = 4;               // list slots beyond KT (near-tie margin)
+constexpr int kPExtra = 8;               // list slots beyond KT (near-tie margin)
 constexpr int kPL = 16;                  // part-list stride (>= kPKMax + kPExtra)
 constexpr int kPMaxSplits = 8;
 constexpr float kPAccumCoef = 0.000244140625f;  // 2^-12
