@@ -49,11 +49,12 @@ typedef enum { REATTN_MODE_FULL = 0, REATTN_MODE_WINDOW = 1, REATTN_MODE_REATTEN
 /* Lane arithmetic of the fp32 score dot (dense_matrix.hpp:41-56); the reference compiles
  * `l += a*b` either unfused or as an FMA depending on compiler/ISA/d. */
 typedef enum { REATTN_LANES_UNFUSED = 0, REATTN_LANES_FMA = 1 } reattn_lanes;
-/* Prefill (n_q > 1) paths, a bit mask.  EXACT (0, default) = CUDA-core scan bit-identical
- * to the reference and the f64 attention.  TENSOR_SCAN = tcgen05 bf16 hi+lo score GEMM with
- * TMEM accumulators (selected indices equal up to the north_star ε-tie rule).
- * TENSOR_ATTN = tcgen05 finite-scope attention (bf16 hi+lo operands, fp32 accumulation;
- * bf16 tolerance).  TENSOR = both.  See DESIGN.md §3. */
+/* Prefill (n_q > 1) paths, a bit mask.  TENSOR_SCAN (the context default) = the tcgen05
+ * score GEMM with bounded-error windowing and exact re-scoring: indices and scores
+ * bit-identical to the reference (bf16 cache, d == 128, k <= 8; other shapes take the
+ * CUDA-core scan).  EXACT (0) = the CUDA-core scan everywhere (also bit-identical) and the
+ * f64 attention.  TENSOR_ATTN = tcgen05 finite-scope attention (bf16 hi+lo operands, fp32
+ * accumulation; bf16 tolerance).  TENSOR = both.  See DESIGN.md §3. */
 typedef enum {
     REATTN_PREFILL_EXACT = 0,
     REATTN_PREFILL_TENSOR_SCAN = 1,

@@ -22,6 +22,7 @@ SPAN_ALIGNED, SPAN_CENTERED = 0, 1
 MODE_FULL, MODE_WINDOW, MODE_REATTENTION = 0, 1, 2
 LANES_UNFUSED, LANES_FMA = 0, 1
 PREFILL_EXACT, PREFILL_TENSOR_SCAN, PREFILL_TENSOR_ATTN, PREFILL_TENSOR = 0, 1, 2, 3
+PREFILL_DEFAULT = PREFILL_TENSOR_SCAN  # a new context's mode
 
 u64 = C.c_uint64
 vp = C.c_void_p
@@ -203,8 +204,9 @@ class Context:
         self.check(self.lib.reattn_ctx_set_lanes(self.h, lanes))
 
     def set_prefill(self, mode: int) -> None:
-        """Bit mask: PREFILL_TENSOR_SCAN (tcgen05 scan, ε-tie), PREFILL_TENSOR_ATTN (tcgen05
-        attention, bf16 tolerance), PREFILL_TENSOR (both); PREFILL_EXACT (0) = CUDA cores."""
+        """Bit mask: PREFILL_TENSOR_SCAN (tcgen05 scan, bit-exact; the default),
+        PREFILL_TENSOR_ATTN (tcgen05 attention, bf16 tolerance), PREFILL_TENSOR (both);
+        PREFILL_EXACT (0) = CUDA-core scan and f64 attention."""
         self.check(self.lib.reattn_ctx_set_prefill(self.h, mode))
 
     @property

@@ -38,7 +38,7 @@ def step(ctx, cache, rope, q, nh, cfg, mode_bits):
     try:
         return N.attend_step(ctx, cache, rope, q, nh, cfg)
     finally:
-        ctx.set_prefill(N.PREFILL_EXACT)
+        ctx.set_prefill(N.PREFILL_DEFAULT)
 
 
 @pytest.mark.parametrize("n_q,total", [(128, 5000), (200, 6000), (37, 4500)])
@@ -92,5 +92,5 @@ def test_prefill_attention_tc_window_mode(ctx):
     try:
         tc = N.attend_step(ctx, cache, rope, q, 32, cfg, N.MODE_WINDOW)
     finally:
-        ctx.set_prefill(N.PREFILL_EXACT)
+        ctx.set_prefill(N.PREFILL_DEFAULT)
     assert (tc.out - exact.out).abs().max().item() <= MEASURED_TOL

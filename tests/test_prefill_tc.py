@@ -28,7 +28,7 @@ def run(ctx, q, n_heads, keys_bf16, k):
     try:
         n_out, _ = ctx.fused_topk(qt, n_heads, kt, n_kv, count, 0, count, d, k, idx, sc, N.BF16)
     finally:
-        ctx.set_prefill(N.PREFILL_EXACT)
+        ctx.set_prefill(N.PREFILL_DEFAULT)
     i = idx.cpu().numpy().view(np.uint32).reshape(n_kv, n_q, k)[:, :, :n_out]
     s = sc.cpu().numpy().reshape(n_kv, n_q, k)[:, :, :n_out]
     return i, s
