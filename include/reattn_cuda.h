@@ -269,6 +269,97 @@ int reattn_shard_combine(reattn_shard_plan* plan);  /* part_recv -> out */
 int reattn_shard_stats(reattn_shard_plan* plan, reattn_step_stats* stats, uint64_t* span_b_host,
                        uint64_t* span_e_host);
 
+/* ---- decoder model + generation engine (reference model.hpp, engine.hpp:115-218) ------
+ * The toy decoder the reference's Engine drives: pre-norm blocks x += attn(norm(x)),
+ * x += ffn(norm(x)), greedy decode.  Weights live on the device (fp32, the reference's
+ * layout: projections input-major, d_in x d_out).  Projections run as fp32 GEMMs
+ * (cuBLAS, no TF32); the K/V projections of an fp32 cache write straight into the cache
+ * rows; attention is the reattn_attend_step pipeline.  Errors carry the reference's
+ * exception kinds and messages (model config / weights file / engine). */
+typedef struct {
+    uint64_t n_layer, n_head, n_kv_head, d_model, d_head, d_ff, vocab_size, pretrain_window;
+    double rope_base;
+    int32_t attention_mode; /* reattn_mode: 0 full, 1 window, 2 reattention */
+    int32_t reserved;
+} reattn_model_config;
+
+/* LayerWeights / ModelWeights tensors (model.hpp:67-86); layer is ignored for globals */
+typedef enum {
+    REATTN_W_EMBEDDING = 0, /* vocab x d_model */
+    REATTN_W_WQ = 1,        /* d_model x n_head*d_head */
+    REATTN_W_WK = 2,        /* d_model x n_kv_head*d_head */
+    REATTN_W_WV = 3,
+    REATTN_W_WO = 4,        /* d_model x d_model */
+    REATTN_W_GATE = 5,      /* d_model x d_ff */
+    REATTN_W_UP = 6,
+    REATTN_W_DOWN = 7,      /* d_ff x d_model */
+    REATTN_W_NORM_ATTN = 8, /* d_model */
+    REATTN_W_NORM_FFN = 9,
+    REATTN_W_NORM_FINAL = 10,
+    REATTN_W_LM_HEAD = 11   /* d_model x vocab */
+} reattn_weight_kind;
+
+typedef struct reattn_weights reattn_weights;
+/* ModelConfig::validate (model.hpp:50-60) */
+int reattn_model_config_validate(reattn_ctx* ctx, const reattn_model_config* cfg);
+/* zero projections, unit norms */
+int reattn_weights_create(reattn_ctx* ctx, const reattn_model_config* cfg, reattn_weights** out);
+/* init_random (model.hpp:127-166): the same mt19937_64 Box-Muller stream, std 0.02 */
+int reattn_weights_init_random(reattn_ctx* ctx, const reattn_model_config* cfg, uint64_t seed,
+                               reattn_weights** out);
+/* RATW weight files (model.hpp:224-339 save_weights / load_weights) */
+int reattn_weights_load(reattn_ctx* ctx, const char* path, reattn_weights** out);
+int reattn_weights_save(reattn_ctx* ctx, const reattn_weights* w, const char* path);
+int reattn_weights_config(const reattn_weights* w, reattn_model_config* cfg);
+int reattn_weights_shape(const reattn_weights* w, int kind, uint64_t* rows, uint64_t* cols);
+int reattn_weights_upload(reattn_ctx* ctx, reattn_weights* w, int kind, uint64_t layer,
+                          const float* host, uint64_t n);
+int reattn_weights_download(reattn_ctx* ctx, const reattn_weights* w, int kind, uint64_t layer,
+                            float* host, uint64_t n);
+void reattn_weights_destroy(reattn_weights* w);
+
+/* RunStats accumulated over an engine's steps (engine.hpp:23-37) */
+typedef struct {
+    uint64_t max_position_used;
+    uint64_t ood_positions;
+    int32_t coverage_total;
+    int32_t reserved;
+    double entropy_max;
+    double entropy_sum;
+    uint64_t entropy_rows;
+    uint64_t scope_len_max;
+    uint64_t peak_scratch_bytes;
+    uint64_t chunks_processed;
+    uint64_t decode_steps;
+} reattn_run_stats;
+
+typedef struct reattn_engine reattn_engine;
+/* Engine(weights, sel, mode) (engine.hpp:118-131): `w` must outlive the engine.
+ * cache_dtype: REATTN_F32 (the reference's storage) or REATTN_BF16. */
+int reattn_engine_create(reattn_ctx* ctx, const reattn_weights* w, const reattn_selection_config* sel,
+                         int mode, int cache_dtype, reattn_engine** out);
+int reattn_engine_reset(reattn_engine* e);
+/* prefill (engine.hpp:146-159): first l_global + l_local tokens, then l_chunk strides; the
+ * final chunk's hidden states stay on the device (rows -> *rows_out) */
+int reattn_engine_prefill(reattn_engine* e, const uint32_t* tokens_host, uint64_t n,
+                          uint64_t* rows_out);
+/* the hidden states of the last forward block, rows x d_model */
+int reattn_engine_hidden(reattn_engine* e, float* host, uint64_t n);
+/* logits(hidden) (engine.hpp:176-179): final norm + lm_head of host rows x d_model */
+int reattn_engine_logits(reattn_engine* e, const float* hidden_host, uint64_t rows,
+                         float* logits_host);
+/* decode_step (engine.hpp:162-173): one token in, greedy next token out */
+int reattn_engine_decode_step(reattn_engine* e, uint32_t last_token, uint32_t* next_token);
+int reattn_engine_last_logits(reattn_engine* e, float* host, uint64_t n);
+int reattn_engine_stats(const reattn_engine* e, reattn_run_stats* st);
+/* decode_latency_ms entries (up to cap); *n = how many exist */
+int reattn_engine_decode_latencies(const reattn_engine* e, double* out, uint64_t cap, uint64_t* n);
+/* spans chosen by the layer's most recent attend_step (engine.hpp:185-186) */
+int reattn_engine_last_spans(const reattn_engine* e, uint64_t layer, uint64_t* begin,
+                             uint64_t* end, uint64_t cap, uint64_t* n);
+const reattn_cache* reattn_engine_cache(const reattn_engine* e, uint64_t layer);
+void reattn_engine_destroy(reattn_engine* e);
+
 /* ---- synthetic inputs (tests and benchmarks; not on the hot path) ---------------- */
 /* dst[i] = splitmix64(seed, offset+i) mapped to [-1, 1) (24 significant bits), stored as
  * fp32 or bf16 (round to nearest even). */

@@ -9,6 +9,7 @@
 #include <exception>
 #include <memory>
 #include <optional>
+#include <random>
 #include <stdexcept>
 #include <span>
 #include <string>
@@ -16,6 +17,9 @@
 
 #include "reattn/attend.hpp"
 #include "reattn/engine.hpp"
+#include "reattn/full_attention.hpp"
+#include "reattn/model.hpp"
+#include "reattn/window_reference.hpp"
 #include "reattn/kv_cache.hpp"
 #include "reattn/rope.hpp"
 #include "reattn/scope.hpp"
@@ -345,6 +349,182 @@ int ref_fma_selfcheck(std::size_t d, std::size_t trials, std::size_t* unfused_hi
     if (un == trials) return 0;
     if (fm == trials) return 1;
     return 2;
+}
+
+
+// ---- decoder model / engine (model.hpp, engine.hpp:115-218, full_attention.hpp) ----
+// cfg8: n_layer, n_head, n_kv_head, d_model, d_head, d_ff, vocab_size, pretrain_window
+void* ref_model_init(const uint64_t* cfg8, double rope_base, int mode, uint64_t seed) {
+    try {
+        ModelConfig c;
+        c.n_layer = cfg8[0];
+        c.n_head = cfg8[1];
+        c.n_kv_head = cfg8[2];
+        c.d_model = cfg8[3];
+        c.d_head = cfg8[4];
+        c.d_ff = cfg8[5];
+        c.vocab_size = cfg8[6];
+        c.pretrain_window = cfg8[7];
+        c.rope_base = rope_base;
+        c.attention_mode = static_cast<AttentionMode>(mode);
+        return new ModelWeights(init_random(c, seed));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+void* ref_model_load(const char* path) {
+    try {
+        return new ModelWeights(load_weights(path));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+int ref_model_save(void* w, const char* path) { REF_TRY(save_weights(*static_cast<ModelWeights*>(w), path)) }
+
+void ref_model_destroy(void* w) { delete static_cast<ModelWeights*>(w); }
+
+// tensor kinds as reattn_weight_kind (include/reattn_cuda.h)
+int ref_model_tensor(void* wp, int kind, std::size_t layer, float* out, std::size_t n) {
+    REF_TRY({
+        const ModelWeights& w = *static_cast<ModelWeights*>(wp);
+        const std::vector<float>* v = nullptr;
+        const LayerWeights* L = kind >= 1 && kind <= 9 ? &w.layers.at(layer) : nullptr;
+        switch (kind) {
+            case 0: v = &w.embedding.values; break;
+            case 1: v = &L->wq.values; break;
+            case 2: v = &L->wk.values; break;
+            case 3: v = &L->wv.values; break;
+            case 4: v = &L->wo.values; break;
+            case 5: v = &L->w_gate.values; break;
+            case 6: v = &L->w_up.values; break;
+            case 7: v = &L->w_down.values; break;
+            case 8: v = &L->norm_attn; break;
+            case 9: v = &L->norm_ffn; break;
+            case 10: v = &w.norm_final; break;
+            case 11: v = &w.lm_head.values; break;
+            default: throw std::invalid_argument("bad kind");
+        }
+        if (v->size() != n) throw std::invalid_argument("size mismatch");
+        std::memcpy(out, v->data(), n * sizeof(float));
+    })
+}
+
+// forward_full (full_attention.hpp:21-69): logits n x vocab
+int ref_forward_full(void* w, const uint32_t* tokens, std::size_t n, float* logits) {
+    REF_TRY({
+        const DenseMatrix o = forward_full(std::span<const uint32_t>(tokens, n), *static_cast<ModelWeights*>(w));
+        std::memcpy(logits, o.values.data(), o.values.size() * sizeof(float));
+    })
+}
+
+struct RefEngine {
+    std::unique_ptr<Engine> eng;
+    std::unique_ptr<WindowReference> win;
+};
+
+// sel7: k, k_prime, span_m, tile, l_global, l_local, l_chunk.  kind 0 = Engine(mode),
+// 1 = WindowReference(w, l_global, l_local, l_chunk)
+void* ref_engine_create(void* w, const uint64_t* sel7, int span_mode, int mode, int kind) {
+    try {
+        SelectionConfig s;
+        s.k = sel7[0];
+        s.k_prime = sel7[1];
+        s.span_m = sel7[2];
+        s.tile_size = sel7[3];
+        s.l_global = sel7[4];
+        s.l_local = sel7[5];
+        s.l_chunk = sel7[6];
+        s.span_mode = span_mode == 0 ? SpanMode::Aligned : SpanMode::Centered;
+        auto* r = new RefEngine();
+        const ModelWeights& mw = *static_cast<ModelWeights*>(w);
+        if (kind == 0)
+            r->eng = std::make_unique<Engine>(mw, s, static_cast<AttentionMode>(mode));
+        else
+            r->win = std::make_unique<WindowReference>(mw, s.l_global, s.l_local, s.l_chunk);
+        return r;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+void ref_engine_destroy(void* e) { delete static_cast<RefEngine*>(e); }
+
+// prefill: hidden of the final chunk (rows x d_model) into `hidden` (capacity cap floats)
+int ref_engine_prefill(void* ep, const uint32_t* tokens, std::size_t n, float* hidden,
+                       std::size_t cap, std::size_t* rows) {
+    REF_TRY({
+        auto* r = static_cast<RefEngine*>(ep);
+        const DenseMatrix h = r->eng ? r->eng->prefill(std::span<const uint32_t>(tokens, n))
+                                     : r->win->prefill(std::span<const uint32_t>(tokens, n));
+        if (h.values.size() > cap) throw std::invalid_argument("hidden capacity");
+        std::memcpy(hidden, h.values.data(), h.values.size() * sizeof(float));
+        *rows = h.rows;
+    })
+}
+
+int ref_engine_logits(void* ep, const float* hidden, std::size_t rows, std::size_t d_model,
+                      float* out) {
+    REF_TRY({
+        auto* r = static_cast<RefEngine*>(ep);
+        if (!r->eng) throw std::invalid_argument("logits: engine only");
+        const DenseMatrix l = r->eng->logits(to_matrix(hidden, rows, d_model));
+        std::memcpy(out, l.values.data(), l.values.size() * sizeof(float));
+    })
+}
+
+// decode_step: next token + last logits (vocab floats)
+int ref_engine_decode(void* ep, uint32_t tok, uint32_t* next, float* logits, std::size_t vocab) {
+    REF_TRY({
+        auto* r = static_cast<RefEngine*>(ep);
+        *next = r->eng ? r->eng->decode_step(tok) : r->win->decode_step(tok);
+        std::span<const float> l = r->eng ? r->eng->last_logits() : r->win->last_logits();
+        if (l.size() != vocab) throw std::invalid_argument("vocab mismatch");
+        std::memcpy(logits, l.data(), vocab * sizeof(float));
+    })
+}
+
+// RunStats: out10 = max_position_used, ood_positions, coverage_total, entropy_max,
+// entropy_sum, entropy_rows, scope_len_max, peak_scratch_bytes, chunks_processed, decode_steps
+int ref_engine_stats(void* ep, double* out10) {
+    REF_TRY({
+        auto* r = static_cast<RefEngine*>(ep);
+        if (!r->eng) throw std::invalid_argument("stats: engine only");
+        const RunStats& s = r->eng->stats();
+        out10[0] = double(s.max_position_used);
+        out10[1] = double(s.ood_positions);
+        out10[2] = double(s.coverage_total);
+        out10[3] = s.entropy_max;
+        out10[4] = s.entropy_sum;
+        out10[5] = double(s.entropy_rows);
+        out10[6] = double(s.scope_len_max);
+        out10[7] = double(s.peak_scratch_bytes);
+        out10[8] = double(s.chunks_processed);
+        out10[9] = double(s.decode_steps);
+    })
+}
+
+
+// the reference tests' random_tokens (test_engine.cpp:50-56): std::mt19937 +
+// uniform_int_distribution<uint32_t>(0, vocab - 1), this build's standard library
+void ref_random_tokens(std::size_t n, uint32_t vocab, uint32_t seed, uint32_t* out) {
+    std::mt19937 rng(seed);
+    std::uniform_int_distribution<std::uint32_t> dist(0, vocab - 1);
+    for (std::size_t i = 0; i < n; ++i) out[i] = dist(rng);
+}
+
+// greedy_decode_full (full_attention.hpp:72-84)
+int ref_greedy_decode_full(void* w, const uint32_t* prompt, std::size_t n, std::size_t steps,
+                           uint32_t* out) {
+    REF_TRY({
+        const std::vector<std::uint32_t> g = greedy_decode_full(
+            std::span<const uint32_t>(prompt, n), *static_cast<ModelWeights*>(w), steps);
+        std::copy(g.begin(), g.end(), out);
+    })
 }
 
 }  // extern "C"

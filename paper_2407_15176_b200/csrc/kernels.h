@@ -235,4 +235,12 @@ cudaError_t launch_synth_uniform(void* dst, int dtype, uint64_t n, uint64_t seed
 cudaError_t launch_entropy_stats(const double* entropy, int n_q, int n_head, double* out2,
                                  cudaStream_t s);
 
+// ---- decoder block around attend_step (model.cu; reference model.hpp) ----------------------
+cudaError_t launch_embed(const uint32_t* tokens, uint64_t rows, const float* emb, uint64_t d_model,
+                         float* out, cudaStream_t s);
+cudaError_t launch_rmsnorm(const float* x, uint64_t rows, uint64_t cols, const float* w, float* out,
+                           cudaStream_t s);
+cudaError_t launch_silu_mul(float* gate, const float* up, uint64_t n, cudaStream_t s);
+cudaError_t launch_argmax(const float* v, uint64_t n, uint32_t* out, cudaStream_t s);
+
 }  // namespace reattn_impl

@@ -50,6 +50,34 @@ class StepStats(C.Structure):
                 ("peak_scratch_bytes", u64)]
 
 
+class ModelConfig(C.Structure):
+    """reattn::ModelConfig (model.hpp:39-61); defaults are the reference's toy model."""
+
+    _fields_ = [("n_layer", u64), ("n_head", u64), ("n_kv_head", u64), ("d_model", u64),
+                ("d_head", u64), ("d_ff", u64), ("vocab_size", u64), ("pretrain_window", u64),
+                ("rope_base", C.c_double), ("attention_mode", C.c_int32), ("reserved", C.c_int32)]
+
+    def __init__(self, n_layer=2, n_head=4, n_kv_head=2, d_model=128, d_head=32, d_ff=512,
+                 vocab_size=512, pretrain_window=4096, rope_base=10000.0,
+                 attention_mode=MODE_REATTENTION):
+        super().__init__(n_layer, n_head, n_kv_head, d_model, d_head, d_ff, vocab_size,
+                         pretrain_window, rope_base, attention_mode, 0)
+
+
+class RunStats(C.Structure):
+    """reattn::RunStats (engine.hpp:23-37) accumulated by an Engine."""
+
+    _fields_ = [("max_position_used", u64), ("ood_positions", u64), ("coverage_total", C.c_int32),
+                ("reserved", C.c_int32), ("entropy_max", C.c_double), ("entropy_sum", C.c_double),
+                ("entropy_rows", u64), ("scope_len_max", u64), ("peak_scratch_bytes", u64),
+                ("chunks_processed", u64), ("decode_steps", u64)]
+
+
+# reattn_weight_kind
+(W_EMBEDDING, W_WQ, W_WK, W_WV, W_WO, W_GATE, W_UP, W_DOWN, W_NORM_ATTN, W_NORM_FFN,
+ W_NORM_FINAL, W_LM_HEAD) = range(12)
+
+
 class ReattnError(RuntimeError):
     pass
 
@@ -137,6 +165,29 @@ SIGNATURES = [
     ("reattn_batch_plan_stats", C.c_int, [vp, C.c_uint32, vp]),
     ("reattn_batch_plan_info", C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(C.c_int)]),
     ("reattn_synth_uniform", C.c_int, [vp, vp, u64, C.c_int, u64, u64]),
+    ("reattn_model_config_validate", C.c_int, [vp, C.POINTER(ModelConfig)]),
+    ("reattn_weights_create", C.c_int, [vp, C.POINTER(ModelConfig), C.POINTER(vp)]),
+    ("reattn_weights_init_random", C.c_int, [vp, C.POINTER(ModelConfig), u64, C.POINTER(vp)]),
+    ("reattn_weights_load", C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
+    ("reattn_weights_save", C.c_int, [vp, vp, C.c_char_p]),
+    ("reattn_weights_config", C.c_int, [vp, C.POINTER(ModelConfig)]),
+    ("reattn_weights_shape", C.c_int, [vp, C.c_int, C.POINTER(u64), C.POINTER(u64)]),
+    ("reattn_weights_upload", C.c_int, [vp, vp, C.c_int, u64, vp, u64]),
+    ("reattn_weights_download", C.c_int, [vp, vp, C.c_int, u64, vp, u64]),
+    ("reattn_weights_destroy", None, [vp]),
+    ("reattn_engine_create", C.c_int, [vp, vp, C.POINTER(SelectionConfig), C.c_int, C.c_int,
+                                       C.POINTER(vp)]),
+    ("reattn_engine_reset", C.c_int, [vp]),
+    ("reattn_engine_prefill", C.c_int, [vp, vp, u64, C.POINTER(u64)]),
+    ("reattn_engine_hidden", C.c_int, [vp, vp, u64]),
+    ("reattn_engine_logits", C.c_int, [vp, vp, u64, vp]),
+    ("reattn_engine_decode_step", C.c_int, [vp, C.c_uint32, C.POINTER(C.c_uint32)]),
+    ("reattn_engine_last_logits", C.c_int, [vp, vp, u64]),
+    ("reattn_engine_stats", C.c_int, [vp, C.POINTER(RunStats)]),
+    ("reattn_engine_decode_latencies", C.c_int, [vp, vp, u64, C.POINTER(u64)]),
+    ("reattn_engine_last_spans", C.c_int, [vp, u64, vp, vp, u64, C.POINTER(u64)]),
+    ("reattn_engine_cache", vp, [vp, u64]),
+    ("reattn_engine_destroy", None, [vp]),
     ("reattn_shard_plan_create", C.c_int, [vp, vp, vp, u64, C.POINTER(SelectionConfig), u64,
                                            C.c_int, C.c_int, C.POINTER(vp)]),
     ("reattn_shard_plan_destroy", None, [vp]),
@@ -531,4 +582,136 @@ class BatchPlan:
     def __del__(self):
         if getattr(self, "h", None) and self.ctx.h:
             self.ctx.lib.reattn_batch_plan_destroy(self.h)
+            self.h = None
+
+
+class Weights:
+    """reattn::ModelWeights (model.hpp:62-86) resident on the device (fp32)."""
+
+    def __init__(self, ctx: Context, h):
+        self.ctx, self.h = ctx, h
+        cfg = ModelConfig()
+        ctx.check(ctx.lib.reattn_weights_config(h, C.byref(cfg)))
+        self.config = cfg
+
+    @classmethod
+    def init_random(cls, ctx: Context, cfg: ModelConfig, seed: int) -> "Weights":
+        """init_random (model.hpp:127-166): the reference's pinned Gaussian stream."""
+        h = vp()
+        ctx.check(ctx.lib.reattn_weights_init_random(ctx.h, C.byref(cfg), seed, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def zeros(cls, ctx: Context, cfg: ModelConfig) -> "Weights":
+        h = vp()
+        ctx.check(ctx.lib.reattn_weights_create(ctx.h, C.byref(cfg), C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def load(cls, ctx: Context, path: str) -> "Weights":
+        """load_weights (model.hpp:311-339), RATW file."""
+        h = vp()
+        ctx.check(ctx.lib.reattn_weights_load(ctx.h, os.fsencode(path), C.byref(h)))
+        return cls(ctx, h)
+
+    def save(self, path: str) -> None:
+        self.ctx.check(self.ctx.lib.reattn_weights_save(self.ctx.h, self.h, os.fsencode(path)))
+
+    def shape(self, kind: int):
+        r, c = u64(), u64()
+        self.ctx.check(self.ctx.lib.reattn_weights_shape(self.h, kind, C.byref(r), C.byref(c)))
+        return r.value, c.value
+
+    def tensor(self, kind: int, layer: int = 0):
+        import numpy as np
+        r, c = self.shape(kind)
+        out = np.zeros((r, c), np.float32)
+        self.ctx.check(self.ctx.lib.reattn_weights_download(self.ctx.h, self.h, kind, layer,
+                                                            out.ctypes.data, out.size))
+        return out
+
+    def set_tensor(self, kind: int, layer: int, values) -> None:
+        import numpy as np
+        v = np.ascontiguousarray(values, dtype=np.float32)
+        self.ctx.check(self.ctx.lib.reattn_weights_upload(self.ctx.h, self.h, kind, layer,
+                                                          v.ctypes.data, v.size))
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.ctx.h:
+            self.ctx.lib.reattn_weights_destroy(self.h)
+            self.h = None
+
+
+class Engine:
+    """reattn::Engine (engine.hpp:115-218) on the device: per-layer caches, chunked
+    prefill, greedy decode.  `weights` must outlive the engine (held here)."""
+
+    def __init__(self, ctx: Context, weights: Weights, sel: SelectionConfig,
+                 mode: int = MODE_REATTENTION, cache_dtype: int = F32):
+        self.ctx, self.weights, self.sel = ctx, weights, sel
+        h = vp()
+        ctx.check(ctx.lib.reattn_engine_create(ctx.h, weights.h, C.byref(sel), mode, cache_dtype,
+                                               C.byref(h)))
+        self.h = h
+        self.config = weights.config
+
+    def reset(self) -> None:
+        self.ctx.check(self.ctx.lib.reattn_engine_reset(self.h))
+
+    def prefill(self, tokens):
+        """Returns the final chunk's hidden states (rows x d_model, numpy)."""
+        import numpy as np
+        t = np.ascontiguousarray(np.asarray(tokens, dtype=np.uint32))
+        rows = u64()
+        self.ctx.check(self.ctx.lib.reattn_engine_prefill(self.h, t.ctypes.data if t.size else None,
+                                                          t.size, C.byref(rows)))
+        out = np.zeros((rows.value, self.config.d_model), np.float32)
+        self.ctx.check(self.ctx.lib.reattn_engine_hidden(self.h, out.ctypes.data, out.size))
+        return out
+
+    def logits(self, hidden):
+        import numpy as np
+        hid = np.ascontiguousarray(hidden, dtype=np.float32)
+        out = np.zeros((hid.shape[0], self.config.vocab_size), np.float32)
+        self.ctx.check(self.ctx.lib.reattn_engine_logits(self.h, hid.ctypes.data, hid.shape[0],
+                                                         out.ctypes.data))
+        return out
+
+    def decode_step(self, last_token: int) -> int:
+        nt = C.c_uint32()
+        self.ctx.check(self.ctx.lib.reattn_engine_decode_step(self.h, last_token, C.byref(nt)))
+        return nt.value
+
+    def last_logits(self):
+        import numpy as np
+        out = np.zeros(self.config.vocab_size, np.float32)
+        self.ctx.check(self.ctx.lib.reattn_engine_last_logits(self.h, out.ctypes.data, out.size))
+        return out
+
+    def stats(self) -> RunStats:
+        st = RunStats()
+        self.ctx.check(self.ctx.lib.reattn_engine_stats(self.h, C.byref(st)))
+        return st
+
+    def decode_latencies(self):
+        import numpy as np
+        n = u64()
+        self.ctx.lib.reattn_engine_decode_latencies(self.h, None, 0, C.byref(n))
+        out = np.zeros(n.value, np.float64)
+        self.ctx.lib.reattn_engine_decode_latencies(self.h, out.ctypes.data, n.value, C.byref(n))
+        return out
+
+    def last_spans(self, layer: int):
+        import numpy as np
+        n = u64()
+        self.ctx.check(self.ctx.lib.reattn_engine_last_spans(self.h, layer, None, None, 0, C.byref(n)))
+        b = np.zeros(n.value, np.uint64)
+        e = np.zeros(n.value, np.uint64)
+        self.ctx.check(self.ctx.lib.reattn_engine_last_spans(self.h, layer, b.ctypes.data,
+                                                             e.ctypes.data, n.value, C.byref(n)))
+        return list(zip(b.tolist(), e.tolist()))
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.ctx.h:
+            self.ctx.lib.reattn_engine_destroy(self.h)
             self.h = None

@@ -156,6 +156,26 @@ def ref() -> C.CDLL | None:
         lib.ref_fma_selfcheck.argtypes = [sz, sz, C.POINTER(sz), C.POINTER(sz)]
         lib.ref_snapshot_write.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), sz]
         lib.ref_snapshot_read.argtypes = [C.c_char_p, sz, C.POINTER(sz), u64p, f32p, f32p, sz]
+        vpp = C.c_void_p
+        lib.ref_model_init.restype = vpp
+        lib.ref_model_init.argtypes = [u64p, C.c_double, C.c_int, C.c_uint64]
+        lib.ref_model_load.restype = vpp
+        lib.ref_model_load.argtypes = [C.c_char_p]
+        lib.ref_model_save.argtypes = [vpp, C.c_char_p]
+        lib.ref_model_destroy.argtypes = [vpp]
+        lib.ref_model_tensor.argtypes = [vpp, C.c_int, sz, f32p, sz]
+        lib.ref_forward_full.argtypes = [vpp, C.POINTER(C.c_uint32), sz, f32p]
+        lib.ref_engine_create.restype = vpp
+        lib.ref_engine_create.argtypes = [vpp, u64p, C.c_int, C.c_int, C.c_int]
+        lib.ref_engine_destroy.argtypes = [vpp]
+        lib.ref_engine_prefill.argtypes = [vpp, C.POINTER(C.c_uint32), sz, f32p, sz, C.POINTER(sz)]
+        lib.ref_engine_logits.argtypes = [vpp, f32p, sz, sz, f32p]
+        lib.ref_engine_decode.argtypes = [vpp, C.c_uint32, C.POINTER(C.c_uint32), f32p, sz]
+        lib.ref_engine_stats.argtypes = [vpp, f64p]
+        lib.ref_random_tokens.argtypes = [sz, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32)]
+        lib.ref_random_tokens.restype = None
+        lib.ref_greedy_decode_full.argtypes = [vpp, C.POINTER(C.c_uint32), sz, sz,
+                                               C.POINTER(C.c_uint32)]
         _ref = lib
     return _ref
 
@@ -299,3 +319,121 @@ def round_bf16(x: np.ndarray) -> np.ndarray:
     u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
     u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
     return u.astype(np.uint32).view(np.float32)
+
+
+# ---------------------------------------------------------------------------------------
+# the reference's decoder model and Engine (model.hpp, engine.hpp:115-218), run in place
+
+def _u32(tokens):
+    t = np.ascontiguousarray(np.asarray(tokens, dtype=np.uint32))
+    return t, t.ctypes.data_as(C.POINTER(C.c_uint32))
+
+
+class RefModel:
+    """reattn::ModelWeights from init_random(cfg, seed) or load_weights(path)."""
+
+    def __init__(self, cfg=None, seed=0, path=None):
+        lib = ref()
+        if lib is None:
+            raise RuntimeError("oracle/_ref not built")
+        self.lib = lib
+        if path is not None:
+            self.h = lib.ref_model_load(os.fsencode(path))
+        else:
+            c8 = np.array([cfg.n_layer, cfg.n_head, cfg.n_kv_head, cfg.d_model, cfg.d_head,
+                           cfg.d_ff, cfg.vocab_size, cfg.pretrain_window], np.uint64)
+            self.h = lib.ref_model_init(c8, cfg.rope_base, cfg.attention_mode, seed)
+        if not self.h:
+            raise RuntimeError(lib.ref_last_error().decode())
+        self.cfg = cfg
+
+    def tensor(self, kind, layer, shape):
+        out = np.zeros(shape, np.float32)
+        rc = self.lib.ref_model_tensor(self.h, kind, layer, out, out.size)
+        if rc:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return out
+
+    def save(self, path):
+        rc = self.lib.ref_model_save(self.h, os.fsencode(path))
+        if rc:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+
+    def forward_full(self, tokens, vocab):
+        t, tp = _u32(tokens)
+        out = np.zeros((t.size, vocab), np.float32)
+        rc = self.lib.ref_forward_full(self.h, tp, t.size, out)
+        if rc:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.ref_model_destroy(self.h)
+            self.h = None
+
+
+class RefEngine:
+    """reattn::Engine (kind 0) or reattn::WindowReference (kind 1) over a RefModel."""
+
+    def __init__(self, model: RefModel, sel, mode=2, kind=0, d_model=None, vocab=None):
+        self.model, self.lib = model, model.lib
+        s7 = np.array([sel.k, sel.k_prime, sel.span_m, sel.tile_size, sel.l_global, sel.l_local,
+                       sel.l_chunk], np.uint64)
+        self.h = self.lib.ref_engine_create(model.h, s7, sel.span_mode, mode, kind)
+        if not self.h:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        self.d_model, self.vocab = d_model, vocab
+
+    def _chk(self, rc):
+        if rc:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+
+    def prefill(self, tokens):
+        t, tp = _u32(tokens)
+        buf = np.zeros(t.size * self.d_model + 1, np.float32)
+        rows = sz(0)
+        self._chk(self.lib.ref_engine_prefill(self.h, tp, t.size, buf, buf.size, C.byref(rows)))
+        return buf[: rows.value * self.d_model].reshape(rows.value, self.d_model).copy()
+
+    def logits(self, hidden):
+        h = np.ascontiguousarray(hidden, np.float32)
+        out = np.zeros((h.shape[0], self.vocab), np.float32)
+        self._chk(self.lib.ref_engine_logits(self.h, h, h.shape[0], self.d_model, out))
+        return out
+
+    def decode_step(self, tok):
+        nt = C.c_uint32()
+        lg = np.zeros(self.vocab, np.float32)
+        self._chk(self.lib.ref_engine_decode(self.h, tok, C.byref(nt), lg, self.vocab))
+        return nt.value, lg
+
+    def stats(self):
+        out = np.zeros(10, np.float64)
+        self._chk(self.lib.ref_engine_stats(self.h, out))
+        keys = ["max_position_used", "ood_positions", "coverage_total", "entropy_max",
+                "entropy_sum", "entropy_rows", "scope_len_max", "peak_scratch_bytes",
+                "chunks_processed", "decode_steps"]
+        return dict(zip(keys, out.tolist()))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.ref_engine_destroy(self.h)
+            self.h = None
+
+
+def random_tokens(n: int, vocab: int, seed: int) -> np.ndarray:
+    """test_engine.cpp:50-56 random_tokens, generated by the reference build itself."""
+    out = np.zeros(n, np.uint32)
+    ref().ref_random_tokens(n, vocab, seed, out.ctypes.data_as(C.POINTER(C.c_uint32)))
+    return out
+
+
+def greedy_decode_full(model: "RefModel", prompt, steps: int) -> list:
+    t, tp = _u32(prompt)
+    out = np.zeros(steps, np.uint32)
+    rc = model.lib.ref_greedy_decode_full(model.h, tp, t.size, steps,
+                                          out.ctypes.data_as(C.POINTER(C.c_uint32)))
+    if rc:
+        raise RuntimeError(model.lib.ref_last_error().decode())
+    return out.tolist()
