@@ -1,8 +1,8 @@
-// Drop-in for the hot-path part of reattn/engine.hpp: AttentionMode (model.hpp:19),
-// RunStats (engine.hpp:23-37) and attend_step (engine.hpp:43-114 in the survey's
-// numbering; :501-572 in the file).  The whole step — selection gated as the reference,
-// vote, spans, scope, RoPE at compact positions, attention — is one device pipeline
-// (reattn_attend_step).  The toy-model Engine around it is out of scope.
+// Drop-in for reattn/engine.hpp: RunStats (engine.hpp:23-37), attend_step (engine.hpp:43-114)
+// and the generation Engine (engine.hpp:115-218).  attend_step -- selection gated as the
+// reference, vote, spans, scope, RoPE at compact positions, attention -- is one device
+// pipeline (reattn_attend_step); the Engine runs every layer of the decoder on the device
+// (reattn_engine_*): projections, cache appends, attend_step, FFN, logits, greedy pick.
 #pragma once
 
 #include <algorithm>
@@ -13,14 +13,13 @@
 
 #include "reattn/attend.hpp"
 #include "reattn/kv_cache.hpp"
+#include "reattn/model.hpp"
 #include "reattn/rope.hpp"
 #include "reattn/runtime.hpp"
 #include "reattn/scope.hpp"
 #include "reattn/selection.hpp"
 
 namespace reattn {
-
-enum class AttentionMode : std::uint32_t { Full = 0, Window = 1, ReAttention = 2 };
 
 struct RunStats {
     std::size_t max_position_used = 0;
@@ -79,5 +78,102 @@ inline DenseMatrix attend_step(const DenseMatrix& q_pre, std::size_t n_head,
     }
     return out;
 }
+
+// Engine (engine.hpp:115-218): per-layer device caches, chunked prefill (first l_global +
+// l_local tokens, then l_chunk strides), greedy decode.  Holds `weights` by reference as the
+// reference does, plus its device copy.  caches() is not mirrored (the device caches are
+// reachable through reattn_engine_cache); everything else keeps the reference's semantics.
+class Engine {
+public:
+    Engine(const ModelWeights& weights, const SelectionConfig& sel, AttentionMode mode)
+        : w_(weights), sel_(sel), mode_(mode), dev_(detail::DeviceWeights::from_host(weights)) {
+        const reattn_selection_config c = sel.to_c();
+        gpu::check(reattn_engine_create(gpu::context(), dev_.get(), &c, static_cast<int>(mode),
+                                        REATTN_F32, &e_));
+        last_spans_.assign(weights.config.n_layer, SpanSet{});
+    }
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+    ~Engine() {
+        if (e_) reattn_engine_destroy(e_);
+    }
+
+    void reset() {
+        gpu::check(reattn_engine_reset(e_));
+        last_spans_.assign(w_.config.n_layer, SpanSet{});
+        last_logits_.clear();
+        refresh();
+    }
+
+    DenseMatrix prefill(std::span<const std::uint32_t> tokens) {
+        std::uint64_t rows = 0;
+        gpu::check(reattn_engine_prefill(e_, tokens.data(), tokens.size(), &rows));
+        DenseMatrix h(rows, w_.config.d_model);
+        gpu::check(reattn_engine_hidden(e_, h.values.data(), h.values.size()));
+        refresh();
+        return h;
+    }
+
+    std::uint32_t decode_step(std::uint32_t last_token) {
+        std::uint32_t next = 0;
+        gpu::check(reattn_engine_decode_step(e_, last_token, &next));
+        last_logits_.resize(w_.config.vocab_size);
+        gpu::check(reattn_engine_last_logits(e_, last_logits_.data(), last_logits_.size()));
+        refresh();
+        return next;
+    }
+
+    DenseMatrix logits(const DenseMatrix& hidden) const {
+        DenseMatrix out(hidden.rows, w_.config.vocab_size);
+        if (hidden.cols != w_.config.d_model) throw std::invalid_argument("rmsnorm: weight width mismatch");
+        gpu::check(reattn_engine_logits(e_, hidden.values.data(), hidden.rows, out.values.data()));
+        return out;
+    }
+
+    const RunStats& stats() const { return stats_; }
+    const std::vector<SpanSet>& last_spans() const { return last_spans_; }
+    const ModelWeights& weights() const { return w_; }
+    const SelectionConfig& selection_config() const { return sel_; }
+    AttentionMode mode() const { return mode_; }
+    std::span<const float> last_logits() const { return last_logits_; }
+    const reattn_cache* cache_handle(std::size_t layer) const { return reattn_engine_cache(e_, layer); }
+
+private:
+    void refresh() {
+        reattn_run_stats s{};
+        gpu::check(reattn_engine_stats(e_, &s));
+        stats_.max_position_used = s.max_position_used;
+        stats_.ood_positions = s.ood_positions;
+        stats_.coverage_total = s.coverage_total != 0;
+        stats_.entropy_max = s.entropy_max;
+        stats_.entropy_sum = s.entropy_sum;
+        stats_.entropy_rows = s.entropy_rows;
+        stats_.scope_len_max = s.scope_len_max;
+        stats_.peak_scratch_bytes = s.peak_scratch_bytes;
+        stats_.chunks_processed = s.chunks_processed;
+        stats_.decode_steps = s.decode_steps;
+        std::uint64_t n = 0;
+        gpu::check(reattn_engine_decode_latencies(e_, nullptr, 0, &n));
+        stats_.decode_latency_ms.resize(n);
+        gpu::check(reattn_engine_decode_latencies(e_, stats_.decode_latency_ms.data(), n, &n));
+        for (std::size_t l = 0; l < last_spans_.size(); ++l) {
+            std::uint64_t k = 0;
+            gpu::check(reattn_engine_last_spans(e_, l, nullptr, nullptr, 0, &k));
+            std::vector<std::uint64_t> b(k), e(k);
+            gpu::check(reattn_engine_last_spans(e_, l, b.data(), e.data(), k, &k));
+            last_spans_[l].spans.clear();
+            for (std::size_t i = 0; i < k; ++i) last_spans_[l].spans.push_back(Span{b[i], e[i]});
+        }
+    }
+
+    const ModelWeights& w_;
+    SelectionConfig sel_;
+    AttentionMode mode_;
+    detail::DeviceWeights dev_;
+    reattn_engine* e_ = nullptr;
+    RunStats stats_;
+    std::vector<SpanSet> last_spans_;
+    std::vector<float> last_logits_;
+};
 
 }  // namespace reattn

@@ -478,6 +478,125 @@ static void test_snapshot() {
     std::remove(path.c_str());
 }
 
+// test_engine.cpp (reference) on the drop-in Engine / ModelWeights / forward_full /
+// WindowReference headers.  Parity against the reference build itself is in
+// tests/test_engine_gpu.py; here the API surface, its identities and its errors.
+static ModelConfig toy_config() {
+    ModelConfig cfg;
+    cfg.n_layer = 2;
+    cfg.n_head = 4;
+    cfg.n_kv_head = 2;
+    cfg.d_model = 64;
+    cfg.d_head = 16;
+    cfg.d_ff = 128;
+    cfg.vocab_size = 128;
+    cfg.pretrain_window = 2048;
+    return cfg;
+}
+
+static SelectionConfig toy_selection() {
+    SelectionConfig sel;
+    sel.l_global = 16;
+    sel.l_local = 256;
+    sel.l_chunk = 128;
+    sel.span_m = 16;
+    sel.k = 4;
+    sel.k_prime = 64;
+    sel.tile_size = 512;
+    return sel;
+}
+
+static std::vector<std::uint32_t> tokens_of(std::size_t n, std::uint32_t vocab, std::uint32_t seed) {
+    std::mt19937 rng(seed);
+    std::uniform_int_distribution<std::uint32_t> dist(0, vocab - 1);
+    std::vector<std::uint32_t> out(n);
+    for (auto& t : out) t = dist(rng);
+    return out;
+}
+
+static void test_engine() {
+    const ModelWeights w = init_random(toy_config(), 22);
+    CHECK(w.layers.size() == 2 && w.embedding.rows == 128 && w.lm_head.cols == 128, "shapes");
+    CHECK(w.layers[0].norm_attn.size() == 64 && w.layers[0].norm_attn[0] == 1.0f, "unit norms");
+    // constructor checks (test_engine.cpp:57-66)
+    CHECK(throws<std::invalid_argument>([&] { Engine(w, toy_selection(), AttentionMode::Full); },
+                                        "full attention is the reference path"), "full mode");
+    SelectionConfig big = toy_selection();
+    big.k_prime = 1000;
+    CHECK(throws<std::invalid_argument>([&] { Engine(w, big, AttentionMode::ReAttention); },
+                                        "exceeds pretrain window"), "budget");
+    // single-token prefill == decode on an empty cache (test_engine.cpp:68-78), bitwise
+    {
+        Engine a(w, toy_selection(), AttentionMode::ReAttention);
+        Engine b(w, toy_selection(), AttentionMode::ReAttention);
+        const std::vector<std::uint32_t> one{42};
+        const DenseMatrix la = a.logits(a.prefill(one));
+        b.decode_step(42);
+        bool same = la.cols == b.last_logits().size();
+        for (std::size_t i = 0; same && i < la.cols; ++i) same = la.at(0, i) == b.last_logits()[i];
+        CHECK(same, "prefill == decode");
+    }
+    // full coverage vs forward_full (test_engine.cpp:80-110), 1e-4
+    {
+        const auto toks = tokens_of(372, 128, 220);
+        SelectionConfig sel = toy_selection();
+        sel.k = 100;
+        sel.k_prime = 100;
+        Engine eng(w, sel, AttentionMode::ReAttention);
+        const DenseMatrix got = eng.logits(eng.prefill(toks));
+        CHECK(eng.stats().coverage_total, "coverage");
+        const DenseMatrix full = forward_full(toks, w);
+        double md = 0;
+        for (std::size_t r = 0; r < got.rows; ++r)
+            for (std::size_t c = 0; c < got.cols; ++c)
+                md = std::max(md, std::abs(double(got.at(r, c)) - double(full.at(372 - got.rows + r, c))));
+        CHECK(got.rows == 100 && md <= 1e-4, "md %g", md);
+    }
+    // selection off == WindowReference, bitwise on the device (C03), and window mode
+    {
+        const auto toks = tokens_of(900, 128, 230);
+        SelectionConfig off = toy_selection();
+        off.k_prime = 0;
+        Engine eng(w, off, AttentionMode::ReAttention);
+        WindowReference ref(w, off.l_global, off.l_local, off.l_chunk);
+        const DenseMatrix a = eng.prefill(toks), b = ref.prefill(toks);
+        CHECK(a.values == b.values, "window reference");
+        for (int s = 0; s < 3; ++s) CHECK(eng.decode_step(s) == ref.decode_step(s), "decode %d", s);
+        CHECK(throws<std::invalid_argument>([&] { WindowReference(w, 16, 0, 1); },
+                                            "window reference: bad local/chunk sizes"), "wr");
+    }
+    // stats (test_engine.cpp:219-231)
+    {
+        Engine eng(w, toy_selection(), AttentionMode::ReAttention);
+        eng.prefill(tokens_of(700, 128, 280));
+        CHECK(eng.stats().chunks_processed == 5, "chunks %zu", eng.stats().chunks_processed);
+        eng.decode_step(1);
+        eng.decode_step(2);
+        CHECK(eng.stats().decode_steps == 2 && eng.stats().decode_latency_ms.size() == 2, "steps");
+        CHECK(eng.last_spans().size() == 2, "spans");
+        CHECK(throws<std::out_of_range>([&] { eng.decode_step(500); }, "token id outside vocabulary"),
+              "vocab");
+    }
+    // weights file round trip + load errors (model.hpp:283-339)
+    {
+        char path[] = "/tmp/reattn_dropin_w_XXXXXX";
+        const int fd = mkstemp(path);
+        close(fd);
+        save_weights(w, path);
+        const ModelWeights back = load_weights(path);
+        CHECK(back.embedding.values == w.embedding.values && back.lm_head.values == w.lm_head.values &&
+                  back.layers[1].w_down.values == w.layers[1].w_down.values,
+              "round trip");
+        FILE* f = std::fopen(path, "ab");
+        std::fputc(0, f);
+        std::fclose(f);
+        CHECK(throws<std::runtime_error>([&] { load_weights(path); },
+                                         "weights file: trailing bytes after lm_head"), "trailing");
+        std::remove(path);
+        CHECK(throws<std::runtime_error>([&] { load_weights(path); }, "cannot open weights file"), "missing");
+    }
+}
+
 // REATTN_TEST_GARBAGE=1: fill (and free) most device memory with 0xFF bytes first, so later
 // allocations start from garbage -- surfaces reads of memory a test never wrote.
 static void fill_device_garbage() {
@@ -501,6 +620,7 @@ int main() {
     test_scope();
     test_rope_attend();
     test_attend_step();
+    test_engine();
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }
