@@ -213,6 +213,10 @@ int reattn_plan_launch_scan(reattn_plan* plan);
 int reattn_plan_run_host(reattn_plan* plan, const float* q_host, float* out_host);
 /* synchronise and read the last replay's stats (errors surface here) */
 int reattn_plan_stats(reattn_plan* plan, reattn_step_stats* stats);
+/* Diagnostics, no reference counterpart: with REATTN_TRACE=1 in the environment when a plan
+ * is built, the decode kernels stamp %globaltimer (ns) into a device trace buffer; this
+ * synchronises the device and copies its first n words (n <= 4096) to the host. */
+int reattn_debug_trace(uint64_t* host_out, uint64_t n);
 /* kernels per replay, and the algorithmic bytes of the dominant kernel (the K scan) */
 int reattn_plan_info(const reattn_plan* plan, uint64_t* kernels_per_step,
                      uint64_t* scan_bytes, uint64_t* scope_bytes);

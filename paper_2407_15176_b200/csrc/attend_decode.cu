@@ -27,6 +27,7 @@
 // Numerics: fp32 logits / accumulation within a CTA, f64 across parts: max-abs ~1e-8 on the
 // reference's f64 attend at the decode geometry (north_star fp32 bar: 1e-5).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -74,6 +75,8 @@ struct BulkArgs {
     float scale_log2;
     unsigned int* tickets;  // [n_kv]
     uint8_t* part;          // [n_slots][n_kv][G] partial rows
+    uint64_t* trace;        // diagnostics (misc.cu layout) or null
+    int warm;               // the producer warp dry-runs the merge (see merge_parts)
 };
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -93,9 +96,152 @@ __device__ __forceinline__ float bx_ex2(float x) {
 // rotated fp32 key row r, float4 column i (XOR-swizzled: conflict-free row-per-lane reads)
 __device__ __forceinline__ int rot_idx4(int r, int i) { return r * (kBD / 4) + (i ^ (r & 7)); }
 
+// The last part of a kv head merges the parts' partial rows in part order and writes the
+// output and entropy (attend.hpp:448-455 normalisation), or one merged partial row per head.
+// `role` is the calling warp's compute-warp index.  This code runs once per launch and
+// would run from a cold instruction cache (~0.5 us per fetch miss: ~9 us measured for the
+// merge), so every CTA first runs it dry (global and shared stores predicated off) while it
+// waits for the scan's merger CTA (griddepcontrol.wait): the lines are then resident in the
+// SM's instruction cache when the last CTA runs it for real.  __noinline__ keeps both calls
+// on the same code.
 template <int G>
-__global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const BulkArgs B) {
+__device__ __noinline__ void merge_parts(const BulkArgs& B, int kv, int role, uint8_t* stages, bool dry) {
     const AttnArgs& a = B.a;
+    const int lane = threadIdx.x & 31;
+    // WPH warps per q head, warp j summing slots j, j + WPH, ...: every load of the step (slot
+    // headers by lane = slot, acc rows by lane = 4 columns) is issued before any is used, so
+    // the merge costs one L2 round trip plus an in-order combine of the WPH partial sums
+    // through shared memory (deterministic).  Few registers (no spills) and no f64 library
+    // calls on the path: this code runs once per launch, cold.
+    constexpr int WPH = G == 1 ? 16 : G == 2 ? 8 : G <= 4 ? 4 : 2;
+    constexpr int kPre = 8;  // acc rows in flight per lane
+    double* xo = (double*)stages;  // [G][WPH][kBD] partial sums
+    if (role < G * WPH) {
+        const int g = role / WPH, j = role % WPH;
+        __syncwarp();
+        auto prow = [&](int p) {
+            return B.part + (((size_t)p * a.n_kv + kv) * G + g) * kBPartBytes;
+        };
+        const int n_slots = B.n_slots;
+        double hm = -INFINITY, ha = 0.0, hb = 0.0;  // header of slot `lane` (first page)
+        if (lane < n_slots) {
+            const double* hd = (const double*)prow(lane);
+            hm = __ldcg(hd);
+            ha = __ldcg(hd + 1);
+            hb = __ldcg(hd + 2);
+        }
+        float4 v[kPre];
+#pragma unroll
+        for (int u = 0; u < kPre; ++u) {
+            const int p = j + WPH * u;
+            v[u] = p < n_slots ? __ldcg(reinterpret_cast<const float4*>(prow(p) + 32) + lane)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        double M = ha > 0.0 ? hm : -INFINITY;
+        for (int p = lane + 32; p < n_slots; p += 32) {  // beyond one page (n_kv < 5)
+            const double* hd = (const double*)prow(p);
+            if (__ldcg(hd + 1) > 0.0) M = fmax(M, __ldcg(hd));
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) M = fmax(M, __shfl_xor_sync(0xFFFFFFFFu, M, off));
+        // slot weight 2^(m_p - M): the m are fp32 values, so the f32 exp2 of their exact f64
+        // difference is within 2^-22 relative
+        auto wgt = [&](double pm, double pa) -> double {
+            return pa > 0.0 ? (double)exp2f((float)(pm - M)) : 0.0;
+        };
+        const double w0 = wgt(hm, ha);
+        double At = ha * w0, Bt = w0 * (hb + (hm - M) * ha);
+        if (!(ha > 0.0)) At = Bt = 0.0;
+        for (int p = lane + 32; p < n_slots; p += 32) {
+            const double* hd = (const double*)prow(p);
+            const double pm = __ldcg(hd), pa = __ldcg(hd + 1), pb = __ldcg(hd + 2);
+            if (pa > 0.0) {
+                const double w = wgt(pm, pa);
+                At += pa * w;
+                Bt += w * (pb + (pm - M) * pa);
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            At += __shfl_xor_sync(0xFFFFFFFFu, At, off);
+            Bt += __shfl_xor_sync(0xFFFFFFFFu, Bt, off);
+        }
+        if (!dry && B.trace && lane == 0 && role == 0 && kv < 64) B.trace[3664 + kv] = globaltimer();
+        auto weight = [&](int p) -> double {  // page 0 by shuffle, later pages from the header
+            if (p < 32) return __shfl_sync(0xFFFFFFFFu, w0, p);
+            const double* hd = (const double*)prow(p);
+            return wgt(__ldcg(hd), __ldcg(hd + 1));
+        };
+        double o0 = 0.0, o1 = 0.0, o2 = 0.0, o3 = 0.0;
+        for (int u0 = 0; j + WPH * u0 < n_slots; u0 += kPre) {
+            if (u0 > 0) {
+#pragma unroll
+                for (int u = 0; u < kPre; ++u) {
+                    const int p = j + WPH * (u0 + u);
+                    v[u] = p < n_slots ? __ldcg(reinterpret_cast<const float4*>(prow(p) + 32) + lane)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kPre; ++u) {
+                const int p = j + WPH * (u0 + u);
+                const double w = weight(min(p, n_slots - 1));  // shuffle: the whole warp
+                if (p < n_slots) {
+                    o0 = fma((double)v[u].x, w, o0);
+                    o1 = fma((double)v[u].y, w, o1);
+                    o2 = fma((double)v[u].z, w, o2);
+                    o3 = fma((double)v[u].w, w, o3);
+                }
+            }
+        }
+        if (!dry) {  // dry: the stage ring is live, keep out of shared memory
+            double* mine = xo + ((size_t)(g * WPH + j) * kBD + 4 * lane);
+            mine[0] = o0;
+            mine[1] = o1;
+            mine[2] = o2;
+            mine[3] = o3;
+            named_bar_sync(6, G * WPH * 32);
+        }
+        if (j == 0) {
+            double r[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int jj = 0; jj < WPH; ++jj) {
+                const double* o = xo + ((size_t)(g * WPH + jj) * kBD + 4 * lane);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) r[c] += o[c];
+            }
+            const double inv = 1.0 / At;
+            const int h = kv * G + g;
+            if (B.merged) {  // one partial row per q head (sharded decode: combined across ranks)
+                uint8_t* row = B.merged + (size_t)h * kBPartBytes;
+                if (!dry)
+                    reinterpret_cast<float4*>(row + 32)[lane] =
+                        make_float4((float)r[0], (float)r[1], (float)r[2], (float)r[3]);
+                if (lane == 0 && !dry) {
+                    double* hd = (double*)row;
+                    hd[0] = M;
+                    hd[1] = At;
+                    hd[2] = Bt;
+                }
+            } else {
+                if (!dry)
+                    reinterpret_cast<float4*>(a.out + (size_t)h * kBD)[lane] =
+                        make_float4((float)(r[0] * inv), (float)(r[1] * inv), (float)(r[2] * inv),
+                                    (float)(r[3] * inv));
+                if (lane == 0 && !dry) {
+                    const double hh = log(At) - Bt * 0.69314718055994530942 * inv;
+                    a.entropy[h] = hh < 0.0 ? 0.0 : hh;
+                }
+            }
+        }
+    }
+}
+
+template <int G>
+__global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const __grid_constant__ BulkArgs B) {
+    const AttnArgs& a = B.a;
+    // while the scan's merger CTA still runs its tail: warm the merge code (see merge_parts)
+    extern __shared__ __align__(16) uint8_t bsm_raw[];
+    if (B.warm && threadIdx.x < 32) merge_parts<G>(B, blockIdx.y, 0, bsm_raw, true);
     // launched as a programmatic dependent of the scan / select: wait for its results
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const bool local = B.mode == kModeLocal;  // runs beside the scan: never reads the header
@@ -104,6 +250,8 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
     const uint32_t rows = B.mode == kModeHead ? L - B.n_local : L;
     const int part = blockIdx.x, kv = blockIdx.y;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int cta_id = blockIdx.y * gridDim.x + blockIdx.x + (local ? 512 : 0);  // trace slot
+    if (B.trace && tid == 0 && cta_id < 1024) B.trace[1536 + cta_id] = globaltimer();
     ShardRanges R;
     R.n = 0;
     int chunks;
@@ -140,7 +288,6 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
 
     // addressed straight from the shared array (an integer round trip for alignment would
     // turn every access into a generic load); bulk copies only need 16-B alignment
-    extern __shared__ __align__(16) uint8_t bsm_raw[];
     uint8_t* stages = bsm_raw;
     float* qs = (float*)(stages + kBStages * kBStageBytes);  // [8][kBD]
     uint8_t* rowok = (uint8_t*)(qs + 8 * kBD);                // [kBStages][kBC]
@@ -386,6 +533,7 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
         }
     }
     // ---- the last part of this kv head merges (attend.hpp:448-455 normalisation) ----
+    if (B.trace && tid == 0 && cta_id < 1024) B.trace[2560 + cta_id] = globaltimer();
     if (local) return;
     __threadfence();
     __syncthreads();
@@ -393,105 +541,22 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    if (warp < 4) {
-        float* w_s = (float*)stages + warp * kBMaxParts;
-        for (int g = warp; g < G; g += 4) {
-            __syncwarp();  // converged: plain SHFLs (see scan_topk.cu flush)
-            auto prow = [&](int p) {
-                return B.part + (((size_t)p * a.n_kv + kv) * G + g) * kBPartBytes;
-            };
-            double M = -INFINITY;
-            for (int p = lane; p < B.n_slots; p += 32) {
-                const double* hd = (const double*)prow(p);
-                if (__ldcg(hd + 1) > 0.0) M = fmax(M, __ldcg(hd));
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) M = fmax(M, __shfl_xor_sync(0xFFFFFFFFu, M, off));
-            double At = 0.0, Bt = 0.0;
-            for (int p = lane; p < B.n_slots; p += 32) {
-                const double* hd = (const double*)prow(p);
-                const double pm = __ldcg(hd), pa = __ldcg(hd + 1), pb = __ldcg(hd + 2);
-                const double w = pa > 0.0 ? exp2(pm - M) : 0.0;
-                w_s[p] = (float)w;
-                if (pa > 0.0) {
-                    At += pa * w;
-                    Bt += w * (pb + (pm - M) * pa);
-                }
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                At += __shfl_xor_sync(0xFFFFFFFFu, At, off);
-                Bt += __shfl_xor_sync(0xFFFFFFFFu, Bt, off);
-            }
-            __syncwarp();
-            // part order, 8 loads in flight per lane (empty parts have w == 0, acc == 0)
-            double o[8][4] = {};
-            int p0 = 0;
-            for (; p0 + 8 <= B.n_slots; p0 += 8) {
-                float4 v[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    v[k] = __ldcg(reinterpret_cast<const float4*>(prow(p0 + k) + 32) + lane);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const double w = (double)w_s[p0 + k];
-                    o[k][0] = fma((double)v[k].x, w, o[k][0]);
-                    o[k][1] = fma((double)v[k].y, w, o[k][1]);
-                    o[k][2] = fma((double)v[k].z, w, o[k][2]);
-                    o[k][3] = fma((double)v[k].w, w, o[k][3]);
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                if (p0 + k >= B.n_slots) break;
-                const float4 v = __ldcg(reinterpret_cast<const float4*>(prow(p0 + k) + 32) + lane);
-                const double w = (double)w_s[p0 + k];
-                o[k][0] = fma((double)v.x, w, o[k][0]);
-                o[k][1] = fma((double)v.y, w, o[k][1]);
-                o[k][2] = fma((double)v.z, w, o[k][2]);
-                o[k][3] = fma((double)v.w, w, o[k][3]);
-            }
-            double r[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                double t = 0.0;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) t += o[k][c];
-                r[c] = t / At;
-            }
-            const int h = kv * G + g;
-            if (B.merged) {  // one partial row per q head (sharded decode: combined across ranks)
-                uint8_t* row = B.merged + (size_t)h * kBPartBytes;
-                double un[4];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) un[c] = r[c] * At;  // back to un-normalised sums
-                reinterpret_cast<float4*>(row + 32)[lane] =
-                    make_float4((float)un[0], (float)un[1], (float)un[2], (float)un[3]);
-                if (lane == 0) {
-                    double* hd = (double*)row;
-                    hd[0] = M;
-                    hd[1] = At;
-                    hd[2] = Bt;
-                }
-            } else {
-                reinterpret_cast<float4*>(a.out + (size_t)h * kBD)[lane] =
-                    make_float4((float)r[0], (float)r[1], (float)r[2], (float)r[3]);
-                if (lane == 0) {
-                    const double hh = log(At) - Bt * 0.69314718055994530942 / At;
-                    a.entropy[h] = hh < 0.0 ? 0.0 : hh;
-                }
-            }
-            __syncwarp();
-        }
-    }
+    if (B.trace && tid == 0 && kv < 64) B.trace[3600 + kv] = globaltimer();
+    merge_parts<G>(B, kv, warp, stages, false);
     if (tid == 0) B.tickets[kv] = 0u;  // re-arm for the next launch (graph replay)
+    if (B.trace) {
+        __syncthreads();
+        if (tid == 0 && kv < 512) B.trace[3584 + kv] = globaltimer();
+    }
 }
 
 int bulk_parts(const AttnArgs& a, int num_sms) {
     return std::max(1, std::min(kBMaxParts - kMaxLocalParts, num_sms / std::max(1, a.n_kv)));
 }
 
-cudaError_t launch_bulk(const BulkArgs& B, int G, int n_kv, cudaStream_t s, bool pdl) {
+cudaError_t launch_bulk(const BulkArgs& Bin, int G, int n_kv, cudaStream_t s, bool pdl) {
+    BulkArgs B = Bin;
+    B.warm = pdl && B.mode != kModeLocal && !std::getenv("REATTN_NO_WARM") ? 1 : 0;
     dim3 grid(B.n_parts, n_kv);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
@@ -537,6 +602,8 @@ BulkArgs bulk_args(const AttnArgs& a, void* ws, int num_sms, const DecodeFork* f
     B.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)kBD));
     B.tickets = (unsigned int*)ws;
     B.part = (uint8_t*)ws + 256;
+    B.trace = trace_buffer();
+    B.warm = 0;
     return B;
 }
 

@@ -958,6 +958,15 @@ int reattn_plan_launch_scan(reattn_plan* p) {
     return enqueue_scan(p->ctx, p->P.scan, p->P.scan_ws, p->ctx->stream, false);
 }
 
+int reattn_debug_trace(uint64_t* host_out, uint64_t n) {
+    uint64_t* t = reattn_impl::trace_buffer();
+    if (!t || n > (uint64_t)reattn_impl::kTraceWords) return REATTN_EINVAL;
+    if (cudaDeviceSynchronize() != cudaSuccess ||
+        cudaMemcpy(host_out, t, n * sizeof(uint64_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return REATTN_ECUDA;
+    return REATTN_OK;
+}
+
 int reattn_plan_run_host(reattn_plan* p, const float* q_host, float* out_host) {
     const size_t bytes = p->P.n_q * p->P.n_head * p->cache->d * sizeof(float);
     reattn_ctx* ctx = p->ctx;

@@ -243,4 +243,9 @@ cudaError_t launch_rmsnorm(const float* x, uint64_t rows, uint64_t cols, const f
 cudaError_t launch_silu_mul(float* gate, const float* up, uint64_t n, cudaStream_t s);
 cudaError_t launch_argmax(const float* v, uint64_t n, uint32_t* out, cudaStream_t s);
 
+// ---- timeline trace (diagnostics): REATTN_TRACE=1 at plan / launch time makes the decode
+// kernels stamp %globaltimer into a device buffer (layout in misc.cu); null otherwise.
+constexpr int kTraceWords = 4096;
+uint64_t* trace_buffer();
+
 }  // namespace reattn_impl

@@ -2,6 +2,8 @@
 // for the assemble_scope API (scope.hpp:274-287), RoPE on device rows (rope.hpp:347-358),
 // the deterministic synthetic-input generator used by tests and bench.py, and the RunStats
 // entropy reduction in the reference's accumulation order (engine.hpp:558-564).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -151,4 +153,28 @@ cudaError_t launch_entropy_stats(const double* entropy, int n_q, int n_head, dou
     return cudaGetLastError();
 }
 
+}  // namespace reattn_impl
+
+// ---- timeline trace ------------------------------------------------------------------
+// Layout (uint64 words, %globaltimer ns):
+//   K1 scan (G CTAs):   [b] CTA start, [512 + b] CTA main loop done,
+//                       [1024] last CTA ticket, [1025] merge done, [1026] select done
+//   K5 decode attention: [1536 + cta] CTA start (after griddepcontrol.wait),
+//                       [2560 + cta] CTA compute done (cta = blockIdx.y * gridDim.x + blockIdx.x,
+//                       + 512 for the local-window launch),
+//                       [3584 + kv] kv head's final merge done
+namespace reattn_impl {
+namespace {
+__device__ uint64_t g_trace[kTraceWords];
+}
+uint64_t* trace_buffer() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = std::getenv("REATTN_TRACE");
+        on = e && std::atoi(e) != 0;
+    }
+    if (!on) return nullptr;
+    void* p = nullptr;
+    return cudaGetSymbolAddress(&p, g_trace) == cudaSuccess ? (uint64_t*)p : nullptr;
+}
 }  // namespace reattn_impl

@@ -22,6 +22,7 @@
 // middle, appending candidates above the running k-th key into a shared buffer and
 // compacting it with a bitonic sort — bounded scratch, exact, deterministic.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -70,7 +71,17 @@ struct FastArgs {
     float* score_out;
     int fuse_select;
     SmallSelectIO sel;
+    uint64_t* trace;  // diagnostics (misc.cu layout) or null
+    uint32_t tiles0;  // tiles of CTA 0 (the merger; see the tail below)
 };
+
+// Static tile partition: CTA 0 (the merger) takes tiles0 tiles, the other G-1 CTAs split
+// the rest evenly.
+__device__ __forceinline__ uint32_t tile_begin(uint32_t b, uint32_t G, uint32_t T, uint32_t T0) {
+    if (b == 0) return 0u;
+    if (b >= G) return T;
+    return T0 + (uint32_t)((uint64_t)(b - 1) * (T - T0) / (G - 1));
+}
 
 template <int KMAX>
 __device__ __forceinline__ void topk_reset(float (&ts)[KMAX], uint32_t (&ti)[KMAX]) {
@@ -155,13 +166,11 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
     float* s_mq = (float*)(empty + C::STAGES);
     float* s_ws = s_mq + C::D;
     uint32_t* s_wi = (uint32_t*)(s_ws + C::CWARPS * KMAX);
-    __shared__ int s_last;
-
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const uint32_t G = gridDim.x, b = blockIdx.x;
-    const uint32_t t_begin = (uint32_t)((uint64_t)b * a.total_tiles / G);
-    const uint32_t t_end = (uint32_t)((uint64_t)(b + 1) * a.total_tiles / G);
+    const uint32_t T = a.total_tiles, T0 = G == 1 ? T : a.tiles0;
+    const uint32_t t_begin = tile_begin(b, G, T, T0), t_end = tile_begin(b + 1, G, T, T0);
     const int k = a.k;
 
     if (tid == 0) {
@@ -172,6 +181,7 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
         fence_barrier_init();
     }
     __syncthreads();
+    if (a.trace && tid == 0) a.trace[b] = globaltimer();
 
     // ===== TMA issue (thread 0): the first STAGES tiles now, then each stage is refilled
     // as soon as every warp has released it (end of the consumer iteration below) =====
@@ -324,60 +334,108 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
         if (cur_kv != kNoIndex) flush(cur_kv);
     }
 
-    // ===== cross-CTA merge by the last CTA to finish =====
+    // ===== cross-CTA merge and select by CTA 0 =====
+    // The merge + vote/spans/scope tail is ~1.5K instructions executed once per launch, so it
+    // runs from a cold instruction cache (~0.3-0.5 us per fetch miss: 10+ us measured).  CTA 0
+    // therefore scans fewer tiles, runs the tail once in dry mode (same code, global stores
+    // predicated off) to warm its instruction cache while the others still scan, waits for
+    // their done count, and runs it for real (~4 us).
     __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        const unsigned int done = atomicAdd(a.ticket, 1u);
-        s_last = (done == G - 1);
+    if (a.trace && tid == 0) a.trace[512 + b] = globaltimer();
+    if (b != 0) {
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(a.ticket, 1u);  // release: this CTA's slots are written
+        }
+        return;
     }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
+    // merged candidate i = kv * kk + r goes straight to the select's shared candidates
+    __shared__ SmallSelectSmem ssel;
+    const int kk = (int)min((uint32_t)k, a.count);
     const int nwarps = C::THREADS / 32;
-    for (int kv = warp; kv < a.n_kv; kv += nwarps) {
-        float ls[KMAX];
-        uint32_t li[KMAX];
-        topk_reset<KMAX>(ls, li);
-        // CTAs covering this head's tiles [h0, h1): CTA b starts at floor(b*T/G) (every CTA
-        // owns >= 1 tile since G <= T), so the first/last coverers follow directly.
-        const uint64_t T = a.total_tiles;
-        const uint64_t h0 = (uint64_t)kv * a.tiles_per_head, h1 = h0 + a.tiles_per_head;
-        const uint32_t b0 = (uint32_t)(((h0 + 1) * G + T - 1) / T - 1);
-        const uint32_t b1 = (uint32_t)((h1 * G + T - 1) / T - 1);
-        const int n = (int)(b1 - b0 + 1) * k;
-        for (int e = lane; e < n; e += 32) {
-            const size_t slot = ((size_t)kv * G + b0 + e / k) * KMAX + e % k;
-            const float s = __ldcg(a.slot_score + slot);
-            const uint32_t i = __ldcg(a.slot_idx + slot);
-            if (i != kNoIndex) topk_insert<KMAX>(ls, li, k, s, i);
-        }
-        for (int r = 0; r < k; ++r) {
-            float bs = ls[0];
-            uint32_t bi = li[0];
-            warp_best(bs, bi);
-            if (lane == 0) {
-                a.idx_out[(size_t)kv * k + r] = bi;
-                a.score_out[(size_t)kv * k + r] = bs;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        const bool dry = pass == 0;
+        if (!dry) {
+            if (tid == 0) {
+                while (ld_acquire_u32(a.ticket) < G - 1) __nanosleep(32);
+                *a.ticket = 0u;  // re-arm for the next launch (graph replay)
+                if (a.trace) a.trace[1024] = globaltimer();
             }
-            if (bi != kNoIndex && li[0] == bi) topk_pop<KMAX>(ls, li);
+            __syncthreads();
         }
-    }
-    if (tid == 0) *a.ticket = 0u;  // re-arm for the next launch (graph replay)
-    if (a.fuse_select) {
-        // vote + spans + scope on the merged candidates [kv][0..kk) (selection.hpp:359-456)
-        __shared__ SmallSelectSmem ssel;
+        for (int kv = warp; kv < a.n_kv; kv += nwarps) {
+            float ls[KMAX];
+            uint32_t li[KMAX];
+            topk_reset<KMAX>(ls, li);
+            // CTAs whose (non-empty) tile range meets this head's tiles [h0, h1): contiguous
+            const uint32_t h0 = (uint32_t)kv * a.tiles_per_head, h1 = h0 + a.tiles_per_head;
+            uint32_t b0 = G, b1 = 0;
+            for (uint32_t c = lane; c < G; c += 32) {
+                const uint32_t cb = tile_begin(c, G, T, T0), ce = tile_begin(c + 1, G, T, T0);
+                const bool meets = cb < ce && cb < h1 && ce > h0;
+                if (meets) {
+                    b0 = min(b0, c);
+                    b1 = max(b1, c);
+                }
+            }
+            b0 = __reduce_min_sync(0xFFFFFFFFu, b0);
+            b1 = __reduce_max_sync(0xFFFFFFFFu, b1);
+            const int n = b0 <= b1 ? (int)(b1 - b0 + 1) * k : 0;
+            // all of a batch's loads are issued before any insert: one L2 round trip per batch
+            for (int e0 = 0; e0 < n; e0 += 128) {
+                float s4[4];
+                uint32_t i4[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + 32 * u + lane;
+                    s4[u] = -INFINITY;
+                    i4[u] = kNoIndex;
+                    if (e < n) {
+                        const size_t slot = ((size_t)kv * G + b0 + e / k) * KMAX + e % k;
+                        s4[u] = __ldcg(a.slot_score + slot);
+                        i4[u] = __ldcg(a.slot_idx + slot);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (i4[u] != kNoIndex) topk_insert<KMAX>(ls, li, k, s4[u], i4[u]);
+            }
+            if (a.trace && !dry && lane == 0 && kv == 0) a.trace[1027] = globaltimer();
+            for (int r = 0; r < k; ++r) {
+                float bs = ls[0];
+                uint32_t bi = li[0];
+                warp_best(bs, bi);
+                if (lane == 0) {
+                    if (!dry) {
+                        a.idx_out[(size_t)kv * k + r] = bi;
+                        a.score_out[(size_t)kv * k + r] = bs;
+                    }
+                    const int c = kv * kk + r;
+                    if (a.fuse_select && r < kk && c < 32) {
+                        ssel.idx[c] = bi;
+                        ssel.key[c] = float_key(bs);
+                    }
+                }
+                if (bi != kNoIndex && li[0] == bi) topk_pop<KMAX>(ls, li);
+            }
+        }
+        if (a.fuse_select) {
+            // vote + spans + scope on the merged candidates [kv][0..kk) (selection.hpp:359-456)
+            const int n = a.n_kv * kk;  // <= 32 (fuse_select condition)
+            if (tid == 0) ssel.vmask = n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u);
+            __syncthreads();
+            if (a.trace && !dry && tid == 0) {
+                a.trace[1025] = a.trace[1028] = globaltimer();
+                a.trace[1040] = clock64();
+            }
+            small_select_scope_smem(a.sel, ssel, dry ? nullptr : a.trace, dry);
+            if (a.trace && !dry) {
+                __syncthreads();
+                if (tid == 0) a.trace[1026] = globaltimer();
+            }
+        }
         __syncthreads();
-        const int kk = (int)min((uint32_t)k, a.count);
-        const int n = a.n_kv * kk;
-        uint32_t ci = 0;
-        float cs = 0.0f;
-        const bool valid = tid < n;
-        if (valid) {
-            ci = a.idx_out[(size_t)(tid / kk) * k + tid % kk];
-            cs = a.score_out[(size_t)(tid / kk) * k + tid % kk];
-        }
-        small_select_scope(a.sel, ci, cs, valid, ssel);
     }
 }
 
@@ -573,6 +631,17 @@ cudaError_t launch_scan_fast(const ScanArgs& a, const CUtensorMap& kmap, void* w
     f.score_out = a.score_out;
     f.fuse_select = a.fuse_select;
     f.sel = a.sel;
+    f.trace = trace_buffer();
+    {
+        // CTA 0 scans kTailTiles fewer tiles than an even share: the time its dry tail pass
+        // takes (~15 us cold; one 64 KB tile per CTA ~1.5 us at the HBM rate).
+        static const int tail_tiles = [] {
+            const char* e = std::getenv("REATTN_TAIL_TILES");
+            return e ? std::atoi(e) : 10;
+        }();
+        const uint32_t share = f.total_tiles / (uint32_t)std::max(1, std::min<int>(num_sms, (int)f.total_tiles));
+        f.tiles0 = share > (uint32_t)tail_tiles ? share - (uint32_t)tail_tiles : 0u;
+    }
     if (a.dtype == kBF16) {
         using C = FastCfg<__nv_bfloat16>;
         if (a.lanes == kLanesFma) {

@@ -152,6 +152,7 @@ SIGNATURES = [
     ("reattn_plan_out", vp, [vp]),
     ("reattn_plan_launch", C.c_int, [vp]),
     ("reattn_plan_launch_scan", C.c_int, [vp]),
+    ("reattn_debug_trace", C.c_int, [C.POINTER(u64), u64]),
     ("reattn_plan_run_host", C.c_int, [vp, vp, vp]),
     ("reattn_plan_stats", C.c_int, [vp, C.POINTER(StepStats)]),
     ("reattn_plan_info", C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
@@ -499,6 +500,16 @@ def attend_step(ctx: Context, cache: Cache, rope: Rope, q, n_head: int, cfg: Sel
                                          sb.ctypes.data, se.ctypes.data, ent.ctypes.data))
     n = st.n_spans
     return StepResult(out, st, (sb[:n].copy(), se[:n].copy()), ent[: n_q * n_head].reshape(n_q, n_head))
+
+
+def debug_trace(n: int = 4096):
+    """Device timeline stamps (REATTN_TRACE=1 at plan build; layout in csrc/misc.cu)."""
+    lib = load_library()
+    buf = (u64 * n)()
+    rc = lib.reattn_debug_trace(buf, n)
+    if rc:
+        raise ReattnError(f"reattn_debug_trace: status {rc} (REATTN_TRACE unset?)")
+    return list(buf)
 
 
 class Plan:
