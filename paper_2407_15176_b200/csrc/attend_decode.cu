@@ -52,7 +52,8 @@ constexpr int kBThreads = kBCompute + 32;
 constexpr int kBPartBytes = kDecodePartBytes;  // double m2, A, B2, pad; float acc[128]
 constexpr int kBMaxParts = 160;          // partial slots per kv head (head + local)
 constexpr int kMaxLocalParts = 4;
-constexpr size_t kBSmem = 1024 + (size_t)kBStages * kBStageBytes + 8ull * kBD * 4 +
+constexpr int kBSxBytes = kBGroups * 4 * 4 * kBC * 4;  // G <= 4 logit partials [gi][warp][h][key]
+constexpr size_t kBSmem = 1024 + (size_t)kBStages * kBStageBytes + 8ull * kBD * 4 + kBSxBytes +
                           (size_t)kBStages * kBC + 256;
 
 enum { kModeScope = 0, kModeLocal = 1, kModeHead = 2, kModeRanges = 3 };
@@ -290,7 +291,8 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
     // turn every access into a generic load); bulk copies only need 16-B alignment
     uint8_t* stages = bsm_raw;
     float* qs = (float*)(stages + kBStages * kBStageBytes);  // [8][kBD]
-    uint8_t* rowok = (uint8_t*)(qs + 8 * kBD);                // [kBStages][kBC]
+    float* sx = qs + 8 * kBD;                                 // kBSxBytes (G <= 4 path)
+    uint8_t* rowok = (uint8_t*)sx + kBSxBytes;                // [kBStages][kBC]
     uint64_t* full = (uint64_t*)(rowok + kBStages * kBC);  // 8-B aligned: offsets are multiples of 64
     uint64_t* empty = full + kBStages;
     __shared__ unsigned int s_last;
@@ -374,6 +376,190 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
             qs[g * kBD + 2 * j + 1] = __fmul_rn(ry, B.scale_log2);
         }
         named_bar_sync(5, kBCompute);
+        if constexpr (G <= 4) {
+        // ---- G <= 4: lane = (key kl of the warp's 8, q head hd); each warp keeps its own
+        // online-softmax state for its key slice (no per-chunk exchange), merged at the end.
+        // Logits read the rotated keys once per warp for all heads (8 rows x 16 B + 4 query
+        // float4 per step: 2 wavefronts), P.V reads each V row once for all heads (lane = 4
+        // columns): ~2x fewer shared-memory wavefronts than one warp per head.
+        const int kl = lane & 7, hd = lane >> 3;
+        const int r = 8 * gw + kl;  // this lane's key row within the chunk
+        // every lane tracks every head's running max (to rescale its acc columns); the f64
+        // sums A (softmax denominator) and B2 (entropy numerator) only for its own head
+        float m2[4];
+        double A = 0.0, B2 = 0.0;
+        f2_t o01[4], o23[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            m2[h] = -INFINITY;
+            o01[h] = o23[h] = 0ull;
+        }
+        for (int c = gi; c < n_ch; c += kBGroups) {
+            const int s = c % kBStages;
+            // see the parity note in the G > 4 path
+            if (c >= kBStages) mbar_wait(&empty[s], ((c / kBStages) - 1) & 1u);
+            mbar_wait(&full[s], (c / kBStages) & 1u);
+            __syncwarp();
+            uint32_t k0;
+            int nk;
+            geom(c_begin + c, k0, nk);
+            uint8_t* st = stages + (size_t)s * kBStageBytes;
+            float4* kr4 = (float4*)(st + 2 * kBKVBytes);  // rotated keys over the cos/sin rows
+            {
+                const uint32_t* kw = (const uint32_t*)st;  // bf16 pairs
+                const float* cs = (const float*)(st + 2 * kBKVBytes);
+                const float* sn = (const float*)(st + 2 * kBKVBytes + kBRopeBytes);
+                float2 rot[kBC * (kBD / 2) / 128];
+#pragma unroll
+                for (int i = 0; i < kBC * (kBD / 2) / 128; ++i) {
+                    const int e = gt + 128 * i, rr = e >> 6, j = e & 63;
+                    const uint32_t w = kw[rr * (kBD / 2) + j];
+                    const float x = __uint_as_float(w << 16), y = __uint_as_float(w & 0xFFFF0000u);
+                    float rx = x, ry = y;
+                    if (a.rope_cos && rr < nk) {
+                        const float cc = cs[rr * (kBD / 2) + j], ss = sn[rr * (kBD / 2) + j];
+                        rx = __fsub_rn(__fmul_rn(x, cc), __fmul_rn(y, ss));
+                        ry = __fadd_rn(__fmul_rn(x, ss), __fmul_rn(y, cc));
+                    }
+                    rot[i] = make_float2(rx, ry);
+                }
+                named_bar_sync(1 + gi, 128);  // every read of cos / sin done
+#pragma unroll
+                for (int i = 0; i < kBC * (kBD / 2) / 128; ++i) {
+                    const int e = gt + 128 * i, rr = e >> 6, j = e & 63;
+                    float* dst = (float*)&kr4[rot_idx4(rr, j >> 1)] + (j & 1) * 2;
+                    *(float2*)dst = rot[i];
+                }
+                named_bar_sync(1 + gi, 128);  // rotated keys ready
+                __syncwarp();
+            }
+            const bool key_ok = hd < G && r < nk && rowok[s * kBC + r];
+            // logits, split over the group's warps by dimension: warp gw sums dims
+            // [32 gw, 32 gw + 32) for all 32 keys (lane = key) and all heads, so one rotated-key
+            // LDS.128 serves G heads and the query float4s are warp-uniform broadcasts; the four
+            // partials meet in shared memory and are summed in warp order
+            {
+                const ulonglong2* kv4 = reinterpret_cast<const ulonglong2*>(kr4);
+                f2_t d01[G], d23[G];
+#pragma unroll
+                for (int h = 0; h < G; ++h) d01[h] = d23[h] = 0ull;
+#pragma unroll
+                for (int i = 8 * gw; i < 8 * gw + 8; ++i) {
+                    const ulonglong2 k4 = kv4[rot_idx4(lane, i)];
+#pragma unroll
+                    for (int h = 0; h < G; ++h) {
+                        const ulonglong2 q4 = reinterpret_cast<const ulonglong2*>(qs + h * kBD)[i];
+                        d01[h] = f2_fma(q4.x, k4.x, d01[h]);
+                        d23[h] = f2_fma(q4.y, k4.y, d23[h]);
+                    }
+                }
+                float* sxg = sx + gi * (4 * 4 * kBC);  // [warp][h][key]
+#pragma unroll
+                for (int h = 0; h < G; ++h)
+                    sxg[(gw * 4 + h) * kBC + lane] =
+                        (f2_lo(d01[h]) + f2_hi(d01[h])) + (f2_lo(d23[h]) + f2_hi(d23[h]));
+                named_bar_sync(1 + gi, 128);  // partial logits ready
+            }
+            float sc = -INFINITY;
+            if (key_ok) {
+                const float* sxg = sx + gi * (4 * 4 * kBC);
+                sc = ((sxg[(0 * 4 + hd) * kBC + r] + sxg[(1 * 4 + hd) * kBC + r]) +
+                      sxg[(2 * 4 + hd) * kBC + r]) + sxg[(3 * 4 + hd) * kBC + r];
+            }
+            float mc = sc;
+#pragma unroll
+            for (int off = 1; off < 8; off <<= 1) mc = fmaxf(mc, __shfl_xor_sync(0xFFFFFFFFu, mc, off));
+            float mn[4], f[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                mn[h] = fmaxf(m2[h], __shfl_sync(0xFFFFFFFFu, mc, 8 * h));
+                // m2 == -inf (only masked rows so far): f == 0 and the state stays empty
+                f[h] = m2[h] != -INFINITY ? bx_ex2(m2[h] - mn[h]) : 0.0f;
+            }
+            const float mine = hd == 0 ? mn[0] : hd == 1 ? mn[1] : hd == 2 ? mn[2] : mn[3];
+            const float fo = hd == 0 ? f[0] : hd == 1 ? f[1] : hd == 2 ? f[2] : f[3];
+            const float mo = hd == 0 ? m2[0] : hd == 1 ? m2[1] : hd == 2 ? m2[2] : m2[3];
+            const float dd = sc - mine;
+            const float p = key_ok ? bx_ex2(dd) : 0.0f;
+            float sa = p, sb = key_ok ? dd * p : 0.0f;
+#pragma unroll
+            for (int off = 1; off < 8; off <<= 1) {
+                sa += __shfl_xor_sync(0xFFFFFFFFu, sa, off);
+                sb += __shfl_xor_sync(0xFFFFFFFFu, sb, off);
+            }
+            B2 = (A > 0.0 ? (double)fo * (B2 + (double)(mo - mine) * A) : 0.0) + (double)sb;
+            A = A * (double)fo + (double)sa;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                m2[h] = mn[h];
+                const f2_t ff = f2_packf(f[h], f[h]);
+                o01[h] = f2_mul(o01[h], ff);
+                o23[h] = f2_mul(o23[h], ff);
+            }
+            // P.V over the warp's 8 keys, all heads (rows >= nk are zero with p == 0)
+            const uint2* vrow = reinterpret_cast<const uint2*>(st + kBKVBytes) + lane;  // 4 bf16
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint2 w = vrow[(8 * gw + j) * (kBD / 4)];
+                const f2_t v01 = bf16x2_to_f2(w.x), v23 = bf16x2_to_f2(w.y);
+#pragma unroll
+                for (int h = 0; h < G; ++h) {
+                    const float pj = __shfl_sync(0xFFFFFFFFu, p, j + 8 * h);
+                    const f2_t pp = f2_packf(pj, pj);
+                    o01[h] = f2_fma(pp, v01, o01[h]);
+                    o23[h] = f2_fma(pp, v23, o23[h]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        // ---- merge the 16 warps' states per head through shared memory ----
+        __syncthreads();  // every stage consumed: reuse the ring as exchange space
+        constexpr int NW = kBCompute / 32;
+        double* xs = (double*)stages;                                  // [warp][g][4]
+        float* xa = (float*)(stages + NW * 4 * 4 * sizeof(double));    // [warp][g][kBD]
+#pragma unroll
+        for (int h = 0; h < G; ++h)
+            reinterpret_cast<float4*>(xa + (warp * 4 + h) * kBD)[lane] =
+                make_float4(f2_lo(o01[h]), f2_hi(o01[h]), f2_lo(o23[h]), f2_hi(o23[h]));
+        if (kl == 0 && hd < G) {
+            xs[(warp * 4 + hd) * 4 + 0] = (double)(hd == 0 ? m2[0] : hd == 1 ? m2[1] : hd == 2 ? m2[2] : m2[3]);
+            xs[(warp * 4 + hd) * 4 + 1] = A;
+            xs[(warp * 4 + hd) * 4 + 2] = B2;
+        }
+        named_bar_sync(5, kBCompute);
+        if (warp < G) {  // warp g combines head g's 16 warp states in warp order
+            const int g = warp;
+            double M = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < NW; ++k)
+                if (xs[(k * 4 + g) * 4 + 1] > 0.0) M = fmax(M, xs[(k * 4 + g) * 4 + 0]);
+            double At = 0.0, Bt = 0.0;
+            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+            for (int k = 0; k < NW; ++k) {
+                const double km = xs[(k * 4 + g) * 4 + 0], ka = xs[(k * 4 + g) * 4 + 1];
+                if (!(ka > 0.0)) continue;
+                const double w = (double)exp2f((float)(km - M));
+                At += ka * w;
+                Bt += w * (xs[(k * 4 + g) * 4 + 2] + (km - M) * ka);
+                const float4 x = reinterpret_cast<const float4*>(xa + (k * 4 + g) * kBD)[lane];
+                const float wf = (float)w;
+                o.x = __fmaf_rn(x.x, wf, o.x);
+                o.y = __fmaf_rn(x.y, wf, o.y);
+                o.z = __fmaf_rn(x.z, wf, o.z);
+                o.w = __fmaf_rn(x.w, wf, o.w);
+            }
+            uint8_t* row = B.part + (((size_t)(B.part_base + part) * a.n_kv + kv) * G + g) * kBPartBytes;
+            reinterpret_cast<float4*>(row + 32)[lane] = o;
+            if (lane == 0) {
+                double* hdp = (double*)row;
+                hdp[0] = M;
+                hdp[1] = At;
+                hdp[2] = Bt;
+            }
+        }
+        } else {
         float m2[HPW];
         double A[HPW], B2[HPW];
         float4 acc[HPW];
@@ -531,6 +717,7 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
                 }
             }
         }
+        }  // G > 4
     }
     // ---- the last part of this kv head merges (attend.hpp:448-455 normalisation) ----
     if (B.trace && tid == 0 && cta_id < 1024) B.trace[2560 + cta_id] = globaltimer();

@@ -80,7 +80,10 @@ struct FastArgs {
 __device__ __forceinline__ uint32_t tile_begin(uint32_t b, uint32_t G, uint32_t T, uint32_t T0) {
     if (b == 0) return 0u;
     if (b >= G) return T;
-    return T0 + (uint32_t)((uint64_t)(b - 1) * (T - T0) / (G - 1));
+    // floor((b-1)(T-T0)/(G-1)) in f64: both operands < 2^53 and a non-integer quotient is at
+    // least 1/(G-1) from the next integer, so the correctly rounded quotient floors exactly
+    // (a 64-bit integer division is a ~100-instruction software routine)
+    return T0 + (uint32_t)floor((double)(b - 1) * (double)(T - T0) / (double)(G - 1));
 }
 
 template <int KMAX>
@@ -341,7 +344,12 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
     // predicated off) to warm its instruction cache while the others still scan, waits for
     // their done count, and runs it for real (~4 us).
     __syncthreads();
-    if (a.trace && tid == 0) a.trace[512 + b] = globaltimer();
+    if (a.trace && tid == 0) {
+        a.trace[512 + b] = globaltimer();
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.trace[1100 + b] = smid;
+    }
     if (b != 0) {
         if (tid == 0) {
             __threadfence();

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between steps")
+    ap.add_argument("--slow", action="store_true", help="list the slowest scan CTAs")
     args = ap.parse_args()
     assert os.environ.get("REATTN_TRACE") == "1", "set REATTN_TRACE=1"
     ctx = N.Context(0)
@@ -56,6 +57,12 @@ def main():
         print(f"--- rep {rep}  ctx {args.ctx}  scan CTAs {G}")
         print("K1 CTA start      ", summarize(rel(t[:G])))
         print("K1 CTA loop done  ", summarize(rel(t[512:512 + G])))
+        if args.slow:
+            order = sorted(range(G), key=lambda c: -(t[512 + c] - t0))
+            print("   slowest CTAs (cta, sm, done us):",
+                  [(c, t[1100 + c], round((t[512 + c] - t0) / 1e3, 1)) for c in order[:12]])
+            print("   fastest CTAs:", [(c, t[1100 + c], round((t[512 + c] - t0) / 1e3, 1))
+                                      for c in order[-6:]])
         print(f"K1 last ticket {(t[1024] - t0) / 1e3:8.2f}  merge done {(t[1025] - t0) / 1e3:8.2f}"
               f"  select done {(t[1026] - t0) / 1e3:8.2f} us")
         print(f"   K1 detail: warp0 slots read {(t[1027] - t0) / 1e3:8.2f}  pre-select {(t[1028] - t0) / 1e3:8.2f}"
