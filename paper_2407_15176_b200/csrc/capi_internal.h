@@ -156,8 +156,11 @@ inline int enqueue_scan(reattn_ctx* ctx, const ScanPlan& sp, void* ws, cudaStrea
         return REATTN_OK;
     }
     if (sp.fast && zero_ticket) CU(ctx, cudaMemsetAsync(ws, 0, 256, s));
-    if (sp.fast)
-        CU(ctx, launch_scan_fast(sp.a, sp.map, ws, sp.grid_sms ? sp.grid_sms : ctx->num_sms, s));
+    if (sp.fast) {
+        ScanArgs a = sp.a;
+        a.balance = zero_ticket ? 0 : 1;
+        CU(ctx, launch_scan_fast(a, sp.map, ws, sp.grid_sms ? sp.grid_sms : ctx->num_sms, s));
+    }
     else
         CU(ctx, launch_scan_generic(sp.a, s));
     return REATTN_OK;

@@ -60,6 +60,9 @@ struct ScanArgs {
     // fast path only: run vote + spans + scope in the last CTA (n_kv * min(k, count) <= 32)
     int fuse_select = 0;
     SmallSelectIO sel = {};
+    // fast path: keep the adaptive tile partition in the workspace (private, zero-initialised
+    // plan workspaces only)
+    int balance = 0;
 };
 
 // Fast path: TMA-staged, one thread per key row, q in registers, register top-k.

@@ -73,17 +73,37 @@ struct FastArgs {
     SmallSelectIO sel;
     uint64_t* trace;  // diagnostics (misc.cu layout) or null
     uint32_t tiles0;  // tiles of CTA 0 (the merger; see the tail below)
+    uint32_t part_q, part_r;  // (T - T0) = part_q (G - 1) + part_r
+    struct Balance* bal;      // adaptive partition state (plans), or null
 };
 
-// Static tile partition: CTA 0 (the merger) takes tiles0 tiles, the other G-1 CTAs split
-// the rest evenly.
-__device__ __forceinline__ uint32_t tile_begin(uint32_t b, uint32_t G, uint32_t T, uint32_t T0) {
+// Adaptive tile partition.  The scan CTAs do not stream at equal rates (with the decode fork
+// the slowest finish ~10 us after the median, on the same SMs every step), so for long scans
+// the partition follows measured rates: every CTA records its loop time, and CTA 0, in the
+// slack before it merges, turns launch e-1's rates (smoothed, clamped to +-30% of the mean)
+// into the table launch e+1 uses.  Tables and durations are double-buffered by epoch parity;
+// a header (T, G, T0) guards against a workspace reused for another geometry.  The top-k is
+// exact under any partition, so results do not depend on it.
+constexpr int kBalMaxG = 160;
+struct Balance {
+    uint32_t T, G, T0, epoch;        // epoch = launches completed with this header
+    uint32_t tbv[2];                 // table p valid for launch tbv[p] - 1
+    uint32_t durv[2];                // dur/cnt p hold launch durv[p] - 1
+    uint32_t tb[2][kBalMaxG + 1];
+    uint32_t dur[2][kBalMaxG];
+    uint32_t cnt[2][kBalMaxG];
+    float rate[kBalMaxG];
+};
+
+// Static tile partition: CTA 0 (the merger) takes T0 tiles, the other G-1 CTAs split the
+// rest evenly: begin(b) = T0 + floor((b-1)(T-T0)/(G-1)) = T0 + (b-1)q + floor((b-1)r/(G-1))
+// with (T-T0) = q(G-1) + r from the host -- 32-bit arithmetic only (a 64-bit integer or f64
+// division is a long software sequence, and this runs in every CTA and in the merge).
+__device__ __forceinline__ uint32_t tile_begin(uint32_t b, uint32_t G, uint32_t T, uint32_t T0,
+                                               uint32_t q, uint32_t r) {
     if (b == 0) return 0u;
     if (b >= G) return T;
-    // floor((b-1)(T-T0)/(G-1)) in f64: both operands < 2^53 and a non-integer quotient is at
-    // least 1/(G-1) from the next integer, so the correctly rounded quotient floors exactly
-    // (a 64-bit integer division is a ~100-instruction software routine)
-    return T0 + (uint32_t)floor((double)(b - 1) * (double)(T - T0) / (double)(G - 1));
+    return T0 + (b - 1) * q + ((b - 1) * r) / (G - 1);
 }
 
 template <int KMAX>
@@ -173,7 +193,19 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
     const int warp = tid >> 5, lane = tid & 31;
     const uint32_t G = gridDim.x, b = blockIdx.x;
     const uint32_t T = a.total_tiles, T0 = G == 1 ? T : a.tiles0;
-    const uint32_t t_begin = tile_begin(b, G, T, T0), t_end = tile_begin(b + 1, G, T, T0);
+    Balance* bal = (a.bal && G <= kBalMaxG && G > 2) ? a.bal : nullptr;
+    uint32_t epoch = 0;
+    const uint32_t* tab = nullptr;
+    if (bal) {
+        epoch = bal->epoch;
+        if (bal->T != T || bal->G != G || bal->T0 != T0) epoch = 0;  // another geometry
+        if (epoch > 0 && bal->tbv[epoch & 1] == epoch + 1) tab = bal->tb[epoch & 1];
+    }
+    auto tbeg = [&](uint32_t c) {
+        return tab ? tab[c] : tile_begin(c, G, T, T0, a.part_q, a.part_r);
+    };
+    const uint32_t t_begin = tbeg(b), t_end = tbeg(b + 1);
+    const uint64_t t_start = bal ? globaltimer() : 0ull;
     const int k = a.k;
 
     if (tid == 0) {
@@ -344,6 +376,10 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
     // predicated off) to warm its instruction cache while the others still scan, waits for
     // their done count, and runs it for real (~4 us).
     __syncthreads();
+    if (bal && tid == 0) {
+        bal->dur[epoch & 1][b] = (uint32_t)min(globaltimer() - t_start, (uint64_t)0xFFFFFFFFu);
+        bal->cnt[epoch & 1][b] = t_end - t_begin;
+    }
     if (a.trace && tid == 0) {
         a.trace[512 + b] = globaltimer();
         uint32_t smid;
@@ -364,6 +400,68 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
 #pragma unroll 1
     for (int pass = 0; pass < 2; ++pass) {
         const bool dry = pass == 0;
+        if (!dry && bal && warp == 0 && epoch > 0 && bal->durv[(epoch + 1) & 1] == epoch) {
+            // next launch's table from launch epoch-1's rates (same parity as the table written)
+            const int p = (epoch + 1) & 1;
+            const uint32_t n = G - 1;  // CTAs 1..G-1 share T - T0
+            const uint32_t per = (n + 31) / 32, lo = 1 + lane * per, hi = min(G, lo + per);
+            float r[6];
+            float rs = 0.0f;
+#pragma unroll
+            for (int u = 0; u < 6; ++u) {
+                const uint32_t c = lo + u;
+                r[u] = 0.0f;
+                if (c < hi) {
+                    const uint32_t d = bal->dur[p][c];
+                    r[u] = d ? (float)bal->cnt[p][c] / (float)d : 0.0f;
+                    rs += r[u];
+                }
+            }
+            float tot = rs;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
+            const float mean = tot / (float)n;
+            float ws = 0.0f;
+#pragma unroll
+            for (int u = 0; u < 6; ++u) {
+                const uint32_t c = lo + u;
+                if (c < hi) {
+                    float x = mean > 0.0f ? fminf(fmaxf(r[u], 0.7f * mean), 1.3f * mean) : 1.0f;
+                    const float old = bal->rate[c];
+                    if (old > 0.0f) x = 0.5f * (old + x);
+                    bal->rate[c] = x;
+                    r[u] = x;
+                    ws += x;
+                } else {
+                    r[u] = 0.0f;
+                }
+            }
+            // exclusive prefix of the lanes' sums (lane order == CTA order)
+            float incl = ws;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const float total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            double run = (double)(incl - ws);
+            uint32_t* tb = bal->tb[(epoch + 1) & 1];
+#pragma unroll
+            for (int u = 0; u < 6; ++u) {
+                const uint32_t c = lo + u;
+                if (c < hi) tb[c] = T0 + (uint32_t)((double)(T - T0) * run / (double)total);
+                run += (double)r[u];
+            }
+            if (lane == 0) {
+                tb[0] = 0u;
+                tb[G] = T;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                bal->tbv[(epoch + 1) & 1] = epoch + 2;
+            }
+        }
         if (!dry) {
             if (tid == 0) {
                 while (ld_acquire_u32(a.ticket) < G - 1) __nanosleep(32);
@@ -380,7 +478,7 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
             const uint32_t h0 = (uint32_t)kv * a.tiles_per_head, h1 = h0 + a.tiles_per_head;
             uint32_t b0 = G, b1 = 0;
             for (uint32_t c = lane; c < G; c += 32) {
-                const uint32_t cb = tile_begin(c, G, T, T0), ce = tile_begin(c + 1, G, T, T0);
+                const uint32_t cb = tbeg(c), ce = tbeg(c + 1);
                 const bool meets = cb < ce && cb < h1 && ce > h0;
                 if (meets) {
                     b0 = min(b0, c);
@@ -444,6 +542,13 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
             }
         }
         __syncthreads();
+    }
+    if (bal && tid == 0) {  // every CTA's duration is in: publish this launch's state
+        bal->durv[epoch & 1] = epoch + 1;
+        bal->T = T;
+        bal->G = G;
+        bal->T0 = T0;
+        bal->epoch = epoch + 1;
     }
 }
 
@@ -573,10 +678,13 @@ static uint32_t fast_tiles_per_head(const ScanArgs& a) {
     return (a.count + rows - 1) / rows;
 }
 
+static size_t slots_bytes(const ScanArgs& a, int num_sms) {
+    return (size_t)a.n_kv * (size_t)std::max(1, num_sms) * 8 * (sizeof(uint32_t) + sizeof(float));
+}
+
 size_t scan_fast_workspace(const ScanArgs& a, int num_sms) {
-    const size_t G = (size_t)std::max(1, num_sms);
-    // ticket (256 B aligned) + slots
-    return 256 + (size_t)a.n_kv * G * 8 * (sizeof(uint32_t) + sizeof(float));
+    // ticket (256 B aligned) + slots + the adaptive partition state
+    return 256 + ((slots_bytes(a, num_sms) + 255) & ~(size_t)255) + sizeof(Balance);
 }
 
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -630,11 +738,11 @@ cudaError_t launch_scan_fast(const ScanArgs& a, const CUtensorMap& kmap, void* w
     f.k = a.k;
     f.tiles_per_head = fast_tiles_per_head(a);
     f.total_tiles = f.tiles_per_head * (uint32_t)a.n_kv;
-    const int G = (int)std::min<uint32_t>((uint32_t)std::max(1, num_sms), f.total_tiles);
     uint8_t* ws = (uint8_t*)workspace;
     f.ticket = (unsigned int*)ws;
     f.slot_idx = (uint32_t*)(ws + 256);
     f.slot_score = (float*)(ws + 256 + (size_t)a.n_kv * num_sms * 8 * sizeof(uint32_t));
+    const int G = (int)std::min<uint32_t>((uint32_t)std::max(1, num_sms), f.total_tiles);
     f.idx_out = a.idx_out;
     f.score_out = a.score_out;
     f.fuse_select = a.fuse_select;
@@ -649,7 +757,17 @@ cudaError_t launch_scan_fast(const ScanArgs& a, const CUtensorMap& kmap, void* w
         }();
         const uint32_t share = f.total_tiles / (uint32_t)std::max(1, std::min<int>(num_sms, (int)f.total_tiles));
         f.tiles0 = share > (uint32_t)tail_tiles ? share - (uint32_t)tail_tiles : 0u;
+        const uint32_t rest = G > 1 ? f.total_tiles - f.tiles0 : 0u;
+        f.part_q = G > 1 ? rest / (uint32_t)(G - 1) : 0u;
+        f.part_r = G > 1 ? rest % (uint32_t)(G - 1) : 0u;
     }
+    // very long scans only (>= 400 tiles per CTA): the table reads cost the start an L2
+    // round trip and the merge a few loads.  Measured A/B: 4M context (885 tiles per CTA)
+    // 1225 -> 1203 us; 1M (233) neutral; 32K-128K a loss
+    const bool long_scan = f.total_tiles / (uint32_t)G >= 400u;
+    f.bal = a.balance && long_scan && !std::getenv("REATTN_NO_BALANCE")
+                ? (Balance*)(ws + 256 + ((slots_bytes(a, num_sms) + 255) & ~(size_t)255))
+                : nullptr;
     if (a.dtype == kBF16) {
         using C = FastCfg<__nv_bfloat16>;
         if (a.lanes == kLanesFma) {
