@@ -51,7 +51,6 @@ constexpr int kBCompute = kBGroups * 128;
 constexpr int kBThreads = kBCompute + 32;
 constexpr int kBPartBytes = kDecodePartBytes;  // double m2, A, B2, pad; float acc[128]
 constexpr int kBMaxParts = 160;          // partial slots per kv head (head + local)
-constexpr int kMaxLocalParts = 4;
 constexpr int kBSxBytes = kBGroups * 4 * 4 * kBC * 4;  // G <= 4 logit partials [gi][warp][h][key]
 constexpr size_t kBSmem = 1024 + (size_t)kBStages * kBStageBytes + 8ull * kBD * 4 + kBSxBytes +
                           (size_t)kBStages * kBC + 256;
@@ -77,7 +76,8 @@ struct BulkArgs {
     unsigned int* tickets;  // [n_kv]
     uint8_t* part;          // [n_slots][n_kv][G] partial rows
     uint64_t* trace;        // diagnostics (misc.cu layout) or null
-    int warm;               // the producer warp dry-runs the merge (see merge_parts)
+    int warm;               // dry-run the merge before griddepcontrol.wait (see merge_parts)
+    int local_post;         // kModeLocal launched after the scan (DecodeFork::post)
 };
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -243,9 +243,12 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
     // while the scan's merger CTA still runs its tail: warm the merge code (see merge_parts)
     extern __shared__ __align__(16) uint8_t bsm_raw[];
     if (B.warm && threadIdx.x < 32) merge_parts<G>(B, blockIdx.y, 0, bsm_raw, true);
-    // launched as a programmatic dependent of the scan / select: wait for its results
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const bool local = B.mode == kModeLocal;  // runs beside the scan: never reads the header
+    const bool local = B.mode == kModeLocal;  // independent of the selection: never reads the header
+    // launched as a programmatic dependent of the scan / select: wait for its results (a
+    // post-scan local launch waits at its end instead: it does not read them)
+    if (!local) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // a post-scan local launch lets the head launch become resident as its CTAs retire
+    if (local && B.local_post) asm volatile("griddepcontrol.launch_dependents;");
     if (!local && a.hdr && a.hdr->error != 0) return;
     const uint32_t L = local ? B.n_local : (a.hdr ? a.hdr->L : a.L_host);
     const uint32_t rows = B.mode == kModeHead ? L - B.n_local : L;
@@ -721,7 +724,12 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
     }
     // ---- the last part of this kv head merges (attend.hpp:448-455 normalisation) ----
     if (B.trace && tid == 0 && cta_id < 1024) B.trace[2560 + cta_id] = globaltimer();
-    if (local) return;
+    if (local) {
+        // complete only after the scan (and its merger CTA): the head launch's
+        // griddepcontrol.wait then covers the scope as well as these partials
+        if (B.local_post) asm volatile("griddepcontrol.wait;" ::: "memory");
+        return;
+    }
     __threadfence();
     __syncthreads();
     if (tid == 0) s_last = atomicAdd(&B.tickets[kv], 1u) == (unsigned)B.n_parts - 1u;
@@ -791,6 +799,7 @@ BulkArgs bulk_args(const AttnArgs& a, void* ws, int num_sms, const DecodeFork* f
     B.part = (uint8_t*)ws + 256;
     B.trace = trace_buffer();
     B.warm = 0;
+    B.local_post = 0;
     return B;
 }
 
@@ -821,7 +830,8 @@ cudaError_t launch_attend_decode_local(const AttnArgs& a, void* ws, int num_sms,
     B.mode = kModeLocal;
     B.part_base = B.n_parts;  // after the head parts
     B.n_parts = f.local_parts;
-    return launch_bulk(B, a.group, a.n_kv, s, false);
+    B.local_post = f.post;
+    return launch_bulk(B, a.group, a.n_kv, s, f.post != 0);
 }
 
 cudaError_t launch_attend_decode_head(const AttnArgs& a, void* ws, int num_sms, const DecodeFork& f,

@@ -126,6 +126,15 @@ void plan_fork(reattn_ctx* ctx, StepPlan& P) {
     const char* env_s = std::getenv("REATTN_FORK");
     const int env = env_s ? std::atoi(env_s) : -1;
     if (env == 0) return;
+    if (env == 2) {
+        // post-scan local launch on every SM (see DecodeFork::post)
+        P.fork = true;
+        P.fk.n_local = (uint32_t)n_local;
+        P.fk.local_row0 = (uint32_t)P.l_start;
+        P.fk.local_parts = std::max(1, std::min(kMaxLocalParts, ctx->num_sms / (int)P.n_kv));
+        P.fk.post = 1;
+        return;
+    }
     int m = env == 1 ? 1 : 0;
     if (!m) {
         const double t_scan = (double)P.middle * P.n_kv * P.d * 2 / 5.8e6;  // us
@@ -141,6 +150,7 @@ void plan_fork(reattn_ctx* ctx, StepPlan& P) {
     P.fk.n_local = (uint32_t)n_local;
     P.fk.local_row0 = (uint32_t)P.l_start;
     P.fk.local_parts = m;
+    P.fk.post = 0;
     P.scan.grid_sms = ctx->num_sms - m * (int)P.n_kv;
 }
 
@@ -228,7 +238,7 @@ int enqueue_select_part(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache,
     sa.hdr = P.hdr;
     // Decode: <= 32 candidates -> vote/spans/scope run in the fast scan's last CTA (one
     // launch fewer, no host round trip); otherwise the standalone select kernel.
-    if (P.fork) {  // local window beside the scan (independent of the selection)
+    if (P.fork && !P.fk.post) {  // local window beside the scan (independent of the selection)
         AttnArgs la = step_attn_args(P, cache, rope, q_dev, out_dev);
         CU(ctx, cudaEventRecord(ctx->ev_fork, s));
         CU(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
@@ -264,6 +274,11 @@ int enqueue_select_part(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache,
         if (rc) return rc;
         ++P.kernels;
     }
+    if (P.fork && P.fk.post) {  // local window after the scan, on the SMs its CTAs release
+        AttnArgs la = step_attn_args(P, cache, rope, q_dev, out_dev);
+        CU(ctx, launch_attend_decode_local(la, P.part, ctx->num_sms, P.fk, s));
+        ++P.kernels;
+    }
     if (!fused && P.large_vote) {
         CU(ctx, launch_vote_large(sa, P.vote_ws, s));
         P.kernels += 8;
@@ -290,8 +305,8 @@ int enqueue_attn_part(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache,
         // the bulk decode attention's tickets sit at the start of P.part (plans: zeroed once)
         if (zero_ticket && decode_bulk_eligible(a)) CU(ctx, cudaMemsetAsync(P.part, 0, 256, s));
         if (P.fork) {
-            CU(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
-            CU(ctx, launch_attend_decode_head(a, P.part, ctx->num_sms, P.fk, s, false));
+            if (!P.fk.post) CU(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
+            CU(ctx, launch_attend_decode_head(a, P.part, ctx->num_sms, P.fk, s, P.fk.post != 0));
             ++P.kernels;
         } else if (P.attn_tc) {
             CU(ctx, launch_attend_tc(a, std::max<uint32_t>(1, P.L_upper), P.attn_tc_ws, s));

@@ -168,8 +168,14 @@ cudaError_t launch_attend_decode_bulk_ex(const AttnArgs& a, void* ws, int num_sm
 struct DecodeFork {
     uint32_t n_local;     // local segment rows (cache total - local start)
     uint32_t local_row0;  // cache row of local row 0
-    int local_parts;      // CTAs per kv head for the local launch (1..4)
+    int local_parts;      // CTAs per kv head for the local launch (1..kMaxLocalParts)
+    int post;             // 1: the local launch follows the scan on the same stream (PDL): its
+                          // CTAs fill the SMs the scan CTAs release while the scan's merger CTA
+                          // runs its tail, and it completes only after the scan (so the head
+                          // launch's griddepcontrol.wait covers both); 0: beside the scan on
+                          // local_parts * n_kv lent SMs (side stream)
 };
+constexpr int kMaxLocalParts = 32;
 cudaError_t launch_attend_decode_local(const AttnArgs& a, void* ws, int num_sms, const DecodeFork& f,
                                        cudaStream_t s);
 cudaError_t launch_attend_decode_head(const AttnArgs& a, void* ws, int num_sms, const DecodeFork& f,
