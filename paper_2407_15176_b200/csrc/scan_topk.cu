@@ -764,7 +764,8 @@ cudaError_t launch_scan_fast(const ScanArgs& a, const CUtensorMap& kmap, void* w
     // very long scans only (>= 400 tiles per CTA): the table reads cost the start an L2
     // round trip and the merge a few loads.  Measured A/B: 4M context (885 tiles per CTA)
     // 1225 -> 1203 us; 1M (233) neutral; 32K-128K a loss
-    const bool long_scan = f.total_tiles / (uint32_t)G >= 400u;
+    const char* bmin = std::getenv("REATTN_BALANCE_MIN_TILES");  // tests force it small
+    const bool long_scan = f.total_tiles / (uint32_t)G >= (bmin ? (uint32_t)std::atoi(bmin) : 400u);
     f.bal = a.balance && long_scan && !std::getenv("REATTN_NO_BALANCE")
                 ? (Balance*)(ws + 256 + ((slots_bytes(a, num_sms) + 255) & ~(size_t)255))
                 : nullptr;

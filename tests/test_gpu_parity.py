@@ -331,6 +331,26 @@ def test_plan_graph_replay_matches_step(ctx):
         assert torch.equal(oh, ref.out.cpu())
 
 
+def test_plan_adaptive_partition_replays(ctx, monkeypatch):
+    """The adaptive scan partition (forced on at this size) changes the CTAs' tile ranges
+    between replays; the selection is exact under any partition, so every replay must equal the
+    synchronous step bitwise."""
+    monkeypatch.setenv("REATTN_BALANCE_MIN_TILES", "1")
+    cfg = N.SelectionConfig()
+    cache, _, _ = make_cache(ctx, 8, 128, 90000, cfg, N.BF16, 23)
+    rope = N.Rope(ctx, 128, 500000.0, 8192)
+    plan = N.Plan(ctx, cache, rope, 1, 32, cfg)
+    for s in range(8):
+        q = dev(synth.uniform(400 + s % 3, 32 * 128).reshape(1, -1))
+        ref = N.attend_step(ctx, cache, rope, q, 32, cfg)
+        plan.q.copy_(q)
+        torch.cuda.synchronize()
+        plan.launch()
+        st = plan.stats()
+        assert torch.equal(plan.out, ref.out), (s, (plan.out - ref.out).abs().max().item())
+        assert st.scope_len == ref.stats.scope_len
+
+
 @pytest.mark.slow
 def test_fast_scan_1m_context(ctx):
     """Full-size config 4 selection (1M ctx, middle 1,044,448 rows x 8 heads): bit-exact vs
