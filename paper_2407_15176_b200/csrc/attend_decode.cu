@@ -78,6 +78,7 @@ struct BulkArgs {
     uint64_t* trace;        // diagnostics (misc.cu layout) or null
     int warm;               // dry-run the merge before griddepcontrol.wait (see merge_parts)
     int local_post;         // kModeLocal launched after the scan (DecodeFork::post)
+    int local_hpc;          // kModeLocal: kv heads per CTA, processed one after the other
 };
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -252,10 +253,16 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
     if (!local && a.hdr && a.hdr->error != 0) return;
     const uint32_t L = local ? B.n_local : (a.hdr ? a.hdr->L : a.L_host);
     const uint32_t rows = B.mode == kModeHead ? L - B.n_local : L;
-    const int part = blockIdx.x, kv = blockIdx.y;
+    const int part = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cta_id = blockIdx.y * gridDim.x + blockIdx.x + (local ? 512 : 0);  // trace slot
     if (B.trace && tid == 0 && cta_id < 1024) B.trace[1536 + cta_id] = globaltimer();
+    // the local window may give a CTA several kv heads (fewer SMs lent by the scan)
+    const int hpc = local ? max(1, B.local_hpc) : 1;
+#pragma unroll 1
+    for (int hh = 0; hh < hpc; ++hh) {
+    const int kv = blockIdx.y * hpc + hh;
+    if (hh > 0) __syncthreads();  // the previous head's stages and barriers are idle
     ShardRanges R;
     R.n = 0;
     int chunks;
@@ -725,6 +732,7 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
     // ---- the last part of this kv head merges (attend.hpp:448-455 normalisation) ----
     if (B.trace && tid == 0 && cta_id < 1024) B.trace[2560 + cta_id] = globaltimer();
     if (local) {
+        if (hh + 1 < hpc) continue;
         // complete only after the scan (and its merger CTA): the head launch's
         // griddepcontrol.wait then covers the scope as well as these partials
         if (B.local_post) asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -743,6 +751,7 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
         __syncthreads();
         if (tid == 0 && kv < 512) B.trace[3584 + kv] = globaltimer();
     }
+    }  // kv heads of this CTA
 }
 
 int bulk_parts(const AttnArgs& a, int num_sms) {
@@ -800,6 +809,7 @@ BulkArgs bulk_args(const AttnArgs& a, void* ws, int num_sms, const DecodeFork* f
     B.trace = trace_buffer();
     B.warm = 0;
     B.local_post = 0;
+    B.local_hpc = 1;
     return B;
 }
 
@@ -831,7 +841,9 @@ cudaError_t launch_attend_decode_local(const AttnArgs& a, void* ws, int num_sms,
     B.part_base = B.n_parts;  // after the head parts
     B.n_parts = f.local_parts;
     B.local_post = f.post;
-    return launch_bulk(B, a.group, a.n_kv, s, f.post != 0);
+    B.local_hpc = std::max(1, f.heads_per_cta);
+    if (a.n_kv % B.local_hpc) return cudaErrorInvalidValue;
+    return launch_bulk(B, a.group, a.n_kv / B.local_hpc, s, f.post != 0);
 }
 
 cudaError_t launch_attend_decode_head(const AttnArgs& a, void* ws, int num_sms, const DecodeFork& f,

@@ -169,6 +169,7 @@ struct DecodeFork {
     uint32_t n_local;     // local segment rows (cache total - local start)
     uint32_t local_row0;  // cache row of local row 0
     int local_parts;      // CTAs per kv head for the local launch (1..kMaxLocalParts)
+    int heads_per_cta;    // kv heads each local CTA processes in turn (divides n_kv)
     int post;             // 1: the local launch follows the scan on the same stream (PDL): its
                           // CTAs fill the SMs the scan CTAs release while the scan's merger CTA
                           // runs its tail, and it completes only after the scan (so the head
