@@ -78,6 +78,10 @@ def main():
         if sl:
             print("K5 local start    ", summarize(sl))
             print("K5 local end      ", summarize(rel(t[3072:3584])))
+        if t[3700]:
+            print(f"   K5 part0/kv0: q rotated {(t[3700] - t0) / 1e3:8.2f}  first copy issued "
+                  f"{(t[3704] - t0) / 1e3:8.2f}  first chunk landed {(t[3701] - t0) / 1e3:8.2f}  "
+                  f"warps merged {(t[3703] - t0) / 1e3:8.2f} us")
         if any(t[3600:3600 + args.n_kv]):
             print("K5 last ticket    ", summarize(rel(t[3600:3600 + args.n_kv])))
             print("K5 M/w loops done ", summarize(rel(t[3664:3664 + args.n_kv])))
