@@ -26,9 +26,15 @@
 //      score GEMM once and the streaming epilogue does no exact math.
 //
 // Warp roles (320 threads, 1 CTA/SM):
-//   warp 0  TMA producer: the CTA's Q hi tile once, then K tiles (4-stage ring of 32 KB)
-//   warp 1  TMEM allocator (512 columns = 4 accumulators of 128) + single-thread MMA issue;
-//           the MMA commit releases both the accumulator's producer slot and the K stage
+//   warp 0  TMA producer: K tiles (5-stage ring of 32 KB)
+//   warp 1  TMEM allocator (512 columns: 3 accumulators of 128 + hi(mq) in 64) + single-
+//           thread MMA issue with A from TMEM (tcgen05.mma TS form); the MMA commit releases
+//           both the accumulator's producer slot and the K stage
+//   The epilogue warps first store the CTA's hi(mq) rows into TMEM (tcgen05.st).
+//   Measured (tools/micro/mma_rate.cu): the MMA alone dispatches 128x128x16 in 64 cycles
+//   (2.1-2.2 PFLOP/s, SS or TS); K2 with its epilogue ablated (REATTN_K2_NULL_EPILOGUE)
+//   reaches ~1.25 PFLOP/s, the same with A in shared memory or TMEM: the K-tile feed, not
+//   the MMA or its shared-memory operand reads, bounds the N = 128 tile loop.
 //   warps 2-9  epilogue, two warps per TMEM lane quarter (one per 64-column half): one
 //           tcgen05.ld 32x32b.x64, release the accumulator, 8 group maxes against the
 //           admission limit, rare per-column list inserts.
@@ -36,6 +42,7 @@
 // Grid: (query tile, kv head, key split): the key range of each query tile is cut into
 // `splits` contiguous parts chosen to fill whole waves; the exact merge reduces them.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -50,9 +57,9 @@ namespace {
 constexpr int kPM = 128;  // queries per CTA = UMMA M
 constexpr int kPN = 128;  // keys per tile = UMMA N
 constexpr int kPD = 128;  // head dim
-constexpr int kPStages = 4;
-constexpr int kPAcc = 4;  // TMEM accumulators of kPN columns
-constexpr int kPQBytes = kPM * kPD * 2;  // hi(mq) tile: 32 KB
+constexpr int kPStages = 5;
+constexpr int kPAcc = 3;  // TMEM accumulators of kPN columns
+constexpr int kPColQ = kPAcc * kPN;  // hi(mq) tile in TMEM: 128 lanes x 64 columns (bf16 pairs)
 constexpr int kPKBytes = kPN * kPD * 2;  // one K stage: 32 KB
 constexpr int kPThreads = 320;           // producer, MMA, 8 epilogue warps
 constexpr int kPKMax = 8;                // largest k
@@ -60,7 +67,7 @@ constexpr int kPExtra = 8;               // list slots beyond KT (near-tie margi
 constexpr int kPL = 16;                  // part-list stride (>= kPKMax + kPExtra)
 constexpr int kPMaxSplits = 8;
 constexpr float kPAccumCoef = 0.000244140625f;  // 2^-12
-constexpr size_t kPSmem = 1024 + kPQBytes + kPStages * kPKBytes + 256 + kPM * (kPL * 8 + 4) + 2 * kPM * 4;
+constexpr size_t kPSmem = 1024 + kPStages * kPKBytes + 256 + kPM * (kPL * 8 + 4) + 2 * kPM * 4;
 
 struct PrefillArgs {
     int n_q, n_qpad, n_kv, k;
@@ -71,6 +78,8 @@ struct PrefillArgs {
     const float* dl;        // [n_kv][n_qpad] delta / max|k|
     const unsigned* kmax;   // [n_kv] max |k| over the middle (float bits)
     unsigned* board;        // [n_kv][n_qpad] best published KT-th S_hi (ordered bits, 0 = none)
+    const __nv_bfloat16* qhi;  // [n_kv][n_qpad][128] hi(mq), the MMA's A operand
+    int null_epilogue;         // ablation (REATTN_K2_NULL_EPILOGUE): load + release only
     uint32_t* part_idx;     // [splits][n_kv][n_qpad][kPL], sorted by better(), kNoIndex-padded
     float* part_score;      // S_hi of those keys
     float* part_dropped;    // [splits][n_kv][n_qpad]
@@ -127,13 +136,11 @@ __device__ __forceinline__ float kth_of_8(const float (&g)[8]) {
 
 template <int KT>
 __global__ void __launch_bounds__(kPThreads, 1)
-    prefill_scan_tc_kernel(const __grid_constant__ CUtensorMap qhi_map,
-                           const __grid_constant__ CUtensorMap k_map, const PrefillArgs a) {
+    prefill_scan_tc_kernel(const __grid_constant__ CUtensorMap k_map, const PrefillArgs a) {
     constexpr int L = KT + kPExtra;
     extern __shared__ uint8_t psm_raw[];
     uint8_t* sm = (uint8_t*)(((uintptr_t)psm_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t* s_qhi = sm;
-    uint8_t* s_k = sm + kPQBytes;
+    uint8_t* s_k = sm;
     uint64_t* bars = (uint64_t*)(s_k + kPStages * kPKBytes);
     uint64_t* q_full = bars;
     uint64_t* full = bars + 1;
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     if (warp == 1) tmem_alloc(s_tmem, 512);
     for (int i = tid; i < 2 * kPM; i += kPThreads) s_thr[i] = -INFINITY;
     if (tid == 0) {
-        mbar_init(q_full, 1);
+        mbar_init(q_full, 256);  // the epilogue threads' tcgen05.st of hi(mq) into TMEM
         for (int s = 0; s < kPStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);  // MMA commit: the stage has been read
@@ -170,14 +177,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ===== TMA producer =====
-            prefetch_tensormap(&qhi_map);
             prefetch_tensormap(&k_map);
-            const uint64_t pol = policy_evict_first();
             const uint64_t keep = policy_evict_last();  // K tiles: re-read by every query tile
-            const int32_t qrow = (int32_t)(kv * a.n_qpad + qtile * kPM);
-            mbar_arrive_expect_tx(q_full, kPQBytes);
-            tma_load_2d(s_qhi, &qhi_map, 0, qrow, q_full, pol);
-            tma_load_2d(s_qhi + kPQBytes / 2, &qhi_map, 64, qrow, q_full, pol);
             for (int t = 0; t < n_tiles; ++t) {
                 const int s = t % kPStages;
                 const uint32_t ph = (t / kPStages) & 1u;
@@ -193,9 +194,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
     } else if (warp == 1) {
         if (lane == 0) {  // ===== MMA issuer: S_hi = hi(mq) · K^T, one pass =====
             const uint32_t idesc = prefill_idesc();
-            mbar_wait(q_full, 0);
+            mbar_wait(q_full, 0);  // hi(mq) is in TMEM
             tc_fence_after();
-            const uint32_t qhi = smem_u32(s_qhi);
             for (int t = 0; t < n_tiles; ++t) {
                 const int s = t % kPStages;
                 const uint32_t ph = (t / kPStages) & 1u;
@@ -206,13 +206,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 tc_fence_after();
                 const uint32_t kbase = smem_u32(s_k + (size_t)s * kPKBytes);
                 const uint32_t d_tmem = tmem + (uint32_t)(b * kPN);
+                // A (hi(mq)) from TMEM: the MMA reads only the K tile from shared memory, which
+                // with the TMA's writes into the ring was the shared-memory bound of the SS form
 #pragma unroll
                 for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
                     for (int ks = 0; ks < 4; ++ks) {
-                        const uint64_t ad = umma_desc_sw128(qhi + kb * (kPQBytes / 2) + ks * 32);
                         const uint64_t bd = umma_desc_sw128(kbase + kb * (kPKBytes / 2) + ks * 32);
-                        mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | ks) ? 1u : 0u);
+                        mma_bf16_ts(d_tmem, tmem + (uint32_t)(kPColQ + kb * 32 + ks * 8), bd, idesc,
+                                    (kb | ks) ? 1u : 0u);
                     }
                 mma_commit(&empty[s]);  // K stage consumed
                 mma_commit(&tfull[b]);  // accumulator ready for the epilogue
@@ -227,6 +229,23 @@ __global__ void __launch_bounds__(kPThreads, 1)
         const int row = quarter * 32 + lane;
         const size_t qrow = (size_t)kv * a.n_qpad + (size_t)qtile * kPM + row;
         const float d2 = 2.0f * a.dl[qrow] * __uint_as_float(a.kmax[kv]);  // 2 delta
+        {
+            // hi(mq) row -> TMEM lane `row`, this thread's half of its 64 packed columns
+            const uint4* src = reinterpret_cast<const uint4*>(a.qhi + qrow * kPD + half * 64);
+            uint32_t w[32];
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+                const uint4 x = __ldg(src + v);
+                w[4 * v] = x.x;
+                w[4 * v + 1] = x.y;
+                w[4 * v + 2] = x.z;
+                w[4 * v + 3] = x.w;
+            }
+            TMEM_ST_X32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(kPColQ + half * 32), w);
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(q_full);
+        }
         float as[L];
         uint32_t ai[L];
 #pragma unroll
@@ -254,6 +273,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
             uint32_t r[64];
             TMEM_LD_X64(taddr, r);
             tmem_wait_ld();
+            if (a.null_epilogue) {  // ablation: the TMA / MMA / TMEM-read floor
+                if (r[0] == 0x7FFFFFFFu && r[63] == 0x7FFFFFFFu) dropped = 1.0f;
+                tc_fence_before();
+                mbar_arrive(&tempty[b]);
+                continue;
+            }
             const uint32_t key0 = (uint32_t)(t_first + t) * kPN + half * 64;
             if (key0 + 64 > a.count) {  // tail tile: keys past the middle never qualify
 #pragma unroll
@@ -689,9 +714,6 @@ cudaError_t launch_prefill_tc(const ScanArgs& a, const CUtensorMap& kmap, void* 
     if (e != cudaSuccess) return e;
     prefill_kmax_kernel<<<dim3(std::max(1, num_sms() * 4 / std::max(1, a.n_kv)), a.n_kv), 256, 0, s>>>(
         (const __nv_bfloat16*)a.keys, a.head_stride, a.row0, a.count, a.n_kv, kmax);
-    CUtensorMap qh;
-    if (!make_key_tensor_map(&qh, hi, kBF16, kPD, (uint64_t)a.n_kv * n_qpad, kPM))
-        return cudaErrorInvalidValue;
     PrefillArgs p;
     p.n_q = a.n_q;
     p.n_qpad = n_qpad;
@@ -708,10 +730,12 @@ cudaError_t launch_prefill_tc(const ScanArgs& a, const CUtensorMap& kmap, void* 
     p.part_idx = part_idx;
     p.part_score = part_score;
     p.part_dropped = part_dropped;
+    p.qhi = hi;
+    p.null_epilogue = std::getenv("REATTN_K2_NULL_EPILOGUE") ? 1 : 0;
     dim3 grid(n_qpad / kPM, a.n_kv, g.splits);
     auto launch = [&](auto kernel) {
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmem);
-        kernel<<<grid, kPThreads, kPSmem, s>>>(qh, kmap, p);
+        kernel<<<grid, kPThreads, kPSmem, s>>>(kmap, p);
     };
     if (a.k <= 1)
         launch(prefill_scan_tc_kernel<1>);
