@@ -80,6 +80,7 @@ struct PrefillArgs {
     unsigned* board;        // [n_kv][n_qpad] best published KT-th S_hi (ordered bits, 0 = none)
     const __nv_bfloat16* qhi;  // [n_kv][n_qpad][128] hi(mq), the MMA's A operand
     int null_epilogue;         // ablation (REATTN_K2_NULL_EPILOGUE): load + release only
+    int no_mma;                // ablation (REATTN_K2_NO_MMA): the K-tile feed alone
     uint32_t* part_idx;     // [splits][n_kv][n_qpad][kPL], sorted by better(), kNoIndex-padded
     float* part_score;      // S_hi of those keys
     float* part_dropped;    // [splits][n_kv][n_qpad]
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const uint32_t d_tmem = tmem + (uint32_t)(b * kPN);
                 // A (hi(mq)) from TMEM: the MMA reads only the K tile from shared memory, which
                 // with the TMA's writes into the ring was the shared-memory bound of the SS form
+                if (!a.no_mma)
 #pragma unroll
                 for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
@@ -732,6 +734,7 @@ cudaError_t launch_prefill_tc(const ScanArgs& a, const CUtensorMap& kmap, void* 
     p.part_dropped = part_dropped;
     p.qhi = hi;
     p.null_epilogue = std::getenv("REATTN_K2_NULL_EPILOGUE") ? 1 : 0;
+    p.no_mma = std::getenv("REATTN_K2_NO_MMA") ? 1 : 0;
     dim3 grid(n_qpad / kPM, a.n_kv, g.splits);
     auto launch = [&](auto kernel) {
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmem);
