@@ -25,21 +25,20 @@
 //      reference (tests/test_prefill_tc.py compares bitwise) while the tensor cores run the
 //      score GEMM once and the streaming epilogue does no exact math.
 //
-// Warp roles (320 threads, 1 CTA/SM):
-//   warp 0  TMA producer: K tiles (5-stage ring of 32 KB)
-//   warp 1  TMEM allocator (512 columns: 3 accumulators of 128 + hi(mq) in 64) + single-
-//           thread MMA issue with A from TMEM (tcgen05.mma TS form); the MMA commit releases
-//           both the accumulator's producer slot and the K stage
-//   The epilogue warps first store the CTA's hi(mq) rows into TMEM (tcgen05.st).
-//   Measured (tools/micro/mma_rate.cu): the MMA alone dispatches 128x128x16 in 64 cycles
-//   (2.1-2.2 PFLOP/s, SS or TS); K2 with its epilogue ablated (REATTN_K2_NULL_EPILOGUE)
-//   reaches ~1.25 PFLOP/s, the same with A in shared memory or TMEM: the K-tile feed, not
-//   the MMA or its shared-memory operand reads, bounds the N = 128 tile loop.
-//   warps 2-9  epilogue, two warps per TMEM lane quarter (one per 64-column half): one
-//           tcgen05.ld 32x32b.x64, release the accumulator, 8 group maxes against the
+// Warp roles (576 threads, 1 CTA/SM):
+//   warp 0  TMA producer: the CTA's two hi(mq) tiles once, then K tiles (4-stage ring of 32 KB)
+//   warp 1  TMEM allocator (512 columns = 2 pairs x 2 query tiles x 128) + single-thread MMA
+//           issue: every K tile feeds BOTH query tiles (M = 256 per K tile), halving the K
+//           feed per FLOP; the MMA commit releases the K stage and the accumulator pair
+//   warps 2-17  epilogue, four per TMEM lane quarter (column half x query tile): one
+//           tcgen05.ld 32x32b.x64, release the accumulator pair, 8 group maxes against the
 //           admission limit, rare per-column list inserts.
-//
-// Grid: (query tile, kv head, key split): the key range of each query tile is cut into
+//   Measured (config 3 chunk, incl. ~0.19 ms prep/kmax/merge): 2.50 ms (0.53 of the bf16
+//   burst) vs 2.67 ms with one query tile per CTA.  Ablations (REATTN_K2_NULL_EPILOGUE /
+//   REATTN_K2_NO_MMA): epilogue ablated 1.69 ms (was 1.96), feed alone 0.63 ms (was 0.85);
+//   the MMA alone dispatches 128x128x16 in 64 cycles (tools/micro/mma_rate.cu).  The two
+//   query tiles made the feed no longer the bound; the epilogue's admissions now are.
+// Grid: (query-tile pair, kv head, key split): the key range of each pair is cut into
 // `splits` contiguous parts chosen to fill whole waves; the exact merge reduces them.
 #include <algorithm>
 #include <cstdlib>
@@ -57,17 +56,20 @@ namespace {
 constexpr int kPM = 128;  // queries per CTA = UMMA M
 constexpr int kPN = 128;  // keys per tile = UMMA N
 constexpr int kPD = 128;  // head dim
-constexpr int kPStages = 5;
-constexpr int kPAcc = 3;  // TMEM accumulators of kPN columns
-constexpr int kPColQ = kPAcc * kPN;  // hi(mq) tile in TMEM: 128 lanes x 64 columns (bf16 pairs)
+constexpr int kPQT = 2;     // query tiles per CTA: every K tile feeds M = 256 queries
+constexpr int kPStages = 4;
+constexpr int kPPairs = 2;  // TMEM: kPPairs x kPQT accumulators of kPN columns = 512
+constexpr int kPQBytes = kPM * kPD * 2;  // hi(mq) tile: 32 KB
 constexpr int kPKBytes = kPN * kPD * 2;  // one K stage: 32 KB
-constexpr int kPThreads = 320;           // producer, MMA, 8 epilogue warps
+constexpr int kPEpi = 16;                // epilogue warps: (lane quarter, column half, query tile)
+constexpr int kPThreads = (2 + kPEpi) * 32;  // producer, MMA, epilogue
 constexpr int kPKMax = 8;                // largest k
 constexpr int kPExtra = 8;               // list slots beyond KT (near-tie margin)
 constexpr int kPL = 16;                  // part-list stride (>= kPKMax + kPExtra)
 constexpr int kPMaxSplits = 8;
 constexpr float kPAccumCoef = 0.000244140625f;  // 2^-12
-constexpr size_t kPSmem = 1024 + kPStages * kPKBytes + 256 + kPM * (kPL * 8 + 4) + 2 * kPM * 4;
+constexpr size_t kPSmem = 1024 + kPQT * kPQBytes + kPStages * kPKBytes + 256 + kPQT * 2 * kPM * 4;
+static_assert(kPStages * kPKBytes >= kPQT * kPM * (kPL * 8 + 4), "half-merge lists reuse the K ring");
 
 struct PrefillArgs {
     int n_q, n_qpad, n_kv, k;
@@ -137,37 +139,39 @@ __device__ __forceinline__ float kth_of_8(const float (&g)[8]) {
 
 template <int KT>
 __global__ void __launch_bounds__(kPThreads, 1)
-    prefill_scan_tc_kernel(const __grid_constant__ CUtensorMap k_map, const PrefillArgs a) {
+    prefill_scan_tc_kernel(const __grid_constant__ CUtensorMap q_map,
+                           const __grid_constant__ CUtensorMap k_map, const PrefillArgs a) {
     constexpr int L = KT + kPExtra;
     extern __shared__ uint8_t psm_raw[];
     uint8_t* sm = (uint8_t*)(((uintptr_t)psm_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t* s_k = sm;
+    uint8_t* s_q = sm;                                   // kPQT hi(mq) tiles, SW128
+    uint8_t* s_k = sm + kPQT * kPQBytes;                 // K ring
     uint64_t* bars = (uint64_t*)(s_k + kPStages * kPKBytes);
     uint64_t* q_full = bars;
     uint64_t* full = bars + 1;
     uint64_t* empty = full + kPStages;
-    uint64_t* tfull = empty + kPStages;
-    uint64_t* tempty = tfull + kPAcc;
-    uint32_t* s_tmem = (uint32_t*)(tempty + kPAcc);
-    uint8_t* aux = (uint8_t*)bars + 256;  // half-merge lists
-    float* s_thr = (float*)(aux + kPM * (kPL * 8 + 4));  // [2][128] KT-th best S_hi per half
+    uint64_t* tfull = empty + kPStages;   // [kPPairs]: both query tiles' accumulators ready
+    uint64_t* tempty = tfull + kPPairs;
+    uint32_t* s_tmem = (uint32_t*)(tempty + kPPairs);
+    float* s_thr = (float*)((uint8_t*)bars + 256);  // [kPQT][2 halves][128] KT-th best S_hi
+    uint8_t* aux = s_k;  // half-merge lists, after the tile loop (the K ring is idle then)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int qtile = blockIdx.x, kv = blockIdx.y, split = blockIdx.z;
+    const int qtile = blockIdx.x, kv = blockIdx.y, split = blockIdx.z;  // qtile: pair index
     const int t_first = (int)((int64_t)split * a.tiles / a.splits);
     const int n_tiles = (int)((int64_t)(split + 1) * a.tiles / a.splits) - t_first;
 
     if (warp == 1) tmem_alloc(s_tmem, 512);
-    for (int i = tid; i < 2 * kPM; i += kPThreads) s_thr[i] = -INFINITY;
+    for (int i = tid; i < kPQT * 2 * kPM; i += kPThreads) s_thr[i] = -INFINITY;
     if (tid == 0) {
-        mbar_init(q_full, 256);  // the epilogue threads' tcgen05.st of hi(mq) into TMEM
+        mbar_init(q_full, 1);
         for (int s = 0; s < kPStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);  // MMA commit: the stage has been read
         }
-        for (int b = 0; b < kPAcc; ++b) {
+        for (int b = 0; b < kPPairs; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 256);
+            mbar_init(&tempty[b], kPEpi * 32);
         }
         fence_barrier_init();
     }
@@ -178,8 +182,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ===== TMA producer =====
+            prefetch_tensormap(&q_map);
             prefetch_tensormap(&k_map);
+            const uint64_t pol = policy_evict_first();
             const uint64_t keep = policy_evict_last();  // K tiles: re-read by every query tile
+            mbar_arrive_expect_tx(q_full, kPQT * kPQBytes);
+#pragma unroll
+            for (int qt = 0; qt < kPQT; ++qt) {
+                const int32_t qrow = (int32_t)(kv * a.n_qpad + (qtile * kPQT + qt) * kPM);
+                tma_load_2d(s_q + qt * kPQBytes, &q_map, 0, qrow, q_full, pol);
+                tma_load_2d(s_q + qt * kPQBytes + kPQBytes / 2, &q_map, 64, qrow, q_full, pol);
+            }
             for (int t = 0; t < n_tiles; ++t) {
                 const int s = t % kPStages;
                 const uint32_t ph = (t / kPStages) & 1u;
@@ -193,61 +206,48 @@ __global__ void __launch_bounds__(kPThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ===== MMA issuer: S_hi = hi(mq) · K^T, one pass =====
+        if (lane == 0) {  // ===== MMA issuer: S_hi = hi(mq) · K^T for both query tiles =====
             const uint32_t idesc = prefill_idesc();
-            mbar_wait(q_full, 0);  // hi(mq) is in TMEM
+            mbar_wait(q_full, 0);
             tc_fence_after();
+            const uint32_t q0 = smem_u32(s_q);
             for (int t = 0; t < n_tiles; ++t) {
                 const int s = t % kPStages;
                 const uint32_t ph = (t / kPStages) & 1u;
-                const int b = t % kPAcc;
-                const uint32_t bph = (t / kPAcc) & 1u;
-                if (t >= kPAcc) mbar_wait(&tempty[b], bph ^ 1u);
+                const int p = t % kPPairs;
+                const uint32_t pph = (t / kPPairs) & 1u;
+                if (t >= kPPairs) mbar_wait(&tempty[p], pph ^ 1u);
                 mbar_wait(&full[s], ph);
                 tc_fence_after();
                 const uint32_t kbase = smem_u32(s_k + (size_t)s * kPKBytes);
-                const uint32_t d_tmem = tmem + (uint32_t)(b * kPN);
-                // A (hi(mq)) from TMEM: the MMA reads only the K tile from shared memory, which
-                // with the TMA's writes into the ring was the shared-memory bound of the SS form
                 if (!a.no_mma)
 #pragma unroll
-                for (int kb = 0; kb < 2; ++kb)
+                    for (int qt = 0; qt < kPQT; ++qt) {
+                        const uint32_t d_tmem = tmem + (uint32_t)((p * kPQT + qt) * kPN);
 #pragma unroll
-                    for (int ks = 0; ks < 4; ++ks) {
-                        const uint64_t bd = umma_desc_sw128(kbase + kb * (kPKBytes / 2) + ks * 32);
-                        mma_bf16_ts(d_tmem, tmem + (uint32_t)(kPColQ + kb * 32 + ks * 8), bd, idesc,
-                                    (kb | ks) ? 1u : 0u);
+                        for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+                            for (int ks = 0; ks < 4; ++ks) {
+                                const uint64_t ad = umma_desc_sw128(q0 + qt * kPQBytes + kb * (kPQBytes / 2) + ks * 32);
+                                const uint64_t bd = umma_desc_sw128(kbase + kb * (kPKBytes / 2) + ks * 32);
+                                mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | ks) ? 1u : 0u);
+                            }
                     }
                 mma_commit(&empty[s]);  // K stage consumed
-                mma_commit(&tfull[b]);  // accumulator ready for the epilogue
+                mma_commit(&tfull[p]);  // both accumulators ready for the epilogue
             }
         }
     } else {
-        // ===== epilogue: 8 warps, two per TMEM lane quarter; the thread owning lane r owns
-        // query row r of the tile for one half (64 columns) of every key tile =====
-        const int ew = warp - 2;          // 0..7
+        // ===== epilogue: 16 warps, four per TMEM lane quarter: warp (quarter, half, qt) owns
+        // query row quarter*32 + lane of query tile qt, for one half (64 columns) of every
+        // key tile =====
+        const int ew = warp - 2;          // 0..15
         const int quarter = warp & 3;     // TMEM lane quarter this warp may access
-        const int half = ew >> 2;         // column half of the 128-key tile
+        const int half = (ew >> 2) & 1;   // column half of the 128-key tile
+        const int qt = ew >> 3;           // query tile of the CTA
         const int row = quarter * 32 + lane;
-        const size_t qrow = (size_t)kv * a.n_qpad + (size_t)qtile * kPM + row;
+        const size_t qrow = (size_t)kv * a.n_qpad + (size_t)(qtile * kPQT + qt) * kPM + row;
         const float d2 = 2.0f * a.dl[qrow] * __uint_as_float(a.kmax[kv]);  // 2 delta
-        {
-            // hi(mq) row -> TMEM lane `row`, this thread's half of its 64 packed columns
-            const uint4* src = reinterpret_cast<const uint4*>(a.qhi + qrow * kPD + half * 64);
-            uint32_t w[32];
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-                const uint4 x = __ldg(src + v);
-                w[4 * v] = x.x;
-                w[4 * v + 1] = x.y;
-                w[4 * v + 2] = x.z;
-                w[4 * v + 3] = x.w;
-            }
-            TMEM_ST_X32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(kPColQ + half * 32), w);
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(q_full);
-        }
         float as[L];
         uint32_t ai[L];
 #pragma unroll
@@ -262,23 +262,26 @@ __global__ void __launch_bounds__(kPThreads, 1)
         // threshold instead of paying k ln(n/k) admissions from -inf.
         unsigned* board = a.board + qrow;
         float tb = ord_dec(*(volatile unsigned*)board);
+        float* thr_mine = s_thr + (qt * 2 + half) * kPM;
+        const float* thr_other = s_thr + (qt * 2 + (half ^ 1)) * kPM;
         for (int t = 0; t < n_tiles; ++t) {
             if ((t & 31) == 31) {
                 if (as[KT - 1] > -INFINITY) atomicMax(board, ord_enc(as[KT - 1]));
                 tb = ord_dec(*(volatile unsigned*)board);
             }
-            const int b = t % kPAcc;
-            const uint32_t bph = (t / kPAcc) & 1u;
-            mbar_wait(&tfull[b], bph);
+            const int p = t % kPPairs;
+            const uint32_t pph = (t / kPPairs) & 1u;
+            mbar_wait(&tfull[p], pph);
             tc_fence_after();
-            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * kPN + half * 64);
+            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) +
+                                   (uint32_t)((p * kPQT + qt) * kPN + half * 64);
             uint32_t r[64];
             TMEM_LD_X64(taddr, r);
             tmem_wait_ld();
             if (a.null_epilogue) {  // ablation: the TMA / MMA / TMEM-read floor
                 if (r[0] == 0x7FFFFFFFu && r[63] == 0x7FFFFFFFu) dropped = 1.0f;
                 tc_fence_before();
-                mbar_arrive(&tempty[b]);
+                mbar_arrive(&tempty[p]);
                 continue;
             }
             const uint32_t key0 = (uint32_t)(t_first + t) * kPN + half * 64;
@@ -298,12 +301,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
             // admission limit: (KT-th best S_hi so far) - 2 delta.  Before the list holds KT
             // keys, the KT-th largest group max of this tile bounds the KT-th best from below;
             // those keys are not listed yet, so one ulp lower keeps an exact tie (delta == 0)
-            // with them admissible
-            // The other column half's KT-th best is a lower bound of the row's k-th best
-            // too (any subset's is): a key at or below it - 2 delta is outside the merge's
-            // window (prefill_exact_merge_kernel).  Its keys are not ordered before ours, so
-            // one ulp lower again.  Read racily: every value ever stored is a valid bound.
-            const float other = ((volatile float*)s_thr)[(half ^ 1) * kPM + row];
+            // with them admissible.  The other column half's KT-th best is a lower bound of
+            // the row's k-th best too (any subset's is): a key at or below it - 2 delta is
+            // outside the merge's window (prefill_exact_merge_kernel).  Its keys are not
+            // ordered before ours, so one ulp lower again.  Read racily: every value ever
+            // stored is a valid bound.
+            const float other = ((volatile const float*)thr_other)[row];
             float lim = fmaxf(as[KT - 1] - d2, nextafterf(fmaxf(other, tb) - d2, -INFINITY));
             if (as[KT - 1] == -INFINITY)
                 lim = fmaxf(lim, nextafterf(kth_of_8<KT>(gx) - d2, -INFINITY));
@@ -333,15 +336,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     }
                 }
             }
-            s_thr[half * kPM + row] = as[KT - 1];
+            thr_mine[row] = as[KT - 1];
             tc_fence_before();
-            mbar_arrive(&tempty[b]);  // accumulator no longer read: the MMA warp may reuse it
+            mbar_arrive(&tempty[p]);  // accumulator no longer read: the MMA warp may reuse it
         }
         // merge the two column halves of each row (disjoint key sets): top L under better(),
-        // anything pushed off the end raises `dropped`
-        float* m_s = (float*)aux;                               // [128][L] scores
-        uint32_t* m_i = (uint32_t*)(aux + kPM * kPL * 4);       // [128][L] indices
-        float* m_d = (float*)(aux + kPM * kPL * 8);             // [128] dropped
+        // anything pushed off the end raises `dropped`.  The K ring is idle now (every MMA
+        // that read it has completed: its tfull commit was waited on above); query tile qt
+        // uses its own part of it.
+        uint8_t* aq = aux + (size_t)qt * kPM * (kPL * 8 + 4);
+        float* m_s = (float*)aq;                               // [128][L] scores
+        uint32_t* m_i = (uint32_t*)(aq + kPM * kPL * 4);       // [128][L] indices
+        float* m_d = (float*)(aq + kPM * kPL * 8);             // [128] dropped
         if (half == 1) {
 #pragma unroll
             for (int j = 0; j < L; ++j) {
@@ -350,7 +356,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             }
             m_d[row] = dropped;
         }
-        named_bar_sync(1, 256);
+        named_bar_sync(1, kPEpi * 32);
         if (half == 0) {
             dropped = fmaxf(dropped, m_d[row]);
 #pragma unroll
@@ -371,7 +377,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 }
                 if (ci != kNoIndex) dropped = fmaxf(dropped, cs);
             }
-            const size_t prow = ((size_t)split * a.n_kv + kv) * a.n_qpad + (size_t)qtile * kPM + row;
+            const size_t prow = (size_t)split * a.n_kv * a.n_qpad + qrow;
             uint32_t* pi = a.part_idx + prow * kPL;
             float* ps = a.part_score + prow * kPL;
 #pragma unroll
@@ -662,9 +668,9 @@ size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
 PrefillGeom prefill_geom(const ScanArgs& a) {
     PrefillGeom g;
-    g.n_qpad = (a.n_q + kPM - 1) / kPM * kPM;
+    g.n_qpad = (a.n_q + kPM * kPQT - 1) / (kPM * kPQT) * (kPM * kPQT);
     g.tiles = (int)((a.count + kPN - 1) / kPN);
-    g.splits = choose_splits(g.n_qpad / kPM * a.n_kv, g.tiles);
+    g.splits = choose_splits(g.n_qpad / (kPM * kPQT) * a.n_kv, g.tiles);
     const size_t rows = (size_t)a.n_kv * g.n_qpad;
     g.hi_bytes = al256(rows * kPD * sizeof(__nv_bfloat16));
     g.mq_bytes = al256(rows * kPD * sizeof(float));
@@ -733,12 +739,15 @@ cudaError_t launch_prefill_tc(const ScanArgs& a, const CUtensorMap& kmap, void* 
     p.part_score = part_score;
     p.part_dropped = part_dropped;
     p.qhi = hi;
+    CUtensorMap qh;
+    if (!make_key_tensor_map(&qh, hi, kBF16, kPD, (uint64_t)a.n_kv * n_qpad, kPM))
+        return cudaErrorInvalidValue;
     p.null_epilogue = std::getenv("REATTN_K2_NULL_EPILOGUE") ? 1 : 0;
     p.no_mma = std::getenv("REATTN_K2_NO_MMA") ? 1 : 0;
-    dim3 grid(n_qpad / kPM, a.n_kv, g.splits);
+    dim3 grid(n_qpad / (kPM * kPQT), a.n_kv, g.splits);
     auto launch = [&](auto kernel) {
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmem);
-        kernel<<<grid, kPThreads, kPSmem, s>>>(kmap, p);
+        kernel<<<grid, kPThreads, kPSmem, s>>>(qh, kmap, p);
     };
     if (a.k <= 1)
         launch(prefill_scan_tc_kernel<1>);
