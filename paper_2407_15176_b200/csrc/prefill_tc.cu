@@ -83,6 +83,7 @@ struct PrefillArgs {
     const __nv_bfloat16* qhi;  // [n_kv][n_qpad][128] hi(mq), the MMA's A operand
     int null_epilogue;         // ablation (REATTN_K2_NULL_EPILOGUE): load + release only
     int no_mma;                // ablation (REATTN_K2_NO_MMA): the K-tile feed alone
+    int no_insert;             // ablation (REATTN_K2_NO_INSERT): admission test, no list work
     uint32_t* part_idx;     // [splits][n_kv][n_qpad][kPL], sorted by better(), kNoIndex-padded
     float* part_score;      // S_hi of those keys
     float* part_dropped;    // [splits][n_kv][n_qpad]
@@ -316,6 +317,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             // rare path, rolled: the warp walks the union of its rows' groups and re-reads
             // each group's 8 columns from TMEM (warp-uniform address, one row per lane)
             uint32_t ug = __reduce_or_sync(0xFFFFFFFFu, gm);
+            if (a.no_insert) ug = 0u;
             while (ug) {
                 const int g = __ffs(ug) - 1;
                 ug &= ug - 1u;
@@ -744,6 +746,7 @@ cudaError_t launch_prefill_tc(const ScanArgs& a, const CUtensorMap& kmap, void* 
         return cudaErrorInvalidValue;
     p.null_epilogue = std::getenv("REATTN_K2_NULL_EPILOGUE") ? 1 : 0;
     p.no_mma = std::getenv("REATTN_K2_NO_MMA") ? 1 : 0;
+    p.no_insert = std::getenv("REATTN_K2_NO_INSERT") ? 1 : 0;
     dim3 grid(n_qpad / (kPM * kPQT), a.n_kv, g.splits);
     auto launch = [&](auto kernel) {
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmem);
