@@ -41,7 +41,7 @@ WINDOW = 8192
 def load_traffic() -> dict | None:
     """dram read+write bytes per scan launch from the committed ncu --set full capture."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1b_decode_1m.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r1c_decode_1m.json")) as f:
             p = json.load(f)
         return {"bytes": int(p["traffic_bytes"]), "source": p["source"]}
     except Exception:
