@@ -395,6 +395,8 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
     }
     // merged candidate i = kv * kk + r goes straight to the select's shared candidates
     __shared__ SmallSelectSmem ssel;
+    constexpr int kMergeCache = 64;  // kv heads whose covering CTA range is cached
+    __shared__ uint32_t s_b0[kMergeCache], s_b1[kMergeCache];
     const int kk = (int)min((uint32_t)k, a.count);
     const int nwarps = C::THREADS / 32;
 #pragma unroll 1
@@ -476,17 +478,28 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
             topk_reset<KMAX>(ls, li);
             // CTAs whose (non-empty) tile range meets this head's tiles [h0, h1): contiguous
             const uint32_t h0 = (uint32_t)kv * a.tiles_per_head, h1 = h0 + a.tiles_per_head;
+            // (computed in the dry pass and kept in shared memory: the partition is fixed for
+            // the launch)
             uint32_t b0 = G, b1 = 0;
-            for (uint32_t c = lane; c < G; c += 32) {
-                const uint32_t cb = tbeg(c), ce = tbeg(c + 1);
-                const bool meets = cb < ce && cb < h1 && ce > h0;
-                if (meets) {
-                    b0 = min(b0, c);
-                    b1 = max(b1, c);
+            if (!dry && kv < kMergeCache) {
+                b0 = s_b0[kv];
+                b1 = s_b1[kv];
+            } else {
+                for (uint32_t c = lane; c < G; c += 32) {
+                    const uint32_t cb = tbeg(c), ce = tbeg(c + 1);
+                    const bool meets = cb < ce && cb < h1 && ce > h0;
+                    if (meets) {
+                        b0 = min(b0, c);
+                        b1 = max(b1, c);
+                    }
+                }
+                b0 = __reduce_min_sync(0xFFFFFFFFu, b0);
+                b1 = __reduce_max_sync(0xFFFFFFFFu, b1);
+                if (dry && kv < kMergeCache && lane == 0) {
+                    s_b0[kv] = b0;
+                    s_b1[kv] = b1;
                 }
             }
-            b0 = __reduce_min_sync(0xFFFFFFFFu, b0);
-            b1 = __reduce_max_sync(0xFFFFFFFFu, b1);
             const int n = b0 <= b1 ? (int)(b1 - b0 + 1) * k : 0;
             // all of a batch's loads are issued before any insert: one L2 round trip per batch
             for (int e0 = 0; e0 < n; e0 += 128) {
