@@ -186,9 +186,13 @@ def run_reference_arm(args) -> None:
     if rank != 0:
         return
     threads = args.cpu_threads or os.cpu_count() or 1
-    r = reference_cpu(max(1, args.steps_ref), 1, threads, CTX)
+    # a step is one attend_step call (1 token, 1 layer, the BASELINE workload); K steps run as
+    # ceil(K / threads) rounds of `threads` concurrent calls on the host cores, W likewise
+    rounds = max(1, -(-args.steps // threads))
+    warm_rounds = max(1, -(-args.warmup // threads))
+    r = reference_cpu(rounds, warm_rounds, threads, CTX)
     line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
-            "n_gpus": args.gpus, "steps": r["steps_timed"], "warmup": 1,
+            "n_gpus": args.gpus, "steps": r["steps_timed"], "warmup": warm_rounds * threads,
             "ms_per_step": r["value"] / 1000.0, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32 (bf16-valued cache upcast)",
             "data": "synthetic (splitmix64 uniform, bf16-rounded)",
