@@ -281,6 +281,7 @@ int enqueue_select_part(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache,
             io.span_e = sa.span_e;
             io.scope_src = sa.scope_src;
             io.hdr = sa.hdr;
+            io.table_local = P.fork ? 0 : 1;
         }
         int rc = enqueue_scan(ctx, P.scan, P.scan_ws, s, zero_ticket);
         if (rc) return rc;

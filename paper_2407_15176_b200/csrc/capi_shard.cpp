@@ -265,6 +265,7 @@ int reattn_shard_select(reattn_shard_plan* p) {
     io.span_e = p->span_e;
     io.scope_src = p->scope_global;
     io.hdr = p->hdr;
+    io.table_local = 1;  // the translation to local rows reads the whole global table
     s.rank = p->rank;
     s.world = p->world;
     s.ranges = p->ranges;

@@ -41,6 +41,9 @@ struct SmallSelectIO {
     uint32_t* span_e;
     uint32_t* scope_src;
     ScopeHeader* hdr;
+    // 0: the table's local rows are not needed (the decode fork attends the local window
+    // straight from the cache and the head launch reads rows [0, L' - n_local) only)
+    int table_local = 1;
 };
 constexpr uint32_t kSmallSelectMax = 32;
 

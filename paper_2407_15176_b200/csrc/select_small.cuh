@@ -234,6 +234,7 @@ __device__ __forceinline__ void small_select_scope_smem(const SmallSelectIO& io,
         }
         // local rows: 16-byte stores (when the table is 16-byte aligned) between scalar ends
         const uint32_t l0 = min(g + cov, L);
+        if (!io.table_local) return;
         const bool al = ((uintptr_t)io.scope_src & 15u) == 0;
         const uint32_t v0 = al ? min(L, (l0 + 3u) & ~3u) : L, v1 = max(v0, L & ~3u);
         for (uint32_t r = l0 + tid; r < v0; r += nthr)
