@@ -106,6 +106,8 @@ __device__ __forceinline__ uint32_t tile_begin(uint32_t b, uint32_t G, uint32_t 
     return T0 + (b - 1) * q + ((b - 1) * r) / (G - 1);
 }
 
+constexpr uint32_t kDryFlush = 0xFFFFFFFEu;  // flush() without slot writes (code warm-up)
+
 template <int KMAX>
 __device__ __forceinline__ void topk_reset(float (&ts)[KMAX], uint32_t (&ti)[KMAX]) {
 #pragma unroll
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
                     float bs = ls[0];
                     uint32_t bi = li[0];
                     warp_best(bs, bi);
-                    if (lane == 0) {
+                    if (lane == 0 && kv != kDryFlush) {
                         const size_t slot = ((size_t)kv * G + b) * KMAX + r;
                         a.slot_score[slot] = bs;
                         a.slot_idx[slot] = bi;
@@ -302,11 +304,17 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
             thr = -INFINITY;
         };
 
+        // One flush call site: a dry flush at the first tile (warms its code while the first
+        // TMA tiles land; it runs once per launch otherwise, so the slowest CTA's final flush
+        // would run cold, ~2 us), the head switches, and the final flush at t == t_end.
         uint32_t it = 0;
-        for (uint32_t t = t_begin; t < t_end; ++t, ++it) {
-            const uint32_t kv = t / a.tiles_per_head, j = t % a.tiles_per_head;
+        cur_kv = kDryFlush;
+        for (uint32_t t = t_begin;; ++t, ++it) {
+            const bool done = t >= t_end;
+            const uint32_t kv = done ? kNoIndex : t / a.tiles_per_head, j = t % a.tiles_per_head;
             if (kv != cur_kv) {
                 if (cur_kv != kNoIndex) flush(cur_kv);
+                if (done) break;
                 // group-mean query for this kv head (selection.hpp:250-258)
                 if (tid < C::D) {
                     const float inv = __fdiv_rn(1.0f, (float)a.group);
@@ -366,7 +374,6 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
                 issue(it + C::STAGES);
             }
         }
-        if (cur_kv != kNoIndex) flush(cur_kv);
     }
 
     // ===== cross-CTA merge and select by CTA 0 =====

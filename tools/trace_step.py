@@ -57,6 +57,9 @@ def main():
         print(f"--- rep {rep}  ctx {args.ctx}  scan CTAs {G}")
         print("K1 CTA start      ", summarize(rel(t[:G])))
         print("K1 CTA loop done  ", summarize(rel(t[512:512 + G])))
+        if any(t[1200:1200 + G]):
+            fl = [t[512 + c] - t[1200 + c] for c in range(G) if t[1200 + c]]
+            print("K1 final flush    ", summarize(fl))
         if args.slow:
             order = sorted(range(G), key=lambda c: -(t[512 + c] - t0))
             print("   slowest CTAs (cta, sm, done us):",
