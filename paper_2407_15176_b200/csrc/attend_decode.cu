@@ -864,31 +864,80 @@ namespace {
 // merge the ranks' partial rows of one q head (fixed source order): lane = 4 columns
 __global__ void __launch_bounds__(32) combine_sources_kernel(const AttnArgs a, const uint8_t* parts,
                                                             int n_src, size_t stride) {
+    // one launch per step after the partial-row all-gather, so cold: every header and acc
+    // row is loaded before use (lane s < n_src: source s's header; all lanes: 4 columns of
+    // up to 8 sources), f32 exp2 of the exact f64 differences, one f64 division
     if (a.hdr && a.hdr->error != 0) return;
     const int h = blockIdx.x, lane = threadIdx.x;
-    double M = -INFINITY;
-    for (int s = 0; s < n_src; ++s) {
-        const double* hd = (const double*)(parts + s * stride + (size_t)h * kBPartBytes);
+    auto row_of = [&](int src) { return parts + src * stride + (size_t)h * kBPartBytes; };
+    double hm = -INFINITY, ha = 0.0, hb = 0.0;
+    if (lane < n_src) {
+        const double* hd = (const double*)row_of(lane);
+        hm = hd[0];
+        ha = hd[1];
+        hb = hd[2];
+    }
+    constexpr int kPre = 8;
+    float4 v[kPre];
+#pragma unroll
+    for (int s = 0; s < kPre; ++s)
+        v[s] = s < n_src ? reinterpret_cast<const float4*>(row_of(s) + 32)[lane]
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    double M = ha > 0.0 ? hm : -INFINITY;
+    for (int s = lane + 32; s < n_src; s += 32) {  // more than 32 sources
+        const double* hd = (const double*)row_of(s);
         if (hd[1] > 0.0) M = fmax(M, hd[0]);
     }
-    double At = 0.0, Bt = 0.0, o[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int s = 0; s < n_src; ++s) {
-        const uint8_t* row = parts + s * stride + (size_t)h * kBPartBytes;
-        const double* hd = (const double*)row;
-        if (!(hd[1] > 0.0)) continue;
-        const double w = exp2(hd[0] - M);
-        At += hd[1] * w;
-        Bt += w * (hd[2] + (hd[0] - M) * hd[1]);
-        const float4 v = reinterpret_cast<const float4*>(row + 32)[lane];
-        o[0] = fma((double)v.x, w, o[0]);
-        o[1] = fma((double)v.y, w, o[1]);
-        o[2] = fma((double)v.z, w, o[2]);
-        o[3] = fma((double)v.w, w, o[3]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) M = fmax(M, __shfl_xor_sync(0xFFFFFFFFu, M, off));
+    auto wgt = [&](double pm, double pa) -> double {
+        return pa > 0.0 ? (double)exp2f((float)(pm - M)) : 0.0;
+    };
+    const double w0 = wgt(hm, ha);
+    double At = ha > 0.0 ? ha * w0 : 0.0, Bt = ha > 0.0 ? w0 * (hb + (hm - M) * ha) : 0.0;
+    for (int s = lane + 32; s < n_src; s += 32) {
+        const double* hd = (const double*)row_of(s);
+        if (hd[1] > 0.0) {
+            const double w = wgt(hd[0], hd[1]);
+            At += hd[1] * w;
+            Bt += w * (hd[2] + (hd[0] - M) * hd[1]);
+        }
     }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        At += __shfl_xor_sync(0xFFFFFFFFu, At, off);
+        Bt += __shfl_xor_sync(0xFFFFFFFFu, Bt, off);
+    }
+    double o[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int s0 = 0; s0 < n_src; s0 += kPre) {
+        if (s0 > 0) {
+#pragma unroll
+            for (int s = 0; s < kPre; ++s)
+                v[s] = s0 + s < n_src ? reinterpret_cast<const float4*>(row_of(s0 + s) + 32)[lane]
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int s = 0; s < kPre; ++s) {
+            const int src = s0 + s;
+            if (src >= n_src) break;
+            double w;
+            if (src < 32) {
+                w = __shfl_sync(0xFFFFFFFFu, w0, src);
+            } else {
+                const double* hd = (const double*)row_of(src);
+                w = wgt(hd[0], hd[1]);
+            }
+            o[0] = fma((double)v[s].x, w, o[0]);
+            o[1] = fma((double)v[s].y, w, o[1]);
+            o[2] = fma((double)v[s].z, w, o[2]);
+            o[3] = fma((double)v[s].w, w, o[3]);
+        }
+    }
+    const double inv = 1.0 / At;
     reinterpret_cast<float4*>(a.out + (size_t)h * kBD)[lane] =
-        make_float4((float)(o[0] / At), (float)(o[1] / At), (float)(o[2] / At), (float)(o[3] / At));
+        make_float4((float)(o[0] * inv), (float)(o[1] * inv), (float)(o[2] * inv), (float)(o[3] * inv));
     if (lane == 0) {
-        const double hh = log(At) - Bt * 0.69314718055994530942 / At;
+        const double hh = log(At) - Bt * 0.69314718055994530942 * inv;
         a.entropy[h] = hh < 0.0 ? 0.0 : hh;
     }
 }
