@@ -140,6 +140,11 @@ void plan_fork(reattn_ctx* ctx, StepPlan& P) {
     // (m * n_kv / hpc) whose local work (~0.8 us per 32-row chunk per CTA, measured) fits in
     // 70% of the scan (estimated at 5.8 TB/s over the middle's keys)
     int m = env == 1 ? 1 : 0, hpc = 1;
+    if (env == 1) {  // forced fork (tests): REATTN_FORK_HPC kv heads per local CTA
+        const char* h = std::getenv("REATTN_FORK_HPC");
+        const int hh = h ? std::atoi(h) : 1;
+        if (hh >= 1 && P.n_kv % (uint64_t)hh == 0) hpc = hh;
+    }
     if (!m) {
         const double t_scan = (double)P.middle * P.n_kv * P.d * 2 / 5.8e6;  // us
         const double chunks_per_head = (double)((n_local + 31) / 32);

@@ -406,6 +406,20 @@ def test_attend_step_decode_local_fork(ctx, total, monkeypatch):
     assert (plain.out - res.out).abs().max().item() <= ATTN_TOL
 
 
+@pytest.mark.parametrize("hpc", [2, 4, 8])
+def test_attend_step_decode_local_fork_heads_per_cta(ctx, hpc, monkeypatch):
+    """The planner's default at long contexts gives each local-window CTA several kv heads in
+    turn (1M: two); forced here at 131072 tokens for 2, 4 and 8 heads per CTA."""
+    monkeypatch.setenv("REATTN_FORK", "1")
+    monkeypatch.setenv("REATTN_FORK_HPC", str(hpc))
+    cfg = N.SelectionConfig()
+    res, out, st, spans = step_vs_oracle(ctx, 8, 32, 128, 131072, cfg, N.BF16, 90 + hpc, 8192)
+    assert res.stats.scope_len == st.scope_len
+    assert np.array_equal(res.spans[0], spans[0]) and np.array_equal(res.spans[1], spans[1])
+    assert np.abs(res.out.cpu().numpy() - out).max() <= ATTN_TOL
+    assert abs(res.stats.entropy_max - st.entropy_max) <= DEC_ENT_TOL
+
+
 @pytest.mark.slow
 def test_config5_geometry_4m_full_size(ctx):
     """BASELINE config 5 geometry at full size on one GPU: LLaMA-3.2-3B heads (24 q / 8 kv,
