@@ -1,8 +1,10 @@
 // K3 for large candidate sets (prefill: n_kv * n_q * k up to 131,072 and beyond): the
 // reference's tally + vote (selection.hpp:359-393) as device-wide passes, all on the
 // stream (graph-capturable), deterministic:
-//   1. sort (index << 32 | score key) ascending            -> runs of equal index
-//   2. run heads + exclusive scan -> run ids; run starts
+//   1. sort (index << 32 | score key) ascending by the index bits only (indices are middle
+//      coordinates: 18 bits at 256K, 3 radix passes instead of 8) -> runs of equal index
+//   2. run heads + exclusive scan -> run ids; run starts; per-run max score key (atomicMax:
+//      order-independent, so deterministic)
 //   3. one rank key per run: (votes << 32 | max score key), payload index
 //   4. stable descending sort by rank key (runs enter in index order, so equal keys keep
 //      index ascending: the reference's (votes desc, score desc, index asc))
@@ -22,7 +24,7 @@ namespace {
 
 struct LargeWs {
     unsigned long long *keys_in, *keys_out, *hi_in, *hi_out;
-    uint32_t *heads, *runid, *rstart, *idx_in, *idx_out;
+    uint32_t *heads, *runid, *rstart, *idx_in, *idx_out, *runmax;
     void* tmp;
     size_t tmp_bytes;
 };
@@ -57,6 +59,7 @@ LargeWs carve_ws(void* base, uint32_t n) {
     w.rstart = (uint32_t*)take(4ull * n);
     w.idx_in = (uint32_t*)take(4ull * n);
     w.idx_out = (uint32_t*)take(4ull * n);
+    w.runmax = (uint32_t*)take(4ull * n);
     w.tmp_bytes = cub_tmp_bytes(n);
     w.tmp = take(w.tmp_bytes);
     return w;
@@ -75,20 +78,25 @@ __global__ void k_heads(const unsigned long long* keys, uint32_t* heads, uint32_
         heads[p] = (p == 0 || (keys[p] >> 32) != (keys[p - 1] >> 32)) ? 1u : 0u;
 }
 
-__global__ void k_starts(const uint32_t* heads, const uint32_t* runid, uint32_t* rstart,
-                         uint32_t n) {
-    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
+__global__ void k_starts(const unsigned long long* keys, const uint32_t* heads, const uint32_t* runid,
+                         uint32_t* rstart, uint32_t* runmax, uint32_t n) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
         if (heads[p]) rstart[runid[p]] = p;
+        // the sort ordered the index bits only: a run's max score key by atomicMax (the
+        // run entries' order within the run is arbitrary)
+        atomicMax(&runmax[runid[p] + heads[p] - 1u], (uint32_t)(keys[p] & 0xFFFFFFFFull));
+    }
 }
 
 __global__ void k_rank(const unsigned long long* keys, const uint32_t* heads, const uint32_t* runid,
-                       const uint32_t* rstart, unsigned long long* hi, uint32_t* idx, uint32_t n) {
+                       const uint32_t* rstart, const uint32_t* runmax, unsigned long long* hi,
+                       uint32_t* idx, uint32_t n) {
     for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
         const bool last = p == n - 1 || (keys[p + 1] >> 32) != (keys[p] >> 32);
         if (last) {
             const uint32_t run = runid[p] + heads[p] - 1u;
             const uint32_t votes = p - rstart[run] + 1u;
-            hi[p] = ((unsigned long long)votes << 32) | (uint32_t)(keys[p] & 0xFFFFFFFFull);
+            hi[p] = ((unsigned long long)votes << 32) | runmax[run];
             idx[p] = (uint32_t)(keys[p] >> 32);
         } else {
             hi[p] = 0ull;  // not a run end: sorts after every real run (votes >= 1)
@@ -130,14 +138,23 @@ cudaError_t launch_vote_large(const SelectArgs& a, void* ws, cudaStream_t s) {
     const int g = grid_for(n);
     k_pack<<<g, 256, 0, s>>>(a, w.keys_in, n);
     size_t tb = w.tmp_bytes;
-    cudaError_t e = cub::DeviceRadixSort::SortKeys(w.tmp, tb, w.keys_in, w.keys_out, (int)n, 0, 64, s);
+    // index bits only (ties keep the input order: the radix sort is stable)
+    int ib = 32;
+    if (a.middle_len > 0) {
+        ib = 1;
+        while (ib < 32 && (1ull << ib) < (unsigned long long)a.middle_len) ++ib;
+    }
+    cudaError_t e = cub::DeviceRadixSort::SortKeys(w.tmp, tb, w.keys_in, w.keys_out, (int)n, 32,
+                                                   32 + ib, s);
     if (e != cudaSuccess) return e;
     k_heads<<<g, 256, 0, s>>>(w.keys_out, w.heads, n);
     tb = w.tmp_bytes;
     e = cub::DeviceScan::ExclusiveSum(w.tmp, tb, w.heads, w.runid, (int)n, s);
     if (e != cudaSuccess) return e;
-    k_starts<<<g, 256, 0, s>>>(w.heads, w.runid, w.rstart, n);
-    k_rank<<<g, 256, 0, s>>>(w.keys_out, w.heads, w.runid, w.rstart, w.hi_in, w.idx_in, n);
+    e = cudaMemsetAsync(w.runmax, 0, 4ull * n, s);
+    if (e != cudaSuccess) return e;
+    k_starts<<<g, 256, 0, s>>>(w.keys_out, w.heads, w.runid, w.rstart, w.runmax, n);
+    k_rank<<<g, 256, 0, s>>>(w.keys_out, w.heads, w.runid, w.rstart, w.runmax, w.hi_in, w.idx_in, n);
     tb = w.tmp_bytes;
     e = cub::DeviceRadixSort::SortPairsDescending(w.tmp, tb, w.hi_in, w.hi_out, w.idx_in,
                                                   w.idx_out, (int)n, 0, 64, s);
