@@ -406,6 +406,29 @@ def test_attend_step_decode_local_fork(ctx, total, monkeypatch):
     assert (plain.out - res.out).abs().max().item() <= ATTN_TOL
 
 
+def test_attend_step_decode_local_after_scan(ctx, monkeypatch):
+    """REATTN_FORK=2: the local window launched after the scan on every SM (a programmatic
+    dependent that completes only after the scan), then the head launch; plan and synchronous
+    step both match the oracle."""
+    monkeypatch.setenv("REATTN_FORK", "2")
+    cfg = N.SelectionConfig()
+    res, out, st, spans = step_vs_oracle(ctx, 8, 32, 128, 131072, cfg, N.BF16, 97, 8192)
+    assert res.stats.scope_len == st.scope_len
+    assert np.array_equal(res.spans[0], spans[0]) and np.array_equal(res.spans[1], spans[1])
+    assert np.abs(res.out.cpu().numpy() - out).max() <= ATTN_TOL
+    cache, _, _ = make_cache(ctx, 8, 128, 131072, cfg, N.BF16, 98)
+    rope = N.Rope(ctx, 128, 500000.0, 8192)
+    plan = N.Plan(ctx, cache, rope, 1, 32, cfg)
+    for s in range(3):
+        q = dev(synth.uniform(700 + s, 32 * 128).reshape(1, -1))
+        ref = N.attend_step(ctx, cache, rope, q, 32, cfg)
+        plan.q.copy_(q)
+        torch.cuda.synchronize()
+        plan.launch()
+        plan.stats()
+        assert torch.equal(plan.out, ref.out), s
+
+
 @pytest.mark.parametrize("hpc", [2, 4, 8])
 def test_attend_step_decode_local_fork_heads_per_cta(ctx, hpc, monkeypatch):
     """The planner's default at long contexts gives each local-window CTA several kv heads in
