@@ -253,7 +253,7 @@ int enqueue_select_part(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache,
     sa.span_e = P.span_e;
     sa.scope_src = P.scope_src;
     sa.hdr = P.hdr;
-    // Decode: <= 32 candidates -> vote/spans/scope run in the fast scan's last CTA (one
+    // Decode: <= 32 candidates -> vote/spans/scope run in the fast scan's merger CTA (one
     // launch fewer, no host round trip); otherwise the standalone select kernel.
     if (P.fork && !P.fk.post) {  // local window beside the scan (independent of the selection)
         AttnArgs la = step_attn_args(P, cache, rope, q_dev, out_dev);

@@ -31,7 +31,7 @@ enum {
 };
 
 // Inputs/outputs of the warp-level vote + spans + scope routine (select_small.cuh), used
-// standalone and fused into the K-scan's last CTA.
+// standalone and fused into the K-scan's merger CTA (CTA 0).
 struct SmallSelectIO {
     uint32_t k_prime, span_m, middle_len;
     int span_mode;
@@ -60,7 +60,7 @@ struct ScanArgs {
     int lanes;             // kLanesUnfused / kLanesFma
     uint32_t* idx_out;     // [n_kv][n_q][k]
     float* score_out;
-    // fast path only: run vote + spans + scope in the last CTA (n_kv * min(k, count) <= 32)
+    // fast path only: run vote + spans + scope in the merger CTA (n_kv * min(k, count) <= 32)
     int fuse_select = 0;
     SmallSelectIO sel = {};
     // fast path: keep the adaptive tile partition in the workspace (private, zero-initialised

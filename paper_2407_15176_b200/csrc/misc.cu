@@ -158,7 +158,7 @@ cudaError_t launch_entropy_stats(const double* entropy, int n_q, int n_head, dou
 // ---- timeline trace ------------------------------------------------------------------
 // Layout (uint64 words, %globaltimer ns):
 //   K1 scan (G CTAs):   [b] CTA start, [512 + b] CTA main loop done,
-//                       [1024] last CTA ticket, [1025] merge done, [1026] select done
+//                       [1024] merger CTA 0 sees every CTA done, [1025] merge done, [1026] select done
 //   K5 decode attention: [1536 + cta] CTA start (after griddepcontrol.wait),
 //                       [2560 + cta] CTA compute done (cta = blockIdx.y * gridDim.x + blockIdx.x,
 //                       + 512 for the local-window launch),

@@ -16,7 +16,8 @@
 // group-mean query in registers as 64 packed fp32x2 pairs and evaluates the 8-lane dot
 // with FMUL2/FADD2 (or FFMA2), then keeps a register top-k (the common reject is one
 // compare against a register threshold, as selection.hpp:230-236).  Per-CTA top-k go to a
-// slot array; the last CTA to finish (atomic ticket) merges them deterministically.
+// slot array; CTA 0 (scanning fewer tiles, its merge code warmed by a dry pass) waits for the
+// others' done count and merges them deterministically, then runs the fused vote/spans/scope.
 //
 // Generic path (any d / n_q / k): one CTA per (query, kv head) streaming the whole
 // middle, appending candidates above the running k-th key into a shared buffer and
