@@ -3,9 +3,9 @@
 K-scan HBM GB/s vs ~8 TB/s).
 
 A step is one single-layer ReAttention decode step (the reference's attend_step,
-engine.hpp:501-572) for one new token: group-mean q·Kᵀ scan + top-k over the middle
-(selection.hpp:275), vote + spans (:359-456), scope assembly (scope.hpp:248), RoPE at
-compact positions and finite-scope attention (attend.hpp:404) — LLaMA-3.1-8B head geometry
+engine.hpp:43-114) for one new token: group-mean q·Kᵀ scan + top-k over the middle
+(selection.hpp:168), vote + spans (selection.hpp:252-349), scope assembly (scope.hpp:37), RoPE at
+compact positions and finite-scope attention (attend.hpp:25) — LLaMA-3.1-8B head geometry
 (32 q / 8 kv heads, d=128), bf16 KV cache of 1,048,576 tokens, selection defaults
 (k=4, k'=127, m=32, g=32, local=4096), batch 1.  Inputs are synthetic (splitmix64 uniform
 [-1,1), the same generator on device and host) and resident in HBM; each step gets a fresh

@@ -1,5 +1,5 @@
 // Drop-in for reattn/engine.hpp: RunStats (engine.hpp:23-37), attend_step (engine.hpp:43-114)
-// and the generation Engine (engine.hpp:115-218).  attend_step -- selection gated as the
+// and the generation Engine (engine.hpp:119-216).  attend_step -- selection gated as the
 // reference, vote, spans, scope, RoPE at compact positions, attention -- is one device
 // pipeline (reattn_attend_step); the Engine runs every layer of the decoder on the device
 // (reattn_engine_*): projections, cache appends, attend_step, FFN, logits, greedy pick.
@@ -66,7 +66,7 @@ inline DenseMatrix attend_step(const DenseMatrix& q_pre, std::size_t n_head,
         spans_out->spans.clear();
         for (std::size_t i = 0; i < st.n_spans; ++i) spans_out->spans.push_back(Span{sb[i], se[i]});
     }
-    if (stats) {  // engine.hpp:522, :558-570 accumulation semantics
+    if (stats) {  // engine.hpp:64, :100-112 accumulation semantics
         if (!st.coverage_total) stats->coverage_total = false;
         stats->ood_positions += st.ood_positions;
         stats->entropy_max = std::max(stats->entropy_max, st.entropy_max);
@@ -79,7 +79,7 @@ inline DenseMatrix attend_step(const DenseMatrix& q_pre, std::size_t n_head,
     return out;
 }
 
-// Engine (engine.hpp:115-218): per-layer device caches, chunked prefill (first l_global +
+// Engine (engine.hpp:119-216): per-layer device caches, chunked prefill (first l_global +
 // l_local tokens, then l_chunk strides), greedy decode.  Holds `weights` by reference as the
 // reference does, plus its device copy.  caches() is not mirrored (the device caches are
 // reachable through reattn_engine_cache); everything else keeps the reference's semantics.

@@ -190,7 +190,7 @@ private:
     std::unique_ptr<reattn_cache, Del> dev_;
 };
 
-// RKVC snapshot container (reference kv_cache.hpp:121-209): magic "RKVC", u32 version,
+// RKVC snapshot container (reference kv_cache.hpp:120-209): magic "RKVC", u32 version,
 // u32 n_layers / n_kv_heads / d_head, per layer u64 {total, l_global, l_local_max} and raw
 // f32 key and value payloads, head-major.  Same signatures, messages and exception types;
 // the payloads stream straight between the file and device storage.

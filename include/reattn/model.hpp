@@ -1,7 +1,7 @@
 // Drop-in for reattn/model.hpp (reference model.hpp:19-341): the decoder's configuration and
 // host-side weights, with the reference's names, defaults and error messages.  The weight
-// stream of init_random (mt19937_64 Box-Muller, model.hpp:91-166) and the RATW file format
-// (model.hpp:224-339) are produced by the library (reattn_weights_*), so the C-ABI and this
+// stream of init_random (mt19937_64 Box-Muller, model.hpp:90-152) and the RATW file format
+// (model.hpp:204-339) are produced by the library (reattn_weights_*), so the C-ABI and this
 // header share one implementation; the host ModelWeights is a copy of the device tensors.
 #pragma once
 
@@ -81,7 +81,7 @@ struct ModelConfig {
     }
 };
 
-// model.hpp:64-86: projections input-major (d_in x d_out)
+// model.hpp:66-84: projections input-major (d_in x d_out)
 struct LayerWeights {
     DenseMatrix wq, wk, wv, wo, w_gate, w_up, w_down;
     std::vector<float> norm_attn, norm_ffn;
@@ -177,7 +177,7 @@ private:
 
 }  // namespace detail
 
-// init_random (model.hpp:127-166): the same pinned Gaussian stream, std 0.02, unit norms
+// init_random (model.hpp:120-152): the same pinned Gaussian stream, std 0.02, unit norms
 inline ModelWeights init_random(const ModelConfig& cfg, std::uint64_t seed) {
     const reattn_model_config c = cfg.to_c();
     reattn_weights* w = nullptr;
@@ -187,7 +187,7 @@ inline ModelWeights init_random(const ModelConfig& cfg, std::uint64_t seed) {
     return m;
 }
 
-// save_weights / load_weights (model.hpp:283-339): the RATW format, same messages
+// save_weights / load_weights (model.hpp:259-339): the RATW format, same messages
 inline void save_weights(const ModelWeights& w, const std::string& path) {
     detail::DeviceWeights d(detail::DeviceWeights::from_host(w));
     gpu::check(reattn_weights_save(gpu::context(), d.get(), path.c_str()));
@@ -199,7 +199,7 @@ inline ModelWeights load_weights(const std::string& path) {
     return detail::DeviceWeights(w).to_host();
 }
 
-// embed (model.hpp:201-211)
+// embed (model.hpp:181-190)
 inline DenseMatrix embed(std::span<const std::uint32_t> tokens, const ModelWeights& w) {
     DenseMatrix out(tokens.size(), w.config.d_model);
     for (std::size_t i = 0; i < tokens.size(); ++i) {
@@ -210,7 +210,7 @@ inline DenseMatrix embed(std::span<const std::uint32_t> tokens, const ModelWeigh
     return out;
 }
 
-// argmax_token (model.hpp:214-220): greedy pick, ties to the lowest token id
+// argmax_token (model.hpp:193-199): greedy pick, ties to the lowest token id
 inline std::uint32_t argmax_token(std::span<const float> logits) {
     if (logits.empty()) throw std::invalid_argument("empty logits");
     std::size_t best = 0;

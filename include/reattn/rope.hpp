@@ -1,6 +1,6 @@
 // Drop-in for reattn/rope.hpp (reference rope.hpp:19-79): rotary tables built exactly as
-// the reference (double -> float, :325-337) and resident on the device; rotations run on
-// the device (unfused fp32 ops, :353-356).
+// the reference (double -> float, :27-39) and resident on the device; rotations run on
+// the device (unfused fp32 ops, :55-58).
 #pragma once
 
 #include <cstddef>
@@ -52,7 +52,7 @@ private:
     std::shared_ptr<reattn_rope> dev_{nullptr, Del{}};
 };
 
-// rope.hpp:368-377
+// rope.hpp:70-79
 inline DenseMatrix rope_rotate(const DenseMatrix& vectors, std::span<const std::size_t> positions,
                                const RotaryTable& table) {
     if (vectors.cols != table.head_dim())

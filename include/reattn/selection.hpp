@@ -120,7 +120,7 @@ inline PerHeadTopk fused_topk_scores(const DenseMatrix& queries, std::size_t n_h
     return result;
 }
 
-// selection.hpp:275 signature: host views (copied to the device for the call).
+// selection.hpp:168 signature: host views (copied to the device for the call).
 inline PerHeadTopk fused_topk_scores(const DenseMatrix& queries, std::size_t n_heads,
                                      std::span<const KeySegmentView> middle,
                                      const SelectionConfig& cfg, ScratchMeter* meter = nullptr) {
@@ -153,7 +153,7 @@ inline void flatten(const PerHeadTopk& per_head, std::vector<std::uint32_t>& idx
 }
 }  // namespace detail
 
-// selection.hpp:359-383 (on the device).
+// selection.hpp:252-276 (on the device).
 inline std::vector<ScoredCandidate> tally_candidates(const PerHeadTopk& per_head) {
     std::vector<std::uint32_t> idx;
     std::vector<float> score;
@@ -174,7 +174,7 @@ inline std::vector<ScoredCandidate> tally_candidates(const PerHeadTopk& per_head
     return out;
 }
 
-// selection.hpp:385-393 (on the device).
+// selection.hpp:278-286 (on the device).
 inline std::vector<std::size_t> vote(const PerHeadTopk& per_head, std::size_t k_prime) {
     std::vector<std::size_t> winners;
     if (k_prime == 0) return winners;
@@ -214,7 +214,7 @@ struct SpanSet {
     bool empty() const { return spans.empty(); }
 };
 
-// selection.hpp:425-456 (on the device).
+// selection.hpp:318-349 (on the device).
 inline SpanSet expand_spans(std::span<const std::size_t> winners, std::size_t span_m,
                             std::size_t middle_len, SpanMode mode = SpanMode::Aligned) {
     SpanSet out;

@@ -62,7 +62,7 @@ typedef enum {
     REATTN_PREFILL_TENSOR = 3
 } reattn_prefill_mode;
 
-/* selection.hpp:127-152 SelectionConfig (tile_size only bounds the reference's CPU scratch;
+/* selection.hpp:20-45 SelectionConfig (tile_size only bounds the reference's CPU scratch;
  * it never changes results and is ignored here). */
 typedef struct {
     uint64_t k, k_prime, span_m, tile_size, l_global, l_local, l_chunk;
@@ -70,7 +70,7 @@ typedef struct {
     int32_t reserved;
 } reattn_selection_config;
 
-/* engine.hpp:481-495 RunStats (per step; the C++ shim folds it into the caller's RunStats) */
+/* engine.hpp:23-37 RunStats (per step; the C++ shim folds it into the caller's RunStats) */
 typedef struct {
     uint64_t max_position_used;
     uint64_t ood_positions;
@@ -121,7 +121,7 @@ int reattn_cache_info(const reattn_cache* cache, uint64_t* n_kv, uint64_t* d, ui
 void* reattn_cache_keys(const reattn_cache* cache);
 void* reattn_cache_values(const reattn_cache* cache);
 
-/* ---- RKVC cache snapshots: kv_cache.hpp:121-209 write/read_cache_snapshot ---------- */
+/* ---- RKVC cache snapshots: kv_cache.hpp:120-209 write/read_cache_snapshot ---------- */
 /* open: parses and validates the whole file in the reference's read order (messages and
  * error kinds as read_cache_snapshot: runtime_error -> ERUNTIME, the SegmentedKvCache
  * constructor's invalid_argument -> EINVAL).  load_layer: a new device cache of `dtype`
@@ -139,19 +139,19 @@ void reattn_snapshot_close(reattn_snapshot* snap);
 int reattn_snapshot_write(reattn_ctx* ctx, const char* path, const reattn_cache* const* layers,
                           uint32_t n_layers);
 
-/* ---- rotary table: rope.hpp:317-366 RotaryTable ----------------------------------- */
+/* ---- rotary table: rope.hpp:19-68 RotaryTable ----------------------------------- */
 int reattn_rope_create(reattn_ctx* ctx, uint64_t head_dim, double base, uint64_t max_position,
                        reattn_rope** out);
 void reattn_rope_destroy(reattn_rope* rope);
 /* host copies of the float tables [max_position][head_dim/2] (may be NULL) */
 int reattn_rope_tables_host(const reattn_rope* rope, float* cos_host, float* sin_host);
-/* rope.hpp:368-377 rope_rotate on device rows [n_rows][head_dim]; positions on the host.
+/* rope.hpp:70-79 rope_rotate on device rows [n_rows][head_dim]; positions on the host.
  * Synchronous.  Position >= max_position -> REATTN_ERANGE "position out of pretrained range". */
 int reattn_rope_rotate(reattn_ctx* ctx, const reattn_rope* rope, float* rows_dev,
                        const uint64_t* positions_host, uint64_t n_rows);
 
-/* ---- selection: selection.hpp:275-456 --------------------------------------------- */
-/* fused_topk_scores (selection.hpp:275).  q_dev: [n_q][n_heads*d] fp32.  keys_dev: head-major
+/* ---- selection: selection.hpp:168-349 --------------------------------------------- */
+/* fused_topk_scores (selection.hpp:168).  q_dev: [n_q][n_heads*d] fp32.  keys_dev: head-major
  * [n_kv][head_stride][d] of key_dtype, middle row 0 at row `row0` of every head, `count`
  * middle rows.  Outputs [n_kv][n_q][k] (score desc, index asc); *n_out = min(k, count).
  * *scratch_bytes = device workspace of the call (constant in `count`).  Synchronous. */
@@ -160,33 +160,33 @@ int reattn_fused_topk(reattn_ctx* ctx, const float* q_dev, uint64_t n_q, uint64_
                       uint64_t row0, uint64_t count, uint64_t d, uint64_t k,
                       uint32_t* idx_out_dev, float* score_out_dev, uint64_t* n_out,
                       uint64_t* scratch_bytes);
-/* tally_candidates + vote (selection.hpp:359-393) over a flat candidate list.  Synchronous. */
+/* tally_candidates + vote (selection.hpp:252-286) over a flat candidate list.  Synchronous. */
 int reattn_vote(reattn_ctx* ctx, const uint32_t* idx_dev, const float* score_dev, uint64_t n,
                 uint64_t k_prime, uint32_t* winners_dev, uint64_t* n_winners);
-/* tally_candidates (selection.hpp:359-383): every distinct index, ranked by (votes desc,
+/* tally_candidates (selection.hpp:252-276): every distinct index, ranked by (votes desc,
  * max score desc, index asc), with its votes and max score.  Synchronous. */
 int reattn_tally(reattn_ctx* ctx, const uint32_t* idx_dev, const float* score_dev, uint64_t n,
                  uint32_t* idx_out_dev, uint32_t* votes_out_dev, float* score_out_dev,
                  uint64_t* n_unique);
-/* expand_spans (selection.hpp:425-456).  Synchronous. */
+/* expand_spans (selection.hpp:318-349).  Synchronous. */
 int reattn_expand_spans(reattn_ctx* ctx, const uint32_t* winners_dev, uint64_t n, uint64_t span_m,
                         uint64_t middle_len, int span_mode, uint32_t* begin_dev,
                         uint32_t* end_dev, uint64_t* n_spans);
 
 /* ---- scope + attention ------------------------------------------------------------ */
-/* assemble_scope (scope.hpp:248-289).  Spans index the middle.  src_dev receives the
+/* assemble_scope (scope.hpp:37-78).  Spans index the middle.  src_dev receives the
  * scope-row -> cache-row table (capacity >= window); keys/values_out_dev (nullable)
  * receive fp32 [n_kv][L][d] copies.  Synchronous. */
 int reattn_assemble_scope(reattn_ctx* ctx, const reattn_cache* cache, const uint32_t* span_b_dev,
                           const uint32_t* span_e_dev, uint64_t n_spans, uint64_t window,
                           uint32_t* src_dev, float* keys_out_dev, float* values_out_dev,
                           uint64_t* length);
-/* attend (attend.hpp:404-456).  q [n_q][d], k [L][d], v [L][dv] fp32 device rows;
+/* attend (attend.hpp:25-77).  q [n_q][d], k [L][d], v [L][dv] fp32 device rows;
  * out [n_q][dv], entropy [n_q] (f64).  Synchronous. */
 int reattn_attend(reattn_ctx* ctx, const float* q_dev, uint64_t n_q, const float* k_dev,
                   const float* v_dev, uint64_t L, uint64_t d, uint64_t dv, int has_boundary,
                   uint64_t boundary, float* out_dev, double* entropy_dev);
-/* attend_step (engine.hpp:501-572): selection (gated as engine.hpp:516), scope, RoPE at
+/* attend_step (engine.hpp:43-114): selection (gated as engine.hpp:58), scope, RoPE at
  * compact positions, attention.  q_dev [n_q][n_head*d] pre-rotation; out_dev
  * [n_q][n_head*d].  span_b/e_host (nullable, capacity >= k_prime) receive the spans,
  * entropy_host (nullable, [n_q][n_head]) the row entropies.  Synchronous. */
@@ -223,7 +223,7 @@ int reattn_plan_info(const reattn_plan* plan, uint64_t* kernels_per_step,
 
 /* ---- batched decode (one graph over n_seq sequences with their own caches) ----------- */
 /* Batch > 1 is a reference non-goal; each sequence's result is exactly its own
- * attend_step (engine.hpp:501, n_q = 1).  bf16 decode with a middle: the scans run back to
+ * attend_step (engine.hpp:43, n_q = 1).  bf16 decode with a middle: the scans run back to
  * back while sequence b's attention runs beside scan b+1 on `side_sms` spare SMs.
  * q / out: [n_seq][n_head * d] fp32 on the device. */
 typedef struct reattn_batch_plan reattn_batch_plan;
@@ -273,7 +273,7 @@ int reattn_shard_combine(reattn_shard_plan* plan);  /* part_recv -> out */
 int reattn_shard_stats(reattn_shard_plan* plan, reattn_step_stats* stats, uint64_t* span_b_host,
                        uint64_t* span_e_host);
 
-/* ---- decoder model + generation engine (reference model.hpp, engine.hpp:115-218) ------
+/* ---- decoder model + generation engine (reference model.hpp, engine.hpp:119-216) ------
  * The toy decoder the reference's Engine drives: pre-norm blocks x += attn(norm(x)),
  * x += ffn(norm(x)), greedy decode.  Weights live on the device (fp32, the reference's
  * layout: projections input-major, d_in x d_out).  Projections run as fp32 GEMMs
@@ -287,7 +287,7 @@ typedef struct {
     int32_t reserved;
 } reattn_model_config;
 
-/* LayerWeights / ModelWeights tensors (model.hpp:67-86); layer is ignored for globals */
+/* LayerWeights / ModelWeights tensors (model.hpp:66-84); layer is ignored for globals */
 typedef enum {
     REATTN_W_EMBEDDING = 0, /* vocab x d_model */
     REATTN_W_WQ = 1,        /* d_model x n_head*d_head */
@@ -304,14 +304,14 @@ typedef enum {
 } reattn_weight_kind;
 
 typedef struct reattn_weights reattn_weights;
-/* ModelConfig::validate (model.hpp:50-60) */
+/* ModelConfig::validate (model.hpp:51-61) */
 int reattn_model_config_validate(reattn_ctx* ctx, const reattn_model_config* cfg);
 /* zero projections, unit norms */
 int reattn_weights_create(reattn_ctx* ctx, const reattn_model_config* cfg, reattn_weights** out);
-/* init_random (model.hpp:127-166): the same mt19937_64 Box-Muller stream, std 0.02 */
+/* init_random (model.hpp:120-152): the same mt19937_64 Box-Muller stream, std 0.02 */
 int reattn_weights_init_random(reattn_ctx* ctx, const reattn_model_config* cfg, uint64_t seed,
                                reattn_weights** out);
-/* RATW weight files (model.hpp:224-339 save_weights / load_weights) */
+/* RATW weight files (model.hpp:204-339 save_weights / load_weights) */
 int reattn_weights_load(reattn_ctx* ctx, const char* path, reattn_weights** out);
 int reattn_weights_save(reattn_ctx* ctx, const reattn_weights* w, const char* path);
 int reattn_weights_config(const reattn_weights* w, reattn_model_config* cfg);
@@ -338,27 +338,27 @@ typedef struct {
 } reattn_run_stats;
 
 typedef struct reattn_engine reattn_engine;
-/* Engine(weights, sel, mode) (engine.hpp:118-131): `w` must outlive the engine.
+/* Engine(weights, sel, mode) (engine.hpp:121-132): `w` must outlive the engine.
  * cache_dtype: REATTN_F32 (the reference's storage) or REATTN_BF16. */
 int reattn_engine_create(reattn_ctx* ctx, const reattn_weights* w, const reattn_selection_config* sel,
                          int mode, int cache_dtype, reattn_engine** out);
 int reattn_engine_reset(reattn_engine* e);
-/* prefill (engine.hpp:146-159): first l_global + l_local tokens, then l_chunk strides; the
+/* prefill (engine.hpp:147-160): first l_global + l_local tokens, then l_chunk strides; the
  * final chunk's hidden states stay on the device (rows -> *rows_out) */
 int reattn_engine_prefill(reattn_engine* e, const uint32_t* tokens_host, uint64_t n,
                           uint64_t* rows_out);
 /* the hidden states of the last forward block, rows x d_model */
 int reattn_engine_hidden(reattn_engine* e, float* host, uint64_t n);
-/* logits(hidden) (engine.hpp:176-179): final norm + lm_head of host rows x d_model */
+/* logits(hidden) (engine.hpp:177-179): final norm + lm_head of host rows x d_model */
 int reattn_engine_logits(reattn_engine* e, const float* hidden_host, uint64_t rows,
                          float* logits_host);
-/* decode_step (engine.hpp:162-173): one token in, greedy next token out */
+/* decode_step (engine.hpp:163-174): one token in, greedy next token out */
 int reattn_engine_decode_step(reattn_engine* e, uint32_t last_token, uint32_t* next_token);
 int reattn_engine_last_logits(reattn_engine* e, float* host, uint64_t n);
 int reattn_engine_stats(const reattn_engine* e, reattn_run_stats* st);
 /* decode_latency_ms entries (up to cap); *n = how many exist */
 int reattn_engine_decode_latencies(const reattn_engine* e, double* out, uint64_t cap, uint64_t* n);
-/* spans chosen by the layer's most recent attend_step (engine.hpp:185-186) */
+/* spans chosen by the layer's most recent attend_step (engine.hpp:183-184) */
 int reattn_engine_last_spans(const reattn_engine* e, uint64_t layer, uint64_t* begin,
                              uint64_t* end, uint64_t cap, uint64_t* n);
 const reattn_cache* reattn_engine_cache(const reattn_engine* e, uint64_t layer);

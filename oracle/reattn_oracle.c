@@ -42,7 +42,7 @@ double oracle_dot_f64(const float* a, const float* b, size_t d) {
     return ((l[0] + l[1]) + (l[2] + l[3])) + ((l[4] + l[5]) + (l[6] + l[7]));
 }
 
-/* ---- selection.hpp:246-263 ----------------------------------------------------- */
+/* ---- selection.hpp:139-156 ----------------------------------------------------- */
 void oracle_group_mean(const float* q, size_t n_q, size_t n_heads, size_t n_kv, size_t d,
                        float* mq) {
     const size_t group = n_heads / n_kv;
@@ -97,7 +97,7 @@ int oracle_topk(const float* q, size_t n_q, size_t n_heads, const float* const* 
     return ORACLE_OK;
 }
 
-/* ---- selection.hpp:359-393 ----------------------------------------------------- */
+/* ---- selection.hpp:252-286 ----------------------------------------------------- */
 typedef struct {
     uint64_t idx;
     float score;
@@ -142,7 +142,7 @@ int oracle_vote(const uint64_t* idx, const float* score, size_t n, size_t k_prim
     return ORACLE_OK;
 }
 
-/* ---- selection.hpp:425-456 ----------------------------------------------------- */
+/* ---- selection.hpp:318-349 ----------------------------------------------------- */
 typedef struct {
     uint64_t b, e;
 } span_t;
@@ -193,7 +193,7 @@ int oracle_expand_spans(const uint64_t* winners, size_t n, size_t span_m, size_t
     return ORACLE_OK;
 }
 
-/* ---- rope.hpp:319-358 ---------------------------------------------------------- */
+/* ---- rope.hpp:21-60 ---------------------------------------------------------- */
 void oracle_rope_table(size_t d, double base, size_t max_position, float* cos_t, float* sin_t) {
     const size_t half = d / 2;
     double* inv_freq = (double*)malloc(sizeof(double) * half);
@@ -216,7 +216,7 @@ void oracle_rotate_row(float* v, size_t d, const float* c, const float* s) {
     }
 }
 
-/* ---- attend.hpp:404-456 -------------------------------------------------------- */
+/* ---- attend.hpp:25-77 -------------------------------------------------------- */
 int oracle_attend(const float* q, size_t n_q, const float* k, const float* v, size_t L, size_t d,
                   size_t dv, int has_boundary, size_t boundary, float* out, double* entropy) {
     if (L == 0) return ORACLE_INVALID_ARGUMENT;
@@ -265,7 +265,7 @@ void oracle_cache_bounds(size_t total, size_t l_global, size_t l_local_max, size
     *local_start = total - (rest < l_local_max ? rest : l_local_max);
 }
 
-/* ---- scope.hpp:248-289 (index part) -------------------------------------------- */
+/* ---- scope.hpp:37-78 (index part) -------------------------------------------- */
 int oracle_scope_indices(size_t total, size_t l_global, size_t l_local_max, const uint64_t* sb,
                          const uint64_t* se, size_t n_spans, size_t pretrain_window,
                          uint64_t* source_indices, size_t* length) {
@@ -290,7 +290,7 @@ int oracle_scope_indices(size_t total, size_t l_global, size_t l_local_max, cons
     return ORACLE_OK;
 }
 
-/* ---- engine.hpp:501-572 -------------------------------------------------------- */
+/* ---- engine.hpp:43-114 -------------------------------------------------------- */
 int oracle_attend_step(const float* q_pre, size_t n_q, size_t n_head, const float* cache_k,
                        const float* cache_v, size_t n_kv, size_t d, size_t cap, size_t total,
                        const oracle_selection_config* cfg, const float* rope_cos,
@@ -314,7 +314,7 @@ int oracle_attend_step(const float* q_pre, size_t n_q, size_t n_head, const floa
         float* cs = (float*)malloc(sizeof(float) * n_kv * n_q * kk);
         size_t nk = 0;
         rc = oracle_topk(q_pre, n_q, n_head, heads, n_kv, middle_len, d, d, kk, ci, cs, &nk);
-        /* flatten [kv][q][0..nk) as tally_candidates does (selection.hpp:361-363) */
+        /* flatten [kv][q][0..nk) as tally_candidates does (selection.hpp:254-256) */
         size_t nf = 0;
         for (size_t l = 0; l < n_kv * n_q; ++l)
             for (size_t j = 0; j < nk; ++j) {

@@ -53,31 +53,31 @@ float oracle_dot_f32(const float* a, const float* b, size_t d);
 /* dense_matrix.hpp:59-74 */
 double oracle_dot_f64(const float* a, const float* b, size_t d);
 
-/* selection.hpp:246-263: out[n_q][n_kv*d], sequential fp32 add, times float(1/group). */
+/* selection.hpp:139-156: out[n_q][n_kv*d], sequential fp32 add, times float(1/group). */
 void oracle_group_mean(const float* q, size_t n_q, size_t n_heads, size_t n_kv, size_t d,
                        float* mq);
 
-/* selection.hpp:275-355 (fused_topk_scores).  keys[h] points at middle row 0 of kv head h,
+/* selection.hpp:168-248 (fused_topk_scores).  keys[h] points at middle row 0 of kv head h,
  * rows are row_stride floats apart.  Output [n_kv][n_q][k] (score desc, index asc);
  * *n_out = min(k, count).  Returns ORACLE_INVALID_ARGUMENT on head mismatch. */
 int oracle_topk(const float* q, size_t n_q, size_t n_heads, const float* const* keys, size_t n_kv,
                 size_t count, size_t d, size_t row_stride, size_t k, uint64_t* idx_out,
                 float* score_out, size_t* n_out);
 
-/* selection.hpp:359-393 (tally_candidates + vote) over a flat candidate list. */
+/* selection.hpp:252-286 (tally_candidates + vote) over a flat candidate list. */
 int oracle_vote(const uint64_t* idx, const float* score, size_t n, size_t k_prime,
                 uint64_t* winners, size_t* n_winners);
 
-/* selection.hpp:425-456.  Returns ORACLE_OUT_OF_RANGE for a winner >= middle_len. */
+/* selection.hpp:318-349.  Returns ORACLE_OUT_OF_RANGE for a winner >= middle_len. */
 int oracle_expand_spans(const uint64_t* winners, size_t n, size_t span_m, size_t middle_len,
                         int mode, uint64_t* begin, uint64_t* end, size_t* n_spans);
 
-/* rope.hpp:319-338: float tables [max_position][d/2] computed in double. */
+/* rope.hpp:21-40: float tables [max_position][d/2] computed in double. */
 void oracle_rope_table(size_t d, double base, size_t max_position, float* cos_t, float* sin_t);
-/* rope.hpp:347-358 (table row already selected). */
+/* rope.hpp:49-60 (table row already selected). */
 void oracle_rotate_row(float* v, size_t d, const float* c, const float* s);
 
-/* attend.hpp:404-456.  q [n_q][d], k [L][d], v [L][dv]; entropy [n_q]. */
+/* attend.hpp:25-77.  q [n_q][d], k [L][d], v [L][dv]; entropy [n_q]. */
 int oracle_attend(const float* q, size_t n_q, const float* k, const float* v, size_t L, size_t d,
                   size_t dv, int has_boundary, size_t boundary, float* out, double* entropy);
 
@@ -85,13 +85,13 @@ int oracle_attend(const float* q, size_t n_q, const float* k, const float* v, si
 void oracle_cache_bounds(size_t total, size_t l_global, size_t l_local_max, size_t* global_end,
                          size_t* local_start);
 
-/* scope.hpp:248-289: source indices for global ++ spans ++ local.  Returns
+/* scope.hpp:37-78: source indices for global ++ spans ++ local.  Returns
  * ORACLE_OUT_OF_RANGE (span outside middle) or ORACLE_INVALID_ARGUMENT (> window). */
 int oracle_scope_indices(size_t total, size_t l_global, size_t l_local_max, const uint64_t* sb,
                          const uint64_t* se, size_t n_spans, size_t pretrain_window,
                          uint64_t* source_indices, size_t* length);
 
-/* engine.hpp:501-572 (attend_step).  Cache K/V are head-major [n_kv][cap][d] fp32 with
+/* engine.hpp:43-114 (attend_step).  Cache K/V are head-major [n_kv][cap][d] fp32 with
  * `total` rows appended.  out [n_q][n_head*d].  spans_begin/end sized >= k_prime (may be
  * NULL).  rope tables from oracle_rope_table(d, base, max_position). */
 int oracle_attend_step(const float* q_pre, size_t n_q, size_t n_head, const float* cache_k,

@@ -73,7 +73,7 @@ extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
 
-// selection.hpp:275 fused_topk_scores.  keys[h]: middle rows of head h (row_stride == d).
+// selection.hpp:168 fused_topk_scores.  keys[h]: middle rows of head h (row_stride == d).
 int ref_fused_topk(const float* q, std::size_t n_q, std::size_t n_heads, const float* const* keys,
                    std::size_t n_kv, std::size_t count, std::size_t d, std::size_t k,
                    std::size_t tile, uint64_t* idx, float* score, std::size_t* n_out,
@@ -109,7 +109,7 @@ int ref_naive_topk(const float* q, std::size_t n_q, std::size_t n_heads, const f
     })
 }
 
-// selection.hpp:385 vote over one flat list (one (kv,q) slot per candidate is enough:
+// selection.hpp:278 vote over one flat list (one (kv,q) slot per candidate is enough:
 // tally_candidates flattens anyway).
 int ref_vote(const uint64_t* idx, const float* score, std::size_t n, std::size_t k_prime,
              uint64_t* winners, std::size_t* n_winners) {
@@ -122,7 +122,7 @@ int ref_vote(const uint64_t* idx, const float* score, std::size_t n, std::size_t
     })
 }
 
-// selection.hpp:425 expand_spans.
+// selection.hpp:318 expand_spans.
 int ref_expand_spans(const uint64_t* winners, std::size_t n, std::size_t span_m,
                      std::size_t middle_len, int mode, uint64_t* begin, uint64_t* end,
                      std::size_t* n_spans) {
@@ -138,7 +138,7 @@ int ref_expand_spans(const uint64_t* winners, std::size_t n, std::size_t span_m,
     })
 }
 
-// rope.hpp:319 RotaryTable tables.
+// rope.hpp:21 RotaryTable tables.
 int ref_rope_table(std::size_t d, double base, std::size_t max_position, float* cos_t,
                    float* sin_t) {
     REF_TRY({
@@ -150,7 +150,7 @@ int ref_rope_table(std::size_t d, double base, std::size_t max_position, float* 
     })
 }
 
-// attend.hpp:404 attend.
+// attend.hpp:25 attend.
 int ref_attend(const float* q, std::size_t n_q, const float* k, const float* v, std::size_t L,
                std::size_t d, std::size_t dv, int has_boundary, std::size_t boundary, float* out,
                double* entropy) {
@@ -164,7 +164,7 @@ int ref_attend(const float* q, std::size_t n_q, const float* k, const float* v, 
     })
 }
 
-// Cache boundary + assemble_scope source indices (kv_cache.hpp:54-68, scope.hpp:248).
+// Cache boundary + assemble_scope source indices (kv_cache.hpp:54-68, scope.hpp:37).
 int ref_scope_indices(std::size_t total, std::size_t l_global, std::size_t l_local_max,
                       const uint64_t* sb, const uint64_t* se, std::size_t n_spans,
                       std::size_t window, uint64_t* src, std::size_t* length) {
@@ -252,7 +252,7 @@ struct RefStats {
     std::size_t entropy_rows, scope_len_max, scope_len, n_spans, coverage;
 };
 
-// engine.hpp:501 attend_step on a ref cache.
+// engine.hpp:43 attend_step on a ref cache.
 int ref_attend_step(void* cache_p, const float* q_pre, std::size_t n_q, std::size_t n_head,
                     std::size_t k, std::size_t k_prime, std::size_t span_m, std::size_t tile,
                     std::size_t l_global, std::size_t l_local, std::size_t l_chunk, int span_mode,
@@ -352,7 +352,7 @@ int ref_fma_selfcheck(std::size_t d, std::size_t trials, std::size_t* unfused_hi
 }
 
 
-// ---- decoder model / engine (model.hpp, engine.hpp:115-218, full_attention.hpp) ----
+// ---- decoder model / engine (model.hpp, engine.hpp:119-216, full_attention.hpp) ----
 // cfg8: n_layer, n_head, n_kv_head, d_model, d_head, d_ff, vocab_size, pretrain_window
 void* ref_model_init(const uint64_t* cfg8, double rope_base, int mode, uint64_t seed) {
     try {

@@ -1,11 +1,11 @@
 // K4+K5 — scope gather + RoPE at compact positions + finite-scope attention, split-KV.
 //
 // Restates (reference /root/reference/proj/include/reattn/):
-//   assemble_scope copies        scope.hpp:274-287  (fused: rows are gathered straight from
+//   assemble_scope copies        scope.hpp:63-76  (fused: rows are gathered straight from
 //                                                    the cache through the scope table)
-//   RotaryTable::rotate_row      rope.hpp:347-358   (keys at compact i, queries at L'-n_q+i,
-//                                                    engine.hpp:536-551; unfused fp32 ops)
-//   attend                       attend.hpp:404-456 (scale 1/sqrt(d) in double, causal
+//   RotaryTable::rotate_row      rope.hpp:49-60   (keys at compact i, queries at L'-n_q+i,
+//                                                    engine.hpp:78-93; unfused fp32 ops)
+//   attend                       attend.hpp:25-77 (scale 1/sqrt(d) in double, causal
 //                                                    boundary, f64 state incl. the entropy
 //                                                    numerator B = sum (s-m) e^{s-m})
 //   dot_f64                      dense_matrix.hpp:59-74 (exact 8-lane order, so logits are
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kAttnThreads) attend_split_kernel(const AttnLa
     const uint32_t boundary = a.boundary_is_tail ? (L - (uint32_t)a.n_q) : a.boundary_host;
     const double scale = 1.0 / sqrt((double)d);
 
-    // ---- queries: rotated at L'-n_q+i (engine.hpp:546-551) ----
+    // ---- queries: rotated at L'-n_q+i (engine.hpp:88-93) ----
     const int half = d / 2;
     for (int e = tid; e < QR * d; e += kAttnThreads) {
         const int r = e / d, c = e % d;
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kAttnThreads) attend_split_kernel(const AttnLa
         const uint32_t k0 = key_begin + (uint32_t)ch * kAttnSplit;
         if (k0 >= L) break;
         const int nk = (int)min((uint32_t)kAttnSplit, L - k0);
-        // ---- gather K (rotated at compact position) and V rows (scope.hpp:282-286) ----
+        // ---- gather K (rotated at compact position) and V rows (scope.hpp:71-75) ----
         for (int e = tid; e < nk * d; e += kAttnThreads) {
             const int r = e / d, c = e % d;
             const uint32_t sr = k0 + r;
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kAttnThreads) attend_split_kernel(const AttnLa
             vs[r * VS + c] = ld_elem<KT>(a.v_base, ((size_t)kv * a.head_stride + cr) * dv + c);
         }
         __syncthreads();
-        // ---- logits: exact dot_f64 lane order, times 1/sqrt(d) (attend.hpp:430) ----
+        // ---- logits: exact dot_f64 lane order, times 1/sqrt(d) (attend.hpp:51) ----
         for (int e = tid; e < QR * kAttnSplit; e += kAttnThreads) {
             const int r = e / kAttnSplit, j = e % kAttnSplit;
             const int i = qblk * P.qb + r / G;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kAttnThreads) attend_split_kernel(const AttnLa
             lg[r * kAttnSplit + j] = s;
         }
         __syncthreads();
-        // ---- online softmax update per row (attend.hpp:432-447) ----
+        // ---- online softmax update per row (attend.hpp:53-68) ----
         for (int r = warp; r < QR; r += nwarps) {
             double mx = -INFINITY;
             for (int j = lane; j < nk; j += 32) mx = fmax(mx, lg[r * kAttnSplit + j]);
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kAttnThreads) attend_split_kernel(const AttnLa
             for (int c = lane; c < dv; c += 32) acc[r * dv + c] *= rs;
         }
         __syncthreads();
-        // ---- value accumulation (attend.hpp:436, :445) ----
+        // ---- value accumulation (attend.hpp:57, :66) ----
         for (int e = tid; e < QR * dv; e += kAttnThreads) {
             const int r = e / dv, c = e % dv;
             const double* w = lg + r * kAttnSplit;
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(128) attend_combine_kernel(const AttnLaunch P)
 //   values   lane owns 4 output columns; p_j broadcast by shuffle, V rows read as float4
 // No block barrier between the phases: the only __syncthreads guard the K/V staging.
 // Numerics: fp32 logits and accumulation inside a CTA, f64 across chunks and CTAs; the
-// reference's f64 attend (attend.hpp:404-456) is matched to ~1e-6 max-abs (the north_star
+// reference's f64 attend (attend.hpp:25-77) is matched to ~1e-6 max-abs (the north_star
 // fp32 bar is 1e-5).  Partials (log2-unit m, A, B in f64 + fp32 acc) are merged by
 // attend_decode_combine.
 constexpr int kDecChunk = 32;
@@ -409,7 +409,7 @@ struct ChunkRegs {
             }
         }
     }
-    // rotate K at its compact position (rope.hpp:347-358, unfused fp32) and stage to smem
+    // rotate K at its compact position (rope.hpp:49-60, unfused fp32) and stage to smem
     __device__ __forceinline__ void store(const AttnArgs& a, int nk, float* ks, float* vs,
                                           uint8_t* rowok) const {
         const int tid = threadIdx.x;
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(kDecThreads) attend_decode_kernel(const Decode
 
     ChunkRegs<KT> cur;
     cur.load(a, kv, key_begin, (int)min((uint32_t)kDecChunk, key_end - key_begin));
-    // queries of the group, rotated at L'-1 (engine.hpp:546-551), times log2(e)/sqrt(d)
+    // queries of the group, rotated at L'-1 (engine.hpp:88-93), times log2(e)/sqrt(d)
     const uint32_t qpos = L - 1u;
     for (int e = tid; e < G * half; e += kDecThreads) {
         const int g = e / half, j = e % half;
@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(kDecThreads) attend_decode_kernel(const Decode
                 d3 = __fmaf_rn(q4.w, k4.w, d3);
             }
             const float s = key_ok ? (d0 + d1) + (d2 + d3) : -INFINITY;
-            // ---- online softmax (attend.hpp:432-447) ----
+            // ---- online softmax (attend.hpp:53-68) ----
             float mc = s;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xFFFFFFFFu, mc, off));

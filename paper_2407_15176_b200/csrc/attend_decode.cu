@@ -1,11 +1,11 @@
 // K5 (decode) — finite-scope flash-decode with a deep bulk-copy ring and a fused combine.
 //
 // Restates, for n_q == 1 and a bf16 cache (d == dv == 128):
-//   assemble_scope copies   scope.hpp:274-287   rows fetched straight from the cache through
+//   assemble_scope copies   scope.hpp:63-76   rows fetched straight from the cache through
 //                                               the device scope table (no assembled copy)
-//   RotaryTable::rotate_row rope.hpp:347-358    keys at compact i, the query at L'-1
-//                                               (engine.hpp:536-551), unfused fp32 ops
-//   attend                  attend.hpp:404-456  scale 1/sqrt(d), row entropy ln A - B/A
+//   RotaryTable::rotate_row rope.hpp:49-60    keys at compact i, the query at L'-1
+//                                               (engine.hpp:78-93), unfused fp32 ops
+//   attend                  attend.hpp:25-77  scale 1/sqrt(d), row entropy ln A - B/A
 //
 // The decode scope is small (L' ~ 5K rows, 21 MB of K+V at 1M context) and the step is
 // latency-bound unless a large part of it is in flight at once, so the layout is:
@@ -99,7 +99,7 @@ __device__ __forceinline__ float bx_ex2(float x) {
 __device__ __forceinline__ int rot_idx4(int r, int i) { return r * (kBD / 4) + (i ^ (r & 7)); }
 
 // The last part of a kv head merges the parts' partial rows in part order and writes the
-// output and entropy (attend.hpp:448-455 normalisation), or one merged partial row per head.
+// output and entropy (attend.hpp:69-76 normalisation), or one merged partial row per head.
 // `role` is the calling warp's compute-warp index.  This code runs once per launch and
 // would run from a cold instruction cache (~0.5 us per fetch miss: ~9 us measured for the
 // merge), so every CTA first runs it dry (global and shared stores predicated off) while it
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
     } else {
         // ===== compute: group gi = warps 4gi .. 4gi+3 takes chunks gi, gi+4, ... =====
         const int gi = warp >> 2, gw = warp & 3, gt = tid & 127;
-        // the group's queries, rotated at L'-1 (engine.hpp:546-551), times log2(e)/sqrt(d)
+        // the group's queries, rotated at L'-1 (engine.hpp:88-93), times log2(e)/sqrt(d)
         const uint32_t qpos = L - 1u;  // kModeLocal: L == n_local (shifted frame)
         for (int e = tid; e < G * (kBD / 2); e += kBCompute) {
             const int g = e / (kBD / 2), j = e % (kBD / 2);
@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
             geom(c_begin + c, k0, nk);
             uint8_t* st = stages + (size_t)s * kBStageBytes;
             float4* kr4 = (float4*)(st + 2 * kBKVBytes);  // rotated keys over the cos/sin rows
-            // ---- rotate the chunk's keys once (rope.hpp:347-358): read all, then write ----
+            // ---- rotate the chunk's keys once (rope.hpp:49-60): read all, then write ----
             {
                 const uint32_t* kw = (const uint32_t*)st;  // bf16 pairs
                 const float* cs = (const float*)(st + 2 * kBKVBytes);
@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
         }
         }  // G > 4
     }
-    // ---- the last part of this kv head merges (attend.hpp:448-455 normalisation) ----
+    // ---- the last part of this kv head merges (attend.hpp:69-76 normalisation) ----
     if (B.trace && tid == 0 && cta_id < 1024) B.trace[2560 + cta_id] = globaltimer();
     if (local) {
         if (hh + 1 < hpc) continue;

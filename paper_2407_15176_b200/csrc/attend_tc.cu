@@ -1,8 +1,8 @@
 // K6 — prefill finite-scope attention on the 5th-gen tensor cores (tcgen05 + TMEM).
 //
 // Same contract as the f64 CUDA-core kernel in attend.cu for a prefill block.  It restates
-// the reference's attend (attend.hpp:404-456) over the assembled scope
-// (scope.hpp:274-287, engine.hpp:536-551): keys rotated at compact position j, queries at
+// the reference's attend (attend.hpp:25-77) over the assembled scope
+// (scope.hpp:63-76, engine.hpp:78-93): keys rotated at compact position j, queries at
 // L'-n_q+i, scale 1/sqrt(d), causal boundary L'-n_q, output acc/denom and row entropy
 // ln A - B/A.  It is opt-in with the prefill scan (reattn_ctx_set_prefill(TENSOR)).
 //
@@ -81,7 +81,7 @@ __device__ __forceinline__ float bf16_lo_half(uint32_t w) { return __uint_as_flo
 __device__ __forceinline__ float bf16_hi_half(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
 // rotate the interleaved pair (x, y) by (c, s) with the reference's unfused fp32 ops
-// (rope.hpp:347-358)
+// (rope.hpp:49-60)
 __device__ __forceinline__ void rotate_pair(float x, float y, float c, float s, float& rx, float& ry) {
     rx = __fsub_rn(__fmul_rn(x, c), __fmul_rn(y, s));
     ry = __fadd_rn(__fmul_rn(x, s), __fmul_rn(y, c));
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
         float* s_max = (float*)(o_done + 2);        // [2 parity][2 half][128]
         double* s_ab = (double*)(s_max + 2 * 2 * kFM);  // [2 half][128][2]
-        // query: rotated at L'-n_q+i (engine.hpp:546-551), times log2(e)/sqrt(d) (so S is
+        // query: rotated at L'-n_q+i (engine.hpp:88-93), times log2(e)/sqrt(d) (so S is
         // already in log2 units), split into bf16 hi + lo; this half writes pairs [32h, 32h+32)
         {
             const float* qrow = a.q + (size_t)(live ? i : 0) * a.q_row_stride + (size_t)h * kFD;

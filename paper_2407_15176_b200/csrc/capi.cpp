@@ -608,7 +608,7 @@ int reattn_rope_create(reattn_ctx* ctx, uint64_t head_dim, double base, uint64_t
     r->max_position = max_position;
     r->base = base;
     const uint64_t half = head_dim / 2;
-    // table constant: float(cos/sin(p * base^(-2i/d))) computed in double (rope.hpp:325-337)
+    // table constant: float(cos/sin(p * base^(-2i/d))) computed in double (rope.hpp:27-39)
     std::vector<double> inv(half);
     for (uint64_t i = 0; i < half; ++i) inv[i] = std::pow(base, -2.0 * double(i) / double(head_dim));
     r->cos_h.resize(max_position * half);

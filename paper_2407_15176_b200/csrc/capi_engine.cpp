@@ -1,8 +1,8 @@
-// Decoder model + generation engine on the device: the reference's Engine (engine.hpp:115-218)
-// around the attend_step pipeline, with ModelWeights (model.hpp:62-86), init_random
-// (model.hpp:127-166) and the RATW weight file (model.hpp:224-339).
+// Decoder model + generation engine on the device: the reference's Engine (engine.hpp:119-216)
+// around the attend_step pipeline, with ModelWeights (model.hpp:66-84), init_random
+// (model.hpp:120-152) and the RATW weight file (model.hpp:204-339).
 //
-// forward_block per layer (engine.hpp:190-205), all on ctx->stream:
+// forward_block per layer (engine.hpp:191-205), all on ctx->stream:
 //   h = rmsnorm(x, norm_attn)                       rmsnorm_kernel (mean square in double)
 //   q = h·wq                                        fp32 GEMM
 //   cache.append(h·wk, h·wv)                        fp32 cache: one strided-batched GEMM per
@@ -77,7 +77,7 @@ void shape_of(const reattn_model_config& c, int kind, uint64_t* rows, uint64_t* 
     *cols = k;
 }
 
-// ModelConfig::validate (model.hpp:50-60), same messages
+// ModelConfig::validate (model.hpp:51-61), same messages
 int validate_model(reattn_ctx* ctx, const reattn_model_config& c) {
     if (c.n_layer == 0 || c.n_head == 0 || c.n_kv_head == 0 || c.d_model == 0 || c.d_head == 0 ||
         c.d_ff == 0 || c.vocab_size == 0 || c.pretrain_window == 0)
@@ -128,7 +128,7 @@ int alloc_weights(reattn_ctx* ctx, const reattn_model_config& c, std::unique_ptr
         shape_of(c, kind, &r, &k);
         CU(ctx, cudaMalloc(p, std::max<uint64_t>(r * k, 1) * sizeof(float)));
         if (kind >= REATTN_W_NORM_ATTN && kind <= REATTN_W_NORM_FINAL) {
-            std::vector<float> ones(k, 1.0f);  // model.hpp:157-163: unit norm weights
+            std::vector<float> ones(k, 1.0f);  // model.hpp:120-152: unit norm weights
             CU(ctx, cudaMemcpy(*p, ones.data(), k * sizeof(float), cudaMemcpyHostToDevice));
         } else {
             CU(ctx, cudaMemset(*p, 0, r * k * sizeof(float)));
@@ -143,7 +143,7 @@ int alloc_weights(reattn_ctx* ctx, const reattn_model_config& c, std::unique_ptr
     return REATTN_OK;
 }
 
-// detail::GaussianSource (model.hpp:91-123): Box-Muller over mt19937_64, the spare sine draw
+// detail::GaussianSource (model.hpp:90-116): Box-Muller over mt19937_64, the spare sine draw
 // returned on the next call.  Restated from the published recipe; the sequence is pinned.
 struct Gaussian {
     std::mt19937_64 rng;
@@ -166,7 +166,7 @@ struct Gaussian {
     }
 };
 
-// ---- RATW file helpers (model.hpp:226-281) ----
+// ---- RATW file helpers (model.hpp:222-257) ----
 constexpr char kMagic[4] = {'R', 'A', 'T', 'W'};
 constexpr uint32_t kVersion = 1;
 
@@ -289,7 +289,7 @@ int append_kv(reattn_engine* e, reattn_cache* cache, uint64_t layer, uint64_t ro
     return reattn_cache_append(ctx, cache, e->kb, e->vb, rows, 1);
 }
 
-// engine.hpp:190-205 over e->x (rows x d_model)
+// engine.hpp:191-205 over e->x (rows x d_model)
 int forward_block(reattn_engine* e, uint64_t rows) {
     reattn_ctx* ctx = e->ctx;
     const reattn_model_config& c = e->w->cfg;
@@ -309,7 +309,7 @@ int forward_block(reattn_engine* e, uint64_t rows) {
         auto& sp = e->spans[l];
         sp.clear();
         for (uint64_t i = 0; i < st.n_spans; ++i) sp.emplace_back(e->sb[i], e->se[i]);
-        reattn_run_stats& S = e->stats;  // engine.hpp:522, :558-570 accumulation
+        reattn_run_stats& S = e->stats;  // engine.hpp:64, :100-112 accumulation
         if (!st.coverage_total) S.coverage_total = 0;
         S.ood_positions += st.ood_positions;
         S.entropy_max = std::max(S.entropy_max, st.entropy_max);
@@ -385,7 +385,7 @@ int reattn_weights_init_random(reattn_ctx* ctx, const reattn_model_config* cfg, 
         CU(ctx, cudaMemcpy(dst, buf.data(), buf.size() * sizeof(float), cudaMemcpyHostToDevice));
         return REATTN_OK;
     };
-    // model.hpp:133-165 draw order: embedding, per layer wq wk wv wo w_gate w_up w_down, lm_head
+    // model.hpp:120-152 draw order: embedding, per layer wq wk wv wo w_gate w_up w_down, lm_head
     if ((rc = fill(w->global[REATTN_W_EMBEDDING], REATTN_W_EMBEDDING))) return rc;
     for (uint64_t l = 0; l < cfg->n_layer; ++l)
         for (int kind = REATTN_W_WQ; kind <= REATTN_W_DOWN; ++kind)
@@ -434,7 +434,7 @@ int reattn_weights_download(reattn_ctx* ctx, const reattn_weights* w, int kind, 
 
 void reattn_weights_destroy(reattn_weights* w) { delete w; }
 
-// save_weights (model.hpp:283-309)
+// save_weights (model.hpp:259-290)
 int reattn_weights_save(reattn_ctx* ctx, const reattn_weights* w, const char* path) {
     const std::string p = path ? path : "";
     File f(std::fopen(p.c_str(), "wb"));
@@ -475,7 +475,7 @@ int reattn_weights_save(reattn_ctx* ctx, const reattn_weights* w, const char* pa
     return REATTN_OK;
 }
 
-// load_weights (model.hpp:311-339): read order, checks and messages as the reference
+// load_weights (model.hpp:292-339): read order, checks and messages as the reference
 int reattn_weights_load(reattn_ctx* ctx, const char* path, reattn_weights** out) {
     *out = nullptr;
     const std::string p = path ? path : "";
@@ -569,7 +569,7 @@ int reattn_engine_create(reattn_ctx* ctx, const reattn_weights* w, const reattn_
     return REATTN_OK;
 }
 
-// reset (engine.hpp:133-142): fresh caches, spans and stats
+// reset (engine.hpp:134-143): fresh caches, spans and stats
 int reattn_engine_reset(reattn_engine* e) {
     reattn_ctx* ctx = e->ctx;
     const reattn_model_config& c = e->w->cfg;
@@ -600,7 +600,7 @@ int reattn_engine_prefill(reattn_engine* e, const uint32_t* tokens, uint64_t n, 
     uint64_t pos = 0;
     while (pos < n) {
         const uint64_t len = pos == 0 ? first : std::min<uint64_t>(e->sel.l_chunk, n - pos);
-        if ((rc = check_tokens(ctx, c, tokens + pos, len))) return rc;  // embed (model.hpp:205-206)
+        if ((rc = check_tokens(ctx, c, tokens + pos, len))) return rc;  // embed (model.hpp:181-190)
         CU(ctx, cudaMemcpyAsync(e->tok, tokens + pos, len * sizeof(uint32_t), cudaMemcpyHostToDevice,
                                 ctx->stream));
         CU(ctx, launch_embed(e->tok, len, cslot(e->w, REATTN_W_EMBEDDING, 0), c.d_model, e->x, ctx->stream));

@@ -1,4 +1,4 @@
-// RKVC cache snapshots (reference kv_cache.hpp:121-209, write_cache_snapshot /
+// RKVC cache snapshots (reference kv_cache.hpp:120-209, write_cache_snapshot /
 // read_cache_snapshot) straight to and from device caches.
 //
 // Format: magic "RKVC", u32 version (1), u32 n_layers, n_kv_heads, d_head; per layer u64
@@ -9,7 +9,7 @@
 //
 // Validation follows the reference's read order and messages: bad magic / version, per
 // layer the three u64 fields ("cache snapshot truncated at <field>"), the SegmentedKvCache
-// constructor checks (kv_cache.hpp:41-47), then the key and value payloads.
+// constructor checks (kv_cache.hpp:40-51), then the key and value payloads.
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -98,7 +98,7 @@ int reattn_snapshot_open(reattn_ctx* ctx, const char* path, reattn_snapshot** ou
                                std::string("cache snapshot truncated at ") + names[i]);
             pos += 8;
         }
-        // SegmentedKvCache(n_kv, d, l_global, l_local_max) (kv_cache.hpp:41-47)
+        // SegmentedKvCache(n_kv, d, l_global, l_local_max) (kv_cache.hpp:40-51)
         if (s->n_kv == 0 || s->d == 0)
             return set_err(ctx, REATTN_EINVAL, "cache needs at least one head and a positive head dim");
         if (L.l_local_max == 0) return set_err(ctx, REATTN_EINVAL, "l_local_max must be positive");

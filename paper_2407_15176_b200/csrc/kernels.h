@@ -47,7 +47,7 @@ struct SmallSelectIO {
 };
 constexpr uint32_t kSmallSelectMax = 32;
 
-// ---- K1: decode scan + top-k (selection.hpp:275-355) -------------------------------
+// ---- K1: decode scan + top-k (selection.hpp:168-248) -------------------------------
 struct ScanArgs {
     const float* q;        // [n_q][n_heads*d] pre-rotation queries
     int n_q, n_heads, n_kv, d;
@@ -94,7 +94,7 @@ cudaError_t launch_prefill_tc(const ScanArgs& a, const CUtensorMap& kmap, void* 
 constexpr int kGenericMaxK = 7936;
 cudaError_t launch_scan_generic(const ScanArgs& a, cudaStream_t s);
 
-// ---- K3: vote + spans + scope (selection.hpp:359-456, scope.hpp:248-289) ----------
+// ---- K3: vote + spans + scope (selection.hpp:252-349, scope.hpp:37-78) ----------
 struct SelectArgs {
     const uint32_t* cand_idx;  // n_lists lists of list_len valid entries, list stride
     const float* cand_score;
@@ -129,7 +129,7 @@ cudaError_t launch_select(const SelectArgs& a, cudaStream_t s);
 size_t vote_large_workspace(uint32_t n_cand);
 cudaError_t launch_vote_large(const SelectArgs& a, void* workspace, cudaStream_t s);
 
-// ---- K4+K5: gather + RoPE + finite-scope attention (attend.hpp, engine.hpp:529-565)
+// ---- K4+K5: gather + RoPE + finite-scope attention (attend.hpp, engine.hpp:71-107)
 struct AttnArgs {
     const float* q;          // query rows, q_row_stride floats apart; head h at +h*d
     uint64_t q_row_stride;
@@ -236,7 +236,7 @@ cudaError_t launch_decode_combine_sources(const AttnArgs& a, const uint8_t* part
 cudaError_t launch_cache_append(const float* src, void* dst, int dtype, uint64_t rows,
                                 uint64_t n_kv, uint64_t d, uint64_t head_stride, uint64_t row0,
                                 cudaStream_t s);
-// scope gather to fp32 [n_kv][L][d] (assemble_scope's copies, scope.hpp:274-287).
+// scope gather to fp32 [n_kv][L][d] (assemble_scope's copies, scope.hpp:63-76).
 cudaError_t launch_gather(const void* base, int dtype, uint64_t n_kv, uint64_t d,
                           uint64_t head_stride, const uint32_t* src, uint32_t L, float* out,
                           cudaStream_t s);
@@ -244,7 +244,7 @@ cudaError_t launch_rope_rotate(float* rows, const uint32_t* pos, uint64_t n_rows
                                const float* cos_t, const float* sin_t, cudaStream_t s);
 cudaError_t launch_synth_uniform(void* dst, int dtype, uint64_t n, uint64_t seed,
                                  uint64_t offset, cudaStream_t s);
-// entropy stats reduction in the reference's order (engine.hpp:558-564): for h, for i.
+// entropy stats reduction in the reference's order (engine.hpp:100-106): for h, for i.
 cudaError_t launch_entropy_stats(const double* entropy, int n_q, int n_head, double* out2,
                                  cudaStream_t s);
 

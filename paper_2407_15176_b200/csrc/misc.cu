@@ -1,7 +1,7 @@
 // Small supporting kernels: cache append (kv_cache.hpp:54-68 layout change), scope gather
-// for the assemble_scope API (scope.hpp:274-287), RoPE on device rows (rope.hpp:347-358),
+// for the assemble_scope API (scope.hpp:63-76), RoPE on device rows (rope.hpp:49-60),
 // the deterministic synthetic-input generator used by tests and bench.py, and the RunStats
-// entropy reduction in the reference's accumulation order (engine.hpp:558-564).
+// entropy reduction in the reference's accumulation order (engine.hpp:100-106).
 #include <cstdlib>
 
 #include "common.cuh"

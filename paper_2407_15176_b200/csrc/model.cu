@@ -1,7 +1,7 @@
 // Elementwise / row kernels of the decoder block around attend_step (reference model.hpp):
-// token embedding gather (model.hpp:201-211), RMS normalisation with the mean square carried
-// in double (model.hpp:177-189), the gated-FFN activation silu(g) * u (model.hpp:192-199)
-// and the greedy argmax with ties to the lowest token id (model.hpp:214-220).  The
+// token embedding gather (model.hpp:181-190), RMS normalisation with the mean square carried
+// in double (model.hpp:155-167), the gated-FFN activation silu(g) * u (model.hpp:170-178)
+// and the greedy argmax with ties to the lowest token id (model.hpp:193-199).  The
 // projections themselves are plain fp32 GEMMs (cuBLAS, capi_engine.cpp).
 #include <cstdint>
 
@@ -27,7 +27,7 @@ __global__ void embed_kernel(const uint32_t* __restrict__ tokens, const float* _
 }
 
 // rmsnorm: ms = sum(double(x)^2) / cols; inv = float(1 / sqrt(ms + 1e-5)); out = x * inv * w
-// (two fp32 multiplies in that order, as model.hpp:186).  One CTA of 256 threads per row.
+// (two fp32 multiplies in that order, as model.hpp:160-163).  One CTA of 256 threads per row.
 __global__ void rmsnorm_kernel(const float* __restrict__ x, uint64_t cols,
                                const float* __restrict__ w, float* __restrict__ out) {
     __shared__ double part[8];
@@ -50,7 +50,7 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, uint64_t cols,
         dst[c] = __fmul_rn(__fmul_rn(src[c], inv), w[c]);
 }
 
-// gate[i] = gate[i] / (1 + exp(-gate[i])) * up[i]   (model.hpp:195-197, fp32 throughout)
+// gate[i] = gate[i] / (1 + exp(-gate[i])) * up[i]   (model.hpp:170-178, fp32 throughout)
 __global__ void silu_mul_kernel(float* __restrict__ gate, const float* __restrict__ up, uint64_t n) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -59,7 +59,7 @@ __global__ void silu_mul_kernel(float* __restrict__ gate, const float* __restric
     }
 }
 
-// argmax over one row, ties to the lowest index (strict > in index order, model.hpp:217-218)
+// argmax over one row, ties to the lowest index (strict > in index order, model.hpp:193-199)
 __global__ void argmax_kernel(const float* __restrict__ v, uint64_t n, uint32_t* __restrict__ out) {
     __shared__ float bs[32];
     __shared__ uint32_t bi[32];

@@ -1,12 +1,12 @@
 // K2 — prefill score scan on the 5th-gen tensor cores (tcgen05 + TMEM), fused exact top-k.
 //
-// Same contract as fused_topk_scores (reference selection.hpp:275-355) for a prefill chunk
+// Same contract as fused_topk_scores (reference selection.hpp:168-248) for a prefill chunk
 // (n_q up to l_chunk = 4096 queries): per (kv head, query) the top-k of mq · k over the
 // middle, ties to the lower index -- with the reference's own fp32 scores, bit for bit.
 //
 //   1. S_hi[q, j] = hi(mq)[q, :] · K[j, :] on tcgen05.mma (kind::f16: bf16 operands, fp32
 //      accumulators in TMEM; 128 queries x 128 keys per tile, d = 128), ONE pass.  mq is the
-//      exact fp32 group mean (selection.hpp:250-258), hi(mq) its bf16 rounding.
+//      exact fp32 group mean (selection.hpp:143-151), hi(mq) its bf16 rounding.
 //   2. Error bound per query row: |dot_f32(mq, k_j) - S_hi[j]| < delta :=
 //      (||mq - hi(mq)||_1 + 2^-12 ||mq||_1) * max|k|.  The first term is the exact rounding
 //      residual of the operand; 2^-12 covers both fp32 accumulations (the reference's 8-lane
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
 }
 
-// group-mean query (selection.hpp:250-258, exact fp32): the fp32 row, its bf16 rounding (the
+// group-mean query (selection.hpp:143-151, exact fp32): the fp32 row, its bf16 rounding (the
 // MMA operand) and delta / max|k| = ||mq - hi||_1 + 2^-12 ||mq||_1 per row (one warp per row)
 __global__ void prefill_prep_kernel(const float* q, int n_q, int n_heads, int n_kv, int n_qpad,
                                     __nv_bfloat16* hi, float* mq, float* dl) {

@@ -1,7 +1,7 @@
 // K1 — position-agnostic q·Kᵀ scan fused with an exact running top-k.
 //
-// Restates reattn::fused_topk_scores (reference selection.hpp:275-355) on sm_100a:
-//   * group-mean query per KV head (selection.hpp:246-263): sequential fp32 adds, then
+// Restates reattn::fused_topk_scores (reference selection.hpp:168-248) on sm_100a:
+//   * group-mean query per KV head (selection.hpp:139-156): sequential fp32 adds, then
 //     multiply by float(1/group);
 //   * score = dot_f32 (dense_matrix.hpp:41-56): eight lanes over elements j, j+8, ...,
 //     then ((l0+l1)+(l2+l3))+((l4+l5)+(l6+l7)).  The lane update is emulated exactly in
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
             if (kv != cur_kv) {
                 if (cur_kv != kNoIndex) flush(cur_kv);
                 if (done) break;
-                // group-mean query for this kv head (selection.hpp:250-258)
+                // group-mean query for this kv head (selection.hpp:143-151)
                 if (tid < C::D) {
                     const float inv = __fdiv_rn(1.0f, (float)a.group);
                     float acc = 0.0f;
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
             }
         }
         if (a.fuse_select) {
-            // vote + spans + scope on the merged candidates [kv][0..kk) (selection.hpp:359-456)
+            // vote + spans + scope on the merged candidates [kv][0..kk) (selection.hpp:252-349)
             const int n = a.n_kv * kk;  // <= 32 (fuse_select condition)
             if (tid == 0) ssel.vmask = n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u);
             __syncthreads();
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(256) scan_generic_kernel(const GenArgs a) {
     __shared__ unsigned int s_nb;
     const int qi = blockIdx.x, kv = blockIdx.y, tid = threadIdx.x;
     const int d = a.d;
-    // group-mean query (selection.hpp:250-258)
+    // group-mean query (selection.hpp:143-151)
     const float inv = __fdiv_rn(1.0f, (float)a.group);
     for (int c = tid; c < d; c += blockDim.x) {
         float acc = 0.0f;

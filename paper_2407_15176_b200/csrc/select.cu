@@ -1,10 +1,10 @@
 // K3 — vote, span expansion and scope assembly in one single-CTA kernel.
 //
 // Restates (reference /root/reference/proj/include/reattn/):
-//   tally_candidates + vote     selection.hpp:359-393  (votes desc, max score desc, idx asc)
-//   expand_spans                selection.hpp:425-456  (aligned / centered, sorted ascending)
-//   assemble_scope (indices)    scope.hpp:248-289      (global ++ spans ++ local, window check)
-//   the n_q <= L' check         engine.hpp:527
+//   tally_candidates + vote     selection.hpp:252-286  (votes desc, max score desc, idx asc)
+//   expand_spans                selection.hpp:318-349  (aligned / centered, sorted ascending)
+//   assemble_scope (indices)    scope.hpp:37-78      (global ++ spans ++ local, window check)
+//   the n_q <= L' check         engine.hpp:69
 // The output is a device ScopeHeader + a scope-row -> cache-row table, so the attention
 // kernels run straight after it without a host round trip.  Ranking uses bitonic sorts of
 // packed keys in shared memory: exact and deterministic (no atomics-order dependence).
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectArgs a)
     const bool have_spans = a.span_b_in != nullptr;
     const bool have_winners = a.winners_in != nullptr;
     if (!have_spans && !have_winners && a.k_prime > 0 && n > 0) {
-        // ---- tally (selection.hpp:359-383) ----
+        // ---- tally (selection.hpp:252-276) ----
         const int NS = pow2_at_least((int)n, 32);
         unsigned long long* key = ssm;                     // [NS]  idx<<32 | score key
         uint32_t* head = (uint32_t*)(key + NS);            // [NS]
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectArgs a)
             ridx[r] = 0xFFFFFFFFu;
         }
         __syncthreads();
-        // ---- rank (selection.hpp:376-381): votes desc, score desc, index asc ----
+        // ---- rank (selection.hpp:269-274): votes desc, score desc, index asc ----
         bitonic_pairs<true>(rhi, ridx, NR);
         const uint32_t nw = min(a.k_prime, U);
         for (uint32_t j = tid; j < nw; j += blockDim.x) {
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectArgs a)
     }
 
     const uint32_t nw = s_nw;
-    // ---- spans (selection.hpp:425-456) ----
+    // ---- spans (selection.hpp:318-349) ----
     {
         const int NP = pow2_at_least((int)max(nw, a.n_spans_in), 32);
         spans_sm = ssm;  // reuse
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectArgs a)
     }
     const uint32_t ns = s_ns, cov = s_cov;
 
-    // ---- scope (scope.hpp:255-272, engine.hpp:527) ----
+    // ---- scope (scope.hpp:44-61, engine.hpp:69) ----
     if (a.build_scope) {
         if (tid == 0) {
             const uint64_t L = (uint64_t)a.g_end + cov + (a.total - a.l_start);

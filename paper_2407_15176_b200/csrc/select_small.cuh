@@ -1,7 +1,7 @@
 // Block-level vote + span expansion + scope table for <= 32 candidates (decode: n_kv*k).
 //
-// Same contract as select_kernel (select.cu), restating selection.hpp:359-456 and
-// scope.hpp:248-289.  Every ranking is an all-pairs count, spread over the block as S = 8
+// Same contract as select_kernel (select.cu), restating selection.hpp:252-349 and
+// scope.hpp:37-78.  Every ranking is an all-pairs count, spread over the block as S = 8
 // (256+ threads) or 4 (128 threads) threads per candidate (32/S comparisons each, then one
 // redux.sync over the S), so each
 // phase is a handful of shared-memory loads and one reduction; the phases are separated by
@@ -52,7 +52,7 @@ __device__ __forceinline__ void small_select_scope_smem(const SmallSelectIO& io,
     const uint32_t vmask = io.k_prime > 0 ? sm.vmask : 0u;
     const bool vi = act && ((vmask >> i) & 1u);
     const uint32_t idx_i = sm.idx[i];
-    // ---- tally: votes, max score, first occurrence (selection.hpp:359-375) ----
+    // ---- tally: votes, max score, first occurrence (selection.hpp:252-268) ----
     uint32_t votes = 0, mk = 0, later = 0;
     if (vi) {
 #pragma unroll
@@ -81,7 +81,7 @@ __device__ __forceinline__ void small_select_scope_smem(const SmallSelectIO& io,
     if (act && s == 0 && rep) atomicOr(&sm.repmask, 1u << i);
     const uint32_t U = (uint32_t)__syncthreads_count(act && s == 0 && rep);
     if (trace && tid == 0) trace[1030] = globaltimer();
-    // ---- rank: votes desc, max score desc, index asc (selection.hpp:376-381) ----
+    // ---- rank: votes desc, max score desc, index asc (selection.hpp:269-274) ----
     const uint32_t repmask = sm.repmask;
     uint32_t rank = 0;
     if (rep) {
@@ -99,7 +99,7 @@ __device__ __forceinline__ void small_select_scope_smem(const SmallSelectIO& io,
     const uint32_t nw = min(io.k_prime, U);
     const bool win = rep && rank < nw;
     if (win && s == 0 && io.winners && !dry) io.winners[rank] = idx_i;
-    // ---- spans (selection.hpp:425-456) ----
+    // ---- spans (selection.hpp:318-349) ----
     const bool do_spans = io.middle_len > 0;
     uint32_t sb = 0, se = 0;
     bool bad = false;
@@ -216,7 +216,7 @@ __device__ __forceinline__ void small_select_scope_smem(const SmallSelectIO& io,
         }
     }
     __syncthreads();
-    // ---- scope table: global ++ spans ++ local (scope.hpp:265-272) ----
+    // ---- scope table: global ++ spans ++ local (scope.hpp:54-61) ----
     // dry (instruction-cache warming, see scan_topk.cu): the same loops over few rows, stores
     // predicated off
     if ((sm.err == 0 || dry) && io.scope_src) {

@@ -6,7 +6,7 @@
 // (kv head, query), the exact top-k of its shard; top-k of the union of all ranks' lists
 // under (score desc, index asc) is the exact global top-k (selection.hpp:81-135 ordering),
 // so after an all-gather every rank merges identically and continues with the reference's
-// vote / expand_spans / assemble_scope (selection.hpp:359-456, scope.hpp:248-272).
+// vote / expand_spans / assemble_scope (selection.hpp:252-349, scope.hpp:37-61).
 // The scope table is translated to this rank's local cache rows (replicated global and local
 // rows exist on every rank; a middle row only at its owner), and the rank's share of the
 // attention is written as ShardRanges: rank 0 the global rows, every rank the span rows of

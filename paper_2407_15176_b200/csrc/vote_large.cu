@@ -1,5 +1,5 @@
 // K3 for large candidate sets (prefill: n_kv * n_q * k up to 131,072 and beyond): the
-// reference's tally + vote (selection.hpp:359-393) as device-wide passes, all on the
+// reference's tally + vote (selection.hpp:252-286) as device-wide passes, all on the
 // stream (graph-capturable), deterministic:
 //   1. sort (index << 32 | score key) ascending by the index bits only (indices are middle
 //      coordinates: 18 bits at 256K, 3 radix passes instead of 8) -> runs of equal index

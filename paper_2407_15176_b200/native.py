@@ -29,7 +29,7 @@ vp = C.c_void_p
 
 
 class SelectionConfig(C.Structure):
-    """reattn::SelectionConfig (selection.hpp:127-152); defaults are the reference's."""
+    """reattn::SelectionConfig (selection.hpp:20-45); defaults are the reference's."""
 
     _fields_ = [("k", u64), ("k_prime", u64), ("span_m", u64), ("tile_size", u64),
                 ("l_global", u64), ("l_local", u64), ("l_chunk", u64), ("span_mode", C.c_int32),
@@ -323,7 +323,7 @@ class Context:
 
 
 class Snapshot:
-    """RKVC cache snapshot (kv_cache.hpp:121-209) read into device caches."""
+    """RKVC cache snapshot (kv_cache.hpp:120-209) read into device caches."""
 
     def __init__(self, ctx: Context, path: str):
         self.ctx = ctx
@@ -365,7 +365,7 @@ def write_snapshot(ctx: Context, path: str, caches) -> None:
 
 
 class Rope:
-    """reattn::RotaryTable (rope.hpp:317-366) with its tables resident on the device."""
+    """reattn::RotaryTable (rope.hpp:19-68) with its tables resident on the device."""
 
     def __init__(self, ctx: Context, head_dim: int, base: float, max_position: int):
         self.ctx = ctx
@@ -484,7 +484,7 @@ class StepResult:
 
 def attend_step(ctx: Context, cache: Cache, rope: Rope, q, n_head: int, cfg: SelectionConfig,
                 mode: int = MODE_REATTENTION, out=None) -> StepResult:
-    """engine.hpp:501 attend_step on device tensors.  q: [n_q, n_head*d] fp32 (cuda)."""
+    """engine.hpp:43 attend_step on device tensors.  q: [n_q, n_head*d] fp32 (cuda)."""
     import numpy as np
     import torch
     n_q = q.shape[0]
@@ -597,7 +597,7 @@ class BatchPlan:
 
 
 class Weights:
-    """reattn::ModelWeights (model.hpp:62-86) resident on the device (fp32)."""
+    """reattn::ModelWeights (model.hpp:66-84) resident on the device (fp32)."""
 
     def __init__(self, ctx: Context, h):
         self.ctx, self.h = ctx, h
@@ -607,7 +607,7 @@ class Weights:
 
     @classmethod
     def init_random(cls, ctx: Context, cfg: ModelConfig, seed: int) -> "Weights":
-        """init_random (model.hpp:127-166): the reference's pinned Gaussian stream."""
+        """init_random (model.hpp:120-152): the reference's pinned Gaussian stream."""
         h = vp()
         ctx.check(ctx.lib.reattn_weights_init_random(ctx.h, C.byref(cfg), seed, C.byref(h)))
         return cls(ctx, h)
@@ -620,7 +620,7 @@ class Weights:
 
     @classmethod
     def load(cls, ctx: Context, path: str) -> "Weights":
-        """load_weights (model.hpp:311-339), RATW file."""
+        """load_weights (model.hpp:292-339), RATW file."""
         h = vp()
         ctx.check(ctx.lib.reattn_weights_load(ctx.h, os.fsencode(path), C.byref(h)))
         return cls(ctx, h)
@@ -654,7 +654,7 @@ class Weights:
 
 
 class Engine:
-    """reattn::Engine (engine.hpp:115-218) on the device: per-layer caches, chunked
+    """reattn::Engine (engine.hpp:119-216) on the device: per-layer caches, chunked
     prefill, greedy decode.  `weights` must outlive the engine (held here)."""
 
     def __init__(self, ctx: Context, weights: Weights, sel: SelectionConfig,

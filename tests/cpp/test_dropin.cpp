@@ -316,7 +316,7 @@ static void test_rope_attend() {
         CHECK(throws<std::invalid_argument>([] { RotaryTable(7, 10000.0, 16); }), "odd dim");
         CHECK(throws<std::invalid_argument>([] { RotaryTable(8, -1.0, 16); }), "base");
         CHECK(throws<std::invalid_argument>([] { RotaryTable(8, 10000.0, 0); }), "max pos");
-        // table bytes equal the oracle restatement (rope.hpp:325-337)
+        // table bytes equal the oracle restatement (rope.hpp:27-39)
         const RotaryTable t4(128, 500000.0, 8192);
         std::vector<float> oc(8192 * 64), os(8192 * 64);
         oracle_rope_table(128, 500000.0, 8192, oc.data(), os.data());
@@ -406,7 +406,7 @@ static void test_attend_step() {
               "attend_step total=%zu n_q=%zu md=%g dH=%g L=%zu/%zu", c.total, c.n_q, md,
               std::abs(st.entropy_max - ost.entropy_max), st.scope_len_max, ost.scope_len);
     }
-    {  // errors: engine.hpp:509-511, scope.hpp:262-263, engine.hpp:527
+    {  // errors: engine.hpp:51-53, scope.hpp:51-52, engine.hpp:69
         SelectionConfig cfg;
         cfg.l_global = 4; cfg.l_local = 8; cfg.k_prime = 2; cfg.span_m = 4;
         SegmentedKvCache cache(1, 4, 4, 8);
@@ -423,7 +423,7 @@ static void test_attend_step() {
     }
 }
 
-// kv_cache.hpp:121-209 snapshot round trip through the drop-in API, plus the reference's
+// kv_cache.hpp:120-209 snapshot round trip through the drop-in API, plus the reference's
 // failure messages (runtime_error / invalid_argument) for corrupt files.
 static void test_snapshot() {
     std::mt19937 rng(91);
@@ -577,7 +577,7 @@ static void test_engine() {
         CHECK(throws<std::out_of_range>([&] { eng.decode_step(500); }, "token id outside vocabulary"),
               "vocab");
     }
-    // weights file round trip + load errors (model.hpp:283-339)
+    // weights file round trip + load errors (model.hpp:259-339)
     {
         char path[] = "/tmp/reattn_dropin_w_XXXXXX";
         const int fd = mkstemp(path);

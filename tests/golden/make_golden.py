@@ -56,7 +56,7 @@ def main():
                 cid += 1
     manifest["cases"]["topk"] = topk_cases
 
-    # ---- vote (selection.hpp:385) and spans (:425) on random lists ----
+    # ---- vote (selection.hpp:278) and spans (:318) on random lists ----
     rng = np.random.default_rng(53)
     vote_cases = []
     for i in range(200):
@@ -83,7 +83,7 @@ def main():
         span_cases.append({"name": f"spans_{i}", "span_m": m, "middle_len": L, "mode": mode})
     manifest["cases"]["spans"] = span_cases
 
-    # ---- attend (attend.hpp:404) ----
+    # ---- attend (attend.hpp:25) ----
     att_cases = []
     for i in range(60):
         n_q, L, d = 1 + i % 8, 1 + (i * 37) % 512, max(4, (8 + (i * 11) % 60) & ~1)
@@ -100,7 +100,7 @@ def main():
                           "dv": dv, "boundary": bd})
     manifest["cases"]["attend"] = att_cases
 
-    # ---- rotary tables (rope.hpp:319): sha of the exact bytes ----
+    # ---- rotary tables (rope.hpp:21): sha of the exact bytes ----
     import hashlib
     ropes = []
     for d, base, mp in ((128, 500000.0, 8192), (128, 1e6, 8192), (16, 10000.0, 2048),
@@ -110,7 +110,7 @@ def main():
                       "sha256": hashlib.sha256(c.tobytes() + s.tobytes()).hexdigest()})
     manifest["cases"]["rope"] = ropes
 
-    # ---- attend_step (engine.hpp:501) ----
+    # ---- attend_step (engine.hpp:43) ----
     step_cases = []
     specs = [
         # LLaMA-3.1-8B heads, bf16-valued cache, defaults

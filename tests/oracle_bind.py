@@ -24,7 +24,7 @@ sz = C.c_size_t
 
 
 class SelectionConfig(C.Structure):
-    """Mirror of oracle_selection_config / reattn::SelectionConfig (selection.hpp:127-152)."""
+    """Mirror of oracle_selection_config / reattn::SelectionConfig (selection.hpp:20-45)."""
 
     _fields_ = [("k", sz), ("k_prime", sz), ("span_m", sz), ("tile_size", sz),
                 ("l_global", sz), ("l_local", sz), ("l_chunk", sz), ("span_mode", C.c_int)]
@@ -322,7 +322,7 @@ def round_bf16(x: np.ndarray) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------------------
-# the reference's decoder model and Engine (model.hpp, engine.hpp:115-218), run in place
+# the reference's decoder model and Engine (model.hpp, engine.hpp:119-216), run in place
 
 def _u32(tokens):
     t = np.ascontiguousarray(np.asarray(tokens, dtype=np.uint32))

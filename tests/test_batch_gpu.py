@@ -1,5 +1,5 @@
 """Batched decode (reattn_batch_plan_*): n_seq independent sequences with their own caches
-in one graph.  Each sequence's output must equal its own attend_step (engine.hpp:501) --
+in one graph.  Each sequence's output must equal its own attend_step (engine.hpp:43) --
 the pipelined path attends sequence b on a few SMs beside scan b+1, so only the order of
 the fp32/f64 partial merges differs (ATTN_TOL) -- and its scope must be identical."""
 import numpy as np

@@ -260,7 +260,7 @@ def step_vs_oracle(ctx, n_kv, nh, d, total, cfg, dtype, seed, window, base=50000
 
 @pytest.mark.parametrize("total", [100, 4128, 4200, 9000, 40000, 131072])
 def test_attend_step_llama_geometry_bf16(ctx, total):
-    """engine.hpp:501 attend_step at LLaMA-3.1-8B head geometry, bf16 cache, defaults."""
+    """engine.hpp:43 attend_step at LLaMA-3.1-8B head geometry, bf16 cache, defaults."""
     cfg = N.SelectionConfig()
     res, out, st, spans = step_vs_oracle(ctx, 8, 32, 128, total, cfg, N.BF16, 11 + total, 8192)
     assert res.stats.scope_len == st.scope_len

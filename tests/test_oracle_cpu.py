@@ -174,7 +174,7 @@ def test_synth_twins_agree():
 
 
 def test_group_mean_multiplies_by_reciprocal():
-    """selection.hpp:250-258: x float(1/group), not /group (differs at group 3)."""
+    """selection.hpp:143-151: x float(1/group), not /group (differs at group 3)."""
     q = synth.uniform(5, 3 * 128).reshape(1, 3 * 128)
     mq = np.zeros((1, 128), np.float32)
     ob.oracle().oracle_group_mean(q, 1, 3, 1, 128, mq)

@@ -1,7 +1,7 @@
 """K6 (prefill finite-scope attention on tcgen05) — attend_step parity with the tensor
 attention enabled (PREFILL_TENSOR_ATTN; the scan stays exact so the scope is identical).
 
-Reference: attend_step (engine.hpp:501-572) -> attend (attend.hpp:404-456).  K6 computes
+Reference: attend_step (engine.hpp:43-114) -> attend (attend.hpp:25-77).  K6 computes
 S with bf16 hi+lo split operands and fp32 TMEM accumulation, so the bar is the north_star
 bf16 tolerance (max-abs 1e-2); the measured error is orders of magnitude below it and the
 tighter bound below pins that."""

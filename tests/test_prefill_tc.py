@@ -3,7 +3,7 @@
 K2 runs the score GEMM once with the bf16 rounding of the fp32 group-mean query, bounds the
 error of those scores (2^-8 * ||mq||_1 * max|k|), and recomputes the reference's exact fp32
 dot_f32 (dense_matrix.hpp:41-56) for every key that could still enter a row's top-k -- so
-the selected indices AND scores must equal fused_topk_scores (selection.hpp:275-355) bit for
+the selected indices AND scores must equal fused_topk_scores (selection.hpp:168-248) bit for
 bit, in both lane arithmetics (unfused mul+add, or FMA: SURVEY §8(c))."""
 import numpy as np
 import pytest

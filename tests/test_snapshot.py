@@ -1,4 +1,4 @@
-"""RKVC cache snapshots (reference kv_cache.hpp:121-209) to and from device caches.
+"""RKVC cache snapshots (reference kv_cache.hpp:120-209) to and from device caches.
 
 Files written by the reference's own write_cache_snapshot (oracle/_ref) are read by
 reattn_snapshot_*; files written by reattn_snapshot_write are read back by the reference's

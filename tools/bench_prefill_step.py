@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Config 3 (BASELINE.json) end to end: one ReAttention prefill step (engine.hpp:501
+"""Config 3 (BASELINE.json) end to end: one ReAttention prefill step (engine.hpp:43
 attend_step) for the last 4096-query chunk at 256K context, Mistral-v0.3 head geometry
 (32 q / 8 kv heads, d = 128, rope base 1e6), bf16 cache, default selection
 (k = 4, k' = 127, m = 32, g = 32, local = 4096).
