@@ -213,6 +213,11 @@ int reattn_plan_launch_scan(reattn_plan* plan);
 int reattn_plan_run_host(reattn_plan* plan, const float* q_host, float* out_host);
 /* synchronise and read the last replay's stats (errors surface here) */
 int reattn_plan_stats(reattn_plan* plan, reattn_step_stats* stats);
+/* synchronise and read the last replay's full attend_step outputs besides `out`: stats,
+ * the chosen spans (nullable, capacity >= k_prime) and the row entropies (nullable,
+ * [n_q][n_head]) -- what reattn_attend_step returns through the same arguments */
+int reattn_plan_result(reattn_plan* plan, reattn_step_stats* stats, uint64_t* span_b_host,
+                       uint64_t* span_e_host, double* entropy_host);
 /* Diagnostics, no reference counterpart: with REATTN_TRACE=1 in the environment when a plan
  * is built, the decode kernels stamp %globaltimer (ns) into a device trace buffer; this
  * synchronises the device and copies its first n words (n <= 4096) to the host. */
@@ -272,6 +277,24 @@ int reattn_shard_combine(reattn_shard_plan* plan);  /* part_recv -> out */
 /* synchronise; header errors surface here */
 int reattn_shard_stats(reattn_shard_plan* plan, reattn_step_stats* stats, uint64_t* span_b_host,
                        uint64_t* span_e_host);
+
+/* NCCL host path: the library owns an NCCL communicator and issues both all-gathers of a
+ * step itself, so a C++ (or any FFI) host runs the sharded decode with no collective
+ * library of its own.  Rank 0 creates the id (reattn_comm_unique_id) and ships the 128
+ * bytes to every rank out of band (e.g. the launcher's store); every rank then calls
+ * reattn_comm_create collectively.  reattn_shard_step enqueues scan -> ncclAllGather ->
+ * select -> attend -> ncclAllGather -> combine on the context stream (or replays the
+ * graph captured by reattn_shard_capture, which must also be called collectively). */
+#define REATTN_COMM_ID_BYTES 128
+typedef struct reattn_comm reattn_comm;
+int reattn_comm_unique_id(uint8_t* id_out /* REATTN_COMM_ID_BYTES */);
+int reattn_comm_create(reattn_ctx* ctx, int world, int rank, const uint8_t* id, reattn_comm** out);
+void reattn_comm_destroy(reattn_comm* comm);
+int reattn_shard_step(reattn_shard_plan* plan, reattn_comm* comm);
+int reattn_shard_capture(reattn_shard_plan* plan, reattn_comm* comm);
+/* end to end from host memory: H2D q, step, D2H out, synchronise */
+int reattn_shard_run_host(reattn_shard_plan* plan, reattn_comm* comm, const float* q_host,
+                          float* out_host);
 
 /* ---- decoder model + generation engine (reference model.hpp, engine.hpp:119-216) ------
  * The toy decoder the reference's Engine drives: pre-norm blocks x += attn(norm(x)),

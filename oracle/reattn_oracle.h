@@ -100,6 +100,25 @@ int oracle_attend_step(const float* q_pre, size_t n_q, size_t n_head, const floa
                        const float* rope_sin, size_t max_position, int mode, float* out,
                        oracle_step_stats* stats, uint64_t* spans_begin, uint64_t* spans_end);
 
+/* ---- storage-generic, multi-threaded variants (full-size parity tests) ---------------
+ * Same arithmetic as above; keys / values are fp32 (ORACLE_DTYPE_F32) or bf16 words
+ * (ORACLE_DTYPE_BF16, widened exactly).  n_threads worker threads (>= 1). */
+enum { ORACLE_DTYPE_F32 = 0, ORACLE_DTYPE_BF16 = 1 };
+int oracle_topk_ex(const float* q, size_t n_q, size_t n_heads, const void* const* keys, int dtype,
+                   size_t n_kv, size_t count, size_t d, size_t row_stride, size_t k,
+                   int n_threads, uint64_t* idx_out, float* score_out, size_t* n_out);
+/* attend_step over a head-major [n_kv][cap][d] cache of `dtype`.  entropy (nullable):
+ * [n_q][n_head] row entropies; winners_out (nullable, >= k_prime): the voted winners;
+ * cand_idx_out / cand_score_out (nullable, [n_kv][n_q][k]): the per-head top-k lists. */
+int oracle_attend_step_ex(const float* q_pre, size_t n_q, size_t n_head, const void* cache_k,
+                          const void* cache_v, int dtype, size_t n_kv, size_t d, size_t cap,
+                          size_t total, const oracle_selection_config* cfg,
+                          const float* rope_cos, const float* rope_sin, size_t max_position,
+                          int mode, int n_threads, float* out, double* entropy,
+                          oracle_step_stats* stats, uint64_t* spans_begin, uint64_t* spans_end,
+                          uint64_t* winners_out, size_t* n_winners_out, uint64_t* cand_idx_out,
+                          float* cand_score_out);
+
 /* bf16 round-to-nearest-even of an fp32 value, returned as fp32 (test input helper). */
 float oracle_round_bf16(float x);
 /* splitmix64(seed, offset+i) -> [-1, 1) (24 significant bits), optionally bf16-rounded;

@@ -106,7 +106,7 @@ __device__ __forceinline__ int rot_idx4(int r, int i) { return r * (kBD / 4) + (
 // waits for the scan's merger CTA (griddepcontrol.wait): the lines are then resident in the
 // SM's instruction cache when the last CTA runs it for real.  __noinline__ keeps both calls
 // on the same code.
-template <int G>
+template <int G, int NW = 16>
 __device__ __noinline__ void merge_parts(const BulkArgs& B, int kv, int role, uint8_t* stages, bool dry) {
     const AttnArgs& a = B.a;
     const int lane = threadIdx.x & 31;
@@ -115,7 +115,9 @@ __device__ __noinline__ void merge_parts(const BulkArgs& B, int kv, int role, ui
     // the merge costs one L2 round trip plus an in-order combine of the WPH partial sums
     // through shared memory (deterministic).  Few registers (no spills) and no f64 library
     // calls on the path: this code runs once per launch, cold.
-    constexpr int WPH = G == 1 ? 16 : G == 2 ? 8 : G <= 4 ? 4 : 2;
+    constexpr int WPH = NW == 16 ? (G == 1 ? 16 : G == 2 ? 8 : G <= 4 ? 4 : 2)
+                                 : (G == 1 ? NW : G == 2 ? NW / 2 : G <= 4 ? NW / 4 : 1);
+    static_assert(WPH >= 1 && G * WPH <= NW, "merge roles exceed the compute warps");
     constexpr int kPre = 8;  // acc rows in flight per lane
     double* xo = (double*)stages;  // [G][WPH][kBD] partial sums
     if (role < G * WPH) {
@@ -243,6 +245,7 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
     const AttnArgs& a = B.a;
     // while the scan's merger CTA still runs its tail: warm the merge code (see merge_parts)
     extern __shared__ __align__(16) uint8_t bsm_raw[];
+    if (B.trace && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) B.trace[3904] = globaltimer();
     if (B.warm && threadIdx.x < 32) merge_parts<G>(B, blockIdx.y, 0, bsm_raw, true);
     const bool local = B.mode == kModeLocal;  // independent of the selection: never reads the header
     // launched as a programmatic dependent of the scan / select: wait for its results (a
@@ -309,6 +312,10 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
 
     if (tid == 0) {
         for (int s = 0; s < kBStages; ++s) {
+            if (hh > 0) {  // the previous kv head's barriers are idle (synced above): retire them
+                mbar_inval(&full[s]);
+                mbar_inval(&empty[s]);
+            }
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 4);  // the 4 warps of the group that consumed the stage
         }
@@ -359,6 +366,8 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
                 bulk_g2s(st + kBKVBytes + lane * kBD * 2, (const __nv_bfloat16*)a.v_base + row, bytes_run,
                          &full[s]);
             }
+            if (B.trace && lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && c < 64)
+                B.trace[3712 + c] = globaltimer();  // chunk c's copies issued (CTA (0, 0))
             if (a.rope_cos && lane < 2) {
                 const float* tab = lane == 0 ? a.rope_cos : a.rope_sin;
                 bulk_g2s(st + 2 * kBKVBytes + lane * kBRopeBytes, tab + (size_t)k0 * (kBD / 2),
@@ -410,6 +419,8 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
             if (c >= kBStages) mbar_wait(&empty[s], ((c / kBStages) - 1) & 1u);
             mbar_wait(&full[s], (c / kBStages) & 1u);
             __syncwarp();
+            const bool tr = B.trace && gw == 0 && lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && c < 64;
+            if (tr) B.trace[3776 + c] = globaltimer();  // chunk c landed (group gi)
             uint32_t k0;
             int nk;
             geom(c_begin + c, k0, nk);
@@ -521,6 +532,7 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
                 }
             }
             __syncwarp();
+            if (tr) B.trace[3840 + c] = globaltimer();  // chunk c consumed
             if (lane == 0) mbar_arrive(&empty[s]);
         }
         // ---- merge the 16 warps' states per head through shared memory ----
@@ -805,7 +817,7 @@ BulkArgs bulk_args(const AttnArgs& a, void* ws, int num_sms, const DecodeFork* f
     B.n_slots = B.n_parts + (f ? f->local_parts : 0);
     B.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)kBD));
     B.tickets = (unsigned int*)ws;
-    B.part = (uint8_t*)ws + 256;
+    B.part = (uint8_t*)ws + decode_ticket_bytes(a.n_kv);
     B.trace = trace_buffer();
     B.warm = 0;
     B.local_post = 0;
@@ -820,8 +832,10 @@ bool decode_bulk_eligible(const AttnArgs& a) {
            a.boundary_is_tail && a.dtype == kBF16 && a.n_head == a.n_kv * a.group;
 }
 
+size_t decode_ticket_bytes(int n_kv) { return ((size_t)4 * std::max(1, n_kv) + 255) & ~(size_t)255; }
+
 size_t decode_bulk_workspace(const AttnArgs& a, int num_sms) {
-    return 256 + (size_t)(bulk_parts(a, num_sms) + kMaxLocalParts) * a.n_kv * a.group * kBPartBytes;
+    return decode_ticket_bytes(a.n_kv) + (size_t)(bulk_parts(a, num_sms) + kMaxLocalParts) * a.n_kv * a.group * kBPartBytes;
 }
 
 cudaError_t launch_attend_decode_bulk(const AttnArgs& a, void* ws, int num_sms, cudaStream_t s) {

@@ -315,13 +315,14 @@ int enqueue_attn_part(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache,
     if (P.n_q > 0) {
         AttnArgs a = step_attn_args(P, cache, rope, q_dev, out_dev);
         if (attn_sms > 0 && attn_sms < ctx->num_sms && decode_bulk_eligible(a) && !P.fork) {
-            if (zero_ticket) CU(ctx, cudaMemsetAsync(P.part, 0, 256, s));
+            if (zero_ticket) CU(ctx, cudaMemsetAsync(P.part, 0, decode_ticket_bytes(a.n_kv), s));
             CU(ctx, launch_attend_decode_bulk_ex(a, P.part, attn_sms, s, false));
             ++P.kernels;
             return REATTN_OK;
         }
         // the bulk decode attention's tickets sit at the start of P.part (plans: zeroed once)
-        if (zero_ticket && decode_bulk_eligible(a)) CU(ctx, cudaMemsetAsync(P.part, 0, 256, s));
+        if (zero_ticket && decode_bulk_eligible(a))
+            CU(ctx, cudaMemsetAsync(P.part, 0, decode_ticket_bytes(a.n_kv), s));
         if (P.fork) {
             if (!P.fk.post) CU(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
             CU(ctx, launch_attend_decode_head(a, P.part, ctx->num_sms, P.fk, s, P.fk.post != 0));
@@ -1016,6 +1017,26 @@ int reattn_plan_stats(reattn_plan* p, reattn_step_stats* st) {
     CU(ctx, cudaMemcpyAsync(&h, p->P.hdr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     return finish_step_stats(ctx, p->P, h, st, nullptr);
+}
+
+int reattn_plan_result(reattn_plan* p, reattn_step_stats* st, uint64_t* span_b_host,
+                       uint64_t* span_e_host, double* entropy_host) {
+    reattn_ctx* ctx = p->ctx;
+    ScopeHeader h;
+    CU(ctx, cudaMemcpyAsync(&h, p->P.hdr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    int rc = finish_step_stats(ctx, p->P, h, st, entropy_host);
+    if (rc) return rc;
+    if (span_b_host && h.n_spans) {
+        std::vector<uint32_t> b(h.n_spans), e(h.n_spans);
+        CU(ctx, cudaMemcpy(b.data(), p->P.span_b, h.n_spans * 4, cudaMemcpyDeviceToHost));
+        CU(ctx, cudaMemcpy(e.data(), p->P.span_e, h.n_spans * 4, cudaMemcpyDeviceToHost));
+        for (uint32_t i = 0; i < h.n_spans; ++i) {
+            span_b_host[i] = b[i];
+            span_e_host[i] = e[i];
+        }
+    }
+    return REATTN_OK;
 }
 
 int reattn_plan_info(const reattn_plan* p, uint64_t* kernels, uint64_t* scan_bytes,

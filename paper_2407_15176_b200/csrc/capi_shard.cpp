@@ -1,4 +1,6 @@
 // C-ABI: sequence-sharded decode plans (include/reattn_cuda.h, "sequence-sharded decode").
+#include <nccl.h>
+
 #include "capi_internal.h"
 
 using namespace reattn_impl;
@@ -39,6 +41,17 @@ struct reattn_shard_plan {
     double* part_recv = nullptr;  // all ranks' [world][n_head]
     size_t part_bytes = 0;
     double* entropy = nullptr;
+    // the whole step (NCCL all-gathers included) captured by reattn_shard_capture
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};
+
+// An NCCL communicator over the ranks of one sharded decode (one process per GPU).  The
+// library issues the two all-gathers of a step itself (reattn_shard_step), so a C++ host
+// drives the whole sharded path through this ABI with no Python on it.
+struct reattn_comm {
+    ncclComm_t comm = nullptr;
+    int world = 1, rank = 0, device = 0;
 };
 
 namespace {
@@ -206,6 +219,8 @@ int reattn_shard_plan_create(reattn_ctx* ctx, const reattn_cache* cache, const r
 void reattn_shard_plan_destroy(reattn_shard_plan* p) {
     if (!p) return;
     cudaDeviceSynchronize();
+    if (p->exec) cudaGraphExecDestroy(p->exec);
+    if (p->graph) cudaGraphDestroy(p->graph);
     cudaFree(p->mem);
     delete p;
 }
@@ -323,6 +338,106 @@ int reattn_shard_stats(reattn_shard_plan* p, reattn_step_stats* st, uint64_t* sb
             se[i] = e[i];
         }
     }
+    return REATTN_OK;
+}
+
+// ---- NCCL host path ---------------------------------------------------------------------
+int reattn_comm_unique_id(uint8_t* id_out) {
+    static_assert(sizeof(ncclUniqueId) == REATTN_COMM_ID_BYTES, "NCCL unique id size");
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return REATTN_ECUDA;
+    std::memcpy(id_out, &id, sizeof(id));
+    return REATTN_OK;
+}
+
+int reattn_comm_create(reattn_ctx* ctx, int world, int rank, const uint8_t* id_in,
+                       reattn_comm** out) {
+    *out = nullptr;
+    if (world < 1 || world > 64 || rank < 0 || rank >= world)
+        return set_err(ctx, REATTN_EINVAL, "comm: world must be 1..64 and rank < world");
+    ncclUniqueId id;
+    std::memcpy(&id, id_in, sizeof(id));
+    CU(ctx, cudaSetDevice(ctx->device));
+    auto* c = new reattn_comm();
+    c->world = world;
+    c->rank = rank;
+    c->device = ctx->device;
+    const ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return set_err(ctx, REATTN_ECUDA, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    *out = c;
+    return REATTN_OK;
+}
+
+void reattn_comm_destroy(reattn_comm* c) {
+    if (!c) return;
+    if (c->comm) ncclCommDestroy(c->comm);
+    delete c;
+}
+
+namespace {
+int nccl_gather(reattn_ctx* ctx, const void* send, void* recv, size_t bytes, reattn_comm* c) {
+    const ncclResult_t r = ncclAllGather(send, recv, bytes, ncclUint8, c->comm, ctx->stream);
+    if (r != ncclSuccess)
+        return set_err(ctx, REATTN_ECUDA, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    return REATTN_OK;
+}
+
+int enqueue_shard_step(reattn_shard_plan* p, reattn_comm* c) {
+    if (c->world != p->world || c->rank != p->rank)
+        return set_err(p->ctx, REATTN_EINVAL, "shard step: communicator world/rank != plan's");
+    int rc = reattn_shard_scan(p);
+    if (!rc) rc = nccl_gather(p->ctx, p->cand_send, p->cand_recv, p->cand_bytes, c);
+    if (!rc) rc = reattn_shard_select(p);
+    if (!rc) rc = reattn_shard_attend(p);
+    if (!rc) rc = nccl_gather(p->ctx, p->part_send, p->part_recv, p->part_bytes, c);
+    if (!rc) rc = reattn_shard_combine(p);
+    return rc;
+}
+}  // namespace
+
+int reattn_shard_step(reattn_shard_plan* p, reattn_comm* c) {
+    if (p->exec) {  // a captured step replays as one graph launch
+        CU(p->ctx, cudaGraphLaunch(p->exec, p->ctx->stream));
+        return REATTN_OK;
+    }
+    return enqueue_shard_step(p, c);
+}
+
+int reattn_shard_capture(reattn_shard_plan* p, reattn_comm* c) {
+    reattn_ctx* ctx = p->ctx;
+    // one eager step first: NCCL connection set-up and kernel attributes happen outside capture
+    int rc = enqueue_shard_step(p, c);
+    if (rc) return rc;
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    if (p->exec) cudaGraphExecDestroy(p->exec);
+    if (p->graph) cudaGraphDestroy(p->graph);
+    p->exec = nullptr;
+    p->graph = nullptr;
+    CU(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    rc = enqueue_shard_step(p, c);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &g);
+    if (rc || ce != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        return rc ? rc : set_err(ctx, REATTN_ECUDA, std::string("shard capture: ") + cudaGetErrorString(ce));
+    }
+    p->graph = g;
+    CU(ctx, cudaGraphInstantiate(&p->exec, g, 0));
+    return REATTN_OK;
+}
+
+int reattn_shard_run_host(reattn_shard_plan* p, reattn_comm* c, const float* q_host,
+                          float* out_host) {
+    reattn_ctx* ctx = p->ctx;
+    const size_t bytes = p->n_head * p->d * sizeof(float);
+    CU(ctx, cudaMemcpyAsync(p->q, q_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    int rc = reattn_shard_step(p, c);
+    if (rc) return rc;
+    CU(ctx, cudaMemcpyAsync(out_host, p->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
     return REATTN_OK;
 }
 

@@ -155,9 +155,11 @@ size_t attend_workspace(const AttnArgs& a, uint32_t L_max);
 cudaError_t launch_attend(const AttnArgs& a, uint32_t L_max, cudaStream_t s);
 int attend_kernel_count(const AttnArgs& a, uint32_t L_max);
 // decode attention with a bulk-copy ring and fused combine (attend_decode.cu): n_q == 1,
-// d == dv == 128, bf16 cache.  ws = a.part: 256 B of per-kv-head tickets (zero before the
-// first launch; the kernel re-arms them) + partial rows.
+// d == dv == 128, bf16 cache.  ws = a.part: per-kv-head tickets (zero before the
+// first launch; the kernel re-arms them) + partial rows.  The tickets take
+// decode_ticket_bytes(n_kv) (one uint32 per kv head, rounded up to 256 B).
 bool decode_bulk_eligible(const AttnArgs& a);
+size_t decode_ticket_bytes(int n_kv);
 size_t decode_bulk_workspace(const AttnArgs& a, int num_sms);
 cudaError_t launch_attend_decode_bulk(const AttnArgs& a, void* ws, int num_sms, cudaStream_t s);
 // same on `num_sms` SMs' worth of CTAs, with or without programmatic dependent launch

@@ -156,6 +156,7 @@ SIGNATURES = [
     ("reattn_plan_run_host", C.c_int, [vp, vp, vp]),
     ("reattn_plan_stats", C.c_int, [vp, C.POINTER(StepStats)]),
     ("reattn_plan_info", C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
+    ("reattn_plan_result", C.c_int, [vp, C.POINTER(StepStats), vp, vp, vp]),
     ("reattn_batch_plan_create", C.c_int, [vp, C.POINTER(vp), C.c_uint32, vp, u64, vp, C.c_int,
                                            C.POINTER(vp)]),
     ("reattn_batch_plan_destroy", None, [vp]),
@@ -202,6 +203,12 @@ SIGNATURES = [
     ("reattn_shard_attend", C.c_int, [vp]),
     ("reattn_shard_combine", C.c_int, [vp]),
     ("reattn_shard_stats", C.c_int, [vp, C.POINTER(StepStats), vp, vp]),
+    ("reattn_comm_unique_id", C.c_int, [vp]),
+    ("reattn_comm_create", C.c_int, [vp, C.c_int, C.c_int, vp, C.POINTER(vp)]),
+    ("reattn_comm_destroy", None, [vp]),
+    ("reattn_shard_step", C.c_int, [vp, vp]),
+    ("reattn_shard_capture", C.c_int, [vp, vp]),
+    ("reattn_shard_run_host", C.c_int, [vp, vp, vp, vp]),
 ]
 
 _lib = None
@@ -541,6 +548,20 @@ class Plan:
         st = StepStats()
         self.ctx.check(self.ctx.lib.reattn_plan_stats(self.h, C.byref(st)))
         return st
+
+    def result(self, k_prime: int) -> "StepResult":
+        """The last replay's attend_step outputs: out (device tensor), stats, spans and the
+        row entropies [n_q, n_head] (reattn_plan_result)."""
+        import numpy as np
+        st = StepStats()
+        sb = np.zeros(max(1, k_prime), np.uint64)
+        se = np.zeros(max(1, k_prime), np.uint64)
+        ent = np.zeros(max(1, self.n_q * self.n_head), np.float64)
+        self.ctx.check(self.ctx.lib.reattn_plan_result(self.h, C.byref(st), sb.ctypes.data,
+                                                        se.ctypes.data, ent.ctypes.data))
+        n = st.n_spans
+        return StepResult(self.out, st, (sb[:n].copy(), se[:n].copy()),
+                          ent[: self.n_q * self.n_head].reshape(self.n_q, self.n_head))
 
     def info(self) -> dict:
         a, b, c = u64(), u64(), u64()

@@ -13,9 +13,14 @@ ranks; the global and local blocks are replicated.  One decode step per rank:
     gather 2  all_gather of the partial states
     combine   fixed-order merge -> the full output on every rank
 
-Collectives go through torch.distributed (NCCL on GPUs); device stages run in the
-library on the same stream.  `ops` is pluggable so the identical protocol code runs
-under gloo on CPU in the tests (tests/test_sharded_cpu.py); the product uses NativeOps.
+Two hosts of the same protocol:
+  * NcclDecodeStep (the product path): the library owns an NCCL communicator
+    (reattn_comm_*) and issues both all-gathers itself -- reattn_shard_step /
+    reattn_shard_capture, exactly what a C++ host calls (include/reattn/sharded.hpp);
+    torch.distributed only ships the 128-byte NCCL id from rank 0 and times the run.
+  * ShardedDecodeStep: the collectives through torch.distributed; `ops` is pluggable so
+    the identical protocol code runs under gloo on CPU in the tests
+    (tests/test_sharded_cpu.py).
 """
 from __future__ import annotations
 
@@ -145,3 +150,57 @@ class ShardedDecodeStep:
         torch.cuda.synchronize()
         self.graph = g
         return self
+
+
+class NcclComm:
+    """The library's own NCCL communicator (reattn_comm_*).  Rank 0's unique id is shipped to
+    the other ranks through torch.distributed (plumbing only: 128 bytes, once)."""
+
+    def __init__(self, ctx: N.Context, world: int, rank: int, group=None):
+        import torch
+        import torch.distributed as dist
+        self.ctx, self.lib = ctx, ctx.lib
+        idb = (C.c_uint8 * 128)()
+        if rank == 0:
+            ctx.check(self.lib.reattn_comm_unique_id(idb))
+        if world > 1:
+            t = torch.tensor(list(idb), dtype=torch.uint8,
+                             device=f"cuda:{ctx.device}" if dist.get_backend(group) == "nccl" else "cpu")
+            dist.broadcast(t, src=0, group=group)
+            for i, v in enumerate(t.cpu().tolist()):
+                idb[i] = v
+        h = N.vp()
+        ctx.check(self.lib.reattn_comm_create(ctx.h, world, rank, idb, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.reattn_comm_destroy(self.h)
+            self.h = None
+
+
+class NcclDecodeStep:
+    """One rank's sharded decode step with the collectives issued by the library
+    (reattn_shard_step): the C-ABI host path.  capture() records the step, both NCCL
+    all-gathers included, as one CUDA graph (reattn_shard_capture; collective)."""
+
+    def __init__(self, ops: NativeOps, comm: NcclComm):
+        self.ops, self.comm = ops, comm
+        self.captured = False
+
+    def step(self, q=None):
+        o = self.ops
+        if q is not None:
+            o.q.copy_(q)
+        o.ctx.check(o.lib.reattn_shard_step(o.h, self.comm.h))
+        return o.out
+
+    def capture(self):
+        o = self.ops
+        o.ctx.check(o.lib.reattn_shard_capture(o.h, self.comm.h))
+        self.captured = True
+        return self
+
+    def run_host(self, q_host, out_host):
+        o = self.ops
+        o.ctx.check(o.lib.reattn_shard_run_host(o.h, self.comm.h, N._ptr(q_host), N._ptr(out_host)))

@@ -74,6 +74,13 @@ def oracle() -> C.CDLL:
         lib.oracle_set_lane_mode.argtypes = [C.c_int]
         lib.oracle_get_lane_mode.restype = C.c_int
         lib.oracle_synth_uniform.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, f32p, C.c_int]
+        vp = C.c_void_p
+        lib.oracle_topk_ex.argtypes = [f32p, sz, sz, C.POINTER(C.c_void_p), C.c_int, sz, sz, sz,
+                                       sz, sz, C.c_int, u64p, f32p, C.POINTER(sz)]
+        lib.oracle_attend_step_ex.argtypes = [f32p, sz, sz, vp, vp, C.c_int, sz, sz, sz, sz,
+                                              C.POINTER(SelectionConfig), f32p, f32p, sz, C.c_int,
+                                              C.c_int, f32p, f64p, C.POINTER(StepStats), u64p,
+                                              u64p, u64p, C.POINTER(sz), vp, vp]
         lib.oracle_round_bf16.restype = C.c_float
         lib.oracle_round_bf16.argtypes = [C.c_float]
         _oracle = lib
@@ -312,6 +319,90 @@ def attend_step(q_pre, n_head, cache_k, cache_v, total, cfg: SelectionConfig, ro
         raise RuntimeError(f"attend_step rc={rc}")
     return out[: n_q * n_head * d].reshape(n_q, n_head * d), st, (sb[: st.n_spans].copy(),
                                                                    se[: st.n_spans].copy())
+
+
+def host_threads() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
+
+
+def _dtype_code(a: np.ndarray) -> int:
+    if a.dtype == np.float32:
+        return 0
+    if a.dtype in (np.uint16, np.int16):
+        return 1  # bf16 words
+    raise TypeError(f"cache storage must be float32 or bf16 words (uint16), got {a.dtype}")
+
+
+def topk_ex(q, n_heads: int, keys_hm: np.ndarray, row0: int, count: int, k: int,
+            threads: int | None = None):
+    """Multi-threaded oracle top-k over a head-major [n_kv, cap, d] fp32 or bf16-word array
+    (middle rows [row0, row0 + count)).  Returns (idx [n_kv, n_q, kk], score)."""
+    lib = oracle()
+    q = np.ascontiguousarray(q, np.float32)
+    n_q = q.shape[0]
+    n_kv, cap, d = keys_hm.shape
+    assert keys_hm.flags.c_contiguous
+    dt = _dtype_code(keys_hm)
+    esz = keys_hm.itemsize
+    base = keys_hm.ctypes.data
+    ptrs = (C.c_void_p * n_kv)(*[base + (h * cap + row0) * d * esz for h in range(n_kv)])
+    idx = np.zeros(max(1, n_kv * n_q * k), np.uint64)
+    sc = np.zeros(max(1, n_kv * n_q * k), np.float32)
+    n_out = sz(0)
+    rc = lib.oracle_topk_ex(q, n_q, n_heads, C.cast(ptrs, C.POINTER(C.c_void_p)), dt, n_kv, count,
+                            d, d, k, threads or host_threads(), idx, sc, C.byref(n_out))
+    if rc != 0:
+        raise ValueError(f"topk_ex rc={rc}")
+    kk = n_out.value
+    return (idx[: n_kv * n_q * k].reshape(n_kv, n_q, k)[:, :, :kk],
+            sc[: n_kv * n_q * k].reshape(n_kv, n_q, k)[:, :, :kk])
+
+
+def attend_step_ex(q_pre, n_head, cache_k, cache_v, total, cfg: SelectionConfig, rope_base,
+                   max_position, mode=2, threads: int | None = None, candidates: bool = False):
+    """Multi-threaded oracle attend_step over a head-major [n_kv, cap, d] cache held as fp32
+    or as bf16 words (uint16; widened exactly).  Returns (out [n_q, n_head*d],
+    entropy [n_q, n_head], stats, (span_begin, span_end), winners), plus the per-head top-k
+    lists (idx [n_kv, n_q, k], score) when candidates=True."""
+    lib = oracle()
+    q_pre = np.ascontiguousarray(q_pre, np.float32)
+    n_q = q_pre.shape[0]
+    n_kv, cap, d = cache_k.shape
+    assert cache_k.flags.c_contiguous and cache_v.flags.c_contiguous
+    assert cache_k.dtype == cache_v.dtype
+    out = np.zeros(max(1, n_q * n_head * d), np.float32)
+    ent = np.zeros(max(1, n_q * n_head), np.float64)
+    st = StepStats()
+    st.coverage_total = 1
+    sb = np.zeros(max(1, cfg.k_prime), np.uint64)
+    se = np.zeros(max(1, cfg.k_prime), np.uint64)
+    wn = np.zeros(max(1, cfg.k_prime), np.uint64)
+    nw = sz(0)
+    cs, sn = rope_table(d, rope_base, max_position)
+    ci = np.zeros(n_kv * n_q * cfg.k if candidates else 1, np.uint64)
+    cf = np.zeros(n_kv * n_q * cfg.k if candidates else 1, np.float32)
+    rc = lib.oracle_attend_step_ex(q_pre, n_q, n_head, cache_k.ctypes.data, cache_v.ctypes.data,
+                                   _dtype_code(cache_k), n_kv, d, cap, total, C.byref(cfg),
+                                   cs.ravel(), sn.ravel(), max_position, mode,
+                                   threads or host_threads(), out, ent, C.byref(st), sb, se, wn,
+                                   C.byref(nw), ci.ctypes.data if candidates else None,
+                                   cf.ctypes.data if candidates else None)
+    if rc != 0:
+        raise RuntimeError(f"attend_step_ex rc={rc}")
+    res = (out[: n_q * n_head * d].reshape(n_q, n_head * d), ent[: n_q * n_head].reshape(n_q, n_head),
+           st, (sb[: st.n_spans].copy(), se[: st.n_spans].copy()), wn[: nw.value].copy())
+    if candidates:
+        res = res + ((ci.reshape(n_kv, n_q, cfg.k), cf.reshape(n_kv, n_q, cfg.k)),)
+    return res
+
+
+def bf16_words(t) -> np.ndarray:
+    """A torch bf16 tensor (any device) as host uint16 words (no widening copy)."""
+    import torch
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
 
 
 def round_bf16(x: np.ndarray) -> np.ndarray:

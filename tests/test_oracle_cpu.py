@@ -95,6 +95,52 @@ def test_golden_attend_step(golden):
         assert abs(st.entropy_max - c["entropy_max"]) <= 1e-8, c["name"]
 
 
+def test_golden_attend_step_ex_bf16_words(golden):
+    """The storage-generic, multi-threaded oracle (used by the full-size GPU parity tests on
+    bf16 caches held as words) reproduces the golden attend_step cases bit for bit in the
+    selection and within the same tolerance in the outputs."""
+    cases, A = golden
+    for c in cases["attend_step"]:
+        if not c["bf16"]:
+            continue
+        K = _keys(c["seed"], c["n_kv"], c["total"], c["d"], True)
+        V = _keys(c["seed"] + 1, c["n_kv"], c["total"], c["d"], True)
+        kw = np.ascontiguousarray(K).view(np.uint32) >> 16
+        vw = np.ascontiguousarray(V).view(np.uint32) >> 16
+        q = synth.uniform(c["seed"] + 2, c["n_q"] * c["nh"] * c["d"]).reshape(c["n_q"], -1)
+        cfg = ob.SelectionConfig(**c["cfg"])
+        with ob.lane_mode(c["lanes"]):
+            o, ent, st, (sb, se), _ = ob.attend_step_ex(q, c["nh"], kw.astype(np.uint16),
+                                                        vw.astype(np.uint16), c["total"], cfg,
+                                                        c["base"], c["window"], 2, threads=5)
+        assert st.scope_len == c["scope_len"], c["name"]
+        assert np.array_equal(sb.astype(np.uint32), A[c["name"] + "_sb"]), c["name"]
+        assert np.array_equal(se.astype(np.uint32), A[c["name"] + "_se"]), c["name"]
+        assert np.abs(o - A[c["name"] + "_out"]).max() <= 1e-7, c["name"]
+        assert abs(st.entropy_max - c["entropy_max"]) <= 1e-8, c["name"]
+        assert abs(ent.max() - c["entropy_max"]) <= 1e-8, c["name"]
+
+
+def test_topk_ex_matches_sequential_oracle():
+    """Range-split, multi-threaded top-k == the sequential TopkBuffer restatement, including
+    planted exact ties across range boundaries (ties keep the lower index)."""
+    rng = np.random.default_rng(5)
+    for it, (count, n_kv, nh, d, k, nq) in enumerate([(5000, 2, 8, 128, 4, 1), (9000, 1, 3, 64, 8, 3),
+                                                      (2049, 3, 3, 16, 1, 2), (20000, 2, 4, 128, 5, 1)]):
+        K = rng.uniform(-1, 1, (n_kv, count, d)).astype(np.float32)
+        K[:, 100] = K[:, 4000 % count] = K[:, count - 1] = K[:, 7]  # exact score ties
+        q = rng.uniform(-1, 1, (nq, nh * d)).astype(np.float32)
+        want = ob.topk(q, nh, [np.ascontiguousarray(K[h]) for h in range(n_kv)], k)
+        for threads in (1, 4, 13):
+            got = ob.topk_ex(q, nh, K, 0, count, k, threads=threads)
+            assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1]), (it, threads)
+        # bf16 words
+        Kb = ob.round_bf16(K)
+        want = ob.topk(q, nh, [np.ascontiguousarray(Kb[h]) for h in range(n_kv)], k)
+        got = ob.topk_ex(q, nh, (Kb.view(np.uint32) >> 16).astype(np.uint16), 0, count, k, threads=6)
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1]), it
+
+
 # ---- oracle vs the live compiled reference (this container only) ------------------------
 needs_ref = pytest.mark.skipif(ob.ref() is None, reason="oracle/_ref not built here")
 

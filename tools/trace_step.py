@@ -85,6 +85,12 @@ def main():
             print(f"   K5 part0/kv0: q rotated {(t[3700] - t0) / 1e3:8.2f}  first copy issued "
                   f"{(t[3704] - t0) / 1e3:8.2f}  first chunk landed {(t[3701] - t0) / 1e3:8.2f}  "
                   f"warps merged {(t[3703] - t0) / 1e3:8.2f} us")
+        if t[3904]:
+            iss = [(c, t[3712 + c], t[3776 + c], t[3840 + c]) for c in range(64) if t[3712 + c]]
+            print(f"   K5 CTA(0,0) resident {(t[3904] - t0) / 1e3:8.2f} us; per chunk: issued / landed / consumed")
+            for c, a_, b_, c_ in iss:
+                f = lambda x: f"{(x - t0) / 1e3:8.2f}" if x else "     -  "  # noqa: E731
+                print(f"      chunk {c:2d}: {f(a_)} {f(b_)} {f(c_)}")
         if any(t[3600:3600 + args.n_kv]):
             print("K5 last ticket    ", summarize(rel(t[3600:3600 + args.n_kv])))
             print("K5 M/w loops done ", summarize(rel(t[3664:3664 + args.n_kv])))
