@@ -227,14 +227,14 @@ __device__ __noinline__ void merge_parts(const BulkArgs& B, int kv, int role, ui
                     hd[2] = Bt;
                 }
             } else {
-                if (!dry)
-                    reinterpret_cast<float4*>(a.out + (size_t)h * kBD)[lane] =
-                        make_float4((float)(r[0] * inv), (float)(r[1] * inv), (float)(r[2] * inv),
-                                    (float)(r[3] * inv));
-                if (lane == 0 && !dry) {
-                    const double hh = log(At) - Bt * 0.69314718055994530942 * inv;
-                    a.entropy[h] = hh < 0.0 ? 0.0 : hh;
-                }
+                const float4 o4 = make_float4((float)(r[0] * inv), (float)(r[1] * inv),
+                                              (float)(r[2] * inv), (float)(r[3] * inv));
+                // computed in the warm-up too (the f64 log is a long routine that would
+                // otherwise run cold); the asm keeps it from sinking into the store branch
+                const double hh = log(At) - Bt * 0.69314718055994530942 * inv;
+                asm volatile("" ::"d"(hh), "f"(o4.x), "f"(o4.y), "f"(o4.z), "f"(o4.w));
+                if (!dry) reinterpret_cast<float4*>(a.out + (size_t)h * kBD)[lane] = o4;
+                if (lane == 0 && !dry) a.entropy[h] = hh < 0.0 ? 0.0 : hh;
             }
         }
     }
