@@ -360,7 +360,10 @@ def run_ours(args) -> None:
     ctx = N.Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
     cid = args.config
-    cache, rope, plan, cfg, meta = build_decode(ctx, cid, total=args.ctx if cid == 4 else None)
+    n_e2e = max(10, args.steps // 4)
+    # headroom for the end-to-end leg, whose steps append a row each (append + attend_step)
+    cache, rope, plan, cfg, meta = build_decode(ctx, cid, total=args.ctx if cid == 4 else None,
+                                                extra_rows=n_e2e + 8)
     info = plan.info()
     K, W = args.steps, args.warmup
     n_head = meta["n_head"]
@@ -387,15 +390,23 @@ def run_ours(args) -> None:
             s1.synchronize()
             scan_ms += s0.elapsed_time(s1)
         scan_ms /= n_scan
-        # end to end through the public C-ABI from pinned host memory
+        # end to end through the public C-ABI from pinned host memory, as a decoder calls it per
+        # token and layer: this step's K/V rows appended to the cache (kv_cache.hpp:54-68)
+        # inside the same graph, then the step (reattn_plan_step_host: H2D q, k, v; replay;
+        # D2H out; synchronise).  The cache grows by one row per call.
+        plan.set_append(True)
         qh = qbank[:1].cpu().pin_memory()
         oh = torch.empty_like(qh).pin_memory()
-        n_e2e = max(10, K // 4)
+        kvw = meta["n_kv"] * D
+        kh = torch.empty(kvw, dtype=torch.float32).pin_memory()
+        vh = torch.empty(kvw, dtype=torch.float32).pin_memory()
+        kh.copy_(torch.from_numpy(__import__("synth").uniform(77, kvw, bf16=True)))
+        vh.copy_(torch.from_numpy(__import__("synth").uniform(78, kvw, bf16=True)))
         for _ in range(3):
-            plan.run_host(qh, oh)
+            plan.step_host(qh, kh, vh, oh)
         t0 = time.perf_counter()
         for i in range(n_e2e):
-            plan.run_host(qh, oh)
+            plan.step_host(qh, kh, vh, oh)
         e2e_us = (time.perf_counter() - t0) / n_e2e * 1e6
 
     peaks = load_peaks()
@@ -430,10 +441,12 @@ def run_ours(args) -> None:
                      "peak_note": "peak is the measured copy (read+write) bandwidth; the scan "
                                   "only reads, so frac can exceed 1",
                      "share_of_step": scan_ms / ms_per_step},
-        "e2e": {"value": e2e_us, "unit": UNIT, "h2d_bytes_per_step": n_head * D * 4,
+        "e2e": {"value": e2e_us, "unit": UNIT,
+                "h2d_bytes_per_step": n_head * D * 4 + 2 * meta["n_kv"] * D * 4,
                 "d2h_bytes_per_step": n_head * D * 4,
-                "path": "reattn_plan_run_host (C-ABI): H2D q from pinned host, graph replay, "
-                        "D2H output, synchronise"},
+                "path": "reattn_plan_step_host (C-ABI): H2D q + the step's K/V rows from pinned "
+                        "host, one graph replay (append node + attend_step), D2H output, "
+                        "synchronise; the cache grows by one row per step"},
         "gpu_launches": int(info["kernels_per_step"]) * K,
         "kernels_per_step": int(info["kernels_per_step"]),
         "wall_s_timed_region": t_wall,

@@ -205,8 +205,25 @@ int reattn_plan_create(reattn_ctx* ctx, const reattn_cache* cache, const reattn_
 void reattn_plan_destroy(reattn_plan* plan);
 float* reattn_plan_q(const reattn_plan* plan);
 float* reattn_plan_out(const reattn_plan* plan);
-/* asynchronous replay on the context stream */
+/* asynchronous replay on the context stream.
+ * A decode plan (n_q == 1, selection on the K1 fast scan with the select fused into its merger
+ * CTA: every BASELINE decode config) reads the cache length from the device, so it stays valid
+ * while the cache grows through reattn_cache_append / _set_total / the plan's own append node:
+ * one graph serves every decode step.  Any other plan is frozen to the cache length it was
+ * built for; launching it after the length changed is an error (ERUNTIME), and so is any plan
+ * after reattn_cache_reserve reallocated the storage it captured. */
 int reattn_plan_launch(reattn_plan* plan);
+/* Append mode (decode plans only): the graph first appends the step's K and V rows
+ * (kv_cache.hpp:54-68, fp32 [n_kv * d] each at reattn_plan_k_in / _v_in) at the device cache
+ * length and advances it, then runs the step -- Engine::forward_block's append-then-attend
+ * (engine.hpp:196-198) in one replay.  Each launch advances the cache's length by one;
+ * ERUNTIME "cache append: capacity exceeded" when the storage is full. */
+int reattn_plan_set_append(reattn_plan* plan, int enable);
+float* reattn_plan_k_in(const reattn_plan* plan);
+float* reattn_plan_v_in(const reattn_plan* plan);
+/* end to end from host memory in append mode: H2D q, k, v; replay; D2H out; synchronise */
+int reattn_plan_step_host(reattn_plan* plan, const float* q_host, const float* k_host,
+                          const float* v_host, float* out_host);
 /* enqueue only the plan's K-scan kernel (no graph) so callers can time it with events */
 int reattn_plan_launch_scan(reattn_plan* plan);
 /* end to end from host memory: H2D q, replay, D2H out, synchronise */

@@ -79,6 +79,9 @@ struct BulkArgs {
     int warm;               // dry-run the merge before griddepcontrol.wait (see merge_parts)
     int local_post;         // kModeLocal launched after the scan (DecodeFork::post)
     int local_hpc;          // kModeLocal: kv heads per CTA, processed one after the other
+    // growing caches: n_local / local_row0 derived from the device-resident cache length
+    const uint32_t* dev_total;
+    uint32_t l_global, l_local;
 };
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -254,8 +257,16 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
     // a post-scan local launch lets the head launch become resident as its CTAs retire
     if (local && B.local_post) asm volatile("griddepcontrol.launch_dependents;");
     if (!local && a.hdr && a.hdr->error != 0) return;
-    const uint32_t L = local ? B.n_local : (a.hdr ? a.hdr->L : a.L_host);
-    const uint32_t rows = B.mode == kModeHead ? L - B.n_local : L;
+    uint32_t n_local = B.n_local, local_row0 = B.local_row0;
+    if (B.dev_total) {  // kv_cache.hpp:65-67 on the device cache length
+        uint32_t total;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(total) : "l"(B.dev_total));
+        const uint32_t g_end = min(total, B.l_global);
+        local_row0 = total - min(total - g_end, B.l_local);
+        n_local = total - local_row0;
+    }
+    const uint32_t L = local ? n_local : (a.hdr ? a.hdr->L : a.L_host);
+    const uint32_t rows = B.mode == kModeHead ? L - n_local : L;
     const int part = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cta_id = blockIdx.y * gridDim.x + blockIdx.x + (local ? 512 : 0);  // trace slot
@@ -334,7 +345,7 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
             uint8_t* st = stages + (size_t)s * kBStageBytes;
             const bool valid = lane < nk;
             const uint32_t cr = !valid ? kNoIndex
-                                : local ? B.local_row0 + k0 + lane
+                                : local ? local_row0 + k0 + lane
                                 : (a.src ? __ldg(a.src + k0 + lane) : k0 + lane);
             const bool own = valid && cr != kNoIndex;  // sharded scopes mask rows owned elsewhere
             const int n_own = __popc(__ballot_sync(0xFFFFFFFFu, own));
@@ -810,6 +821,9 @@ BulkArgs bulk_args(const AttnArgs& a, void* ws, int num_sms, const DecodeFork* f
     B.mode = f ? kModeHead : kModeScope;
     B.n_local = f ? f->n_local : 0;
     B.local_row0 = f ? f->local_row0 : 0;
+    B.dev_total = f ? f->dev_total : nullptr;
+    B.l_global = f ? f->l_global : 0;
+    B.l_local = f ? f->l_local : 0;
     B.ranges = nullptr;
     B.merged = nullptr;
     B.n_parts = bulk_parts(a, num_sms);

@@ -49,13 +49,16 @@ struct StepPlan {
     void* attn_tc_ws = nullptr;
     size_t scratch_bytes = 0;
     uint64_t kernels = 0;
+    // decode plans read the cache length from the device (reattn_cache::dev_total): one graph
+    // serves every decode step while the cache grows (engine.hpp:163-198 appends every step)
+    bool dynamic = false;
 };
 
 void plan_fork(reattn_ctx* ctx, StepPlan& P);
 
 int plan_step(reattn_ctx* ctx, const reattn_cache* cache, const reattn_rope* rope, uint64_t n_q,
               uint64_t n_head, const reattn_selection_config* cfg, int mode, StepPlan& P,
-              const float* q_dev, float* out_dev) {
+              const float* q_dev, float* out_dev, bool allow_dynamic = false) {
     if (n_head % cache->n_kv != 0)
         return set_err(ctx, REATTN_EINVAL, "attend_step: n_head must be a multiple of kv heads");
     if (rope->head_dim != cache->d)
@@ -107,8 +110,32 @@ int plan_step(reattn_ctx* ctx, const reattn_cache* cache, const reattn_rope* rop
     P.attn_tc = (ctx->prefill & REATTN_PREFILL_TENSOR_ATTN) && n_q > 1 && cache->d == 128 &&
                 cache->dtype == kBF16;
     plan_fork(ctx, P);
+    // a decode plan whose selection runs in K1's merger CTA can follow a growing cache: the
+    // scan, the select and the decode attention derive the segments from the device length
+    if (allow_dynamic && P.select && n_q == 1 && P.scan.fast && P.kk == cfg->k &&
+        P.n_kv * cfg->k <= kSmallSelectMax && cache->dev_total) {
+        P.dynamic = true;
+        P.scan.a.dev_total = cache->dev_total;
+        P.scan.a.l_global = (uint32_t)cfg->l_global;
+        P.scan.a.l_local = (uint32_t)cfg->l_local;
+        P.fk.dev_total = cache->dev_total;
+        P.fk.l_global = (uint32_t)cfg->l_global;
+        P.fk.l_local = (uint32_t)cfg->l_local;
+        // buffers sized for the largest scope any later step can have
+        const uint64_t wmax = std::min<uint64_t>(cfg->k_prime, P.n_kv * cfg->k);
+        P.L_upper = (uint32_t)std::min<uint64_t>(P.window, cfg->l_global + wmax * cfg->span_m + cfg->l_local);
+    }
     (void)out_dev;
     return REATTN_OK;
+}
+
+// host copy of the step geometry at the cache's current length (dynamic plans)
+void refresh_geometry(StepPlan& P, const reattn_cache* cache) {
+    if (!P.dynamic) return;
+    P.total = cache->total;
+    P.g_end = cache->global_end();
+    P.l_start = cache->local_start();
+    P.middle = P.l_start - P.g_end;
 }
 
 // Decode local-window fork (DecodeFork in kernels.h): lend R = m * n_kv SMs to the local
@@ -382,15 +409,70 @@ int finish_step_stats(reattn_ctx* ctx, const StepPlan& P, const ScopeHeader& h,
 
 struct reattn_plan {
     reattn_ctx* ctx;
-    const reattn_cache* cache;
+    reattn_cache* cache;
     const reattn_rope* rope;
     StepPlan P;
     void* mem = nullptr;
     float* q = nullptr;
     float* out = nullptr;
+    float* k_in = nullptr;  // append mode: this step's K / V rows [n_kv * d] fp32
+    float* v_in = nullptr;
+    bool append = false;
+    uint64_t generation = 0;  // the cache storage the graph was captured over
+    uint64_t total0 = 0;      // the cache length a frozen (non-dynamic) plan was built for
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
 };
+
+namespace {
+// The plan's graph: [append the step's K/V rows] + the attend_step pipeline.
+int capture_plan(reattn_plan* p) {
+    reattn_ctx* ctx = p->ctx;
+    if (p->exec) cudaGraphExecDestroy(p->exec);
+    if (p->graph) cudaGraphDestroy(p->graph);
+    p->exec = nullptr;
+    p->graph = nullptr;
+    cudaStream_t cs;
+    CU(ctx, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CU(ctx, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    int rc = REATTN_OK;
+    if (p->append) {
+        const cudaError_t e = launch_cache_append_step(p->k_in, p->v_in, p->cache->keys,
+                                                       p->cache->values, p->cache->dtype,
+                                                       p->cache->n_kv, p->cache->d,
+                                                       p->cache->capacity, p->cache->dev_total, cs);
+        if (e != cudaSuccess) rc = set_err(ctx, REATTN_ECUDA, std::string("append capture: ") + cudaGetErrorString(e));
+    }
+    if (!rc) rc = enqueue_step(ctx, p->P, p->cache, p->rope, p->q, p->out, cs, false);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+    cudaStreamDestroy(cs);
+    if (rc || ce != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        return rc ? rc : set_err(ctx, REATTN_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    }
+    p->graph = g;
+    const cudaError_t e = cudaGraphInstantiate(&p->exec, g, 0);
+    if (e != cudaSuccess)
+        return set_err(ctx, REATTN_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    return REATTN_OK;
+}
+
+// A plan replays the graph it captured: the cache storage must be the one it was built over
+// (reserve reallocates), and a frozen plan also its length (replays used to attend
+// a stale scope silently).  Append mode: one more row must fit.
+int check_plan(reattn_plan* p) {
+    if (p->cache->generation != p->generation)
+        return set_err(p->ctx, REATTN_ERUNTIME,
+                       "plan: the cache storage was reallocated (reserve) since the plan was built; rebuild the plan");
+    if (!p->P.dynamic && p->cache->total != p->total0)
+        return set_err(p->ctx, REATTN_ERUNTIME,
+                       "plan: the cache length changed since the plan was built (this plan shape is frozen); rebuild the plan");
+    if (p->append && p->cache->total + 1 > p->cache->capacity)
+        return set_err(p->ctx, REATTN_ERUNTIME, "cache append: capacity exceeded");
+    return REATTN_OK;
+}
+}  // namespace
 
 extern "C" {
 
@@ -506,8 +588,11 @@ int reattn_cache_create(reattn_ctx* ctx, uint64_t n_kv, uint64_t d, uint64_t l_g
     const size_t bytes = n_kv * c->capacity * d * (dtype == REATTN_BF16 ? 2 : 4);
     cudaError_t e = cudaMalloc(&c->keys, bytes);
     if (e == cudaSuccess) e = cudaMalloc(&c->values, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&c->dev_total, sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->dev_total, 0, sizeof(uint32_t), ctx->stream);
     if (e != cudaSuccess) {
         if (c->keys) cudaFree(c->keys);
+        if (c->values) cudaFree(c->values);
         delete c;
         return set_err(ctx, REATTN_ECUDA, std::string("cache allocation: ") + cudaGetErrorString(e));
     }
@@ -519,6 +604,7 @@ void reattn_cache_destroy(reattn_cache* c) {
     if (!c) return;
     cudaFree(c->keys);
     cudaFree(c->values);
+    if (c->dev_total) cudaFree(c->dev_total);
     delete c;
 }
 
@@ -544,8 +630,10 @@ int reattn_cache_append(reattn_ctx* ctx, reattn_cache* c, const float* keys, con
                                 ctx->stream));
     CU(ctx, launch_cache_append(vs, c->values, c->dtype, rows, c->n_kv, c->d, c->capacity,
                                 c->total, ctx->stream));
-    CU(ctx, cudaStreamSynchronize(ctx->stream));
     c->total += rows;  // boundaries follow kv_cache.hpp:65-67 (computed on demand)
+    int rc = cache_sync_total(ctx, c, ctx->stream);
+    if (rc) return rc;
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
     return REATTN_OK;
 }
 
@@ -569,13 +657,14 @@ int reattn_cache_reserve(reattn_ctx* ctx, reattn_cache* c, uint64_t cap) {
     c->keys = nk;
     c->values = nv;
     c->capacity = cap;
+    ++c->generation;  // plans over the old storage are invalid (checked at launch)
     return REATTN_OK;
 }
 
 int reattn_cache_set_total(reattn_ctx* ctx, reattn_cache* c, uint64_t total) {
     if (total > c->capacity) return set_err(ctx, REATTN_EINVAL, "cache: total exceeds capacity");
     c->total = total;
-    return REATTN_OK;
+    return cache_sync_total(ctx, c, ctx->stream);
 }
 
 int reattn_cache_info(const reattn_cache* c, uint64_t* n_kv, uint64_t* d, uint64_t* l_global,
@@ -923,9 +1012,11 @@ int reattn_plan_create(reattn_ctx* ctx, const reattn_cache* cache, const reattn_
     *out = nullptr;
     auto* p = new reattn_plan();
     p->ctx = ctx;
-    p->cache = cache;
+    p->cache = const_cast<reattn_cache*>(cache);  // append mode writes rows (through the graph)
     p->rope = rope;
-    int rc = plan_step(ctx, cache, rope, n_q, n_head, cfg, mode, p->P, nullptr, nullptr);
+    p->generation = cache->generation;
+    p->total0 = cache->total;
+    int rc = plan_step(ctx, cache, rope, n_q, n_head, cfg, mode, p->P, nullptr, nullptr, true);
     if (rc) {
         delete p;
         return rc;
@@ -933,6 +1024,8 @@ int reattn_plan_create(reattn_ctx* ctx, const reattn_cache* cache, const reattn_
     Carver sizer{nullptr, 0, 0};
     sizer.take<float>(n_q * n_head * cache->d);
     sizer.take<float>(n_q * n_head * cache->d);
+    sizer.take<float>(cache->n_kv * cache->d);
+    sizer.take<float>(cache->n_kv * cache->d);
     carve_step(p->P, cache, rope, sizer);
     cudaError_t e = cudaMalloc(&p->mem, sizer.off + 256);
     if (e == cudaSuccess) e = cudaMemset(p->mem, 0, sizer.off + 256);
@@ -944,28 +1037,13 @@ int reattn_plan_create(reattn_ctx* ctx, const reattn_cache* cache, const reattn_
     Carver c{(uint8_t*)p->mem, 0, sizer.off + 256};
     p->q = c.take<float>(n_q * n_head * cache->d);
     p->out = c.take<float>(n_q * n_head * cache->d);
+    p->k_in = c.take<float>(cache->n_kv * cache->d);
+    p->v_in = c.take<float>(cache->n_kv * cache->d);
     carve_step(p->P, cache, rope, c);
-    // capture the step as a graph on a private stream
-    cudaStream_t cs;
-    CU(ctx, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    CU(ctx, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    rc = enqueue_step(ctx, p->P, cache, rope, p->q, p->out, cs, false);
-    cudaGraph_t g = nullptr;
-    cudaError_t ce = cudaStreamEndCapture(cs, &g);
-    cudaStreamDestroy(cs);
-    if (rc || ce != cudaSuccess) {
-        if (g) cudaGraphDestroy(g);
-        cudaFree(p->mem);
-        delete p;
-        return rc ? rc : set_err(ctx, REATTN_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-    }
-    p->graph = g;
-    e = cudaGraphInstantiate(&p->exec, g, 0);
-    if (e != cudaSuccess) {
-        cudaGraphDestroy(g);
-        cudaFree(p->mem);
-        delete p;
-        return set_err(ctx, REATTN_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    rc = capture_plan(p);
+    if (rc) {
+        reattn_plan_destroy(p);
+        return rc;
     }
     *out = p;
     return REATTN_OK;
@@ -983,12 +1061,49 @@ float* reattn_plan_q(const reattn_plan* p) { return p->q; }
 float* reattn_plan_out(const reattn_plan* p) { return p->out; }
 
 int reattn_plan_launch(reattn_plan* p) {
+    int rc = check_plan(p);
+    if (rc) return rc;
     CU(p->ctx, cudaGraphLaunch(p->exec, p->ctx->stream));
+    if (p->append) ++p->cache->total;  // the host mirror of the row the graph appends
+    return REATTN_OK;
+}
+
+int reattn_plan_set_append(reattn_plan* p, int enable) {
+    if (enable && !p->P.dynamic)
+        return set_err(p->ctx, REATTN_EINVAL,
+                       "plan append: needs a decode plan that follows the cache length "
+                       "(n_q == 1, selection on the K1 fast scan with the fused select)");
+    if ((enable != 0) == p->append) return REATTN_OK;
+    CU(p->ctx, cudaStreamSynchronize(p->ctx->stream));
+    p->append = enable != 0;
+    return capture_plan(p);
+}
+float* reattn_plan_k_in(const reattn_plan* p) { return p->k_in; }
+float* reattn_plan_v_in(const reattn_plan* p) { return p->v_in; }
+
+int reattn_plan_step_host(reattn_plan* p, const float* q_host, const float* k_host,
+                          const float* v_host, float* out_host) {
+    reattn_ctx* ctx = p->ctx;
+    int rc = check_plan(p);
+    if (rc) return rc;
+    const size_t qb = p->P.n_q * p->P.n_head * p->cache->d * sizeof(float);
+    const size_t kb = p->cache->n_kv * p->cache->d * sizeof(float);
+    CU(ctx, cudaMemcpyAsync(p->q, q_host, qb, cudaMemcpyHostToDevice, ctx->stream));
+    if (p->append) {
+        CU(ctx, cudaMemcpyAsync(p->k_in, k_host, kb, cudaMemcpyHostToDevice, ctx->stream));
+        CU(ctx, cudaMemcpyAsync(p->v_in, v_host, kb, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    CU(ctx, cudaGraphLaunch(p->exec, ctx->stream));
+    if (p->append) ++p->cache->total;
+    CU(ctx, cudaMemcpyAsync(out_host, p->out, qb, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
     return REATTN_OK;
 }
 
 int reattn_plan_launch_scan(reattn_plan* p) {
     if (!p->P.select) return REATTN_OK;
+    int rc = check_plan(p);
+    if (rc) return rc;
     return enqueue_scan(p->ctx, p->P.scan, p->P.scan_ws, p->ctx->stream, false);
 }
 
@@ -1004,6 +1119,10 @@ int reattn_debug_trace(uint64_t* host_out, uint64_t n) {
 int reattn_plan_run_host(reattn_plan* p, const float* q_host, float* out_host) {
     const size_t bytes = p->P.n_q * p->P.n_head * p->cache->d * sizeof(float);
     reattn_ctx* ctx = p->ctx;
+    if (p->append)
+        return set_err(ctx, REATTN_EINVAL, "plan: append mode takes the step's K/V too (reattn_plan_step_host)");
+    int rc = check_plan(p);
+    if (rc) return rc;
     CU(ctx, cudaMemcpyAsync(p->q, q_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
     CU(ctx, cudaGraphLaunch(p->exec, ctx->stream));
     CU(ctx, cudaMemcpyAsync(out_host, p->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1013,6 +1132,7 @@ int reattn_plan_run_host(reattn_plan* p, const float* q_host, float* out_host) {
 
 int reattn_plan_stats(reattn_plan* p, reattn_step_stats* st) {
     reattn_ctx* ctx = p->ctx;
+    refresh_geometry(p->P, p->cache);
     ScopeHeader h;
     CU(ctx, cudaMemcpyAsync(&h, p->P.hdr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
@@ -1022,6 +1142,7 @@ int reattn_plan_stats(reattn_plan* p, reattn_step_stats* st) {
 int reattn_plan_result(reattn_plan* p, reattn_step_stats* st, uint64_t* span_b_host,
                        uint64_t* span_e_host, double* entropy_host) {
     reattn_ctx* ctx = p->ctx;
+    refresh_geometry(p->P, p->cache);
     ScopeHeader h;
     CU(ctx, cudaMemcpyAsync(&h, p->P.hdr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
@@ -1043,7 +1164,8 @@ int reattn_plan_info(const reattn_plan* p, uint64_t* kernels, uint64_t* scan_byt
                      uint64_t* scope_bytes) {
     const uint64_t esz = p->cache->dtype == REATTN_BF16 ? 2 : 4;
     if (kernels) *kernels = p->P.kernels;
-    if (scan_bytes) *scan_bytes = p->P.select ? p->P.n_kv * p->P.middle * p->P.d * esz : 0;
+    const uint64_t middle = p->P.dynamic ? p->cache->local_start() - p->cache->global_end() : p->P.middle;
+    if (scan_bytes) *scan_bytes = p->P.select ? p->P.n_kv * middle * p->P.d * esz : 0;
     if (scope_bytes) *scope_bytes = p->P.n_kv * (uint64_t)p->P.L_upper * 2 * p->P.d * esz;
     return REATTN_OK;
 }

@@ -280,7 +280,7 @@ int append_kv(reattn_engine* e, reattn_cache* cache, uint64_t layer, uint64_t ro
                                               (int)d, (long long)(cache->capacity * d), (int)nkv));
         }
         cache->total += rows;
-        return REATTN_OK;
+        return cache_sync_total(ctx, cache, ctx->stream);
     }
     int rc = gemm(e, rows, nkv * d, c.d_model, e->h, c.d_model, wk, nkv * d, e->kb, nkv * d, 0.0f);
     if (rc) return rc;

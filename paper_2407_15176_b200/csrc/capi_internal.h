@@ -32,6 +32,10 @@ struct reattn_cache {
     int dtype;
     void* keys = nullptr;
     void* values = nullptr;
+    // the length mirrored on the device (plans read it, so one graph serves every decode step
+    // while the cache grows), and the storage generation (bumped when reserve reallocates)
+    uint32_t* dev_total = nullptr;
+    uint64_t generation = 0;
     uint64_t global_end() const { return std::min(total, l_global); }
     uint64_t local_start() const {
         const uint64_t g = global_end();
@@ -93,6 +97,12 @@ inline int ensure_arena(reattn_ctx* ctx, size_t bytes) {
     // could land after the caller's first copy into the arena
     CU(ctx, cudaMemsetAsync(ctx->arena, 0, nb, ctx->stream));
     ctx->arena_bytes = nb;
+    return REATTN_OK;
+}
+
+// enqueue the device mirror of cache->total (stream-ordered with the plans that read it)
+inline int cache_sync_total(reattn_ctx* ctx, reattn_cache* c, cudaStream_t s) {
+    if (c->dev_total) CU(ctx, launch_set_u32(c->dev_total, (uint32_t)c->total, s));
     return REATTN_OK;
 }
 

@@ -176,6 +176,8 @@ int reattn_snapshot_load_layer(reattn_ctx* ctx, reattn_snapshot* s, uint32_t lay
             }
         }
         c->total = L.total;
+        int rc = cache_sync_total(ctx, c, ctx->stream);
+        if (rc) return rc;
     }
     *out = guard.release();
     return REATTN_OK;

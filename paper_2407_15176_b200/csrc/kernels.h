@@ -66,6 +66,11 @@ struct ScanArgs {
     // fast path: keep the adaptive tile partition in the workspace (private, zero-initialised
     // plan workspaces only)
     int balance = 0;
+    // fast path: a device-resident cache length (plans that survive cache growth).  When set,
+    // count / row0 and the fused select's geometry come from it (kv_cache.hpp:65-67 with
+    // l_global / l_local), and the grid is the full num_sms.
+    const uint32_t* dev_total = nullptr;
+    uint32_t l_global = 0, l_local = 0;
 };
 
 // Fast path: TMA-staged, one thread per key row, q in registers, register top-k.
@@ -180,6 +185,9 @@ struct DecodeFork {
                           // runs its tail, and it completes only after the scan (so the head
                           // launch's griddepcontrol.wait covers both); 0: beside the scan on
                           // local_parts * n_kv lent SMs (side stream)
+    // growing caches: n_local / local_row0 from the device-resident cache length (null: above)
+    const uint32_t* dev_total = nullptr;
+    uint32_t l_global = 0, l_local = 0;
 };
 constexpr int kMaxLocalParts = 32;
 cudaError_t launch_attend_decode_local(const AttnArgs& a, void* ws, int num_sms, const DecodeFork& f,
@@ -238,6 +246,12 @@ cudaError_t launch_decode_combine_sources(const AttnArgs& a, const uint8_t* part
 cudaError_t launch_cache_append(const float* src, void* dst, int dtype, uint64_t rows,
                                 uint64_t n_kv, uint64_t d, uint64_t head_stride, uint64_t row0,
                                 cudaStream_t s);
+// one row per head (rows = 1, [n_kv * d] fp32 K and V) at the device cache length *dev_total,
+// which the kernel then advances by one (a decode step's append inside a plan's graph)
+cudaError_t launch_cache_append_step(const float* k_in, const float* v_in, void* keys, void* values,
+                                     int dtype, uint64_t n_kv, uint64_t d, uint64_t head_stride,
+                                     uint32_t* dev_total, cudaStream_t s);
+cudaError_t launch_set_u32(uint32_t* p, uint32_t v, cudaStream_t s);
 // scope gather to fp32 [n_kv][L][d] (assemble_scope's copies, scope.hpp:63-76).
 cudaError_t launch_gather(const void* base, int dtype, uint64_t n_kv, uint64_t d,
                           uint64_t head_stride, const uint32_t* src, uint32_t L, float* out,

@@ -117,6 +117,50 @@ cudaError_t launch_cache_append(const float* src, void* dst, int dtype, uint64_t
     return cudaGetLastError();
 }
 
+namespace {
+// One decode step's K and V rows (DenseMatrix layout [1][n_kv * d] fp32, kv_cache.hpp:54-68)
+// appended at the device-resident cache length, which is then advanced: the append node of a
+// plan whose graph serves every decode step.  One CTA; thread 0 publishes the new length after
+// the CTA's stores (the next kernel in the stream reads it).
+template <typename T>
+__global__ void __launch_bounds__(256) cache_append_step_kernel(const float* __restrict__ k_in,
+                                                                const float* __restrict__ v_in,
+                                                                T* keys, T* values, uint32_t n_kv,
+                                                                uint32_t d, uint64_t head_stride,
+                                                                uint32_t* dev_total) {
+    const uint32_t row = *(volatile uint32_t*)dev_total;
+    for (uint32_t e = threadIdx.x; e < n_kv * d; e += blockDim.x) {
+        const uint32_t h = e / d, c = e % d;
+        const size_t o = ((size_t)h * head_stride + row) * d + c;
+        store_from_float<T>(keys + o, k_in[e]);
+        store_from_float<T>(values + o, v_in[e]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *(volatile uint32_t*)dev_total = row + 1u;
+}
+
+__global__ void set_u32_kernel(uint32_t* p, uint32_t v) { *p = v; }
+}  // namespace
+
+cudaError_t launch_cache_append_step(const float* k_in, const float* v_in, void* keys, void* values,
+                                     int dtype, uint64_t n_kv, uint64_t d, uint64_t head_stride,
+                                     uint32_t* dev_total, cudaStream_t s) {
+    if (dtype == kBF16)
+        cache_append_step_kernel<__nv_bfloat16><<<1, 256, 0, s>>>(
+            k_in, v_in, (__nv_bfloat16*)keys, (__nv_bfloat16*)values, (uint32_t)n_kv, (uint32_t)d,
+            head_stride, dev_total);
+    else
+        cache_append_step_kernel<float><<<1, 256, 0, s>>>(k_in, v_in, (float*)keys, (float*)values,
+                                                          (uint32_t)n_kv, (uint32_t)d, head_stride,
+                                                          dev_total);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_set_u32(uint32_t* p, uint32_t v, cudaStream_t s) {
+    set_u32_kernel<<<1, 1, 0, s>>>(p, v);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gather(const void* base, int dtype, uint64_t n_kv, uint64_t d,
                           uint64_t head_stride, const uint32_t* src, uint32_t L, float* out,
                           cudaStream_t s) {

@@ -76,7 +76,46 @@ struct FastArgs {
     uint32_t tiles0;  // tiles of CTA 0 (the merger; see the tail below)
     uint32_t part_q, part_r;  // (T - T0) = part_q (G - 1) + part_r
     struct Balance* bal;      // adaptive partition state (plans), or null
+    // device-resident cache length (plans that survive cache growth): when non-null, the middle
+    // (kv_cache.hpp:65-67), the tile partition and the select's geometry are derived from it
+    const uint32_t* dev_total;
+    uint32_t l_global, l_local;
+    int tail_tiles;
 };
+
+// The launch's geometry: from the host (a frozen plan) or from the device cache length.
+struct FastGeo {
+    uint32_t count, tph, T, T0, pq, pr, g_end, l_start, total;
+};
+__device__ __forceinline__ FastGeo fast_geo(const FastArgs& a, uint32_t G, int rows) {
+    FastGeo g;
+    if (!a.dev_total) {
+        g.count = a.count;
+        g.tph = a.tiles_per_head;
+        g.T = a.total_tiles;
+        g.T0 = G == 1 ? g.T : a.tiles0;
+        g.pq = a.part_q;
+        g.pr = a.part_r;
+        g.g_end = a.sel.g_end;
+        g.l_start = a.sel.l_start;
+        g.total = a.sel.total;
+        return g;
+    }
+    uint32_t total;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(total) : "l"(a.dev_total));
+    g.total = total;
+    g.g_end = min(total, a.l_global);
+    g.l_start = total - min(total - g.g_end, a.l_local);
+    g.count = g.l_start - g.g_end;
+    g.tph = (g.count + rows - 1) / rows;
+    g.T = g.tph * (uint32_t)a.n_kv;
+    const uint32_t share = g.T / G;
+    g.T0 = G == 1 ? g.T : (share > (uint32_t)a.tail_tiles ? share - (uint32_t)a.tail_tiles : 0u);
+    const uint32_t rest = g.T - g.T0;
+    g.pq = G > 1 ? rest / (G - 1) : 0u;
+    g.pr = G > 1 ? rest % (G - 1) : 0u;
+    return g;
+}
 
 // Adaptive tile partition.  The scan CTAs do not stream at equal rates (with the decode fork
 // the slowest finish ~10 us after the median, on the same SMs every step), so for long scans
@@ -195,7 +234,8 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const uint32_t G = gridDim.x, b = blockIdx.x;
-    const uint32_t T = a.total_tiles, T0 = G == 1 ? T : a.tiles0;
+    const FastGeo fg = fast_geo(a, G, C::ROWS);
+    const uint32_t T = fg.T, T0 = fg.T0;
     Balance* bal = (a.bal && G <= kBalMaxG && G > 2) ? a.bal : nullptr;
     uint32_t epoch = 0;
     const uint32_t* tab = nullptr;
@@ -205,7 +245,7 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
         if (epoch > 0 && bal->tbv[epoch & 1] == epoch + 1) tab = bal->tb[epoch & 1];
     }
     auto tbeg = [&](uint32_t c) {
-        return tab ? tab[c] : tile_begin(c, G, T, T0, a.part_q, a.part_r);
+        return tab ? tab[c] : tile_begin(c, G, T, T0, fg.pq, fg.pr);
     };
     const uint32_t t_begin = tbeg(b), t_end = tbeg(b + 1);
     const uint64_t t_start = bal ? globaltimer() : 0ull;
@@ -227,8 +267,9 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
     auto issue = [&](uint32_t it) {
         const uint32_t t = t_begin + it;
         const int s = it % C::STAGES;
-        const uint32_t kv = t / a.tiles_per_head, j = t % a.tiles_per_head;
-        const int32_t row = (int32_t)(kv * a.head_stride + a.row0 + (uint64_t)j * C::ROWS);
+        const uint32_t kv = t / fg.tph, j = t % fg.tph;
+        const int32_t row = (int32_t)(kv * a.head_stride + (a.dev_total ? fg.g_end : a.row0) +
+                                      (uint64_t)j * C::ROWS);
         mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
 #pragma unroll
         for (int box = 0; box < C::NBOX; ++box)
@@ -312,7 +353,7 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
         cur_kv = kDryFlush;
         for (uint32_t t = t_begin;; ++t, ++it) {
             const bool done = t >= t_end;
-            const uint32_t kv = done ? kNoIndex : t / a.tiles_per_head, j = t % a.tiles_per_head;
+            const uint32_t kv = done ? kNoIndex : t / fg.tph, j = t % fg.tph;
             if (kv != cur_kv) {
                 if (cur_kv != kNoIndex) flush(cur_kv);
                 if (done) break;
@@ -333,7 +374,7 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
             const uint32_t ph = (it / C::STAGES) & 1u;
             mbar_wait(&full[s], ph);
             const uint32_t row = j * C::ROWS + (uint32_t)tid;
-            if (row < a.count) {
+            if (row < fg.count) {
                 const uint32_t sbase =
                     smem_u32(stages + (size_t)s * C::STAGE_BYTES) + (uint32_t)tid * 128u;
                 f2_t a0 = f2_pack(0u, 0u), a1 = a0, a2 = a0, a3 = a0;
@@ -405,7 +446,14 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
     __shared__ SmallSelectSmem ssel;
     constexpr int kMergeCache = 64;  // kv heads whose covering CTA range is cached
     __shared__ uint32_t s_b0[kMergeCache], s_b1[kMergeCache];
-    const int kk = (int)min((uint32_t)k, a.count);
+    const int kk = (int)min((uint32_t)k, fg.count);
+    SmallSelectIO sel = a.sel;  // the select's geometry (device-derived for growing caches)
+    if (a.dev_total) {
+        sel.middle_len = fg.count;
+        sel.g_end = fg.g_end;
+        sel.l_start = fg.l_start;
+        sel.total = fg.total;
+    }
     const int nwarps = C::THREADS / 32;
 #pragma unroll 1
     for (int pass = 0; pass < 2; ++pass) {
@@ -485,7 +533,7 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
             uint32_t li[KMAX];
             topk_reset<KMAX>(ls, li);
             // CTAs whose (non-empty) tile range meets this head's tiles [h0, h1): contiguous
-            const uint32_t h0 = (uint32_t)kv * a.tiles_per_head, h1 = h0 + a.tiles_per_head;
+            const uint32_t h0 = (uint32_t)kv * fg.tph, h1 = h0 + fg.tph;
             // (computed in the dry pass and kept in shared memory: the partition is fixed for
             // the launch)
             uint32_t b0 = G, b1 = 0;
@@ -556,7 +604,7 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
                 a.trace[1025] = a.trace[1028] = globaltimer();
                 a.trace[1040] = clock64();
             }
-            small_select_scope_smem(a.sel, ssel, dry ? nullptr : a.trace, dry);
+            small_select_scope_smem(sel, ssel, dry ? nullptr : a.trace, dry);
             if (a.trace && !dry) {
                 __syncthreads();
                 if (tid == 0) a.trace[1026] = globaltimer();
@@ -763,7 +811,12 @@ cudaError_t launch_scan_fast(const ScanArgs& a, const CUtensorMap& kmap, void* w
     f.ticket = (unsigned int*)ws;
     f.slot_idx = (uint32_t*)(ws + 256);
     f.slot_score = (float*)(ws + 256 + (size_t)a.n_kv * num_sms * 8 * sizeof(uint32_t));
-    const int G = (int)std::min<uint32_t>((uint32_t)std::max(1, num_sms), f.total_tiles);
+    // a growing cache keeps the grid of the plan: CTAs without tiles are fine
+    const int G = a.dev_total ? std::max(1, num_sms)
+                              : (int)std::min<uint32_t>((uint32_t)std::max(1, num_sms), f.total_tiles);
+    f.dev_total = a.dev_total;
+    f.l_global = a.l_global;
+    f.l_local = a.l_local;
     f.idx_out = a.idx_out;
     f.score_out = a.score_out;
     f.fuse_select = a.fuse_select;
@@ -776,6 +829,7 @@ cudaError_t launch_scan_fast(const ScanArgs& a, const CUtensorMap& kmap, void* w
             const char* e = std::getenv("REATTN_TAIL_TILES");
             return e ? std::atoi(e) : 10;
         }();
+        f.tail_tiles = tail_tiles;
         const uint32_t share = f.total_tiles / (uint32_t)std::max(1, std::min<int>(num_sms, (int)f.total_tiles));
         f.tiles0 = share > (uint32_t)tail_tiles ? share - (uint32_t)tail_tiles : 0u;
         const uint32_t rest = G > 1 ? f.total_tiles - f.tiles0 : 0u;

@@ -157,6 +157,10 @@ SIGNATURES = [
     ("reattn_plan_stats", C.c_int, [vp, C.POINTER(StepStats)]),
     ("reattn_plan_info", C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
     ("reattn_plan_result", C.c_int, [vp, C.POINTER(StepStats), vp, vp, vp]),
+    ("reattn_plan_set_append", C.c_int, [vp, C.c_int]),
+    ("reattn_plan_k_in", vp, [vp]),
+    ("reattn_plan_v_in", vp, [vp]),
+    ("reattn_plan_step_host", C.c_int, [vp, vp, vp, vp, vp]),
     ("reattn_batch_plan_create", C.c_int, [vp, C.POINTER(vp), C.c_uint32, vp, u64, vp, C.c_int,
                                            C.POINTER(vp)]),
     ("reattn_batch_plan_destroy", None, [vp]),
@@ -537,6 +541,19 @@ class Plan:
 
     def launch(self) -> None:
         self.ctx.check(self.ctx.lib.reattn_plan_launch(self.h))
+
+    def set_append(self, enable: bool = True) -> None:
+        """Append mode: each launch first appends the step's K/V rows (self.k_in / self.v_in,
+        [n_kv * d] fp32 in DenseMatrix layout) to the cache, then runs the step."""
+        import torch
+        self.ctx.check(self.ctx.lib.reattn_plan_set_append(self.h, int(enable)))
+        n = self.cache.n_kv * self.cache.d
+        self.k_in = _wrap_device(self.ctx.lib.reattn_plan_k_in(self.h), n, torch.float32, self.ctx.device)
+        self.v_in = _wrap_device(self.ctx.lib.reattn_plan_v_in(self.h), n, torch.float32, self.ctx.device)
+
+    def step_host(self, q_host, k_host, v_host, out_host) -> None:
+        self.ctx.check(self.ctx.lib.reattn_plan_step_host(self.h, _ptr(q_host), _ptr(k_host),
+                                                          _ptr(v_host), _ptr(out_host)))
 
     def launch_scan(self) -> None:
         self.ctx.check(self.ctx.lib.reattn_plan_launch_scan(self.h))
