@@ -109,7 +109,8 @@ int reattn_cache_create(reattn_ctx* ctx, uint64_t n_kv, uint64_t d, uint64_t l_g
 void reattn_cache_destroy(reattn_cache* cache);
 /* Grow the storage to new_capacity rows per head (existing rows are kept). */
 int reattn_cache_reserve(reattn_ctx* ctx, reattn_cache* cache, uint64_t new_capacity);
-/* kv_cache.hpp:54-68 append: rows x (n_kv*d) fp32 in DenseMatrix layout (host or device). */
+/* kv_cache.hpp:54-68 append: rows x (n_kv*d) fp32 in DenseMatrix layout (host or device;
+ * device rows are appended in stream order, host rows synchronously). */
 int reattn_cache_append(reattn_ctx* ctx, reattn_cache* cache, const float* keys,
                         const float* values, uint64_t rows, int src_on_device);
 /* Declare `total` rows already written into the storage (bulk fills, e.g. benchmarks). */
@@ -219,6 +220,10 @@ int reattn_plan_launch(reattn_plan* plan);
  * (engine.hpp:196-198) in one replay.  Each launch advances the cache's length by one;
  * ERUNTIME "cache append: capacity exceeded" when the storage is full. */
 int reattn_plan_set_append(reattn_plan* plan, int enable);
+/* 1 when the plan follows the cache length (a decode plan, see reattn_plan_launch), else 0 */
+int reattn_plan_follows_cache(const reattn_plan* plan);
+/* the cache storage generation the plan was captured over (a reserve bumps the cache's) */
+uint64_t reattn_plan_cache_generation(const reattn_plan* plan);
 float* reattn_plan_k_in(const reattn_plan* plan);
 float* reattn_plan_v_in(const reattn_plan* plan);
 /* end to end from host memory in append mode: H2D q, k, v; replay; D2H out; synchronise */

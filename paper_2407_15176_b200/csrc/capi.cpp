@@ -633,7 +633,9 @@ int reattn_cache_append(reattn_ctx* ctx, reattn_cache* c, const float* keys, con
     c->total += rows;  // boundaries follow kv_cache.hpp:65-67 (computed on demand)
     int rc = cache_sync_total(ctx, c, ctx->stream);
     if (rc) return rc;
-    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    // host rows were staged in the context arena: drain before it can be reused (device
+    // sources stay asynchronous, stream-ordered with the steps that read them)
+    if (!src_on_device) CU(ctx, cudaStreamSynchronize(ctx->stream));
     return REATTN_OK;
 }
 
@@ -1078,6 +1080,8 @@ int reattn_plan_set_append(reattn_plan* p, int enable) {
     p->append = enable != 0;
     return capture_plan(p);
 }
+int reattn_plan_follows_cache(const reattn_plan* p) { return p->P.dynamic ? 1 : 0; }
+uint64_t reattn_plan_cache_generation(const reattn_plan* p) { return p->generation; }
 float* reattn_plan_k_in(const reattn_plan* p) { return p->k_in; }
 float* reattn_plan_v_in(const reattn_plan* p) { return p->v_in; }
 

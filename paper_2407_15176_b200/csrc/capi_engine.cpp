@@ -204,7 +204,11 @@ struct reattn_engine {
     float *x = nullptr, *h = nullptr, *q = nullptr, *kb = nullptr, *vb = nullptr, *attn = nullptr,
           *gate = nullptr, *up = nullptr, *logits = nullptr;
     std::vector<uint64_t> sb, se;
+    // decode: one CUDA-graph plan per layer that follows the growing cache (reattn_plan_*),
+    // launched without a host synchronisation; their stats are read once per forward block
+    std::vector<reattn_plan*> plans;
     ~reattn_engine() {
+        for (auto* p : plans) reattn_plan_destroy(p);
         for (auto* c : caches) reattn_cache_destroy(c);
         if (rope) reattn_rope_destroy(rope);
         if (blas) cublasDestroy(blas);
@@ -289,37 +293,76 @@ int append_kv(reattn_engine* e, reattn_cache* cache, uint64_t layer, uint64_t ro
     return reattn_cache_append(ctx, cache, e->kb, e->vb, rows, 1);
 }
 
+// The layer's decode plan, when the layer's cache has a middle to select from (the plan then
+// follows the cache as it grows, engine.hpp:163-198); rebuilt after a reserve reallocated the
+// cache.  nullptr: this step runs the synchronous attend_step.
+reattn_plan* layer_plan(reattn_engine* e, uint64_t l) {
+    reattn_plan*& p = e->plans[l];
+    const reattn_cache* cache = e->caches[l];
+    if (p && reattn_plan_cache_generation(p) != cache->generation) {
+        reattn_plan_destroy(p);
+        p = nullptr;
+    }
+    if (p) return p;
+    const uint64_t middle = cache->local_start() - cache->global_end();
+    if (e->mode != REATTN_MODE_REATTENTION || e->sel.k_prime == 0 || middle < e->sel.k) return nullptr;
+    reattn_plan* np = nullptr;
+    if (reattn_plan_create(e->ctx, cache, e->rope, 1, e->w->cfg.n_head, &e->sel, e->mode, &np))
+        return nullptr;  // (the synchronous step reports any error itself)
+    if (!reattn_plan_follows_cache(np)) {
+        reattn_plan_destroy(np);
+        return nullptr;
+    }
+    return p = np;
+}
+
+void fold_stats(reattn_engine* e, uint64_t l, const reattn_step_stats& st) {
+    auto& sp = e->spans[l];
+    sp.clear();
+    for (uint64_t i = 0; i < st.n_spans; ++i) sp.emplace_back(e->sb[i], e->se[i]);
+    reattn_run_stats& S = e->stats;  // engine.hpp:64, :100-112 accumulation
+    if (!st.coverage_total) S.coverage_total = 0;
+    S.ood_positions += st.ood_positions;
+    S.entropy_max = std::max(S.entropy_max, st.entropy_max);
+    S.entropy_sum += st.entropy_sum;
+    S.entropy_rows += st.entropy_rows;
+    S.scope_len_max = std::max(S.scope_len_max, st.scope_len);
+    S.max_position_used = std::max(S.max_position_used, st.max_position_used);
+    S.peak_scratch_bytes = std::max(S.peak_scratch_bytes, st.peak_scratch_bytes);
+}
+
 // engine.hpp:191-205 over e->x (rows x d_model)
 int forward_block(reattn_engine* e, uint64_t rows) {
     reattn_ctx* ctx = e->ctx;
     const reattn_model_config& c = e->w->cfg;
     const uint64_t D = c.d_model, QW = c.n_head * c.d_head, F = c.d_ff;
+    const uint64_t cap = std::max<uint64_t>(1, e->sel.k_prime);
+    e->sb.resize(cap);
+    e->se.resize(cap);
+    if (e->plans.size() != c.n_layer) e->plans.assign(c.n_layer, nullptr);
+    std::vector<reattn_plan*> launched(c.n_layer, nullptr);
     for (uint64_t l = 0; l < c.n_layer; ++l) {
         CU(ctx, launch_rmsnorm(e->x, rows, D, cslot(e->w, REATTN_W_NORM_ATTN, l), e->h, ctx->stream));
-        int rc = gemm(e, rows, QW, D, e->h, D, cslot(e->w, REATTN_W_WQ, l), QW, e->q, QW, 0.0f);
+        int rc = append_kv(e, e->caches[l], l, rows);  // before attend_step (engine.hpp:196-198)
         if (rc) return rc;
-        if ((rc = append_kv(e, e->caches[l], l, rows))) return rc;
-        reattn_step_stats st{};
-        const uint64_t cap = std::max<uint64_t>(1, e->sel.k_prime);
-        e->sb.resize(cap);
-        e->se.resize(cap);
-        rc = reattn_attend_step(ctx, e->caches[l], e->rope, e->q, rows, c.n_head, &e->sel, e->mode,
-                                e->attn, &st, e->sb.data(), e->se.data(), nullptr);
-        if (rc) return rc;
-        auto& sp = e->spans[l];
-        sp.clear();
-        for (uint64_t i = 0; i < st.n_spans; ++i) sp.emplace_back(e->sb[i], e->se[i]);
-        reattn_run_stats& S = e->stats;  // engine.hpp:64, :100-112 accumulation
-        if (!st.coverage_total) S.coverage_total = 0;
-        S.ood_positions += st.ood_positions;
-        S.entropy_max = std::max(S.entropy_max, st.entropy_max);
-        S.entropy_sum += st.entropy_sum;
-        S.entropy_rows += st.entropy_rows;
-        S.scope_len_max = std::max(S.scope_len_max, st.scope_len);
-        S.max_position_used = std::max(S.max_position_used, st.max_position_used);
-        S.peak_scratch_bytes = std::max(S.peak_scratch_bytes, st.peak_scratch_bytes);
+        reattn_plan* pl = rows == 1 ? layer_plan(e, l) : nullptr;
+        float* qd = pl ? reattn_plan_q(pl) : e->q;
+        if ((rc = gemm(e, rows, QW, D, e->h, D, cslot(e->w, REATTN_W_WQ, l), QW, qd, QW, 0.0f)))
+            return rc;
+        const float* attn = e->attn;
+        if (pl) {  // the graph replay, no host synchronisation; stats after the block
+            if ((rc = reattn_plan_launch(pl))) return rc;
+            launched[l] = pl;
+            attn = reattn_plan_out(pl);
+        } else {
+            reattn_step_stats st{};
+            rc = reattn_attend_step(ctx, e->caches[l], e->rope, e->q, rows, c.n_head, &e->sel,
+                                    e->mode, e->attn, &st, e->sb.data(), e->se.data(), nullptr);
+            if (rc) return rc;
+            fold_stats(e, l, st);
+        }
         // x += attn · wo
-        if ((rc = gemm(e, rows, D, D, e->attn, D, cslot(e->w, REATTN_W_WO, l), D, e->x, D, 1.0f)))
+        if ((rc = gemm(e, rows, D, D, attn, D, cslot(e->w, REATTN_W_WO, l), D, e->x, D, 1.0f)))
             return rc;
         CU(ctx, launch_rmsnorm(e->x, rows, D, cslot(e->w, REATTN_W_NORM_FFN, l), e->h, ctx->stream));
         if ((rc = gemm(e, rows, F, D, e->h, D, cslot(e->w, REATTN_W_GATE, l), F, e->gate, F, 0.0f)))
@@ -329,6 +372,14 @@ int forward_block(reattn_engine* e, uint64_t rows) {
         CU(ctx, launch_silu_mul(e->gate, e->up, rows * F, ctx->stream));
         if ((rc = gemm(e, rows, D, F, e->gate, F, cslot(e->w, REATTN_W_DOWN, l), D, e->x, D, 1.0f)))
             return rc;
+    }
+    // the plans' stats, in layer order (one synchronisation per block, inside plan_result)
+    for (uint64_t l = 0; l < c.n_layer; ++l) {
+        if (!launched[l]) continue;
+        reattn_step_stats st{};
+        int rc = reattn_plan_result(launched[l], &st, e->sb.data(), e->se.data(), nullptr);
+        if (rc) return rc;
+        fold_stats(e, l, st);
     }
     e->last_rows = rows;
     return REATTN_OK;
@@ -573,6 +624,8 @@ int reattn_engine_create(reattn_ctx* ctx, const reattn_weights* w, const reattn_
 int reattn_engine_reset(reattn_engine* e) {
     reattn_ctx* ctx = e->ctx;
     const reattn_model_config& c = e->w->cfg;
+    for (auto* p : e->plans) reattn_plan_destroy(p);
+    e->plans.assign(c.n_layer, nullptr);
     for (auto* cache : e->caches) reattn_cache_destroy(cache);
     e->caches.assign(c.n_layer, nullptr);
     const uint64_t cap0 = std::max<uint64_t>(e->sel.l_global + e->sel.l_local, 1024);

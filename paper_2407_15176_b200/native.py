@@ -158,6 +158,8 @@ SIGNATURES = [
     ("reattn_plan_info", C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
     ("reattn_plan_result", C.c_int, [vp, C.POINTER(StepStats), vp, vp, vp]),
     ("reattn_plan_set_append", C.c_int, [vp, C.c_int]),
+    ("reattn_plan_follows_cache", C.c_int, [vp]),
+    ("reattn_plan_cache_generation", u64, [vp]),
     ("reattn_plan_k_in", vp, [vp]),
     ("reattn_plan_v_in", vp, [vp]),
     ("reattn_plan_step_host", C.c_int, [vp, vp, vp, vp, vp]),
