@@ -85,6 +85,77 @@ struct ScoredCandidate {
 
 using PerHeadTopk = std::vector<std::vector<std::vector<TopkEntry>>>;
 
+namespace detail {
+
+// selection.hpp:81-135: the running top-k buffer (host; the device scans keep the same rule in
+// registers).  Filled unsorted; once full, the worst entry -- lowest score, then highest
+// index -- is cached, and only a strictly greater score replaces it, so equal scores keep the
+// lower (earlier) index.  sorted() orders by score desc, index asc.
+struct TopkBuffer {
+    std::vector<TopkEntry> entries;
+    std::size_t cap = 0;
+    std::size_t worst = 0;
+    float threshold = 0.0f;
+
+    void init(std::size_t k) {
+        cap = k;
+        entries.clear();
+        entries.reserve(k);
+        worst = 0;
+        threshold = 0.0f;
+    }
+    bool full() const { return entries.size() == cap; }
+    void refresh_worst() {
+        std::size_t w = 0;
+        for (std::size_t i = 1; i < entries.size(); ++i) {
+            const bool lower = entries[i].score < entries[w].score;
+            const bool tie_later = entries[i].score == entries[w].score && entries[i].index > entries[w].index;
+            if (lower || tie_later) w = i;
+        }
+        worst = w;
+        threshold = entries.empty() ? 0.0f : entries[w].score;
+    }
+    void fill(std::size_t index, float score) {
+        entries.push_back(TopkEntry{index, score});
+        if (full()) refresh_worst();
+    }
+    void replace_worst(std::size_t index, float score) {  // caller checked score > threshold
+        entries[worst] = TopkEntry{index, score};
+        refresh_worst();
+    }
+    void offer(std::size_t index, float score) {
+        if (!full())
+            fill(index, score);
+        else if (score > threshold)
+            replace_worst(index, score);
+    }
+    std::vector<TopkEntry> sorted() const {
+        std::vector<TopkEntry> out(entries);
+        std::stable_sort(out.begin(), out.end(), [](const TopkEntry& x, const TopkEntry& y) {
+            return x.score != y.score ? x.score > y.score : x.index < y.index;
+        });
+        return out;
+    }
+};
+
+// selection.hpp:139-156 on the device (csrc/dense.cu): each kv group's mean query, a sequential
+// fp32 sum times float(1 / group).
+inline DenseMatrix group_mean_queries(const DenseMatrix& queries, std::size_t n_heads,
+                                      std::size_t n_kv_heads, std::size_t d) {
+    DenseMatrix mq(queries.rows, n_kv_heads * d);
+    if (n_kv_heads == 0 || n_heads % n_kv_heads != 0)
+        throw std::invalid_argument("fused_topk_scores: n_heads must be a multiple of kv heads");
+    if (mq.values.empty()) return mq;
+    gpu::DeviceBuffer<float> q, out(mq.values.size());
+    q.upload(queries.values.data(), queries.values.size());
+    gpu::check(reattn_group_mean(gpu::context(), q.get(), queries.rows, n_heads, n_kv_heads, d,
+                                 out.get()));
+    mq.values = out.to_vector(mq.values.size());
+    return mq;
+}
+
+}  // namespace detail
+
 // fused_topk_scores on a device view (no copy of the middle).
 inline PerHeadTopk fused_topk_scores(const DenseMatrix& queries, std::size_t n_heads,
                                      const DeviceKeySegmentView& mid, const SelectionConfig& cfg,

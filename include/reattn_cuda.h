@@ -161,6 +161,30 @@ int reattn_fused_topk(reattn_ctx* ctx, const float* q_dev, uint64_t n_q, uint64_
                       uint64_t row0, uint64_t count, uint64_t d, uint64_t k,
                       uint32_t* idx_out_dev, float* score_out_dev, uint64_t* n_out,
                       uint64_t* scratch_bytes);
+/* naive_topk_scores (selection_reference.hpp:18-69): the same lists as reattn_fused_topk by an
+ * independent route -- the full middle x n_q score matrix materialised (scratch linear in
+ * `count`, the reference's point of comparison), then each row's top-k.  k <= 64.  Same
+ * arguments as reattn_fused_topk.  Synchronous. */
+int reattn_naive_topk(reattn_ctx* ctx, const float* q_dev, uint64_t n_q, uint64_t n_heads,
+                      const void* keys_dev, int key_dtype, uint64_t n_kv, uint64_t head_stride,
+                      uint64_t row0, uint64_t count, uint64_t d, uint64_t k,
+                      uint32_t* idx_out_dev, float* score_out_dev, uint64_t* n_out,
+                      uint64_t* scratch_bytes);
+/* detail::group_mean_queries (selection.hpp:139-156): q [n_q][n_heads*d] -> [n_q][n_kv*d],
+ * sequential fp32 adds times float(1/group).  Synchronous. */
+int reattn_group_mean(reattn_ctx* ctx, const float* q_dev, uint64_t n_q, uint64_t n_heads,
+                      uint64_t n_kv, uint64_t d, float* out_dev);
+/* dot_f32 (dense_matrix.hpp:41-56) of n row pairs a[i], b[i] of length d: the reference's 8
+ * lanes and tree, with the context's lane arithmetic (reattn_ctx_set_lanes).  Synchronous. */
+int reattn_dot_f32(reattn_ctx* ctx, const float* a_dev, const float* b_dev, uint64_t n, uint64_t d,
+                   float* out_dev);
+/* dot_f64 (dense_matrix.hpp:59-74), same layout.  Synchronous. */
+int reattn_dot_f64(reattn_ctx* ctx, const float* a_dev, const float* b_dev, uint64_t n, uint64_t d,
+                   double* out_dev);
+/* matmul (dense_matrix.hpp:77-90): c[m][n] = a[m][k] b[k][n], row-major, each element summed
+ * in k order with unfused fp32 multiply-adds, as the reference.  Synchronous. */
+int reattn_matmul(reattn_ctx* ctx, const float* a_dev, const float* b_dev, uint64_t m, uint64_t k,
+                  uint64_t n, float* c_dev);
 /* tally_candidates + vote (selection.hpp:252-286) over a flat candidate list.  Synchronous. */
 int reattn_vote(reattn_ctx* ctx, const uint32_t* idx_dev, const float* score_dev, uint64_t n,
                 uint64_t k_prime, uint32_t* winners_dev, uint64_t* n_winners);

@@ -801,6 +801,77 @@ int reattn_fused_topk(reattn_ctx* ctx, const float* q_dev, uint64_t n_q, uint64_
     return REATTN_OK;
 }
 
+int reattn_naive_topk(reattn_ctx* ctx, const float* q_dev, uint64_t n_q, uint64_t n_heads,
+                      const void* keys_dev, int key_dtype, uint64_t n_kv, uint64_t head_stride,
+                      uint64_t row0, uint64_t count, uint64_t d, uint64_t k, uint32_t* idx_out,
+                      float* score_out, uint64_t* n_out, uint64_t* scratch_bytes) {
+    if (n_kv == 0 || n_heads % n_kv != 0)
+        return set_err(ctx, REATTN_EINVAL, "naive_topk_scores: n_heads must be a multiple of kv heads");
+    if (k == 0) return set_err(ctx, REATTN_EINVAL, "selection: k must be >= 1");
+    if (k > 64) return set_err(ctx, REATTN_EINVAL, "naive_topk_scores: k exceeds device capacity (64)");
+    if (count >= (1ull << 32)) return set_err(ctx, REATTN_EINVAL, "naive_topk_scores: middle too long");
+    if (n_out) *n_out = std::min(k, count);
+    // the reference's meter (selection_reference.hpp:37-41): mq + the score matrix (+ its
+    // order buffer, which the device selection does not need)
+    const size_t ws = naive_topk_workspace(n_q, n_kv, count, d);
+    if (scratch_bytes) *scratch_bytes = ws;
+    if (count == 0 || n_q == 0) return REATTN_OK;
+    int rc = ensure_arena(ctx, ws + 256);
+    if (rc) return rc;
+    ScanArgs a{};
+    a.q = q_dev;
+    a.n_q = (int)n_q;
+    a.n_heads = (int)n_heads;
+    a.n_kv = (int)n_kv;
+    a.d = (int)d;
+    a.keys = keys_dev;
+    a.dtype = key_dtype;
+    a.head_stride = head_stride;
+    a.row0 = row0;
+    a.count = (uint32_t)count;
+    a.k = (int)k;
+    a.lanes = ctx->lanes;
+    a.idx_out = idx_out;
+    a.score_out = score_out;
+    CU(ctx, launch_naive_topk(a, ctx->arena, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_dot_f32(reattn_ctx* ctx, const float* a, const float* b, uint64_t n, uint64_t d,
+                   float* out) {
+    if (n == 0) return REATTN_OK;
+    CU(ctx, launch_dot_f32(a, b, n, d, ctx->lanes, out, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_dot_f64(reattn_ctx* ctx, const float* a, const float* b, uint64_t n, uint64_t d,
+                   double* out) {
+    if (n == 0) return REATTN_OK;
+    CU(ctx, launch_dot_f64(a, b, n, d, out, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_matmul(reattn_ctx* ctx, const float* a, const float* b, uint64_t m, uint64_t k,
+                  uint64_t n, float* c) {
+    if (m * n == 0) return REATTN_OK;
+    CU(ctx, launch_matmul(a, b, m, k, n, c, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_group_mean(reattn_ctx* ctx, const float* q, uint64_t n_q, uint64_t n_heads,
+                      uint64_t n_kv, uint64_t d, float* out) {
+    if (n_kv == 0 || n_heads % n_kv != 0)
+        return set_err(ctx, REATTN_EINVAL, "fused_topk_scores: n_heads must be a multiple of kv heads");
+    if (n_q * n_kv * d == 0) return REATTN_OK;
+    CU(ctx, launch_group_mean(q, n_q, n_heads, n_kv, d, out, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
 int reattn_vote(reattn_ctx* ctx, const uint32_t* idx_dev, const float* score_dev, uint64_t n,
                 uint64_t k_prime, uint32_t* winners_dev, uint64_t* n_winners) {
     *n_winners = 0;

@@ -241,6 +241,20 @@ cudaError_t launch_attend_decode_ranges(const AttnArgs& a, void* ws, int num_sms
 cudaError_t launch_decode_combine_sources(const AttnArgs& a, const uint8_t* parts, int n_src,
                                           size_t src_stride, cudaStream_t s);
 
+// ---- dense numerics of the drop-in API (dense.cu) ------------------------------------
+cudaError_t launch_dot_f32(const float* a, const float* b, uint64_t n, uint64_t d, int lanes,
+                           float* out, cudaStream_t s);
+cudaError_t launch_dot_f64(const float* a, const float* b, uint64_t n, uint64_t d, double* out,
+                           cudaStream_t s);
+cudaError_t launch_matmul(const float* a, const float* b, uint64_t m, uint64_t k, uint64_t n,
+                          float* c, cudaStream_t s);
+cudaError_t launch_group_mean(const float* q, uint64_t n_q, uint64_t n_heads, uint64_t n_kv,
+                              uint64_t d, float* out, cudaStream_t s);
+// naive_topk_scores (selection_reference.hpp:18-69): materialised scores, then row top-k
+// (k <= 64); ws: naive_topk_workspace bytes
+size_t naive_topk_workspace(uint64_t n_q, uint64_t n_kv, uint64_t count, uint64_t d);
+cudaError_t launch_naive_topk(const ScanArgs& a, void* ws, cudaStream_t s);
+
 // ---- misc kernels ------------------------------------------------------------------
 // rows x (n_kv*d) fp32 (DenseMatrix layout) -> head-major [n_kv][head_stride][d] at row0.
 cudaError_t launch_cache_append(const float* src, void* dst, int dtype, uint64_t rows,

@@ -138,6 +138,12 @@ SIGNATURES = [
     ("reattn_rope_rotate", C.c_int, [vp, vp, vp, vp, u64]),
     ("reattn_fused_topk", C.c_int, [vp, vp, u64, u64, vp, C.c_int, u64, u64, u64, u64, u64, u64,
                                     vp, vp, C.POINTER(u64), C.POINTER(u64)]),
+    ("reattn_naive_topk", C.c_int, [vp, vp, u64, u64, vp, C.c_int, u64, u64, u64, u64, u64, u64,
+                                    vp, vp, C.POINTER(u64), C.POINTER(u64)]),
+    ("reattn_group_mean", C.c_int, [vp, vp, u64, u64, u64, u64, vp]),
+    ("reattn_dot_f32", C.c_int, [vp, vp, vp, u64, u64, vp]),
+    ("reattn_dot_f64", C.c_int, [vp, vp, vp, u64, u64, vp]),
+    ("reattn_matmul", C.c_int, [vp, vp, vp, u64, u64, u64, vp]),
     ("reattn_vote", C.c_int, [vp, vp, vp, u64, u64, vp, C.POINTER(u64)]),
     ("reattn_tally", C.c_int, [vp, vp, vp, u64, vp, vp, vp, C.POINTER(u64)]),
     ("reattn_expand_spans", C.c_int, [vp, vp, u64, u64, u64, C.c_int, vp, vp, C.POINTER(u64)]),
@@ -301,6 +307,28 @@ class Context:
                                               _ptr(idx_out), _ptr(score_out), C.byref(n_out),
                                               C.byref(scratch)))
         return n_out.value, scratch.value
+
+    def naive_topk(self, q, n_heads: int, keys, n_kv: int, head_stride: int, row0: int,
+                   count: int, d: int, k: int, idx_out, score_out, key_dtype: int) -> tuple:
+        n_out, scratch = u64(), u64()
+        self.check(self.lib.reattn_naive_topk(self.h, _ptr(q), q.shape[0], n_heads, _ptr(keys),
+                                              key_dtype, n_kv, head_stride, row0, count, d, k,
+                                              _ptr(idx_out), _ptr(score_out), C.byref(n_out),
+                                              C.byref(scratch)))
+        return n_out.value, scratch.value
+
+    def group_mean(self, q, n_heads: int, n_kv: int, d: int, out) -> None:
+        self.check(self.lib.reattn_group_mean(self.h, _ptr(q), q.shape[0], n_heads, n_kv, d, _ptr(out)))
+
+    def dot_f32(self, a, b, out) -> None:
+        self.check(self.lib.reattn_dot_f32(self.h, _ptr(a), _ptr(b), a.shape[0], a.shape[1], _ptr(out)))
+
+    def dot_f64(self, a, b, out) -> None:
+        self.check(self.lib.reattn_dot_f64(self.h, _ptr(a), _ptr(b), a.shape[0], a.shape[1], _ptr(out)))
+
+    def matmul(self, a, b, out) -> None:
+        self.check(self.lib.reattn_matmul(self.h, _ptr(a), _ptr(b), a.shape[0], a.shape[1],
+                                          b.shape[1], _ptr(out)))
 
     def vote(self, idx, score, k_prime: int, winners_out) -> int:
         n = u64()

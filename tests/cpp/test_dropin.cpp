@@ -597,6 +597,143 @@ static void test_engine() {
     }
 }
 
+static void test_dense_and_naive() {
+    std::mt19937 rng(1234);
+    std::uniform_real_distribution<float> dist(-1.0f, 1.0f);
+    // dense_matrix.hpp:41-74 dot lanes (test_numerics.cpp:335-347 style), bit for bit
+    for (std::size_t d : {1, 5, 8, 16, 31, 64, 128, 200}) {
+        std::vector<float> a(d), b(d);
+        for (auto& v : a) v = dist(rng);
+        for (auto& v : b) v = dist(rng);
+        const float f = dot_f32(a.data(), b.data(), d), fo = oracle_dot_f32(a.data(), b.data(), d);
+        CHECK(std::memcmp(&f, &fo, 4) == 0 || (f == 0.0f && fo == 0.0f), "dot_f32 d=%zu %g %g", d, f, fo);
+        const double g = dot_f64(a.data(), b.data(), d), go = oracle_dot_f64(a.data(), b.data(), d);
+        CHECK(g == go, "dot_f64 d=%zu %.17g %.17g", d, g, go);
+    }
+    // dense_matrix.hpp:77-90 matmul: k-ordered unfused sums, bit for bit
+    {
+        const DenseMatrix A = random_rows(7, 33, rng), B = random_rows(33, 5, rng);
+        const DenseMatrix C = matmul(A, B);
+        bool same = C.rows == 7 && C.cols == 5;
+        for (std::size_t i = 0; i < 7 && same; ++i)
+            for (std::size_t j = 0; j < 5; ++j) {
+                float acc = 0.0f;
+                for (std::size_t kk = 0; kk < 33; ++kk) {
+                    const float p = A.at(i, kk) * B.at(kk, j);
+                    acc = acc + p;
+                }
+                same = same && acc == C.at(i, j);
+            }
+        CHECK(same, "matmul differs from the k-ordered sum");
+        CHECK(throws<std::invalid_argument>([&] { matmul(A, A); }, "inner dimensions differ"), "matmul shapes");
+    }
+    // selection.hpp:139-156 group means (groups 1, 3, 4)
+    for (std::size_t g : {1, 3, 4}) {
+        const std::size_t n_kv = 2, d = 16, nh = n_kv * g;
+        const DenseMatrix q = random_rows(3, nh * d, rng);
+        const DenseMatrix mq = detail::group_mean_queries(q, nh, n_kv, d);
+        std::vector<float> want(3 * n_kv * d);
+        oracle_group_mean(q.values.data(), 3, nh, n_kv, d, want.data());
+        CHECK(std::memcmp(mq.values.data(), want.data(), want.size() * 4) == 0, "group mean g=%zu", g);
+    }
+    // selection.hpp:81-135 TopkBuffer: ties keep the lower index (test_selection.cpp:168-191)
+    {
+        detail::TopkBuffer buf;
+        buf.init(4);
+        for (std::size_t i = 0; i < 64; ++i) {
+            const bool tied = i == 0 || i == 7 || i == 15 || i == 16 || i == 17 || i == 31;
+            buf.offer(i, tied ? 1.0f : -1.0f);
+        }
+        const auto s = buf.sorted();
+        CHECK(s.size() == 4 && s[0].index == 0 && s[1].index == 7 && s[2].index == 15 && s[3].index == 16,
+              "TopkBuffer tie order");
+        // against the oracle's top-k on random scores offered in index order
+        const std::size_t d = 16, count = 3000;
+        std::vector<std::vector<float>> heads(1, std::vector<float>(count * d));
+        for (auto& v : heads[0]) v = dist(rng);
+        const DenseMatrix q = random_rows(1, d, rng);
+        const PerHeadTopk want = oracle_topk(q, 1, heads, count, d, 5);
+        detail::TopkBuffer b2;
+        b2.init(5);
+        for (std::size_t i = 0; i < count; ++i) b2.offer(i, oracle_dot_f32(q.values.data(), heads[0].data() + i * d, d));
+        const auto got = b2.sorted();
+        bool same = got.size() == want[0][0].size();
+        for (std::size_t j = 0; same && j < got.size(); ++j)
+            same = got[j].index == want[0][0][j].index && got[j].score == want[0][0][j].score;
+        CHECK(same, "TopkBuffer vs oracle");
+    }
+    // selection_reference.hpp:18-69 naive scorer == fused scorer == oracle, bit for bit
+    // (test_selection.cpp:89-103); its scratch grows with the middle, the fused one's does not
+    std::size_t naive_small = 0, naive_large = 0, fused_small = 0, fused_large = 0;
+    for (std::size_t count : {0, 1, 4, 5, 127, 1000, 2049, 10000}) {
+        for (std::size_t k : {1, 4, 8}) {
+            const std::size_t n_kv = 2, nh = 4, d = 32;
+            std::vector<std::vector<float>> heads(n_kv, std::vector<float>(std::max<std::size_t>(1, count) * d));
+            for (auto& h : heads)
+                for (auto& v : h) v = dist(rng);
+            std::vector<KeySegmentView> views;
+            for (auto& h : heads) views.push_back(KeySegmentView{h.data(), count, d});
+            const DenseMatrix q = random_rows(3, nh * d, rng);
+            SelectionConfig cfg;
+            cfg.k = k;
+            ScratchMeter mn, mf;
+            const PerHeadTopk naive = naive_topk_scores(q, nh, views, cfg, &mn);
+            const PerHeadTopk fused = fused_topk_scores(q, nh, views, cfg, &mf);
+            const PerHeadTopk want = oracle_topk(q, nh, heads, count, d, k);
+            bool same = naive.size() == n_kv;
+            for (std::size_t kv = 0; same && kv < n_kv; ++kv)
+                for (std::size_t qq = 0; same && qq < 3; ++qq) {
+                    same = naive[kv][qq].size() == want[kv][qq].size() &&
+                           fused[kv][qq].size() == want[kv][qq].size();
+                    for (std::size_t j = 0; same && j < want[kv][qq].size(); ++j)
+                        same = naive[kv][qq][j].index == want[kv][qq][j].index &&
+                               naive[kv][qq][j].score == want[kv][qq][j].score &&
+                               fused[kv][qq][j].index == want[kv][qq][j].index &&
+                               fused[kv][qq][j].score == want[kv][qq][j].score;
+                }
+            CHECK(same, "naive/fused/oracle top-k count=%zu k=%zu", count, k);
+            if (count == 1000 && k == 4) naive_small = mn.peak, fused_small = mf.peak;
+            if (count == 10000 && k == 4) naive_large = mn.peak, fused_large = mf.peak;
+        }
+    }
+    CHECK(naive_large > 5 * naive_small, "naive scratch grows with the middle (%zu %zu)", naive_small, naive_large);
+    CHECK(fused_large == fused_small, "fused scratch is flat (%zu %zu)", fused_small, fused_large);
+    CHECK(throws<std::invalid_argument>([&] {
+              std::vector<float> h(32 * 10);
+              std::vector<KeySegmentView> v{KeySegmentView{h.data(), 10, 32}, KeySegmentView{h.data(), 10, 32}};
+              naive_topk_scores(random_rows(1, 3 * 32, rng), 3, v, SelectionConfig{});
+          }, "naive_topk_scores: n_heads must be a multiple of kv heads"),
+          "naive head mismatch");
+}
+
+static void test_sharded_world1() {
+    // include/reattn/sharded.hpp at world 1: the library's own NCCL communicator (one rank on
+    // this GPU) and the captured sharded step equal the single-GPU attend_step
+    std::mt19937 rng(17);
+    const std::size_t n_kv = 8, nh = 32, d = 128, total = 20000;
+    SegmentedKvCache cache(n_kv, d, 32, 4096, SegmentedKvCache::Storage::BF16, total);
+    DenseMatrix K = random_rows(total, n_kv * d, rng), V = random_rows(total, n_kv * d, rng);
+    for (float* m : {K.values.data(), V.values.data()})
+        for (std::size_t i = 0; i < K.values.size(); ++i) m[i] = oracle_round_bf16(m[i]);
+    cache.append(K, V);
+    const RotaryTable rope(d, 500000.0, 8192);
+    const SelectionConfig cfg;
+    ShardedDecoder dec(cache, rope, nh, cfg, total, 1, 0, ShardedDecoder::new_comm_id());
+    for (int rep = 0; rep < 3; ++rep) {
+        if (rep == 1) dec.capture();
+        const DenseMatrix q = random_rows(1, nh * d, rng);
+        RunStats st;
+        const DenseMatrix want = attend_step(q, nh, cache, cfg, rope, AttentionMode::ReAttention, &st);
+        const DenseMatrix got = dec.step(q);
+        double md = 0;
+        for (std::size_t i = 0; i < got.values.size(); ++i)
+            md = std::max(md, std::abs(double(got.values[i]) - want.values[i]));
+        const reattn_step_stats ss = dec.stats();
+        CHECK(md <= 1e-6 && ss.scope_len == st.scope_len_max, "sharded world-1 rep %d md=%g L=%llu/%zu", rep,
+              md, (unsigned long long)ss.scope_len, st.scope_len_max);
+    }
+}
+
 // REATTN_TEST_GARBAGE=1: fill (and free) most device memory with 0xFF bytes first, so later
 // allocations start from garbage -- surfaces reads of memory a test never wrote.
 static void fill_device_garbage() {
@@ -615,6 +752,8 @@ static void fill_device_garbage() {
 int main() {
     if (std::getenv("REATTN_TEST_GARBAGE")) fill_device_garbage();
     test_snapshot();
+    test_dense_and_naive();
+    test_sharded_world1();
     test_fused_topk();
     test_vote_spans();
     test_scope();

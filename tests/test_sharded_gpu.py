@@ -87,3 +87,33 @@ def test_shard_range_matches_c_rule(ctx):
                 assert b.value == prev and (b.value % 32 == 0 or b.value == M)
                 prev = b.value + n.value
             assert prev == M
+
+
+def test_library_nccl_step_world1(ctx):
+    """The product host path (sharded.NcclDecodeStep over reattn_shard_step / _capture: the
+    library's own NCCL communicator issues both all-gathers) at world size 1 on this GPU,
+    eager and graph-captured, equals the unsharded step; end to end through
+    reattn_shard_run_host as well."""
+    cfg = N.SelectionConfig()
+    n_kv, nh, d, total = 8, 32, 128, 60000
+    cache = N.Cache(ctx, n_kv, d, cfg.l_global, cfg.l_local, total, N.BF16)
+    ctx.synth_uniform(cache.keys_tensor(), 81)
+    ctx.synth_uniform(cache.values_tensor(), 82)
+    cache.set_total(total)
+    rope = N.Rope(ctx, d, 500000.0, 8192)
+    ops = S.NativeOps(ctx, cache, rope, nh, cfg, total, 1, 0)
+    step = S.NcclDecodeStep(ops, S.NcclComm(ctx, 1, 0))
+    for rep in range(3):
+        if rep == 1:
+            step.capture()
+        q = torch.from_numpy(synth.uniform(900 + rep, nh * d).reshape(1, -1)).cuda()
+        ref = N.attend_step(ctx, cache, rope, q, nh, cfg)
+        out = step.step(q)
+        torch.cuda.synchronize()
+        assert (out - ref.out).abs().max().item() <= 1e-6, rep
+        st, spans = ops.stats(cfg.k_prime)
+        assert st.scope_len == ref.stats.scope_len and np.array_equal(spans[0], ref.spans[0])
+    qh = q.cpu().pin_memory()
+    oh = torch.empty_like(qh).pin_memory()
+    step.run_host(qh, oh)
+    assert (oh - ref.out.cpu()).abs().max().item() <= 1e-6

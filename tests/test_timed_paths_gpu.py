@@ -106,3 +106,13 @@ def test_config3_prefill_chunk_full_shape(ctx):
     err = float(np.abs(res.out.cpu().numpy() - out).max())
     assert err <= 2e-4, err
     assert float(np.abs(res.entropy - ent).max()) <= 2e-3
+
+
+def test_reference_lane_mode_on_this_host():
+    """The compiled reference (oracle/_ref, loaded for this host's ISA level) must score d=128
+    keys with the lane arithmetic the library uses by default (unfused): checked
+    on the GPU box's own CPU, where the bench's reference arm and the CPU baseline run."""
+    mode = ob.ref_lane_mode(128)
+    if ob.ref() is None:
+        pytest.skip("oracle/_ref not shipped to this host")
+    assert mode == N.LANES_UNFUSED == ob.LANES_UNFUSED, mode
