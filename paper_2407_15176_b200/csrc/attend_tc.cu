@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
     uint64_t* s_full = v_empty + kFStages;
     uint64_t* p_full = s_full + 2;
     uint64_t* o_done = p_full + 2;
-    uint32_t* s_tmem = (uint32_t*)(o_done + 1);  // then s_max / s_ab (softmax exchange)
+    uint64_t* o_final = o_done + 1;              // completes once: the last P·V landed
+    uint32_t* s_tmem = (uint32_t*)(o_final + 1);  // then s_max / s_ab (softmax exchange)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int qblk = blockIdx.x, h = blockIdx.y, kv = h / a.group;
@@ -184,6 +185,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
             mbar_init(&p_full[b], 256);
         }
         mbar_init(o_done, 1);
+        mbar_init(o_final, 1);
         fence_barrier_init();
     }
     tc_fence_before();
@@ -261,6 +263,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
                     mma_commit(o_done);
                 }
             }
+            mma_commit(o_final);
         }
     } else {
         // ===== softmax: two warps per TMEM lane quarter; thread = (query row, 64-column
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const int i = q0 + row;
         const bool live = i < a.n_q;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-        float* s_max = (float*)(o_done + 2);        // [2 parity][2 half][128]
+        float* s_max = (float*)(o_final + 2);       // [2 parity][2 half][128]
         double* s_ab = (double*)(s_max + 2 * 2 * kFM);  // [2 half][128][2]
         // query: rotated at L'-n_q+i (engine.hpp:88-93), times log2(e)/sqrt(d) (so S is
         // already in log2 units), split into bf16 hi + lo; this half writes pairs [32h, 32h+32)
@@ -380,15 +383,16 @@ __global__ void __launch_bounds__(kFThreads, 1)
             A += (double)__fadd_rn(f2_lo(at), f2_hi(at));
             B2 += (double)__fadd_rn(f2_lo(bt), f2_hi(bt));
         }
-        // combine the halves' (A, B2) and wait for all P·V: phases n_tiles-2 (may still be
-        // pending) and n_tiles-1 of o_done
+        // combine the halves' (A, B2) and wait for all P·V.  (o_done cannot tell: when this
+        // thread gets here it may be 0, 1 or 2 completions short of n_tiles, and parity waits
+        // for "n_tiles - 2" then "n_tiles - 1" hung whenever the last P·V had already landed
+        // -- a rare race, seen as a hang after tens of replays.  o_final completes once.)
         s_ab[(half * kFM + row) * 2 + 0] = A;
         s_ab[(half * kFM + row) * 2 + 1] = B2;
         named_bar_sync(1 + quarter, 64);
         const double At = s_ab[row * 2 + 0] + s_ab[(kFM + row) * 2 + 0];
         const double Bt = s_ab[row * 2 + 1] + s_ab[(kFM + row) * 2 + 1];
-        if (n_tiles >= 2) mbar_wait(o_done, (uint32_t)(n_tiles - 2) & 1u);
-        mbar_wait(o_done, (uint32_t)(n_tiles - 1) & 1u);
+        mbar_wait(o_final, 0u);
         tc_fence_after();
         const double inv = 1.0 / At;
 #pragma unroll 1

@@ -515,6 +515,31 @@ __device__ __forceinline__ float exact_dot8(const float (&qv)[16], const __nv_bf
     return s;
 }
 
+// Exact dot_f32 of a whole key row by ONE thread (the re-scan path: lane = key): element
+// block c (16 bytes of the row) holds the c-th element of each of the reference's 8 lanes,
+// l_t += q[8c + t] * k[8c + t] in order, then the fixed tree -- the same bits as exact_dot8.
+template <int LANES>
+__device__ __forceinline__ float exact_dot_row(const float* __restrict__ sq, const __nv_bfloat16* krow) {
+    float l[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const uint4* k4 = reinterpret_cast<const uint4*>(krow);
+#pragma unroll 4
+    for (int c = 0; c < kPD / 8; ++c) {
+        const uint4 w = __ldg(k4 + c);
+        const float4 qa = reinterpret_cast<const float4*>(sq + 8 * c)[0];
+        const float4 qb = reinterpret_cast<const float4*>(sq + 8 * c)[1];
+        const float kf[8] = {__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
+                             __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u),
+                             __uint_as_float(w.z << 16), __uint_as_float(w.z & 0xFFFF0000u),
+                             __uint_as_float(w.w << 16), __uint_as_float(w.w & 0xFFFF0000u)};
+        const float qf[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            l[t] = LANES == kLanesFma ? __fmaf_rn(qf[t], kf[t], l[t]) : __fadd_rn(l[t], __fmul_rn(qf[t], kf[t]));
+    }
+    return __fadd_rn(__fadd_rn(__fadd_rn(l[0], l[1]), __fadd_rn(l[2], l[3])),
+                     __fadd_rn(__fadd_rn(l[4], l[5]), __fadd_rn(l[6], l[7])));
+}
+
 // One warp per (kv head, query): T = k-th best S_hi over the parts' lists, exact re-scoring
 // of the listed keys with S_hi >= T - 2 delta, exact re-scan of any part whose dropped S_hi
 // reaches that window, exact top-k of the union (every lane holds the same list).
@@ -522,9 +547,14 @@ template <int LANES>
 __global__ void __launch_bounds__(256) prefill_exact_merge_kernel(const PrefillMergeArgs m) {
     __shared__ float s_sc[8][kPMaxSplits * kPL];
     __shared__ uint32_t s_ix[8][kPMaxSplits * kPL];
+    __shared__ __align__(16) float s_q[8][kPD];  // the row's query (re-scans: lane = key)
+    __shared__ uint32_t s_resc[8];                // parts of row `warp` to re-scan
+    __shared__ float s_pts[8][kPKMax];            // the row's top-k before its re-scan
+    __shared__ uint32_t s_pti[8][kPKMax];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int e = blockIdx.x * 8 + wib;
-    if (e >= m.n_kv * m.n_q) return;  // warp-uniform
+    if (lane == 0) s_resc[wib] = 0u;
+    if (e < m.n_kv * m.n_q) {  // (no early return: the re-scans below are CTA-wide)
     const int kv = e / m.n_q, query = e % m.n_q;
     const size_t qrow = (size_t)kv * m.n_qpad + query;
     const int n = m.splits * kPL;
@@ -613,16 +643,17 @@ __global__ void __launch_bounds__(256) prefill_exact_merge_kernel(const PrefillM
         const bool live = p + j < nc;
         consume(live ? ix[p + j] : 0u, live);
     }
-    for (int s = 0; s < m.splits; ++s) {
-        if (!((rescan >> s) & 1u)) continue;
-        const uint32_t lo = (uint32_t)((int64_t)s * m.tiles / m.splits) * kPN;
-        const uint32_t hi = min(m.count, (uint32_t)((int64_t)(s + 1) * m.tiles / m.splits) * kPN);
-        for (uint32_t b0 = lo; b0 < hi; b0 += 4) {
-            const bool live = b0 + j < hi;
-            consume(live ? b0 + j : 0u, live);
+    if (rescan) {  // finished by the whole CTA below
+        for (int c = lane; c < kPD; c += 32) s_q[wib][c] = m.mq[qrow * kPD + c];
+        if (lane == 0) {
+            s_resc[wib] = rescan;
+#pragma unroll
+            for (int q = 0; q < kPKMax; ++q) {
+                s_pts[wib][q] = ts[q];
+                s_pti[wib][q] = ti[q];
+            }
         }
-    }
-    if (lane == 0) {
+    } else if (lane == 0) {
         const size_t o = ((size_t)kv * m.n_q + query) * m.k;
 #pragma unroll
         for (int q = 0; q < kPKMax; ++q)
@@ -630,6 +661,83 @@ __global__ void __launch_bounds__(256) prefill_exact_merge_kernel(const PrefillM
                 m.idx_out[o + q] = ti[q];
                 m.score_out[o + q] = ts[q];
             }
+    }
+    }  // valid row
+    // A part whose list overflowed inside the window (near-ties, ~1e-6 of rows) is scanned
+    // again exactly by all 8 warps of the CTA: 32 keys per warp step, one key row per lane
+    // (16-byte loads), each warp keeping the top-k of its keys; the row's warp merges them.
+    // (One warp with 8 lanes per key took ~20 ms for one 60K-key part.)
+    __syncthreads();
+#pragma unroll 1
+    for (int p = 0; p < 8; ++p) {
+        const uint32_t rescan = s_resc[p];
+        if (!rescan) continue;  // CTA-uniform
+        const int ep = blockIdx.x * 8 + p, kvp = ep / m.n_q, qp = ep % m.n_q;
+        const __nv_bfloat16* kb = m.keys + ((size_t)kvp * m.head_stride + m.row0) * kPD;
+        float ts[kPKMax];
+        uint32_t ti[kPKMax];
+#pragma unroll
+        for (int q = 0; q < kPKMax; ++q) {
+            ts[q] = -INFINITY;
+            ti[q] = kNoIndex;
+        }
+        for (int s = 0; s < m.splits; ++s) {
+            if (!((rescan >> s) & 1u)) continue;
+            const uint32_t lo = (uint32_t)((int64_t)s * m.tiles / m.splits) * kPN;
+            const uint32_t hi = min(m.count, (uint32_t)((int64_t)(s + 1) * m.tiles / m.splits) * kPN);
+            for (uint32_t b0 = lo + 32u * (uint32_t)wib; b0 < hi; b0 += 32u * 8u) {
+                const uint32_t key = b0 + (uint32_t)lane;
+                const bool live = key < hi;
+                const float v = live ? exact_dot_row<LANES>(s_q[p], kb + (size_t)key * kPD) : -INFINITY;
+                float ws = ts[kPKMax - 1];
+                uint32_t wi = ti[kPKMax - 1];
+#pragma unroll
+                for (int q = 0; q < kPKMax; ++q)
+                    if (q == m.k - 1) {
+                        ws = ts[q];
+                        wi = ti[q];
+                    }
+                uint32_t cand = __ballot_sync(0xFFFFFFFFu, live && better(v, key, ws, wi));
+                while (cand) {
+                    const int src = __ffs(cand) - 1;
+                    cand &= cand - 1u;
+                    insert_better(ts, ti, m.k, __shfl_sync(0xFFFFFFFFu, v, src), b0 + (uint32_t)src);
+                }
+            }
+        }
+        // every warp's list -> shared memory; the row's warp merges them into its own top-k
+        float* ws_ = s_sc[wib];
+        uint32_t* wi_ = s_ix[wib];
+        if (lane == 0) {
+#pragma unroll
+            for (int q = 0; q < kPKMax; ++q) {
+                ws_[q] = ts[q];
+                wi_[q] = ti[q];
+            }
+        }
+        __syncthreads();
+        if (wib == p) {
+            float fs[kPKMax];
+            uint32_t fi[kPKMax];
+#pragma unroll
+            for (int q = 0; q < kPKMax; ++q) {
+                fs[q] = s_pts[p][q];
+                fi[q] = s_pti[p][q];
+            }
+            for (int w = 0; w < 8; ++w)
+                for (int q = 0; q < m.k; ++q)
+                    if (s_ix[w][q] != kNoIndex) insert_better(fs, fi, m.k, s_sc[w][q], s_ix[w][q]);
+            if (lane == 0) {
+                const size_t o = ((size_t)kvp * m.n_q + qp) * m.k;
+#pragma unroll
+                for (int q = 0; q < kPKMax; ++q)
+                    if (q < m.k) {
+                        m.idx_out[o + q] = fi[q];
+                        m.score_out[o + q] = fs[q];
+                    }
+            }
+        }
+        __syncthreads();
     }
 }
 
