@@ -82,7 +82,7 @@ def build_decode(ctx, cid: int, total: int | None = None, extra_rows: int = 0):
 def load_traffic() -> dict | None:
     """dram read+write bytes per scan launch from the committed ncu --set full capture."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1c_decode_1m.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_decode_1m.json")) as f:
             p = json.load(f)
         return {"bytes": int(p["traffic_bytes"]), "source": p["source"]}
     except Exception:
@@ -349,6 +349,71 @@ def per_config_lines(ctx, stream, flush, peaks, cids, steps: int) -> list:
     return out
 
 
+def batch_sweep_lines(ctx, stream, flush, batches, steps: int) -> list:
+    """Config 5's batch dimension on this GPU (LLaMA-3.2-3B heads, 4M tokens per sequence,
+    each sequence its own 17 GB cache): one BatchPlan graph per batch size, device time per
+    replay over the batch (µs per token-layer per sequence)."""
+    import torch
+    from paper_2407_15176_b200 import native as N
+    c = DECODE_CONFIGS[5]
+    out = []
+    cfg = N.SelectionConfig()
+    rope = N.Rope(ctx, D, ROPE_BASE, WINDOW)
+    caches = []
+    try:
+        for B in batches:
+            while len(caches) < B:
+                i = len(caches)
+                cache = N.Cache(ctx, c["n_kv"], D, cfg.l_global, cfg.l_local, c["total"], N.BF16)
+                ks, vs, _ = config_seeds(5)
+                ctx.synth_uniform(cache.keys_tensor(), ks + 7919 * i)
+                ctx.synth_uniform(cache.values_tensor(), vs + 7919 * i)
+                cache.set_total(c["total"])
+                caches.append(cache)
+            bp = N.BatchPlan(ctx, caches[:B], rope, c["n_head"], cfg)
+            qb = torch.empty(B, c["n_head"] * D, device=f"cuda:{ctx.device}")
+            ctx.synth_uniform(qb, 5051)
+            bp.q.copy_(qb)
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    bp.launch()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                tot = 0.0
+                for _ in range(steps):
+                    flush.sum()
+                    e0.record(stream)
+                    bp.launch()
+                    e1.record(stream)
+                    e1.synchronize()
+                    tot += e0.elapsed_time(e1)
+            ms = tot / steps
+            info = bp.info()
+            out.append({"config": 5, "batch": B, "ms_per_step": ms,
+                        "us_per_token_layer_per_sequence": ms * 1e3 / B,
+                        "scan_gbs": info["scan_bytes"] / (ms * 1e-3) / 1e9,
+                        "kernels_per_step": int(info["kernels_per_step"])})
+            del bp
+    except Exception as e:  # (memory: 17 GB per sequence) reported, never fatal
+        out.append({"config": 5, "error": str(e)[:200]})
+    del caches
+    torch.cuda.empty_cache()
+    return out
+
+
+def prefill_config3_line(ctx) -> dict:
+    """Config 3: one layer's chunked prefill to 256K (tools/bench_prefill_layer.py)."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_prefill_layer as bpl
+        a = argparse.Namespace(ctx=256 * 1024, chunk=4096, every=1, start=0)
+        r = bpl.run(ctx, a)
+        r.pop("last_chunk", None)
+        return r
+    except Exception as e:
+        return {"error": str(e)[:200]}
+
+
 def run_ours(args) -> None:
     import torch
 
@@ -457,6 +522,8 @@ def run_ours(args) -> None:
         torch.cuda.empty_cache()
         others = [c for c in (1, 2, 4, 5) if c != cid]
         line["per_config"] = per_config_lines(ctx, stream, flush, peaks, others, args.per_config_steps)
+        line["config5_batch_sweep_1gpu"] = batch_sweep_lines(ctx, stream, flush, (1, 2, 4, 8), 10)
+        line["prefill_config3"] = prefill_config3_line(ctx)
     if not args.no_cpu_baseline and cid == 4:
         try:
             # the same synthetic cache, regenerated on the host in fp32 (bf16-rounded values)

@@ -1,10 +1,12 @@
 """Batched decode (reattn_batch_plan_*): n_seq independent sequences with their own caches
-in one graph.  Each sequence's output must equal its own attend_step (engine.hpp:43) --
-the pipelined path attends sequence b on a few SMs beside scan b+1, so only the order of
-the fp32/f64 partial merges differs (ATTN_TOL) -- and its scope must be identical."""
+in one graph.  Each sequence's output must equal the CPU oracle's attend_step (engine.hpp:
+43-114) on that sequence's cache -- spans and L' identical, outputs and entropies within
+1e-6 -- and the GPU's own single-sequence step (the pipelined path attends sequence b on a
+few SMs beside scan b+1, so only the order of the fp32/f64 partial merges differs)."""
 import numpy as np
 import pytest
 
+import oracle_bind as ob
 import synth
 
 torch = pytest.importorskip("torch")
@@ -47,6 +49,17 @@ def test_batch_plan_equals_single_steps(ctx, dtype, totals, nh):
             err = (bp.out[i:i + 1] - ref.out).abs().max().item()
             assert err <= ATTN_TOL, (i, err)
             assert abs(st.entropy_max - ref.stats.entropy_max) <= 1e-6
+            if rep == 0:  # the oracle, on the cache's own bytes
+                hk = c.keys_tensor().cpu().numpy() if dtype == N.F32 else ob.bf16_words(c.keys_tensor())
+                hv = c.values_tensor().cpu().numpy() if dtype == N.F32 else ob.bf16_words(c.values_tensor())
+                out, ent, ost, (sb, se), _ = ob.attend_step_ex(q[i:i + 1].cpu().numpy(), nh, hk, hv,
+                                                               totals[i], ob.SelectionConfig(),
+                                                               500000.0, 8192)
+                assert st.scope_len == ost.scope_len, i
+                assert np.array_equal(ref.spans[0], sb) and np.array_equal(ref.spans[1], se), i
+                oerr = float(np.abs(bp.out[i:i + 1].cpu().numpy() - out).max())
+                assert oerr <= ATTN_TOL, (i, oerr)
+                assert abs(st.entropy_max - ost.entropy_max) <= 1e-6, i
     qh = q.cpu().pin_memory()
     oh = torch.empty_like(qh).pin_memory()
     bp.run_host(qh, oh)

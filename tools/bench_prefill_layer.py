@@ -24,15 +24,8 @@ import bench  # noqa: E402
 from paper_2407_15176_b200 import native as N  # noqa: E402
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--ctx", type=int, default=256 * 1024)
-    ap.add_argument("--chunk", type=int, default=4096)
-    ap.add_argument("--every", type=int, default=1, help="time every n-th chunk, interpolate the rest")
-    ap.add_argument("--start", type=int, default=0, help="debugging: skip the chunks before this one")
-    args = ap.parse_args()
+def run(ctx, args) -> dict:
     n_kv, nh, d = 8, 32, 128
-    ctx = N.Context(0)
     stream = torch.cuda.ExternalStream(ctx.stream)
     cfg = N.SelectionConfig(l_chunk=args.chunk)
     total = args.ctx
@@ -40,7 +33,7 @@ def main():
     ctx.synth_uniform(cache.keys_tensor(), 3100)
     ctx.synth_uniform(cache.values_tensor(), 3101)
     rope = N.Rope(ctx, d, 1.0e6, 8192)
-    flush = bench._flush_buffer(torch, "cuda:0")
+    flush = bench._flush_buffer(torch, f"cuda:{ctx.device}")
     first = min(total, cfg.l_global + cfg.l_local)
     ends = [first]
     while ends[-1] < total:
@@ -114,7 +107,19 @@ def main():
             "score_gemm_frac_of_bf16_burst": (scan_tflop / (total_scan_ms * 1e-3)) / peaks["bf16_tflops"]
             if total_scan_ms else None,
             "target_score_gemm_ms": 72.0, "last_chunk": rows[-1]}
-    print(json.dumps(line), flush=True)
+    del cache
+    torch.cuda.empty_cache()
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ctx", type=int, default=256 * 1024)
+    ap.add_argument("--chunk", type=int, default=4096)
+    ap.add_argument("--every", type=int, default=1, help="time every n-th chunk, interpolate the rest")
+    ap.add_argument("--start", type=int, default=0, help="debugging: skip the chunks before this one")
+    args = ap.parse_args()
+    print(json.dumps(run(N.Context(0), args)), flush=True)
 
 
 if __name__ == "__main__":
