@@ -380,6 +380,11 @@ int reattn_weights_create(reattn_ctx* ctx, const reattn_model_config* cfg, reatt
 /* init_random (model.hpp:120-152): the same mt19937_64 Box-Muller stream, std 0.02 */
 int reattn_weights_init_random(reattn_ctx* ctx, const reattn_model_config* cfg, uint64_t seed,
                                reattn_weights** out);
+/* benchmarking only, no reference counterpart: projections, embedding and lm_head filled on
+ * the device with splitmix64 uniform values times 0.02, unit norms (init_random draws its
+ * Gaussian stream on the host, minutes for an 8B-parameter shape) */
+int reattn_weights_synth(reattn_ctx* ctx, const reattn_model_config* cfg, uint64_t seed,
+                         reattn_weights** out);
 /* RATW weight files (model.hpp:204-339 save_weights / load_weights) */
 int reattn_weights_load(reattn_ctx* ctx, const char* path, reattn_weights** out);
 int reattn_weights_save(reattn_ctx* ctx, const reattn_weights* w, const char* path);
@@ -431,6 +436,9 @@ int reattn_engine_decode_latencies(const reattn_engine* e, double* out, uint64_t
 int reattn_engine_last_spans(const reattn_engine* e, uint64_t layer, uint64_t* begin,
                              uint64_t* end, uint64_t cap, uint64_t* n);
 const reattn_cache* reattn_engine_cache(const reattn_engine* e, uint64_t layer);
+/* benchmarking only: every layer's cache holds `total` synthetic rows (as if a prompt of that
+ * length had been prefilled), so decode throughput can be measured at long contexts */
+int reattn_engine_synth_context(reattn_engine* e, uint64_t total, uint64_t seed);
 void reattn_engine_destroy(reattn_engine* e);
 
 /* ---- synthetic inputs (tests and benchmarks; not on the hot path) ---------------- */

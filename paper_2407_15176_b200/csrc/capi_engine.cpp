@@ -18,6 +18,7 @@
 // C = A·B is issued as the column-major C^T = B^T·A^T.
 #include <cublas_v2.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -207,7 +208,12 @@ struct reattn_engine {
     // decode: one CUDA-graph plan per layer that follows the growing cache (reattn_plan_*),
     // launched without a host synchronisation; their stats are read once per forward block
     std::vector<reattn_plan*> plans;
+    // decode-token projections: GEMV workspace (split-k partials + self-resetting tickets)
+    void* gemv_ws = nullptr;
+    uint64_t gemv_n_max = 0;
+    bool gemv_ok = false;  // every projection width a multiple of 4 (float4 columns)
     ~reattn_engine() {
+        if (gemv_ws) cudaFree(gemv_ws);
         for (auto* p : plans) reattn_plan_destroy(p);
         for (auto* c : caches) reattn_cache_destroy(c);
         if (rope) reattn_rope_destroy(rope);
@@ -232,6 +238,10 @@ namespace {
 int gemm(reattn_engine* e, uint64_t M, uint64_t N, uint64_t K, const float* A, uint64_t lda,
          const float* B, uint64_t ldb, float* C, uint64_t ldc, float beta) {
     if (M == 0 || N == 0) return REATTN_OK;
+    if (M == 1 && e->gemv_ok && N <= e->gemv_n_max && gemv_supported(N, K, ldb, A, B, C)) {
+        CU(e->ctx, launch_gemv(A, B, ldb, N, K, C, beta, e->gemv_ws, e->gemv_n_max, e->ctx->stream));
+        return REATTN_OK;
+    }
     const float one = 1.0f;
     BL(e->ctx, cublasSgemm(e->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)N, (int)M, (int)K, &one, B,
                            (int)ldb, A, (int)lda, &beta, C, (int)ldc));
@@ -263,14 +273,16 @@ int ensure_rows(reattn_engine* e, uint64_t rows) {
 
 // K/V of `rows` tokens appended to the layer's cache (kv_cache.hpp:54-68): the fp32 cache
 // takes the projection straight into its head-major rows, one strided-batched GEMM per tensor
+int ensure_capacity(reattn_engine* e, reattn_cache* cache, uint64_t rows) {
+    if (cache->total + rows <= cache->capacity) return REATTN_OK;
+    return reattn_cache_reserve(e->ctx, cache, std::max(cache->capacity * 2, cache->total + rows));
+}
+
 int append_kv(reattn_engine* e, reattn_cache* cache, uint64_t layer, uint64_t rows) {
     reattn_ctx* ctx = e->ctx;
     const reattn_model_config& c = e->w->cfg;
     const uint64_t d = c.d_head, nkv = c.n_kv_head;
-    if (cache->total + rows > cache->capacity) {
-        int rc = reattn_cache_reserve(ctx, cache, std::max(cache->capacity * 2, cache->total + rows));
-        if (rc) return rc;
-    }
+    if (int rc = ensure_capacity(e, cache, rows)) return rc;
     const float* wk = cslot(e->w, REATTN_W_WK, layer);
     const float* wv = cslot(e->w, REATTN_W_WV, layer);
     if (cache->dtype == REATTN_F32) {
@@ -341,14 +353,30 @@ int forward_block(reattn_engine* e, uint64_t rows) {
     e->se.resize(cap);
     if (e->plans.size() != c.n_layer) e->plans.assign(c.n_layer, nullptr);
     std::vector<reattn_plan*> launched(c.n_layer, nullptr);
+    // a decode token (one row, bf16 cache): the q/k/v projections are one GEMV launch and the
+    // gate/up projections another, with the activation in its epilogue
+    const bool token = rows == 1 && e->gemv_ok;
+    const uint64_t KW = c.n_kv_head * c.d_head;
     for (uint64_t l = 0; l < c.n_layer; ++l) {
         CU(ctx, launch_rmsnorm(e->x, rows, D, cslot(e->w, REATTN_W_NORM_ATTN, l), e->h, ctx->stream));
-        int rc = append_kv(e, e->caches[l], l, rows);  // before attend_step (engine.hpp:196-198)
-        if (rc) return rc;
-        reattn_plan* pl = rows == 1 ? layer_plan(e, l) : nullptr;
-        float* qd = pl ? reattn_plan_q(pl) : e->q;
-        if ((rc = gemm(e, rows, QW, D, e->h, D, cslot(e->w, REATTN_W_WQ, l), QW, qd, QW, 0.0f)))
-            return rc;
+        reattn_cache* cache = e->caches[l];
+        int rc;
+        reattn_plan* pl = nullptr;
+        if (token && cache->dtype == REATTN_BF16) {
+            if ((rc = ensure_capacity(e, cache, 1))) return rc;
+            pl = layer_plan(e, l);
+            const GemvDesc m[3] = {{cslot(e->w, REATTN_W_WQ, l), QW, QW, pl ? reattn_plan_q(pl) : e->q, 0.0f},
+                                   {cslot(e->w, REATTN_W_WK, l), KW, KW, e->kb, 0.0f},
+                                   {cslot(e->w, REATTN_W_WV, l), KW, KW, e->vb, 0.0f}};
+            CU(ctx, launch_gemv_batch(e->h, D, m, 3, false, e->gemv_ws, e->gemv_n_max, ctx->stream));
+            if ((rc = reattn_cache_append(ctx, cache, e->kb, e->vb, 1, 1))) return rc;  // engine.hpp:196-198
+        } else {
+            if ((rc = append_kv(e, cache, l, rows))) return rc;  // before attend_step (engine.hpp:196-198)
+            pl = rows == 1 ? layer_plan(e, l) : nullptr;
+            float* qd = pl ? reattn_plan_q(pl) : e->q;
+            if ((rc = gemm(e, rows, QW, D, e->h, D, cslot(e->w, REATTN_W_WQ, l), QW, qd, QW, 0.0f)))
+                return rc;
+        }
         const float* attn = e->attn;
         if (pl) {  // the graph replay, no host synchronisation; stats after the block
             if ((rc = reattn_plan_launch(pl))) return rc;
@@ -365,11 +393,17 @@ int forward_block(reattn_engine* e, uint64_t rows) {
         if ((rc = gemm(e, rows, D, D, attn, D, cslot(e->w, REATTN_W_WO, l), D, e->x, D, 1.0f)))
             return rc;
         CU(ctx, launch_rmsnorm(e->x, rows, D, cslot(e->w, REATTN_W_NORM_FFN, l), e->h, ctx->stream));
-        if ((rc = gemm(e, rows, F, D, e->h, D, cslot(e->w, REATTN_W_GATE, l), F, e->gate, F, 0.0f)))
-            return rc;
-        if ((rc = gemm(e, rows, F, D, e->h, D, cslot(e->w, REATTN_W_UP, l), F, e->up, F, 0.0f)))
-            return rc;
-        CU(ctx, launch_silu_mul(e->gate, e->up, rows * F, ctx->stream));
+        if (token) {
+            const GemvDesc m[2] = {{cslot(e->w, REATTN_W_GATE, l), F, F, e->gate, 0.0f},
+                                   {cslot(e->w, REATTN_W_UP, l), F, F, e->up, 0.0f}};
+            CU(ctx, launch_gemv_batch(e->h, D, m, 2, true, e->gemv_ws, e->gemv_n_max, ctx->stream));
+        } else {
+            if ((rc = gemm(e, rows, F, D, e->h, D, cslot(e->w, REATTN_W_GATE, l), F, e->gate, F, 0.0f)))
+                return rc;
+            if ((rc = gemm(e, rows, F, D, e->h, D, cslot(e->w, REATTN_W_UP, l), F, e->up, F, 0.0f)))
+                return rc;
+            CU(ctx, launch_silu_mul(e->gate, e->up, rows * F, ctx->stream));
+        }
         if ((rc = gemm(e, rows, D, F, e->gate, F, cslot(e->w, REATTN_W_DOWN, l), D, e->x, D, 1.0f)))
             return rc;
     }
@@ -442,6 +476,29 @@ int reattn_weights_init_random(reattn_ctx* ctx, const reattn_model_config* cfg, 
         for (int kind = REATTN_W_WQ; kind <= REATTN_W_DOWN; ++kind)
             if ((rc = fill(w->layer[l][kind], kind))) return rc;
     if ((rc = fill(w->global[REATTN_W_LM_HEAD], REATTN_W_LM_HEAD))) return rc;
+    *out = w.release();
+    return REATTN_OK;
+}
+
+int reattn_weights_synth(reattn_ctx* ctx, const reattn_model_config* cfg, uint64_t seed,
+                         reattn_weights** out) {
+    *out = nullptr;
+    std::unique_ptr<reattn_weights> w;
+    int rc = alloc_weights(ctx, *cfg, w);  // unit norms
+    if (rc) return rc;
+    auto fill = [&](float* dst, int kind, uint64_t salt) -> int {
+        uint64_t r, k;
+        shape_of(*cfg, kind, &r, &k);
+        CU(ctx, launch_synth_uniform(dst, kF32, r * k, seed * 131 + salt, 0, ctx->stream));
+        CU(ctx, launch_scale(dst, r * k, 0.02f, ctx->stream));
+        return REATTN_OK;
+    };
+    if ((rc = fill(w->global[REATTN_W_EMBEDDING], REATTN_W_EMBEDDING, 1))) return rc;
+    for (uint64_t l = 0; l < cfg->n_layer; ++l)
+        for (int kind = REATTN_W_WQ; kind <= REATTN_W_DOWN; ++kind)
+            if ((rc = fill(w->layer[l][kind], kind, 100 + l * 16 + kind))) return rc;
+    if ((rc = fill(w->global[REATTN_W_LM_HEAD], REATTN_W_LM_HEAD, 2))) return rc;
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
     *out = w.release();
     return REATTN_OK;
 }
@@ -615,6 +672,13 @@ int reattn_engine_create(reattn_ctx* ctx, const reattn_weights* w, const reattn_
     if ((rc = reattn_rope_create(ctx, w->cfg.d_head, w->cfg.rope_base, w->cfg.pretrain_window, &e->rope)))
         return rc;
     CU(ctx, cudaMalloc(&e->next, sizeof(uint32_t)));
+    const reattn_model_config& mc = w->cfg;
+    e->gemv_n_max = std::max({mc.vocab_size, mc.d_ff, mc.d_model, mc.n_head * mc.d_head,
+                              mc.n_kv_head * mc.d_head});
+    CU(ctx, cudaMalloc(&e->gemv_ws, gemv_workspace_bytes(e->gemv_n_max)));
+    CU(ctx, cudaMemsetAsync(e->gemv_ws, 0, gemv_workspace_bytes(e->gemv_n_max), ctx->stream));
+    e->gemv_ok = mc.d_model % 4 == 0 && mc.d_ff % 4 == 0 && (mc.n_head * mc.d_head) % 4 == 0 &&
+                 (mc.n_kv_head * mc.d_head) % 4 == 0 && getenv("REATTN_ENGINE_CUBLAS") == nullptr;
     if ((rc = reattn_engine_reset(e.get()))) return rc;
     *out = e.release();
     return REATTN_OK;
@@ -747,6 +811,23 @@ int reattn_engine_last_spans(const reattn_engine* e, uint64_t layer, uint64_t* b
         begin[i] = sp[i].first;
         end[i] = sp[i].second;
     }
+    return REATTN_OK;
+}
+
+int reattn_engine_synth_context(reattn_engine* e, uint64_t total, uint64_t seed) {
+    reattn_ctx* ctx = e->ctx;
+    const reattn_model_config& c = e->w->cfg;
+    for (uint64_t l = 0; l < c.n_layer; ++l) {
+        reattn_cache* cache = e->caches[l];
+        int rc = reattn_cache_reserve(ctx, cache, total + 4096);
+        if (rc) return rc;
+        const int dt = cache->dtype == REATTN_BF16 ? kBF16 : kF32;
+        const uint64_t n = cache->n_kv * cache->capacity * cache->d;
+        CU(ctx, launch_synth_uniform(cache->keys, dt, n, seed * 977 + 2 * l, 0, ctx->stream));
+        CU(ctx, launch_synth_uniform(cache->values, dt, n, seed * 977 + 2 * l + 1, 0, ctx->stream));
+        if ((rc = reattn_cache_set_total(ctx, cache, total))) return rc;
+    }
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
     return REATTN_OK;
 }
 

@@ -285,6 +285,22 @@ cudaError_t launch_rmsnorm(const float* x, uint64_t rows, uint64_t cols, const f
                            cudaStream_t s);
 cudaError_t launch_silu_mul(float* gate, const float* up, uint64_t n, cudaStream_t s);
 cudaError_t launch_argmax(const float* v, uint64_t n, uint32_t* out, cudaStream_t s);
+cudaError_t launch_scale(float* x, uint64_t n, float a, cudaStream_t s);
+// decode projections: y[N] = x[K] . W[K][N] (+ beta y), workspace sized for N <= n_max
+// (zeroed once: the split tickets reset themselves)
+size_t gemv_workspace_bytes(uint64_t n_max);
+bool gemv_supported(uint64_t N, uint64_t K, uint64_t ldw, const void* x, const void* W, const void* y);
+cudaError_t launch_gemv(const float* x, const float* W, uint64_t ldw, uint64_t N, uint64_t K, float* y,
+                        float beta, void* ws, uint64_t n_max, cudaStream_t s);
+struct GemvDesc {
+    const float* W;
+    uint64_t ldw, N;
+    float* y;
+    float beta;
+};
+// up to 3 matrices sharing x in one launch; silu_pair: mats = {gate, up}, gate <- silu(g) * u
+cudaError_t launch_gemv_batch(const float* x, uint64_t K, const GemvDesc* mats, int count, bool silu_pair,
+                              void* ws, uint64_t n_max, cudaStream_t s);
 
 // ---- timeline trace (diagnostics): REATTN_TRACE=1 at plan / launch time makes the decode
 // kernels stamp %globaltimer into a device buffer (layout in misc.cu); null otherwise.

@@ -1,9 +1,12 @@
+#include <algorithm>
 // Elementwise / row kernels of the decoder block around attend_step (reference model.hpp):
 // token embedding gather (model.hpp:181-190), RMS normalisation with the mean square carried
 // in double (model.hpp:155-167), the gated-FFN activation silu(g) * u (model.hpp:170-178)
 // and the greedy argmax with ties to the lowest token id (model.hpp:193-199).  The
-// projections themselves are plain fp32 GEMMs (cuBLAS, capi_engine.cpp).
+// projections of a prefill block are plain fp32 GEMMs (cuBLAS, capi_engine.cpp); a decode
+// token's projections are fp32 GEMVs (gemv_kernel below), a pure weight stream bound by HBM.
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -11,6 +14,12 @@
 namespace reattn_impl {
 
 namespace {
+
+// REATTN_NO_PDL=1: the decode-token kernels launch without programmatic stream serialisation
+bool gemv_pdl_env() {
+    static const bool off = getenv("REATTN_NO_PDL") != nullptr;
+    return !off;
+}
 
 // one row per CTA: out[r][c] = emb[tok[r]][c]
 __global__ void embed_kernel(const uint32_t* __restrict__ tokens, const float* __restrict__ emb,
@@ -27,16 +36,29 @@ __global__ void embed_kernel(const uint32_t* __restrict__ tokens, const float* _
 }
 
 // rmsnorm: ms = sum(double(x)^2) / cols; inv = float(1 / sqrt(ms + 1e-5)); out = x * inv * w
-// (two fp32 multiplies in that order, as model.hpp:160-163).  One CTA of 256 threads per row.
+// (two fp32 multiplies in that order, as model.hpp:160-163).  One CTA per row, one float4 per
+// thread per pass where the row allows (a decode row is one round trip, not a strided loop).
 __global__ void rmsnorm_kernel(const float* __restrict__ x, uint64_t cols,
                                const float* __restrict__ w, float* __restrict__ out) {
-    __shared__ double part[8];
+    __shared__ double part[32];
+    asm volatile("griddepcontrol.launch_dependents;");  // the projection after us may start
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // its weight stream under our tail
     const uint64_t r = blockIdx.x;
     const float* src = x + r * cols;
+    float* dst = out + r * cols;
+    const bool vec = (cols & 3) == 0 && ((uintptr_t)x & 15) == 0 && ((uintptr_t)w & 15) == 0 &&
+                     ((uintptr_t)out & 15) == 0;
     double s = 0.0;
-    for (uint64_t c = threadIdx.x; c < cols; c += blockDim.x) {
-        const double v = (double)src[c];
-        s += v * v;
+    if (vec) {
+        for (uint64_t c = threadIdx.x; c < cols / 4; c += blockDim.x) {
+            const float4 v = reinterpret_cast<const float4*>(src)[c];
+            s += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+        }
+    } else {
+        for (uint64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+            const double v = (double)src[c];
+            s += v * v;
+        }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, off);
@@ -45,9 +67,18 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, uint64_t cols,
     double ms = 0.0;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) ms += part[i];
     const float inv = (float)(1.0 / sqrt(ms / (double)cols + 1e-5));
-    float* dst = out + r * cols;
-    for (uint64_t c = threadIdx.x; c < cols; c += blockDim.x)
-        dst[c] = __fmul_rn(__fmul_rn(src[c], inv), w[c]);
+    if (vec) {
+        for (uint64_t c = threadIdx.x; c < cols / 4; c += blockDim.x) {
+            const float4 v = reinterpret_cast<const float4*>(src)[c];
+            const float4 g = reinterpret_cast<const float4*>(w)[c];
+            reinterpret_cast<float4*>(dst)[c] =
+                make_float4(__fmul_rn(__fmul_rn(v.x, inv), g.x), __fmul_rn(__fmul_rn(v.y, inv), g.y),
+                            __fmul_rn(__fmul_rn(v.z, inv), g.z), __fmul_rn(__fmul_rn(v.w, inv), g.w));
+        }
+    } else {
+        for (uint64_t c = threadIdx.x; c < cols; c += blockDim.x)
+            dst[c] = __fmul_rn(__fmul_rn(src[c], inv), w[c]);
+    }
 }
 
 // gate[i] = gate[i] / (1 + exp(-gate[i])) * up[i]   (model.hpp:170-178, fp32 throughout)
@@ -65,12 +96,38 @@ __global__ void argmax_kernel(const float* __restrict__ v, uint64_t n, uint32_t*
     __shared__ uint32_t bi[32];
     float best = -INFINITY;
     uint32_t idx = 0xFFFFFFFFu;
-    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const float x = v[i];
-        if (idx == 0xFFFFFFFFu || x > best) {  // per thread: ascending indices, strict >
+    auto take = [&](float x, uint64_t i) {  // per thread: ascending indices, strict >
+        if (idx == 0xFFFFFFFFu || x > best) {
             best = x;
             idx = (uint32_t)i;
         }
+    };
+    if ((n & 3) == 0 && ((uintptr_t)v & 15) == 0) {  // 8 float4 loads in flight per thread
+        const float4* v4 = reinterpret_cast<const float4*>(v);
+        const uint64_t n4 = n / 4, bd = blockDim.x;
+        uint64_t i = threadIdx.x;
+        for (; i + 7 * bd < n4; i += 8 * bd) {
+            float4 c[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) c[u] = v4[i + u * bd];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint64_t b = 4 * (i + u * bd);
+                take(c[u].x, b);
+                take(c[u].y, b + 1);
+                take(c[u].z, b + 2);
+                take(c[u].w, b + 3);
+            }
+        }
+        for (; i < n4; i += bd) {
+            const float4 c = v4[i];
+            take(c.x, 4 * i);
+            take(c.y, 4 * i + 1);
+            take(c.z, 4 * i + 2);
+            take(c.w, 4 * i + 3);
+        }
+    } else {
+        for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) take(v[i], i);
     }
     auto better = [](float a, uint32_t ia, float b, uint32_t ib) {
         if (ia == 0xFFFFFFFFu) return false;
@@ -115,8 +172,17 @@ cudaError_t launch_embed(const uint32_t* tokens, uint64_t rows, const float* emb
 cudaError_t launch_rmsnorm(const float* x, uint64_t rows, uint64_t cols, const float* w, float* out,
                            cudaStream_t s) {
     if (rows == 0) return cudaSuccess;
-    rmsnorm_kernel<<<(unsigned)rows, 256, 0, s>>>(x, cols, w, out);
-    return cudaGetLastError();
+    const unsigned threads = (unsigned)std::min<uint64_t>(1024, std::max<uint64_t>(32, ((cols + 3) / 4 + 31) & ~31ull));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)rows);
+    cfg.blockDim = dim3(threads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = gemv_pdl_env() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, rmsnorm_kernel, x, cols, w, out);
 }
 
 cudaError_t launch_silu_mul(float* gate, const float* up, uint64_t n, cudaStream_t s) {
@@ -129,6 +195,254 @@ cudaError_t launch_silu_mul(float* gate, const float* up, uint64_t n, cudaStream
 cudaError_t launch_argmax(const float* v, uint64_t n, uint32_t* out, cudaStream_t s) {
     argmax_kernel<<<1, 1024, 0, s>>>(v, n, out);
     return cudaGetLastError();
+}
+
+namespace {
+__global__ void scale_kernel(float* x, uint64_t n, float a) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        x[i] *= a;
+}
+}  // namespace
+
+cudaError_t launch_scale(float* x, uint64_t n, float a, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const int g = (int)std::min<uint64_t>((n + 255) / 256, 148 * 32);
+    scale_kernel<<<g, 256, 0, s>>>(x, n, a);
+    return cudaGetLastError();
+}
+
+// y[n] = sum_k x[k] W[k][n] (+ beta y[n]) for one row x, for up to three matrices sharing x
+// (the q/k/v projections; gate/up) in one launch: the weights are read exactly once, so the
+// kernel is an HBM stream.  A CTA owns 128 columns (a lane one float4) of a k-slice of one
+// matrix; its 8 warps take the slice's rows round-robin with a register double buffer of 8
+// float4 rows in flight per lane, reduce through shared memory in warp order, and split-k
+// partials are summed in a fixed order by the last CTA of the column tile (a ticket), so the
+// result is deterministic.  In the gated-FFN pair mode the gate and up tiles of the same
+// columns share one ticket and the last CTA writes silu(g) * u (model.hpp:170-178) into the
+// gate buffer.  Launched with programmatic stream serialisation: a CTA issues its first
+// weight rows before griddepcontrol.wait, so the stream of one projection starts under the
+// tail of the kernel before it.  fp32 throughout, one fused multiply-add per row.
+namespace {
+constexpr int kGemvWarps = 8, kGemvCols = 128, kGemvUnroll = 8, kGemvTargetCtas = 148 * 3,
+              kGemvMaxCtas = 148 * 8;
+int gemv_target_env() {
+    static const int t = getenv("REATTN_GEMV_CTAS") ? atoi(getenv("REATTN_GEMV_CTAS")) : kGemvTargetCtas;
+    return t;
+}
+
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ void add4(float4& a, const float4& b) {
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+}
+
+struct GemvMat {
+    const float* W;
+    uint64_t ldw;
+    float* y;
+    uint32_t N, tile0;  // columns; first global tile of this matrix
+    float beta;
+};
+
+struct GemvBatch {
+    GemvMat m[3];
+    int count;
+    int silu_pair;       // m[0] gate, m[1] up (same N): gate <- silu(g) * u
+    uint32_t S, kc, K;   // splits, rows per split, rows
+    uint32_t tiles;      // tiles over all matrices (grid.x)
+};
+
+__global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const float* __restrict__ x, GemvBatch B,
+                                                               float* ws, uint32_t* tickets) {
+    __shared__ float4 red[kGemvWarps * 32];
+    __shared__ uint32_t s_last;
+    asm volatile("griddepcontrol.launch_dependents;");
+    const uint32_t gt = blockIdx.x, split = blockIdx.y, S = B.S;
+    const int mi = B.count > 2 && gt >= B.m[2].tile0 ? 2 : B.count > 1 && gt >= B.m[1].tile0 ? 1 : 0;
+    const GemvMat& M = B.m[mi];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t k0 = split * B.kc, rows = min(B.K, k0 + B.kc) - k0;
+    const uint32_t col = (gt - M.tile0) * kGemvCols + lane * 4;
+    const bool ok = col < M.N;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    {
+        const float* wp = M.W + (uint64_t)k0 * M.ldw + col;
+        const float* xp = x + k0;
+        float4 w[2][kGemvUnroll];
+        float xv[2][kGemvUnroll];
+        auto load_w = [&](uint32_t r0, int b) {
+#pragma unroll
+            for (int u = 0; u < kGemvUnroll; ++u) {
+                const uint32_t r = r0 + u * kGemvWarps;
+                w[b][u] = ok && r < rows ? ld_stream4(wp + (uint64_t)r * M.ldw) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        };
+        auto load_x = [&](uint32_t r0, int b) {
+#pragma unroll
+            for (int u = 0; u < kGemvUnroll; ++u) {
+                const uint32_t r = r0 + u * kGemvWarps;
+                xv[b][u] = r < rows ? xp[r] : 0.f;
+            }
+        };
+        auto fma_rows = [&](int b) {
+#pragma unroll
+            for (int u = 0; u < kGemvUnroll; ++u) {
+                acc.x = fmaf(xv[b][u], w[b][u].x, acc.x);
+                acc.y = fmaf(xv[b][u], w[b][u].y, acc.y);
+                acc.z = fmaf(xv[b][u], w[b][u].z, acc.z);
+                acc.w = fmaf(xv[b][u], w[b][u].w, acc.w);
+            }
+        };
+        constexpr uint32_t step = kGemvUnroll * kGemvWarps;
+        uint32_t r = warp;
+        load_w(r, 0);                                       // weights: constant
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // x (and y, ws) from the kernel before
+        load_x(r, 0);
+        for (;;) {
+            if (r + step < rows) {
+                load_w(r + step, 1);
+                load_x(r + step, 1);
+            }
+            fma_rows(0);
+            r += step;
+            if (r >= rows) break;
+            if (r + step < rows) {
+                load_w(r + step, 0);
+                load_x(r + step, 0);
+            }
+            fma_rows(1);
+            r += step;
+            if (r >= rows) break;
+        }
+    }
+    // the CTA's partial: warps summed in order
+    red[warp * 32 + lane] = acc;
+    __syncthreads();
+    float4 p = red[lane];
+#pragma unroll
+    for (int i = 1; i < kGemvWarps; ++i) add4(p, red[i * 32 + lane]);
+    const bool pair = B.silu_pair != 0;
+    if (S > 1 || pair) {
+        const uint32_t pair_tiles = B.m[1].tile0;  // pair mode: gate tiles, then up tiles
+        const uint32_t ticket = pair ? gt % pair_tiles : gt;
+        const uint32_t arrivals = pair ? 2 * S : S;
+        if (warp == 0 && ok) reinterpret_cast<float4*>(ws)[((uint64_t)split * B.tiles + gt) * 32 + lane] = p;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_last = atomicAdd(&tickets[ticket], 1u) == arrivals - 1;
+            if (s_last) tickets[ticket] = 0;  // the next launch on the stream starts from zero
+        }
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        // the last CTA: warp w sums splits w, w + 8, ... of a tile (loads issued together),
+        // then the 8 warp sums in order
+        auto reduce_tile = [&](uint32_t t) -> float4 {
+            constexpr int kPer = 8;
+            float4 v[kPer];
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const uint32_t s2 = warp + j * kGemvWarps;
+                v[j] = ok && s2 < S ? __ldcg(reinterpret_cast<const float4*>(ws) + ((uint64_t)s2 * B.tiles + t) * 32 + lane)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            for (uint32_t s2 = warp + kPer * kGemvWarps; ok && s2 < S; s2 += kGemvWarps)
+                add4(v[kPer - 1], __ldcg(reinterpret_cast<const float4*>(ws) + ((uint64_t)s2 * B.tiles + t) * 32 + lane));
+            float4 q = v[0];
+#pragma unroll
+            for (int j = 1; j < kPer; ++j) add4(q, v[j]);
+            __syncthreads();
+            red[warp * 32 + lane] = q;
+            __syncthreads();
+            float4 o = red[lane];
+#pragma unroll
+            for (int i = 1; i < kGemvWarps; ++i) add4(o, red[i * 32 + lane]);
+            return o;
+        };
+        if (pair) {
+            const uint32_t tg = gt % pair_tiles;
+            const float4 g = reduce_tile(tg), u = reduce_tile(tg + pair_tiles);
+            if (warp != 0 || !ok) return;
+            auto silu = [](float gv, float uv) { return __fmul_rn(__fdiv_rn(gv, __fadd_rn(1.0f, expf(-gv))), uv); };
+            *reinterpret_cast<float4*>(B.m[0].y + col) =
+                make_float4(silu(g.x, u.x), silu(g.y, u.y), silu(g.z, u.z), silu(g.w, u.w));
+            return;
+        }
+        p = reduce_tile(gt);
+    }
+    if (warp != 0 || !ok) return;
+    float4* yp = reinterpret_cast<float4*>(M.y + col);
+    if (M.beta != 0.0f) {
+        const float4 o = *yp;
+        p.x = fmaf(M.beta, o.x, p.x);
+        p.y = fmaf(M.beta, o.y, p.y);
+        p.z = fmaf(M.beta, o.z, p.z);
+        p.w = fmaf(M.beta, o.w, p.w);
+    }
+    *yp = p;
+}
+}  // namespace
+
+size_t gemv_workspace_bytes(uint64_t n_max) {
+    const uint64_t tiles = 3 * ((n_max + kGemvCols - 1) / kGemvCols);
+    return (size_t)(kGemvMaxCtas + tiles) * kGemvCols * sizeof(float) + tiles * sizeof(uint32_t) + 256;
+}
+
+bool gemv_supported(uint64_t N, uint64_t K, uint64_t ldw, const void* x, const void* W, const void* y) {
+    return N % 4 == 0 && ldw % 4 == 0 && N <= UINT32_MAX && K > 0 && K <= UINT32_MAX &&
+           ((uintptr_t)W & 15) == 0 && ((uintptr_t)y & 15) == 0 && ((uintptr_t)x & 3) == 0;
+}
+
+cudaError_t launch_gemv_batch(const float* x, uint64_t K, const GemvDesc* mats, int count, bool silu_pair,
+                              void* ws, uint64_t n_max, cudaStream_t s) {
+    if (count < 1 || count > 3 || (silu_pair && (count != 2 || mats[0].N != mats[1].N)))
+        return cudaErrorInvalidValue;
+    GemvBatch B{};
+    uint32_t tiles = 0;
+    for (int i = 0; i < count; ++i) {
+        if (mats[i].N > n_max) return cudaErrorInvalidValue;
+        B.m[i] = GemvMat{mats[i].W, mats[i].ldw, mats[i].y, (uint32_t)mats[i].N, tiles, mats[i].beta};
+        tiles += (uint32_t)((mats[i].N + kGemvCols - 1) / kGemvCols);
+    }
+    if (tiles == 0) return cudaSuccess;
+    B.count = count;
+    B.silu_pair = silu_pair ? 1 : 0;
+    B.tiles = tiles;
+    B.K = (uint32_t)K;
+    const uint64_t target = std::min<int>(std::max(gemv_target_env(), 1), kGemvMaxCtas);
+    uint64_t S = (target + tiles - 1) / tiles;
+    S = std::max<uint64_t>(1, std::min<uint64_t>(S, K / (kGemvUnroll * kGemvWarps)));
+    B.S = (uint32_t)S;
+    B.kc = (uint32_t)((K + S - 1) / S);
+    float* part = (float*)ws;
+    uint32_t* tickets = (uint32_t*)(part + (kGemvMaxCtas + 3 * ((n_max + kGemvCols - 1) / kGemvCols)) * kGemvCols);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(tiles, (unsigned)S);
+    cfg.blockDim = dim3(kGemvWarps * 32);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = gemv_pdl_env() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, gemv_kernel, x, B, part, tickets);
+}
+
+cudaError_t launch_gemv(const float* x, const float* W, uint64_t ldw, uint64_t N, uint64_t K, float* y,
+                        float beta, void* ws, uint64_t n_max, cudaStream_t s) {
+    if (N == 0) return cudaSuccess;
+    const GemvDesc m{W, ldw, N, y, beta};
+    return launch_gemv_batch(x, K, &m, 1, false, ws, n_max, s);
 }
 
 }  // namespace reattn_impl

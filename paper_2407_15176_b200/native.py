@@ -189,6 +189,8 @@ SIGNATURES = [
     ("reattn_weights_upload", C.c_int, [vp, vp, C.c_int, u64, vp, u64]),
     ("reattn_weights_download", C.c_int, [vp, vp, C.c_int, u64, vp, u64]),
     ("reattn_weights_destroy", None, [vp]),
+    ("reattn_weights_synth", C.c_int, [vp, C.POINTER(ModelConfig), u64, C.POINTER(vp)]),
+    ("reattn_engine_synth_context", C.c_int, [vp, u64, u64]),
     ("reattn_engine_create", C.c_int, [vp, vp, C.POINTER(SelectionConfig), C.c_int, C.c_int,
                                        C.POINTER(vp)]),
     ("reattn_engine_reset", C.c_int, [vp]),
@@ -681,6 +683,13 @@ class Weights:
         return cls(ctx, h)
 
     @classmethod
+    def synth(cls, ctx: Context, cfg: ModelConfig, seed: int) -> "Weights":
+        """Benchmarking weights filled on the device (reattn_weights_synth)."""
+        h = vp()
+        ctx.check(ctx.lib.reattn_weights_synth(ctx.h, C.byref(cfg), seed, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
     def zeros(cls, ctx: Context, cfg: ModelConfig) -> "Weights":
         h = vp()
         ctx.check(ctx.lib.reattn_weights_create(ctx.h, C.byref(cfg), C.byref(h)))
@@ -736,6 +745,10 @@ class Engine:
 
     def reset(self) -> None:
         self.ctx.check(self.ctx.lib.reattn_engine_reset(self.h))
+
+    def synth_context(self, total: int, seed: int = 1) -> None:
+        """Benchmarking: every layer's cache holds `total` synthetic rows."""
+        self.ctx.check(self.ctx.lib.reattn_engine_synth_context(self.h, total, seed))
 
     def prefill(self, tokens):
         """Returns the final chunk's hidden states (rows x d_model, numpy)."""
