@@ -1,40 +1,73 @@
 #!/usr/bin/env python
-"""Summarise an ncu --csv launch list (gpu__time_duration.sum, optionally dram__bytes_read.sum):
-per kernel name, launches, total / mean time and, when present, achieved read bandwidth."""
-import collections
+"""Summarise ncu reports / launch lists into profiles/ (committed evidence).
+usage: python tools/ncu_summary.py OUT.md [--launches launches.csv] [REPORT.ncu-rep ...]"""
 import csv
+import io
+import subprocess
 import sys
+from collections import defaultdict
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 
 
-def main(path, top=25):
-    hdr, launches = None, collections.OrderedDict()
-    for r in csv.reader(open(path)):
-        if r and r[0] == "ID":
-            hdr = r
-            continue
-        if not hdr or len(r) != len(hdr):
-            continue
-        d = dict(zip(hdr, r))
-        key = (d["ID"], d["Kernel Name"])
-        launches.setdefault(key, {})[d["Metric Name"]] = (float(d["Metric Value"].replace(",", "")),
-                                                         d["Metric Unit"])
-    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
-    for (_, name), m in launches.items():
-        t, unit = m["gpu__time_duration.sum"]
-        t = t * {"ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3}.get(unit, 1e-9)
-        b = 0.0
-        if "dram__bytes_read.sum" in m:
-            v, u = m["dram__bytes_read.sum"]
-            b = v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-        a = agg[name[:90]]
-        a[0] += 1
-        a[1] += t
-        a[2] += b
-    tot = sum(a[1] for a in agg.values())
-    print(f"{'n':>5} {'total ms':>9} {'mean us':>8} {'share':>6} {'GB/s':>7}  kernel")
-    for k, (n, t, b) in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
-        print(f"{n:5d} {t*1e3:9.3f} {t/n*1e6:8.2f} {t/tot:6.1%} {b/t/1e9 if b else 0:7.0f}  {k}")
+def report(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units = rows[0], rows[1]
+    res = []
+    for v in rows[2:]:
+        d = dict(zip(h, v))
+        u = dict(zip(h, units))
+        res.append((d.get("Kernel Name", "?"), {k: (d.get(k, ""), u.get(k, "")) for k in KEYS},
+                    sorted(((k.replace("smsp__average_warps_issue_stalled_", "").replace(
+                        "_per_issue_active.ratio", ""), float(x or 0)) for k, x in d.items()
+                        if "average_warps_issue_stalled" in k and "per_issue_active" in k),
+                        key=lambda t: -t[1])[:6]))
+    return res
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hdr]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    agg = defaultdict(list)
+    for r in rows[hdr + 1:]:
+        if len(r) > vi:
+            agg[r[ki]].append(float(r[vi].replace(",", "")))
+    return agg
+
+
+def main():
+    out = sys.argv[1]
+    args = sys.argv[2:]
+    lines = []
+    if args and args[0] == "--launches":
+        agg = launches(args[1])
+        args = args[2:]
+        lines.append("## Launch list (ncu gpu__time_duration.sum, cold-cache, serialised)\n")
+        lines.append("| launches | avg µs | kernel |\n|---:|---:|---|")
+        for k, v in agg.items():
+            lines.append(f"| {len(v)} | {sum(v) / len(v) / 1000:.2f} | `{k[:110]}` |")
+        lines.append("")
+    for p in args:
+        for name, m, stalls in report(p):
+            lines.append(f"## `{name[:110]}`\n\nfrom `{p}`\n")
+            lines.append("| metric | value | unit |\n|---|---:|---|")
+            for k, (v, u) in m.items():
+                if v:
+                    lines.append(f"| {k} | {v} | {u} |")
+            lines.append("\ntop stall reasons (cycles per issued instruction): " +
+                         ", ".join(f"{k} {v:.2f}" for k, v in stalls) + "\n")
+    with open(out, "w") as f:
+        f.write("\n".join(lines) + "\n")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main()
