@@ -264,6 +264,13 @@ int reattn_plan_stats(reattn_plan* plan, reattn_step_stats* stats);
  * [n_q][n_head]) -- what reattn_attend_step returns through the same arguments */
 int reattn_plan_result(reattn_plan* plan, reattn_step_stats* stats, uint64_t* span_b_host,
                        uint64_t* span_e_host, double* entropy_host);
+/* the same outputs without a synchronisation per plan (a decoder runs one plan per layer):
+ * stage enqueues their copies into pinned host memory behind the replay on the context
+ * stream; after the caller synchronised that stream, staged_result reads them (ELOGIC when
+ * nothing was staged) */
+int reattn_plan_stage_result(reattn_plan* plan);
+int reattn_plan_staged_result(reattn_plan* plan, reattn_step_stats* stats, uint64_t* span_b_host,
+                              uint64_t* span_e_host, double* entropy_host);
 /* Diagnostics, no reference counterpart: with REATTN_TRACE=1 in the environment when a plan
  * is built, the decode kernels stamp %globaltimer (ns) into a device trace buffer; this
  * synchronises the device and copies its first n words (n <= 4096) to the host. */

@@ -372,6 +372,9 @@ int enqueue_step(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache, const 
     return enqueue_attn_part(ctx, P, cache, rope, q_dev, out_dev, s, zero_ticket, 0);
 }
 
+int stats_from_host(reattn_ctx* ctx, const StepPlan& P, const ScopeHeader& h, const double* ent,
+                    reattn_step_stats* st, double* entropy_host);
+
 int finish_step_stats(reattn_ctx* ctx, const StepPlan& P, const ScopeHeader& h,
                       reattn_step_stats* st, double* entropy_host) {
     int rc = status_from_scope(ctx, h.error);
@@ -381,13 +384,23 @@ int finish_step_stats(reattn_ctx* ctx, const StepPlan& P, const ScopeHeader& h,
     if (!ent.empty())
         CU(ctx, cudaMemcpy(ent.data(), P.entropy, ent.size() * sizeof(double),
                            cudaMemcpyDeviceToHost));
-    if (entropy_host) std::copy(ent.begin(), ent.end(), entropy_host);
+    return stats_from_host(ctx, P, h, ent.data(), st, entropy_host);
+}
+
+// the step's stats from its header and entropies already on the host
+int stats_from_host(reattn_ctx* ctx, const StepPlan& P, const ScopeHeader& h, const double* ent_p,
+                    reattn_step_stats* st, double* entropy_host) {
+    int rc = status_from_scope(ctx, h.error);
+    if (rc) return rc;
+    if (P.n_q == 0 && h.L == 0) return set_err(ctx, REATTN_EINVAL, "empty key set");
+    const uint64_t n_ent = P.n_q * P.n_head;
+    if (entropy_host) std::copy(ent_p, ent_p + n_ent, entropy_host);
     if (st) {
         std::memset(st, 0, sizeof(*st));
         double mx = 0.0, sum = 0.0;
         for (uint64_t hh = 0; hh < P.n_head; ++hh)
             for (uint64_t i = 0; i < P.n_q; ++i) {
-                const double e = ent[i * P.n_head + hh];
+                const double e = ent_p[i * P.n_head + hh];
                 mx = std::max(mx, e);
                 sum += e;
             }
@@ -422,6 +435,10 @@ struct reattn_plan {
     uint64_t total0 = 0;      // the cache length a frozen (non-dynamic) plan was built for
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    // staged results (reattn_plan_stage_result): pinned host copies of the step's header,
+    // entropies and spans, filled by copies enqueued behind the replay
+    void* staged = nullptr;
+    bool staged_pending = false;
 };
 
 namespace {
@@ -1128,6 +1145,7 @@ void reattn_plan_destroy(reattn_plan* p) {
     if (p->exec) cudaGraphExecDestroy(p->exec);
     if (p->graph) cudaGraphDestroy(p->graph);
     cudaFree(p->mem);
+    if (p->staged) cudaFreeHost(p->staged);
     delete p;
 }
 float* reattn_plan_q(const reattn_plan* p) { return p->q; }
@@ -1232,6 +1250,57 @@ int reattn_plan_result(reattn_plan* p, reattn_step_stats* st, uint64_t* span_b_h
             span_e_host[i] = e[i];
         }
     }
+    return REATTN_OK;
+}
+
+// Decode loops that run many plans per token (one per layer) read every plan's result after
+// one synchronisation: stage enqueues the copies, staged_result reads them after the caller
+// synchronised the context stream.
+namespace {
+size_t staged_bytes(const StepPlan& P) {
+    const uint64_t kp = std::max<uint64_t>(1, P.cfg.k_prime);
+    return sizeof(ScopeHeader) + P.n_q * P.n_head * sizeof(double) + 2 * kp * sizeof(uint32_t);
+}
+}  // namespace
+
+int reattn_plan_stage_result(reattn_plan* p) {
+    reattn_ctx* ctx = p->ctx;
+    const StepPlan& P = p->P;
+    if (!p->staged) CU(ctx, cudaHostAlloc(&p->staged, staged_bytes(P), cudaHostAllocDefault));
+    uint8_t* h = (uint8_t*)p->staged;
+    const uint64_t kp = std::max<uint64_t>(1, P.cfg.k_prime);
+    const size_t ent = P.n_q * P.n_head * sizeof(double);
+    CU(ctx, cudaMemcpyAsync(h, P.hdr, sizeof(ScopeHeader), cudaMemcpyDeviceToHost, ctx->stream));
+    h += sizeof(ScopeHeader);
+    if (ent) CU(ctx, cudaMemcpyAsync(h, P.entropy, ent, cudaMemcpyDeviceToHost, ctx->stream));
+    h += ent;
+    CU(ctx, cudaMemcpyAsync(h, P.span_b, kp * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(h + kp * 4, P.span_e, kp * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    p->staged_pending = true;
+    return REATTN_OK;
+}
+
+int reattn_plan_staged_result(reattn_plan* p, reattn_step_stats* st, uint64_t* span_b_host,
+                              uint64_t* span_e_host, double* entropy_host) {
+    reattn_ctx* ctx = p->ctx;
+    if (!p->staged_pending)
+        return set_err(ctx, REATTN_ELOGIC, "plan: no staged result (reattn_plan_stage_result first)");
+    p->staged_pending = false;
+    refresh_geometry(p->P, p->cache);
+    const StepPlan& P = p->P;
+    const uint8_t* h = (const uint8_t*)p->staged;
+    ScopeHeader hdr;
+    std::memcpy(&hdr, h, sizeof(hdr));
+    const double* ent = (const double*)(h + sizeof(ScopeHeader));
+    const uint64_t kp = std::max<uint64_t>(1, P.cfg.k_prime);
+    const uint32_t* b = (const uint32_t*)(h + sizeof(ScopeHeader) + P.n_q * P.n_head * sizeof(double));
+    int rc = stats_from_host(ctx, P, hdr, ent, st, entropy_host);
+    if (rc) return rc;
+    if (span_b_host)
+        for (uint32_t i = 0; i < std::min<uint64_t>(hdr.n_spans, kp); ++i) {
+            span_b_host[i] = b[i];
+            span_e_host[i] = b[kp + i];
+        }
     return REATTN_OK;
 }
 

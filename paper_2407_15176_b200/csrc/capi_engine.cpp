@@ -208,6 +208,7 @@ struct reattn_engine {
     // decode: one CUDA-graph plan per layer that follows the growing cache (reattn_plan_*),
     // launched without a host synchronisation; their stats are read once per forward block
     std::vector<reattn_plan*> plans;
+    std::vector<reattn_plan*> pending;  // plans whose staged results the next sync completes
     // decode-token projections: GEMV workspace (split-k partials + self-resetting tickets)
     void* gemv_ws = nullptr;
     uint64_t gemv_n_max = 0;
@@ -380,6 +381,7 @@ int forward_block(reattn_engine* e, uint64_t rows) {
         const float* attn = e->attn;
         if (pl) {  // the graph replay, no host synchronisation; stats after the block
             if ((rc = reattn_plan_launch(pl))) return rc;
+            if ((rc = reattn_plan_stage_result(pl))) return rc;
             launched[l] = pl;
             attn = reattn_plan_out(pl);
         } else {
@@ -407,15 +409,24 @@ int forward_block(reattn_engine* e, uint64_t rows) {
         if ((rc = gemm(e, rows, D, F, e->gate, F, cslot(e->w, REATTN_W_DOWN, l), D, e->x, D, 1.0f)))
             return rc;
     }
-    // the plans' stats, in layer order (one synchronisation per block, inside plan_result)
-    for (uint64_t l = 0; l < c.n_layer; ++l) {
-        if (!launched[l]) continue;
+    // the plans' results are copied behind the block; folded in layer order after the next
+    // synchronisation of the stream (fold_pending)
+    e->pending = launched;
+    e->last_rows = rows;
+    return REATTN_OK;
+}
+
+// fold the staged results of the last block's plans (engine.hpp:100-112, layer order); the
+// caller has synchronised the context stream
+int fold_pending(reattn_engine* e) {
+    for (uint64_t l = 0; l < e->pending.size(); ++l) {
+        if (!e->pending[l]) continue;
         reattn_step_stats st{};
-        int rc = reattn_plan_result(launched[l], &st, e->sb.data(), e->se.data(), nullptr);
+        int rc = reattn_plan_staged_result(e->pending[l], &st, e->sb.data(), e->se.data(), nullptr);
         if (rc) return rc;
         fold_stats(e, l, st);
     }
-    e->last_rows = rows;
+    e->pending.clear();
     return REATTN_OK;
 }
 
@@ -688,6 +699,7 @@ int reattn_engine_create(reattn_ctx* ctx, const reattn_weights* w, const reattn_
 int reattn_engine_reset(reattn_engine* e) {
     reattn_ctx* ctx = e->ctx;
     const reattn_model_config& c = e->w->cfg;
+    e->pending.clear();
     for (auto* p : e->plans) reattn_plan_destroy(p);
     e->plans.assign(c.n_layer, nullptr);
     for (auto* cache : e->caches) reattn_cache_destroy(cache);
@@ -726,6 +738,7 @@ int reattn_engine_prefill(reattn_engine* e, const uint32_t* tokens, uint64_t n, 
         ++e->stats.chunks_processed;
     }
     CU(ctx, cudaStreamSynchronize(ctx->stream));
+    if ((rc = fold_pending(e))) return rc;
     if (rows_out) *rows_out = e->last_rows;
     return REATTN_OK;
 }
@@ -776,6 +789,7 @@ int reattn_engine_decode_step(reattn_engine* e, uint32_t last_token, uint32_t* n
                             cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaMemcpyAsync(&nt, e->next, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
+    if ((rc = fold_pending(e))) return rc;
     const auto t1 = std::chrono::steady_clock::now();
     e->latency_ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
     ++e->stats.decode_steps;

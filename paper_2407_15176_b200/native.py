@@ -163,6 +163,8 @@ SIGNATURES = [
     ("reattn_plan_stats", C.c_int, [vp, C.POINTER(StepStats)]),
     ("reattn_plan_info", C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
     ("reattn_plan_result", C.c_int, [vp, C.POINTER(StepStats), vp, vp, vp]),
+    ("reattn_plan_stage_result", C.c_int, [vp]),
+    ("reattn_plan_staged_result", C.c_int, [vp, C.POINTER(StepStats), vp, vp, vp]),
     ("reattn_plan_set_append", C.c_int, [vp, C.c_int]),
     ("reattn_plan_follows_cache", C.c_int, [vp]),
     ("reattn_plan_cache_generation", u64, [vp]),
@@ -598,19 +600,23 @@ class Plan:
         self.ctx.check(self.ctx.lib.reattn_plan_stats(self.h, C.byref(st)))
         return st
 
-    def result(self, k_prime: int) -> "StepResult":
+    def result(self, k_prime: int, staged: bool = False) -> "StepResult":
         """The last replay's attend_step outputs: out (device tensor), stats, spans and the
-        row entropies [n_q, n_head] (reattn_plan_result)."""
+        row entropies [n_q, n_head] (reattn_plan_result; staged=True: the copies enqueued by
+        stage_result, read after the caller synchronised -- reattn_plan_staged_result)."""
         import numpy as np
         st = StepStats()
         sb = np.zeros(max(1, k_prime), np.uint64)
         se = np.zeros(max(1, k_prime), np.uint64)
         ent = np.zeros(max(1, self.n_q * self.n_head), np.float64)
-        self.ctx.check(self.ctx.lib.reattn_plan_result(self.h, C.byref(st), sb.ctypes.data,
-                                                        se.ctypes.data, ent.ctypes.data))
+        fn = self.ctx.lib.reattn_plan_staged_result if staged else self.ctx.lib.reattn_plan_result
+        self.ctx.check(fn(self.h, C.byref(st), sb.ctypes.data, se.ctypes.data, ent.ctypes.data))
         n = st.n_spans
         return StepResult(self.out, st, (sb[:n].copy(), se[:n].copy()),
                           ent[: self.n_q * self.n_head].reshape(self.n_q, self.n_head))
+
+    def stage_result(self) -> None:
+        self.ctx.check(self.ctx.lib.reattn_plan_stage_result(self.h))
 
     def info(self) -> dict:
         a, b, c = u64(), u64(), u64()

@@ -65,7 +65,16 @@ def test_one_plan_follows_appends(ctx, dtype, fork, monkeypatch):
         plan.q.copy_(q)
         torch.cuda.synchronize()
         plan.launch()
+        plan.stage_result()  # the engine's per-layer path: copies behind the replay, one sync
+        torch.cuda.synchronize()
+        staged = plan.result(127, staged=True)
         check_vs_oracle(plan, cache, dtype, q, total, label=f"step {step} total {total}")
+        direct = plan.result(127)
+        assert staged.stats.scope_len == direct.stats.scope_len
+        assert staged.stats.entropy_max == direct.stats.entropy_max
+        assert np.array_equal(staged.spans[0], direct.spans[0])
+        assert np.array_equal(staged.spans[1], direct.spans[1])
+        assert np.array_equal(staged.entropy, direct.entropy)
 
 
 @pytest.mark.parametrize("fork", ["0", "1"])
