@@ -212,23 +212,22 @@ cudaError_t launch_scale(float* x, uint64_t n, float a, cudaStream_t s) {
 }
 
 // y[n] = sum_k x[k] W[k][n] (+ beta y[n]) for one row x, for up to three matrices sharing x
-// (the q/k/v projections; gate/up) in one launch: the weights are read exactly once, so the
-// kernel is an HBM stream.  A CTA owns 128 columns (a lane one float4) of a k-slice of one
-// matrix; its 8 warps take the slice's rows round-robin with a register double buffer of 8
-// float4 rows in flight per lane, reduce through shared memory in warp order, and split-k
-// partials are summed in a fixed order by the last CTA of the column tile (a ticket), so the
-// result is deterministic.  In the gated-FFN pair mode the gate and up tiles of the same
-// columns share one ticket and the last CTA writes silu(g) * u (model.hpp:170-178) into the
-// gate buffer.  Launched with programmatic stream serialisation: a CTA issues its first
-// weight rows before griddepcontrol.wait, so the stream of one projection starts under the
-// tail of the kernel before it.  fp32 throughout, one fused multiply-add per row.
+// (the q/k/v projections; gate/up) in one launch.  The weights are read exactly once, so the
+// kernel is an HBM stream, and its work is split stream-K style so that every SM streams the
+// same number of bytes whatever the shape: a tile is 128 columns of one matrix (a lane one
+// float4), a unit is 64 rows of a tile (8 warps x 8 rows), and the tiles' units, laid end to
+// end, are cut into one contiguous range per resident CTA.  A warp keeps the next unit's 8
+// rows in flight (register double buffer) while it accumulates the current one, across tile
+// boundaries too.  Where a CTA's range ends a tile segment it reduces its warps in order and,
+// when the tile has several contributors, stores the partial at slot (cta + tile) -- unique,
+// since contributors of consecutive tiles overlap in at most one CTA -- and the last
+// contributor (a ticket counting units) sums the partials in CTA order: deterministic.  In
+// the gated-FFN pair mode the gate and up tiles of the same columns share one ticket and the
+// last contributor writes silu(g) * u (model.hpp:170-178) into the gate buffer.  Launched
+// with programmatic stream serialisation: the first unit's weight rows are issued before
+// griddepcontrol.wait, under the tail of the kernel before.  fp32, one FMA per row.
 namespace {
-constexpr int kGemvWarps = 8, kGemvCols = 128, kGemvUnroll = 8, kGemvTargetCtas = 148 * 3,
-              kGemvMaxCtas = 148 * 8;
-int gemv_target_env() {
-    static const int t = getenv("REATTN_GEMV_CTAS") ? atoi(getenv("REATTN_GEMV_CTAS")) : kGemvTargetCtas;
-    return t;
-}
+constexpr int kGemvWarps = 8, kGemvCols = 128, kGemvRows = 8, kGemvUnitRows = kGemvWarps * kGemvRows;
 
 __device__ __forceinline__ float4 ld_stream4(const float* p) {
     float4 v;
@@ -256,150 +255,184 @@ struct GemvMat {
 struct GemvBatch {
     GemvMat m[3];
     int count;
-    int silu_pair;       // m[0] gate, m[1] up (same N): gate <- silu(g) * u
-    uint32_t S, kc, K;   // splits, rows per split, rows
-    uint32_t tiles;      // tiles over all matrices (grid.x)
+    int silu_pair;      // m[0] gate, m[1] up (same N): gate <- silu(g) * u
+    uint32_t K, upt;    // rows; units per tile
+    uint32_t tiles;     // tiles over all matrices
+    uint64_t units;     // tiles * upt
 };
 
-__global__ void __launch_bounds__(kGemvWarps * 32) gemv_kernel(const float* __restrict__ x, GemvBatch B,
-                                                               float* ws, uint32_t* tickets) {
-    __shared__ float4 red[kGemvWarps * 32];
-    __shared__ uint32_t s_last;
+__device__ __forceinline__ uint32_t unit_begin(uint64_t c, uint64_t units, uint32_t G) {
+    return (uint32_t)(c * units / G);
+}
+// the CTA whose range holds unit u: the largest c with unit_begin(c) <= u
+__device__ __forceinline__ uint32_t unit_owner(uint64_t u, uint64_t units, uint32_t G) {
+    return (uint32_t)(((u + 1) * G - 1) / units);
+}
+
+__device__ __forceinline__ int mat_of(const GemvBatch& B, uint32_t t) {
+    return B.count > 2 && t >= B.m[2].tile0 ? 2 : B.count > 1 && t >= B.m[1].tile0 ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(const float* __restrict__ x, GemvBatch B,
+                                                                  float* ws, uint32_t* tickets) {
+    __shared__ float4 red[2][kGemvWarps * 32];
     asm volatile("griddepcontrol.launch_dependents;");
-    const uint32_t gt = blockIdx.x, split = blockIdx.y, S = B.S;
-    const int mi = B.count > 2 && gt >= B.m[2].tile0 ? 2 : B.count > 1 && gt >= B.m[1].tile0 ? 1 : 0;
-    const GemvMat& M = B.m[mi];
+    const uint32_t G = gridDim.x, c = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t k0 = split * B.kc, rows = min(B.K, k0 + B.kc) - k0;
-    const uint32_t col = (gt - M.tile0) * kGemvCols + lane * 4;
-    const bool ok = col < M.N;
+    const uint32_t u0 = unit_begin(c, B.units, G), u1 = unit_begin(c + 1, B.units, G);
+    float4 w[2][kGemvRows];
+    float xv[2][kGemvRows];
+    auto load_w = [&](uint32_t u, int b) {
+        const uint32_t t = u / B.upt;
+        const GemvMat& M = B.m[mat_of(B, t)];
+        const uint32_t col = (t - M.tile0) * kGemvCols + lane * 4;
+        const uint32_t r0 = (u % B.upt) * kGemvUnitRows + warp;
+        const float* wp = M.W + (uint64_t)r0 * M.ldw + col;
+#pragma unroll
+        for (int i = 0; i < kGemvRows; ++i)
+            w[b][i] = col < M.N && r0 + i * kGemvWarps < B.K ? ld_stream4(wp + (uint64_t)i * kGemvWarps * M.ldw)
+                                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    auto load_x = [&](uint32_t u, int b) {
+        const uint32_t r0 = (u % B.upt) * kGemvUnitRows + warp;
+#pragma unroll
+        for (int i = 0; i < kGemvRows; ++i) xv[b][i] = r0 + i * kGemvWarps < B.K ? x[r0 + i * kGemvWarps] : 0.f;
+    };
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    {
-        const float* wp = M.W + (uint64_t)k0 * M.ldw + col;
-        const float* xp = x + k0;
-        float4 w[2][kGemvUnroll];
-        float xv[2][kGemvUnroll];
-        auto load_w = [&](uint32_t r0, int b) {
+    auto fma_rows = [&](int b) {
 #pragma unroll
-            for (int u = 0; u < kGemvUnroll; ++u) {
-                const uint32_t r = r0 + u * kGemvWarps;
-                w[b][u] = ok && r < rows ? ld_stream4(wp + (uint64_t)r * M.ldw) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        };
-        auto load_x = [&](uint32_t r0, int b) {
-#pragma unroll
-            for (int u = 0; u < kGemvUnroll; ++u) {
-                const uint32_t r = r0 + u * kGemvWarps;
-                xv[b][u] = r < rows ? xp[r] : 0.f;
-            }
-        };
-        auto fma_rows = [&](int b) {
-#pragma unroll
-            for (int u = 0; u < kGemvUnroll; ++u) {
-                acc.x = fmaf(xv[b][u], w[b][u].x, acc.x);
-                acc.y = fmaf(xv[b][u], w[b][u].y, acc.y);
-                acc.z = fmaf(xv[b][u], w[b][u].z, acc.z);
-                acc.w = fmaf(xv[b][u], w[b][u].w, acc.w);
-            }
-        };
-        constexpr uint32_t step = kGemvUnroll * kGemvWarps;
-        uint32_t r = warp;
-        load_w(r, 0);                                       // weights: constant
-        asm volatile("griddepcontrol.wait;" ::: "memory");  // x (and y, ws) from the kernel before
-        load_x(r, 0);
-        for (;;) {
-            if (r + step < rows) {
-                load_w(r + step, 1);
-                load_x(r + step, 1);
-            }
-            fma_rows(0);
-            r += step;
-            if (r >= rows) break;
-            if (r + step < rows) {
-                load_w(r + step, 0);
-                load_x(r + step, 0);
-            }
-            fma_rows(1);
-            r += step;
-            if (r >= rows) break;
+        for (int i = 0; i < kGemvRows; ++i) {
+            acc.x = fmaf(xv[b][i], w[b][i].x, acc.x);
+            acc.y = fmaf(xv[b][i], w[b][i].y, acc.y);
+            acc.z = fmaf(xv[b][i], w[b][i].z, acc.z);
+            acc.w = fmaf(xv[b][i], w[b][i].w, acc.w);
         }
-    }
-    // the CTA's partial: warps summed in order
-    red[warp * 32 + lane] = acc;
-    __syncthreads();
-    float4 p = red[lane];
-#pragma unroll
-    for (int i = 1; i < kGemvWarps; ++i) add4(p, red[i * 32 + lane]);
-    const bool pair = B.silu_pair != 0;
-    if (S > 1 || pair) {
-        const uint32_t pair_tiles = B.m[1].tile0;  // pair mode: gate tiles, then up tiles
-        const uint32_t ticket = pair ? gt % pair_tiles : gt;
-        const uint32_t arrivals = pair ? 2 * S : S;
-        if (warp == 0 && ok) reinterpret_cast<float4*>(ws)[((uint64_t)split * B.tiles + gt) * 32 + lane] = p;
-        __threadfence();
+    };
+    auto silu = [](float gv, float uv) { return __fmul_rn(__fdiv_rn(gv, __fadd_rn(1.0f, expf(-gv))), uv); };
+    int rb = 0;  // shared-memory reduction buffer of the next epilogue
+    // the end of tile t's segment in this CTA: reduce the warps; a tile with one contributor
+    // is written here, otherwise its partial goes to the workspace and the last contributor
+    // of the tile (pair: of both tiles) finishes it (warp 0 only; the other warps stream on)
+    auto epilogue = [&](uint32_t t) {
+        red[rb][warp * 32 + lane] = acc;
+        acc = make_float4(0.f, 0.f, 0.f, 0.f);
         __syncthreads();
-        if (threadIdx.x == 0) {
-            s_last = atomicAdd(&tickets[ticket], 1u) == arrivals - 1;
-            if (s_last) tickets[ticket] = 0;  // the next launch on the stream starts from zero
-        }
-        __syncthreads();
-        if (!s_last) return;
-        __threadfence();
-        // the last CTA: warp w sums splits w, w + 8, ... of a tile (loads issued together),
-        // then the 8 warp sums in order
-        auto reduce_tile = [&](uint32_t t) -> float4 {
-            constexpr int kPer = 8;
-            float4 v[kPer];
+        const int b = rb;
+        rb ^= 1;
+        if (warp != 0) return;
+        float4 p = red[b][lane];
 #pragma unroll
-            for (int j = 0; j < kPer; ++j) {
-                const uint32_t s2 = warp + j * kGemvWarps;
-                v[j] = ok && s2 < S ? __ldcg(reinterpret_cast<const float4*>(ws) + ((uint64_t)s2 * B.tiles + t) * 32 + lane)
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = 1; i < kGemvWarps; ++i) add4(p, red[b][i * 32 + lane]);
+        const bool pair = B.silu_pair != 0;
+        const GemvMat& M = B.m[mat_of(B, t)];
+        const uint32_t col = (t - M.tile0) * kGemvCols + lane * 4;
+        const bool ok = col < M.N;
+        const uint32_t cf = unit_owner((uint64_t)t * B.upt, B.units, G);
+        const uint32_t cl = unit_owner((uint64_t)(t + 1) * B.upt - 1, B.units, G);
+        if (!pair && cf == cl) {
+            if (!ok) return;
+            float4* yp = reinterpret_cast<float4*>(M.y + col);
+            if (M.beta != 0.0f) {
+                const float4 o = *yp;
+                p.x = fmaf(M.beta, o.x, p.x);
+                p.y = fmaf(M.beta, o.y, p.y);
+                p.z = fmaf(M.beta, o.z, p.z);
+                p.w = fmaf(M.beta, o.w, p.w);
             }
-            for (uint32_t s2 = warp + kPer * kGemvWarps; ok && s2 < S; s2 += kGemvWarps)
-                add4(v[kPer - 1], __ldcg(reinterpret_cast<const float4*>(ws) + ((uint64_t)s2 * B.tiles + t) * 32 + lane));
-            float4 q = v[0];
-#pragma unroll
-            for (int j = 1; j < kPer; ++j) add4(q, v[j]);
-            __syncthreads();
-            red[warp * 32 + lane] = q;
-            __syncthreads();
-            float4 o = red[lane];
-#pragma unroll
-            for (int i = 1; i < kGemvWarps; ++i) add4(o, red[i * 32 + lane]);
-            return o;
+            *yp = p;
+            return;
+        }
+        if (ok) reinterpret_cast<float4*>(ws)[(uint64_t)(c + t) * 32 + lane] = p;
+        // units of tile t in this CTA
+        const uint64_t tb = (uint64_t)t * B.upt, te = tb + B.upt;
+        const uint32_t mine = (uint32_t)((te < u1 ? te : (uint64_t)u1) - (tb > u0 ? tb : (uint64_t)u0));
+        const uint32_t pt = pair ? B.m[1].tile0 : 0;  // pair: gate tiles [0, pt), up [pt, 2pt)
+        const uint32_t ticket = pair ? t % pt : t;
+        const uint32_t need = pair ? 2 * B.upt : B.upt;
+        __threadfence();
+        __syncwarp();
+        uint32_t last = 0;
+        if (lane == 0) {
+            last = atomicAdd(&tickets[ticket], mine) + mine == need;
+            if (last) tickets[ticket] = 0;  // the next launch on the stream starts from zero
+        }
+        if (!__shfl_sync(0xFFFFFFFFu, last, 0)) return;
+        __threadfence();
+        auto total_of = [&](uint32_t tt) {
+            const uint32_t f = unit_owner((uint64_t)tt * B.upt, B.units, G);
+            const uint32_t l = unit_owner((uint64_t)(tt + 1) * B.upt - 1, B.units, G);
+            float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (!ok) return q;
+            for (uint32_t j = f; j <= l; ++j)
+                add4(q, __ldcg(reinterpret_cast<const float4*>(ws) + (uint64_t)(j + tt) * 32 + lane));
+            return q;
         };
+        if (!ok) return;
         if (pair) {
-            const uint32_t tg = gt % pair_tiles;
-            const float4 g = reduce_tile(tg), u = reduce_tile(tg + pair_tiles);
-            if (warp != 0 || !ok) return;
-            auto silu = [](float gv, float uv) { return __fmul_rn(__fdiv_rn(gv, __fadd_rn(1.0f, expf(-gv))), uv); };
+            const uint32_t tg = t % pt;
+            const float4 g = total_of(tg), u = total_of(tg + pt);
             *reinterpret_cast<float4*>(B.m[0].y + col) =
                 make_float4(silu(g.x, u.x), silu(g.y, u.y), silu(g.z, u.z), silu(g.w, u.w));
             return;
         }
-        p = reduce_tile(gt);
+        p = total_of(t);
+        float4* yp = reinterpret_cast<float4*>(M.y + col);
+        if (M.beta != 0.0f) {
+            const float4 o = *yp;
+            p.x = fmaf(M.beta, o.x, p.x);
+            p.y = fmaf(M.beta, o.y, p.y);
+            p.z = fmaf(M.beta, o.z, p.z);
+            p.w = fmaf(M.beta, o.w, p.w);
+        }
+        *yp = p;
+    };
+    if (u0 >= u1) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        return;
     }
-    if (warp != 0 || !ok) return;
-    float4* yp = reinterpret_cast<float4*>(M.y + col);
-    if (M.beta != 0.0f) {
-        const float4 o = *yp;
-        p.x = fmaf(M.beta, o.x, p.x);
-        p.y = fmaf(M.beta, o.y, p.y);
-        p.z = fmaf(M.beta, o.z, p.z);
-        p.w = fmaf(M.beta, o.w, p.w);
+    load_w(u0, 0);                                      // weights: constant
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // x, y, workspace: the kernel before
+    load_x(u0, 0);
+    for (uint32_t u = u0;;) {
+        if (u + 1 < u1) {
+            load_w(u + 1, 1);
+            load_x(u + 1, 1);
+        }
+        fma_rows(0);
+        if (u + 1 >= u1 || (u + 1) / B.upt != u / B.upt) epilogue(u / B.upt);
+        if (++u >= u1) break;
+        if (u + 1 < u1) {
+            load_w(u + 1, 0);
+            load_x(u + 1, 0);
+        }
+        fma_rows(1);
+        if (u + 1 >= u1 || (u + 1) / B.upt != u / B.upt) epilogue(u / B.upt);
+        if (++u >= u1) break;
     }
-    *yp = p;
+}
+
+int gemv_ctas() {
+    static int g = [] {
+        int dev = 0, sms = 148, occ = 2;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_kernel, kGemvWarps * 32, 0);
+        const char* e = getenv("REATTN_GEMV_CTAS");
+        return e ? std::max(1, atoi(e)) : sms * std::max(1, occ);
+    }();
+    return g;
 }
 }  // namespace
 
 size_t gemv_workspace_bytes(uint64_t n_max) {
+    // partial slots cta + tile < ctas + tiles; one ticket per tile
     const uint64_t tiles = 3 * ((n_max + kGemvCols - 1) / kGemvCols);
-    return (size_t)(kGemvMaxCtas + tiles) * kGemvCols * sizeof(float) + tiles * sizeof(uint32_t) + 256;
+    const uint64_t ctas = 148 * 8;
+    return (size_t)(ctas + tiles) * kGemvCols * sizeof(float) + tiles * sizeof(uint32_t) + 256;
 }
 
 bool gemv_supported(uint64_t N, uint64_t K, uint64_t ldw, const void* x, const void* W, const void* y) {
-    return N % 4 == 0 && ldw % 4 == 0 && N <= UINT32_MAX && K > 0 && K <= UINT32_MAX &&
+    return N % 4 == 0 && ldw % 4 == 0 && N <= UINT32_MAX && K > 0 && K <= (1ull << 31) &&
            ((uintptr_t)W & 15) == 0 && ((uintptr_t)y & 15) == 0 && ((uintptr_t)x & 3) == 0;
 }
 
@@ -419,15 +452,15 @@ cudaError_t launch_gemv_batch(const float* x, uint64_t K, const GemvDesc* mats, 
     B.silu_pair = silu_pair ? 1 : 0;
     B.tiles = tiles;
     B.K = (uint32_t)K;
-    const uint64_t target = std::min<int>(std::max(gemv_target_env(), 1), kGemvMaxCtas);
-    uint64_t S = (target + tiles - 1) / tiles;
-    S = std::max<uint64_t>(1, std::min<uint64_t>(S, K / (kGemvUnroll * kGemvWarps)));
-    B.S = (uint32_t)S;
-    B.kc = (uint32_t)((K + S - 1) / S);
+    B.upt = (uint32_t)((K + kGemvUnitRows - 1) / kGemvUnitRows);
+    B.units = (uint64_t)tiles * B.upt;
+    if (B.units > UINT32_MAX) return cudaErrorInvalidValue;
+    const uint32_t G = (uint32_t)std::min<uint64_t>(std::min(gemv_ctas(), 148 * 8), B.units);
+    const uint64_t tiles_max = 3 * ((n_max + kGemvCols - 1) / kGemvCols);
     float* part = (float*)ws;
-    uint32_t* tickets = (uint32_t*)(part + (kGemvMaxCtas + 3 * ((n_max + kGemvCols - 1) / kGemvCols)) * kGemvCols);
+    uint32_t* tickets = (uint32_t*)(part + (148 * 8 + tiles_max) * kGemvCols);
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(tiles, (unsigned)S);
+    cfg.gridDim = dim3(G);
     cfg.blockDim = dim3(kGemvWarps * 32);
     cfg.stream = s;
     cudaLaunchAttribute at[1];
