@@ -90,7 +90,8 @@ int plan_step(reattn_ctx* ctx, const reattn_cache* cache, const reattn_rope* rop
         if (n_cand >= (1ull << 31))
             return set_err(ctx, REATTN_ERUNTIME, "vote: candidate count exceeds 2^31");
         P.large_vote = n_cand > kVoteMaxSmem;
-        P.vote_ws_bytes = P.large_vote ? vote_large_workspace((uint32_t)n_cand) : 0;
+        P.vote_ws_bytes = P.large_vote ? vote_large_workspace((uint32_t)n_cand, (uint32_t)P.middle,
+                                                              (uint32_t)cfg->k_prime) : 0;
         ScanArgs& a = P.scan.a;
         a.q = q_dev;
         a.n_q = (int)n_q;
@@ -325,8 +326,11 @@ int enqueue_select_part(reattn_ctx* ctx, StepPlan& P, const reattn_cache* cache,
         ++P.kernels;
     }
     if (!fused && P.large_vote) {
+        // the bounded vote's tallies stay clean across replays; a fresh (arena) workspace
+        // is zeroed first -- plans zero theirs at creation
+        if (zero_ticket) CU(ctx, cudaMemsetAsync(P.vote_ws, 0, P.vote_ws_bytes, s));
         CU(ctx, launch_vote_large(sa, P.vote_ws, s));
-        P.kernels += 8;
+        P.kernels += vote_large_kernels(sa.n_lists * sa.list_len, sa.middle_len, sa.k_prime);
     } else if (!fused) {
         CU(ctx, launch_select(sa, s));
         ++P.kernels;
@@ -895,7 +899,7 @@ int reattn_vote(reattn_ctx* ctx, const uint32_t* idx_dev, const float* score_dev
     if (k_prime == 0 || n == 0) return REATTN_OK;
     if (n >= (1ull << 31)) return set_err(ctx, REATTN_ERUNTIME, "vote: candidate count exceeds 2^31");
     const bool large = n > kVoteMaxSmem;
-    int rc = ensure_arena(ctx, 4096 + (large ? vote_large_workspace((uint32_t)n) : 0));
+    int rc = ensure_arena(ctx, 4096 + (large ? vote_large_workspace((uint32_t)n, 0, 0) : 0));
     if (rc) return rc;
     SelectArgs sa;
     std::memset(&sa, 0, sizeof(sa));
@@ -926,7 +930,7 @@ int reattn_tally(reattn_ctx* ctx, const uint32_t* idx_dev, const float* score_de
     if (n == 0) return REATTN_OK;
     if (n >= (1ull << 31)) return set_err(ctx, REATTN_ERUNTIME, "vote: candidate count exceeds 2^31");
     const bool large = n > kVoteMaxSmem;
-    int rc = ensure_arena(ctx, 4096 + (large ? vote_large_workspace((uint32_t)n) : 0));
+    int rc = ensure_arena(ctx, 4096 + (large ? vote_large_workspace((uint32_t)n, 0, 0) : 0));
     if (rc) return rc;
     SelectArgs sa;
     std::memset(&sa, 0, sizeof(sa));

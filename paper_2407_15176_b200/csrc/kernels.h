@@ -131,7 +131,10 @@ constexpr uint32_t kVoteMaxSmem = 8192;
 size_t select_smem_bytes(uint32_t n_cand, uint32_t k_prime);
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t s);
 // > kVoteMaxSmem candidates: device-wide radix-sort vote (vote_large.cu), then spans+scope
-size_t vote_large_workspace(uint32_t n_cand);
+// bounded path (middle_len > 0, k' <= 1024): the workspace must be zeroed once (it stays
+// clean across launches)
+size_t vote_large_workspace(uint32_t n_cand, uint32_t middle_len, uint32_t k_prime);
+uint32_t vote_large_kernels(uint32_t n_cand, uint32_t middle_len, uint32_t k_prime);
 cudaError_t launch_vote_large(const SelectArgs& a, void* workspace, cudaStream_t s);
 
 // ---- K4+K5: gather + RoPE + finite-scope attention (attend.hpp, engine.hpp:71-107)

@@ -374,6 +374,31 @@ def test_attend_step_prefill_chunk_large_vote(ctx):
     assert np.abs(res.out.cpu().numpy() - out).max() <= ATTN_TOL
 
 
+@pytest.mark.parametrize("kp,total", [(600, 20000), (127, 150000), (1000, 60000)])
+def test_attend_step_prefill_bounded_vote(ctx, kp, total):
+    """The plans' large vote (histogram tally, per-CTA bitonic rank of 2048 middle rows, 4-ary
+    merge tree): k' up to 1024 kept rows, several tree levels, against the oracle -- through
+    the synchronous step (fresh workspace) and a plan replayed twice (its tallies must come
+    back clean)."""
+    cfg = N.SelectionConfig(k=8, k_prime=kp, span_m=2, l_global=16, l_local=256, l_chunk=512)
+    n_kv, nh, d, n_q, window, base = 4, 8, 32, 300, 4096, 10000.0
+    res, out, st, spans = step_vs_oracle(ctx, n_kv, nh, d, total, cfg, N.BF16, 1700 + kp, window,
+                                         base=base, n_q=n_q)
+    assert res.stats.scope_len == st.scope_len
+    assert np.array_equal(res.spans[0], spans[0]) and np.array_equal(res.spans[1], spans[1])
+    assert np.abs(res.out.cpu().numpy() - out).max() <= ATTN_TOL
+    cache, _, _ = make_cache(ctx, n_kv, d, total, cfg, N.BF16, 1700 + kp)
+    rope = N.Rope(ctx, d, base, window)
+    plan = N.Plan(ctx, cache, rope, n_q, nh, cfg)
+    plan.q.copy_(dev(synth.uniform(1700 + kp + 7, n_q * nh * d).reshape(n_q, nh * d)))
+    for _ in range(2):
+        plan.launch()
+        r = plan.result(kp)
+        assert r.stats.scope_len == st.scope_len
+        assert np.array_equal(r.spans[0], spans[0]) and np.array_equal(r.spans[1], spans[1])
+        assert np.abs(r.out.cpu().numpy() - out).max() <= ATTN_TOL
+
+
 @pytest.mark.parametrize("total", [9000, 40000, 131072])
 def test_attend_step_decode_local_fork(ctx, total, monkeypatch):
     """Decode with the local-window attention forked beside the scan (REATTN_FORK=1): the
