@@ -30,11 +30,16 @@
 //   warp 1  TMEM allocator (512 columns = 2 pairs x 2 query tiles x 128) + single-thread MMA
 //           issue: every K tile feeds BOTH query tiles (M = 256 per K tile), halving the K
 //           feed per FLOP; the MMA commit releases the K stage and the accumulator pair
-//   warps 2-17  epilogue, four per TMEM lane quarter (column half x query tile): one
-//           tcgen05.ld 32x32b.x64, release the accumulator pair, 8 group maxes against the
-//           admission limit, rare per-column list inserts.
+//   warps 2-17  epilogue, four per TMEM lane quarter (column half x query tile): two
+//           tcgen05.ld 32x32b.x32, 8 group maxes against the admission limit, a warp vote,
+//           rare per-column list inserts, release the accumulator pair.  The limit is kept
+//           in a register and recomputed only when an input changes (an insert, the other
+//           half's KT-th best, the board): round 2 cut the common path from ~244 to ~118
+//           instructions per tile and warp (2.50 -> 2.33 ms per config-3 chunk).  Tried and
+//           dropped: releasing the accumulator right after the loads with a one-group
+//           shared-memory stash for the inserts (2.86 ms: the stash bookkeeping spilled).
 //   Measured (config 3 chunk, incl. ~0.19 ms prep/kmax/merge): 2.50 ms (0.53 of the bf16
-//   burst) vs 2.67 ms with one query tile per CTA.  Ablations (REATTN_K2_NULL_EPILOGUE /
+//   burst) in round 1, 2.33 ms (0.57) in round 2, vs 2.67 ms with one query tile per CTA.  Ablations (REATTN_K2_NULL_EPILOGUE /
 //   REATTN_K2_NO_MMA): epilogue ablated 1.69 ms (was 1.96), feed alone 0.63 ms (was 0.85);
 //   the MMA alone dispatches 128x128x16 in 64 cycles (tools/micro/mma_rate.cu).  The two
 //   query tiles made the feed no longer the bound; the epilogue's admissions now are.
@@ -106,6 +111,14 @@ __device__ __forceinline__ void insert_in_order(float (&ts)[N], uint32_t (&ti)[N
             ti[j] = above ? ti[j - (j > 0)] : ci;
         }
     }
+}
+
+// nextafterf(x, -inf) for the admission limit's values (finite or -inf), without the
+// library call's NaN / denormal branches
+__device__ __forceinline__ float next_down(float x) {
+    const uint32_t u = __float_as_uint(x);
+    if (x == 0.0f) return __uint_as_float(0x80000001u);  // -denorm_min, from +0 and -0
+    return __uint_as_float(x > 0.0f ? u - 1u : (x == -INFINITY ? u : u + 1u));
 }
 
 // float <-> unsigned with the same order (for atomicMax); 0 encodes "nothing published"
@@ -264,11 +277,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
         unsigned* board = a.board + qrow;
         float tb = ord_dec(*(volatile unsigned*)board);
         float* thr_mine = s_thr + (qt * 2 + half) * kPM;
-        const float* thr_other = s_thr + (qt * 2 + (half ^ 1)) * kPM;
+        const uint32_t thr_other = smem_u32(s_thr + (qt * 2 + (half ^ 1)) * kPM + row);
+        // the limit's inputs change rarely (an insert, the other half's list, the board every
+        // 32 tiles): it is recomputed only then -- the common tile is 64 columns reduced to 8
+        // group maxima, one compare against the limit and a warp vote
+        float other_seen = -INFINITY;
+        float lim = -INFINITY;
+        bool dirty = true;
         for (int t = 0; t < n_tiles; ++t) {
             if ((t & 31) == 31) {
                 if (as[KT - 1] > -INFINITY) atomicMax(board, ord_enc(as[KT - 1]));
                 tb = ord_dec(*(volatile unsigned*)board);
+                dirty = true;
             }
             const int p = t % kPPairs;
             const uint32_t pph = (t / kPPairs) & 1u;
@@ -276,69 +296,94 @@ __global__ void __launch_bounds__(kPThreads, 1)
             tc_fence_after();
             const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) +
                                    (uint32_t)((p * kPQT + qt) * kPN + half * 64);
-            uint32_t r[64];
-            TMEM_LD_X64(taddr, r);
-            tmem_wait_ld();
+            const uint32_t key0 = (uint32_t)(t_first + t) * kPN + half * 64;
             if (a.null_epilogue) {  // ablation: the TMA / MMA / TMEM-read floor
+                uint32_t r[64];
+                TMEM_LD_X64(taddr, r);
+                tmem_wait_ld();
                 if (r[0] == 0x7FFFFFFFu && r[63] == 0x7FFFFFFFu) dropped = 1.0f;
                 tc_fence_before();
                 mbar_arrive(&tempty[p]);
                 continue;
             }
-            const uint32_t key0 = (uint32_t)(t_first + t) * kPN + half * 64;
-            if (key0 + 64 > a.count) {  // tail tile: keys past the middle never qualify
-#pragma unroll
-                for (int c = 0; c < 64; ++c)
-                    if (key0 + c >= a.count) r[c] = __float_as_uint(-INFINITY);
-            }
+            // 8 group maxima, 32 columns at a time (register pressure)
             float gx[8];
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                float m = __uint_as_float(r[8 * g]);
+            for (int hh = 0; hh < 2; ++hh) {
+                uint32_t r[32];
+                TMEM_LD_X32(taddr + 32 * hh, r);
+                tmem_wait_ld();
+                if (key0 + 64 > a.count) {  // tail tile: keys past the middle never qualify
 #pragma unroll
-                for (int u = 1; u < 8; ++u) m = fmaxf(m, __uint_as_float(r[8 * g + u]));
-                gx[g] = m;
+                    for (int c = 0; c < 32; ++c)
+                        if (key0 + 32 * hh + c >= a.count) r[c] = __float_as_uint(-INFINITY);
+                }
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    float m = __uint_as_float(r[8 * g]);
+#pragma unroll
+                    for (int u = 1; u < 8; ++u) m = fmaxf(m, __uint_as_float(r[8 * g + u]));
+                    gx[4 * hh + g] = m;
+                }
             }
-            // admission limit: (KT-th best S_hi so far) - 2 delta.  Before the list holds KT
-            // keys, the KT-th largest group max of this tile bounds the KT-th best from below;
-            // those keys are not listed yet, so one ulp lower keeps an exact tie (delta == 0)
-            // with them admissible.  The other column half's KT-th best is a lower bound of
-            // the row's k-th best too (any subset's is): a key at or below it - 2 delta is
-            // outside the merge's window (prefill_exact_merge_kernel).  Its keys are not
-            // ordered before ours, so one ulp lower again.  Read racily: every value ever
-            // stored is a valid bound.
-            const float other = ((volatile const float*)thr_other)[row];
-            float lim = fmaxf(as[KT - 1] - d2, nextafterf(fmaxf(other, tb) - d2, -INFINITY));
-            if (as[KT - 1] == -INFINITY)
-                lim = fmaxf(lim, nextafterf(kth_of_8<KT>(gx) - d2, -INFINITY));
+            // admission limit: (KT-th best S_hi so far) - 2 delta.  The other column half's
+            // KT-th best is a lower bound of the row's k-th best too (any subset's is): a key
+            // at or below it - 2 delta is outside the merge's window
+            // (prefill_exact_merge_kernel).  Its keys are not ordered before ours, so one ulp
+            // lower.  Read racily: every value ever stored is a valid bound.
+            float other;
+            asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(other) : "r"(thr_other));
+            if (other != other_seen) {
+                other_seen = other;
+                dirty = true;
+            }
+            if (dirty) {
+                lim = fmaxf(as[KT - 1] - d2, next_down(fmaxf(other, tb) - d2));
+                dirty = false;
+            }
+            const float tmax = fmaxf(fmaxf(fmaxf(gx[0], gx[1]), fmaxf(gx[2], gx[3])),
+                                     fmaxf(fmaxf(gx[4], gx[5]), fmaxf(gx[6], gx[7])));
             uint32_t gm = 0;  // this row's groups holding an admissible column
+            float lim_t = lim;
+            if (tmax > lim) {
+                // Before the list holds KT keys, the KT-th largest group max of this tile
+                // bounds the KT-th best from below; those keys are not listed yet, so one ulp
+                // lower keeps an exact tie (delta == 0) with them admissible.
+                if (as[KT - 1] == -INFINITY) lim_t = fmaxf(lim_t, next_down(kth_of_8<KT>(gx) - d2));
 #pragma unroll
-            for (int g = 0; g < 8; ++g) gm |= (gx[g] > lim ? 1u : 0u) << g;
+                for (int g = 0; g < 8; ++g) gm |= (gx[g] > lim_t ? 1u : 0u) << g;
+            }
             // rare path, rolled: the warp walks the union of its rows' groups and re-reads
             // each group's 8 columns from TMEM (warp-uniform address, one row per lane)
             uint32_t ug = __reduce_or_sync(0xFFFFFFFFu, gm);
             if (a.no_insert) ug = 0u;
-            while (ug) {
-                const int g = __ffs(ug) - 1;
-                ug &= ug - 1u;
-                uint32_t v8[8];
-                tmem_ld8(taddr + (uint32_t)(8 * g), v8);
-                if ((gm >> g) & 1u) {
+            if (ug) {
+                const float kth0 = as[KT - 1];
+                while (ug) {
+                    const int g = __ffs(ug) - 1;
+                    ug &= ug - 1u;
+                    uint32_t v8[8];
+                    tmem_ld8(taddr + (uint32_t)(8 * g), v8);
+                    if ((gm >> g) & 1u) {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const float v = __uint_as_float(v8[u]);
-                        if (v > lim && key0 + (uint32_t)(8 * g + u) < a.count) {
-                            if (v > as[L - 1]) {
-                                dropped = fmaxf(dropped, as[L - 1]);
-                                insert_in_order<L>(as, ai, v, key0 + (uint32_t)(8 * g + u));
-                            } else {
-                                dropped = fmaxf(dropped, v);
+                        for (int u = 0; u < 8; ++u) {
+                            const float v = __uint_as_float(v8[u]);
+                            if (v > lim_t && key0 + (uint32_t)(8 * g + u) < a.count) {
+                                if (v > as[L - 1]) {
+                                    dropped = fmaxf(dropped, as[L - 1]);
+                                    insert_in_order<L>(as, ai, v, key0 + (uint32_t)(8 * g + u));
+                                } else {
+                                    dropped = fmaxf(dropped, v);
+                                }
                             }
                         }
                     }
                 }
+                if (as[KT - 1] != kth0) {
+                    thr_mine[row] = as[KT - 1];
+                    dirty = true;
+                }
             }
-            thr_mine[row] = as[KT - 1];
             tc_fence_before();
             mbar_arrive(&tempty[p]);  // accumulator no longer read: the MMA warp may reuse it
         }
