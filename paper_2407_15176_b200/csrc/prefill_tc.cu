@@ -516,13 +516,20 @@ struct PrefillMergeArgs {
     const unsigned* kmax;
     uint32_t* idx_out;
     float* score_out;
+    // rows whose part lists overflowed inside the window: re-scanned by prefill_rescan_kernel
+    uint32_t* resc_count;  // zeroed before the merge
+    uint32_t* resc_row;    // [rows] e = kv * n_q + query
+    uint32_t* resc_mask;   // [rows] parts to re-scan
+    float* resc_ts;        // [rows][kPKMax] the row's top-k of the other parts
+    uint32_t* resc_ti;
 };
 
 // Insert (cs, ci) into the top-k list under better() (any arrival order).
-__device__ __forceinline__ void insert_better(float (&ts)[kPKMax], uint32_t (&ti)[kPKMax], int k,
-                                              float cs, uint32_t ci) {
+template <int N>
+__device__ __forceinline__ void insert_better(float (&ts)[N], uint32_t (&ti)[N], int k, float cs,
+                                              uint32_t ci) {
 #pragma unroll
-    for (int j = 0; j < kPKMax; ++j) {
+    for (int j = 0; j < N; ++j) {
         if (j < k && better(cs, ci, ts[j], ti[j])) {
             const float tt = ts[j];
             const uint32_t uu = ti[j];
@@ -588,18 +595,14 @@ __device__ __forceinline__ float exact_dot_row(const float* __restrict__ sq, con
 // One warp per (kv head, query): T = k-th best S_hi over the parts' lists, exact re-scoring
 // of the listed keys with S_hi >= T - 2 delta, exact re-scan of any part whose dropped S_hi
 // reaches that window, exact top-k of the union (every lane holds the same list).
-template <int LANES>
-__global__ void __launch_bounds__(256) prefill_exact_merge_kernel(const PrefillMergeArgs m) {
+template <int LANES, int KT>
+__global__ void __launch_bounds__(256, 4) prefill_exact_merge_kernel(const PrefillMergeArgs m) {
     __shared__ float s_sc[8][kPMaxSplits * kPL];
     __shared__ uint32_t s_ix[8][kPMaxSplits * kPL];
-    __shared__ __align__(16) float s_q[8][kPD];  // the row's query (re-scans: lane = key)
-    __shared__ uint32_t s_resc[8];                // parts of row `warp` to re-scan
-    __shared__ float s_pts[8][kPKMax];            // the row's top-k before its re-scan
-    __shared__ uint32_t s_pti[8][kPKMax];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int e = blockIdx.x * 8 + wib;
-    if (lane == 0) s_resc[wib] = 0u;
-    if (e < m.n_kv * m.n_q) {  // (no early return: the re-scans below are CTA-wide)
+    if (e >= m.n_kv * m.n_q) return;
+    {
     const int kv = e / m.n_q, query = e % m.n_q;
     const size_t qrow = (size_t)kv * m.n_qpad + query;
     const int n = m.splits * kPL;
@@ -667,10 +670,10 @@ __global__ void __launch_bounds__(256) prefill_exact_merge_kernel(const PrefillM
 #pragma unroll
     for (int c = 0; c < 16; ++c) qv[c] = m.mq[qrow * kPD + t + 8 * c];
     const __nv_bfloat16* kbase = m.keys + ((size_t)kv * m.head_stride + m.row0) * kPD;
-    float ts[kPKMax];
-    uint32_t ti[kPKMax];
+    float ts[KT];
+    uint32_t ti[KT];
 #pragma unroll
-    for (int q = 0; q < kPKMax; ++q) {
+    for (int q = 0; q < KT; ++q) {
         ts[q] = -INFINITY;
         ti[q] = kNoIndex;
     }
@@ -688,41 +691,57 @@ __global__ void __launch_bounds__(256) prefill_exact_merge_kernel(const PrefillM
         const bool live = p + j < nc;
         consume(live ? ix[p + j] : 0u, live);
     }
-    if (rescan) {  // finished by the whole CTA below
-        for (int c = lane; c < kPD; c += 32) s_q[wib][c] = m.mq[qrow * kPD + c];
+    if (rescan) {  // finished by prefill_rescan_kernel
+        uint32_t slot = 0;
+        if (lane == 0) slot = atomicAdd(m.resc_count, 1u);
+        slot = __shfl_sync(0xFFFFFFFFu, slot, 0);
         if (lane == 0) {
-            s_resc[wib] = rescan;
+            m.resc_row[slot] = (uint32_t)e;
+            m.resc_mask[slot] = rescan;
 #pragma unroll
             for (int q = 0; q < kPKMax; ++q) {
-                s_pts[wib][q] = ts[q];
-                s_pti[wib][q] = ti[q];
+                m.resc_ts[(size_t)slot * kPKMax + q] = q < KT ? ts[q < KT ? q : 0] : -INFINITY;
+                m.resc_ti[(size_t)slot * kPKMax + q] = q < KT ? ti[q < KT ? q : 0] : kNoIndex;
             }
         }
     } else if (lane == 0) {
         const size_t o = ((size_t)kv * m.n_q + query) * m.k;
 #pragma unroll
-        for (int q = 0; q < kPKMax; ++q)
+        for (int q = 0; q < KT; ++q)
             if (q < m.k) {
                 m.idx_out[o + q] = ti[q];
                 m.score_out[o + q] = ts[q];
             }
     }
-    }  // valid row
-    // A part whose list overflowed inside the window (near-ties, ~1e-6 of rows) is scanned
-    // again exactly by all 8 warps of the CTA: 32 keys per warp step, one key row per lane
-    // (16-byte loads), each warp keeping the top-k of its keys; the row's warp merges them.
-    // (One warp with 8 lanes per key took ~20 ms for one 60K-key part.)
-    __syncthreads();
+    }
+}
+
+// A part whose list overflowed inside the window (near-ties, ~1e-6 of rows) is scanned again
+// exactly by all 8 warps of a CTA: 32 keys per warp step, one key row per lane (16-byte
+// loads), each warp keeping the top-k of its keys; warp 0 merges them with the row's top-k of
+// the other parts.  (One warp with 8 lanes per key took ~20 ms for one 60K-key part.)  A
+// separate launch keeps the re-scan's registers out of the merge's occupancy; with nothing
+// queued its CTAs exit at once.
+template <int LANES, int KT>
+__global__ void __launch_bounds__(256) prefill_rescan_kernel(const PrefillMergeArgs m) {
+    __shared__ __align__(16) float s_q[kPD];
+    __shared__ float s_ws[8][KT];
+    __shared__ uint32_t s_wi[8][KT];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t n = *(volatile const uint32_t*)m.resc_count;
 #pragma unroll 1
-    for (int p = 0; p < 8; ++p) {
-        const uint32_t rescan = s_resc[p];
-        if (!rescan) continue;  // CTA-uniform
-        const int ep = blockIdx.x * 8 + p, kvp = ep / m.n_q, qp = ep % m.n_q;
+    for (uint32_t it = blockIdx.x; it < n; it += gridDim.x) {
+        const uint32_t ep = m.resc_row[it], rescan = m.resc_mask[it];
+        const int kvp = (int)(ep / m.n_q), qp = (int)(ep % m.n_q);
+        const size_t qrow = (size_t)kvp * m.n_qpad + qp;
+        __syncthreads();  // the previous row's shared state is consumed
+        for (int c = threadIdx.x; c < kPD; c += blockDim.x) s_q[c] = m.mq[qrow * kPD + c];
+        __syncthreads();
         const __nv_bfloat16* kb = m.keys + ((size_t)kvp * m.head_stride + m.row0) * kPD;
-        float ts[kPKMax];
-        uint32_t ti[kPKMax];
+        float ts[KT];
+        uint32_t ti[KT];
 #pragma unroll
-        for (int q = 0; q < kPKMax; ++q) {
+        for (int q = 0; q < KT; ++q) {
             ts[q] = -INFINITY;
             ti[q] = kNoIndex;
         }
@@ -733,11 +752,11 @@ __global__ void __launch_bounds__(256) prefill_exact_merge_kernel(const PrefillM
             for (uint32_t b0 = lo + 32u * (uint32_t)wib; b0 < hi; b0 += 32u * 8u) {
                 const uint32_t key = b0 + (uint32_t)lane;
                 const bool live = key < hi;
-                const float v = live ? exact_dot_row<LANES>(s_q[p], kb + (size_t)key * kPD) : -INFINITY;
-                float ws = ts[kPKMax - 1];
-                uint32_t wi = ti[kPKMax - 1];
+                const float v = live ? exact_dot_row<LANES>(s_q, kb + (size_t)key * kPD) : -INFINITY;
+                float ws = ts[KT - 1];
+                uint32_t wi = ti[KT - 1];
 #pragma unroll
-                for (int q = 0; q < kPKMax; ++q)
+                for (int q = 0; q < KT; ++q)
                     if (q == m.k - 1) {
                         ws = ts[q];
                         wi = ti[q];
@@ -750,39 +769,35 @@ __global__ void __launch_bounds__(256) prefill_exact_merge_kernel(const PrefillM
                 }
             }
         }
-        // every warp's list -> shared memory; the row's warp merges them into its own top-k
-        float* ws_ = s_sc[wib];
-        uint32_t* wi_ = s_ix[wib];
         if (lane == 0) {
 #pragma unroll
-            for (int q = 0; q < kPKMax; ++q) {
-                ws_[q] = ts[q];
-                wi_[q] = ti[q];
+            for (int q = 0; q < KT; ++q) {
+                s_ws[wib][q] = ts[q];
+                s_wi[wib][q] = ti[q];
             }
         }
         __syncthreads();
-        if (wib == p) {
-            float fs[kPKMax];
-            uint32_t fi[kPKMax];
+        if (wib == 0) {
+            float fs[KT];
+            uint32_t fi[KT];
 #pragma unroll
-            for (int q = 0; q < kPKMax; ++q) {
-                fs[q] = s_pts[p][q];
-                fi[q] = s_pti[p][q];
+            for (int q = 0; q < KT; ++q) {
+                fs[q] = m.resc_ts[(size_t)it * kPKMax + q];
+                fi[q] = m.resc_ti[(size_t)it * kPKMax + q];
             }
             for (int w = 0; w < 8; ++w)
-                for (int q = 0; q < m.k; ++q)
-                    if (s_ix[w][q] != kNoIndex) insert_better(fs, fi, m.k, s_sc[w][q], s_ix[w][q]);
+                for (int q = 0; q < m.k && q < KT; ++q)
+                    if (s_wi[w][q] != kNoIndex) insert_better(fs, fi, m.k, s_ws[w][q], s_wi[w][q]);
             if (lane == 0) {
                 const size_t o = ((size_t)kvp * m.n_q + qp) * m.k;
 #pragma unroll
-                for (int q = 0; q < kPKMax; ++q)
+                for (int q = 0; q < KT; ++q)
                     if (q < m.k) {
                         m.idx_out[o + q] = fi[q];
                         m.score_out[o + q] = fs[q];
                     }
             }
         }
-        __syncthreads();
     }
 }
 
@@ -816,7 +831,7 @@ int choose_splits(int ctas, int tiles) {
 
 struct PrefillGeom {
     int n_qpad, tiles, splits;
-    size_t hi_bytes, mq_bytes, dl_bytes, kmax_bytes, board_bytes, list_bytes, dropped_bytes;
+    size_t hi_bytes, mq_bytes, dl_bytes, kmax_bytes, board_bytes, list_bytes, dropped_bytes, resc_bytes;
 };
 
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
@@ -834,6 +849,8 @@ PrefillGeom prefill_geom(const ScanArgs& a) {
     g.board_bytes = al256(rows * sizeof(unsigned));
     g.list_bytes = al256((size_t)g.splits * rows * kPL * 4);  // one of indices / scores
     g.dropped_bytes = al256((size_t)g.splits * rows * 4);
+    // re-scan queue: count, row, mask, top-k scores and indices per queued row
+    g.resc_bytes = al256(4) + 2 * al256(rows * 4) + 2 * al256(rows * kPKMax * 4);
     return g;
 }
 
@@ -845,7 +862,8 @@ bool prefill_tc_supported(const ScanArgs& a) {
 
 size_t prefill_tc_workspace(const ScanArgs& a) {
     const PrefillGeom g = prefill_geom(a);
-    return g.hi_bytes + g.mq_bytes + g.dl_bytes + g.kmax_bytes + g.board_bytes + 2 * g.list_bytes + g.dropped_bytes + 1024;
+    return g.hi_bytes + g.mq_bytes + g.dl_bytes + g.kmax_bytes + g.board_bytes + 2 * g.list_bytes + g.dropped_bytes +
+           g.resc_bytes + 1024;
 }
 
 cudaError_t launch_prefill_tc(const ScanArgs& a, const CUtensorMap& kmap, void* ws,
@@ -868,7 +886,17 @@ cudaError_t launch_prefill_tc(const ScanArgs& a, const CUtensorMap& kmap, void* 
     float* part_score = (float*)w;
     w += g.list_bytes;
     float* part_dropped = (float*)w;
+    w += g.dropped_bytes;
     const size_t rows = (size_t)a.n_kv * n_qpad;
+    uint32_t* resc_count = (uint32_t*)w;
+    w += al256(4);
+    uint32_t* resc_row = (uint32_t*)w;
+    w += al256(rows * 4);
+    uint32_t* resc_mask = (uint32_t*)w;
+    w += al256(rows * 4);
+    float* resc_ts = (float*)w;
+    w += al256(rows * kPKMax * 4);
+    uint32_t* resc_ti = (uint32_t*)w;
     prefill_prep_kernel<<<(int)std::min<size_t>(148 * 16, (rows * 32 + 255) / 256), 256, 0, s>>>(
         a.q, a.n_q, a.n_heads, a.n_kv, n_qpad, hi, mq, dl);
     cudaError_t e = cudaMemsetAsync(kmax, 0, (size_t)a.n_kv * sizeof(unsigned), s);
@@ -932,11 +960,30 @@ cudaError_t launch_prefill_tc(const ScanArgs& a, const CUtensorMap& kmap, void* 
     mg.kmax = kmax;
     mg.idx_out = a.idx_out;
     mg.score_out = a.score_out;
+    mg.resc_count = resc_count;
+    mg.resc_row = resc_row;
+    mg.resc_mask = resc_mask;
+    mg.resc_ts = resc_ts;
+    mg.resc_ti = resc_ti;
+    if ((e = cudaMemsetAsync(resc_count, 0, 4, s)) != cudaSuccess) return e;
     const int nw = a.n_kv * a.n_q;
-    if (a.lanes == kLanesFma)
-        prefill_exact_merge_kernel<kLanesFma><<<(nw + 7) / 8, 256, 0, s>>>(mg);
+    auto merge = [&](auto mk, auto rk) {
+        mk<<<(nw + 7) / 8, 256, 0, s>>>(mg);
+        rk<<<num_sms(), 256, 0, s>>>(mg);
+    };
+    const bool fma = a.lanes == kLanesFma;
+    if (a.k <= 1)
+        fma ? merge(prefill_exact_merge_kernel<kLanesFma, 1>, prefill_rescan_kernel<kLanesFma, 1>)
+            : merge(prefill_exact_merge_kernel<kLanesUnfused, 1>, prefill_rescan_kernel<kLanesUnfused, 1>);
+    else if (a.k <= 2)
+        fma ? merge(prefill_exact_merge_kernel<kLanesFma, 2>, prefill_rescan_kernel<kLanesFma, 2>)
+            : merge(prefill_exact_merge_kernel<kLanesUnfused, 2>, prefill_rescan_kernel<kLanesUnfused, 2>);
+    else if (a.k <= 4)
+        fma ? merge(prefill_exact_merge_kernel<kLanesFma, 4>, prefill_rescan_kernel<kLanesFma, 4>)
+            : merge(prefill_exact_merge_kernel<kLanesUnfused, 4>, prefill_rescan_kernel<kLanesUnfused, 4>);
     else
-        prefill_exact_merge_kernel<kLanesUnfused><<<(nw + 7) / 8, 256, 0, s>>>(mg);
+        fma ? merge(prefill_exact_merge_kernel<kLanesFma, 8>, prefill_rescan_kernel<kLanesFma, 8>)
+            : merge(prefill_exact_merge_kernel<kLanesUnfused, 8>, prefill_rescan_kernel<kLanesUnfused, 8>);
     return cudaGetLastError();
 }
 

@@ -57,7 +57,7 @@ def run(ctx, args) -> dict:
     for ci, end in enumerate(ends):
         n_q = end - prev
         timed = ci == 0 or ci == len(ends) - 1 or ci % args.every == 0
-        if timed and ci >= args.start:
+        if timed and args.start <= ci <= args.stop:
             dbg = (lambda *m: print(ci, *m, file=sys.stderr, flush=True)) if os.environ.get("VERBOSE") else (lambda *m: None)
             cache.set_total(end)
             plan = N.Plan(ctx, cache, rope, n_q, nh, cfg)
@@ -82,7 +82,7 @@ def run(ctx, args) -> dict:
             del plan
         prev = end
     ctx.set_prefill(N.PREFILL_TENSOR_SCAN)
-    if args.start:  # debugging / profiling a few chunks: no layer total
+    if args.start or args.stop < len(ends) - 1:  # debugging / profiling a few chunks: no total
         return {"rows": rows}
     # interpolate untimed chunks linearly in the chunk index between timed neighbours
     timed_idx = [r["chunk"] for r in rows]
@@ -120,6 +120,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=4096)
     ap.add_argument("--every", type=int, default=1, help="time every n-th chunk, interpolate the rest")
     ap.add_argument("--start", type=int, default=0, help="debugging: skip the chunks before this one")
+    ap.add_argument("--stop", type=int, default=1 << 30, help="debugging: skip the chunks after this one")
     args = ap.parse_args()
     print(json.dumps(run(N.Context(0), args)), flush=True)
 
