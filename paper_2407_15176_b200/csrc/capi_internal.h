@@ -17,7 +17,7 @@ struct reattn_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int lanes = REATTN_LANES_UNFUSED;
-    int prefill = REATTN_PREFILL_TENSOR_SCAN;  // reattn_prefill_mode bits (tcgen05 scan / attention)
+    int prefill = REATTN_PREFILL_TENSOR;  // reattn_prefill_mode bits (tcgen05 scan / attention)
     int num_sms = 148;
     std::string err;
     void* arena = nullptr;  // scratch for synchronous calls

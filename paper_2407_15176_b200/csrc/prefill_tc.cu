@@ -841,6 +841,8 @@ PrefillGeom prefill_geom(const ScanArgs& a) {
     g.n_qpad = (a.n_q + kPM * kPQT - 1) / (kPM * kPQT) * (kPM * kPQT);
     g.tiles = (int)((a.count + kPN - 1) / kPN);
     g.splits = choose_splits(g.n_qpad / (kPM * kPQT) * a.n_kv, g.tiles);
+    if (const char* e = std::getenv("REATTN_K2_SPLITS"))  // experiments only
+        g.splits = std::max(1, std::min(kPMaxSplits, std::atoi(e)));
     const size_t rows = (size_t)a.n_kv * g.n_qpad;
     g.hi_bytes = al256(rows * kPD * sizeof(__nv_bfloat16));
     g.mq_bytes = al256(rows * kPD * sizeof(float));

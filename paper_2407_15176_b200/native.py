@@ -22,7 +22,7 @@ SPAN_ALIGNED, SPAN_CENTERED = 0, 1
 MODE_FULL, MODE_WINDOW, MODE_REATTENTION = 0, 1, 2
 LANES_UNFUSED, LANES_FMA = 0, 1
 PREFILL_EXACT, PREFILL_TENSOR_SCAN, PREFILL_TENSOR_ATTN, PREFILL_TENSOR = 0, 1, 2, 3
-PREFILL_DEFAULT = PREFILL_TENSOR_SCAN  # a new context's mode
+PREFILL_DEFAULT = PREFILL_TENSOR  # a new context's mode
 
 u64 = C.c_uint64
 vp = C.c_void_p

@@ -91,7 +91,7 @@ def test_config3_prefill_chunk_full_shape(ctx):
         ctx.fused_topk(q, nh, cache.keys_tensor(), n_kv, info["capacity"], g, ls - g, d, cfg.k,
                        idx, sc, N.BF16)
     finally:
-        ctx.set_prefill(N.PREFILL_TENSOR_SCAN)
+        ctx.set_prefill(N.PREFILL_DEFAULT)
     hk, hv = host_cache(cache, "bf16")
     ocfg = ob.SelectionConfig(l_chunk=4096)
     out, ent, st, (sb, se), _, (ci, cs) = ob.attend_step_ex(q.cpu().numpy(), nh, hk, hv, total,

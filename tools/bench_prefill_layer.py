@@ -81,7 +81,7 @@ def run(ctx, args) -> dict:
                 print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
             del plan
         prev = end
-    ctx.set_prefill(N.PREFILL_TENSOR_SCAN)
+    ctx.set_prefill(N.PREFILL_DEFAULT)
     if args.start or args.stop < len(ends) - 1:  # debugging / profiling a few chunks: no total
         return {"rows": rows}
     # interpolate untimed chunks linearly in the chunk index between timed neighbours
