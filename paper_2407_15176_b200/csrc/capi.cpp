@@ -443,12 +443,19 @@ struct reattn_plan {
     // entropies and spans, filled by copies enqueued behind the replay
     void* staged = nullptr;
     bool staged_pending = false;
+    // zero-copy host I/O (step_host / run_host on pinned buffers): the plan's graph with the
+    // host reads before it and the output write after it, for the last host pointers seen
+    cudaGraphExec_t io_exec = nullptr;
+    const void* io_key[4] = {nullptr, nullptr, nullptr, nullptr};
+    bool io_append = false;
 };
 
 namespace {
 // The plan's graph: [append the step's K/V rows] + the attend_step pipeline.
 int capture_plan(reattn_plan* p) {
     reattn_ctx* ctx = p->ctx;
+    if (p->io_exec) cudaGraphExecDestroy(p->io_exec);  // holds a copy of the old graph
+    p->io_exec = nullptr;
     if (p->exec) cudaGraphExecDestroy(p->exec);
     if (p->graph) cudaGraphDestroy(p->graph);
     p->exec = nullptr;
@@ -477,6 +484,73 @@ int capture_plan(reattn_plan* p) {
     if (e != cudaSuccess)
         return set_err(ctx, REATTN_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
     return REATTN_OK;
+}
+
+bool host_pinned(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// The I/O graph: host q (and K/V rows) -> device, the plan's own graph as a child, device
+// output -> host.  Rebuilt when the host pointers, the append mode or the plan graph change.
+int ensure_io_graph(reattn_plan* p, const float* q_host, const float* k_host, const float* v_host,
+                    float* out_host) {
+    const void* key[4] = {q_host, k_host, v_host, out_host};
+    if (p->io_exec && p->io_append == p->append && std::equal(key, key + 4, p->io_key)) return REATTN_OK;
+    reattn_ctx* ctx = p->ctx;
+    if (p->io_exec) cudaGraphExecDestroy(p->io_exec);
+    p->io_exec = nullptr;
+    const uint64_t qn = p->P.n_q * p->P.n_head * p->cache->d, kn = p->cache->n_kv * p->cache->d;
+    cudaStream_t cs;
+    CU(ctx, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CU(ctx, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    const float* src[3] = {q_host, k_host, v_host};
+    float* dst[3] = {p->q, p->k_in, p->v_in};
+    const uint64_t n[3] = {qn, kn, kn};
+    cudaError_t e = launch_host_io(src, dst, n, p->append ? 3 : 1, cs);
+    cudaGraphNode_t child = nullptr;
+    if (e == cudaSuccess) {
+        // the plan's graph as a child node of the capture
+        cudaGraph_t cap = nullptr;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        cudaStreamCaptureStatus st;
+        e = cudaStreamGetCaptureInfo(cs, &st, nullptr, &cap, &deps, &nd);
+        if (e == cudaSuccess) e = cudaGraphAddChildGraphNode(&child, cap, deps, nd, p->graph);
+        if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(cs, &child, 1, cudaStreamSetCaptureDependencies);
+    }
+    if (e == cudaSuccess) {
+        const float* osrc[1] = {p->out};
+        float* odst[1] = {out_host};
+        const uint64_t on[1] = {qn};
+        e = launch_host_io(osrc, odst, on, 1, cs);
+    }
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+    cudaStreamDestroy(cs);
+    if (e != cudaSuccess || ce != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        return set_err(ctx, REATTN_ECUDA, std::string("host I/O graph: ") +
+                                              cudaGetErrorString(e != cudaSuccess ? e : ce));
+    }
+    e = cudaGraphInstantiate(&p->io_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+        p->io_exec = nullptr;
+        return set_err(ctx, REATTN_ECUDA, std::string("host I/O graph instantiate: ") + cudaGetErrorString(e));
+    }
+    std::copy(key, key + 4, p->io_key);
+    p->io_append = p->append;
+    return REATTN_OK;
+}
+
+bool zero_copy_enabled() {
+    static const bool off = std::getenv("REATTN_NO_ZERO_COPY") != nullptr;
+    return !off;
 }
 
 // A plan replays the graph it captured: the cache storage must be the one it was built over
@@ -1150,6 +1224,7 @@ void reattn_plan_destroy(reattn_plan* p) {
     if (p->graph) cudaGraphDestroy(p->graph);
     cudaFree(p->mem);
     if (p->staged) cudaFreeHost(p->staged);
+    if (p->io_exec) cudaGraphExecDestroy(p->io_exec);
     delete p;
 }
 float* reattn_plan_q(const reattn_plan* p) { return p->q; }
@@ -1185,6 +1260,18 @@ int reattn_plan_step_host(reattn_plan* p, const float* q_host, const float* k_ho
     if (rc) return rc;
     const size_t qb = p->P.n_q * p->P.n_head * p->cache->d * sizeof(float);
     const size_t kb = p->cache->n_kv * p->cache->d * sizeof(float);
+    const void* key[4] = {q_host, p->append ? k_host : nullptr, p->append ? v_host : nullptr, out_host};
+    const bool io_ready = p->io_exec && p->io_append == p->append && std::equal(key, key + 4, p->io_key);
+    if (io_ready || (zero_copy_enabled() && host_pinned(q_host) && host_pinned(out_host) &&
+                     (!p->append || (host_pinned(k_host) && host_pinned(v_host))))) {
+        if ((rc = ensure_io_graph(p, q_host, p->append ? k_host : nullptr, p->append ? v_host : nullptr,
+                                  out_host)))
+            return rc;
+        CU(ctx, cudaGraphLaunch(p->io_exec, ctx->stream));
+        if (p->append) ++p->cache->total;
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+        return REATTN_OK;
+    }
     CU(ctx, cudaMemcpyAsync(p->q, q_host, qb, cudaMemcpyHostToDevice, ctx->stream));
     if (p->append) {
         CU(ctx, cudaMemcpyAsync(p->k_in, k_host, kb, cudaMemcpyHostToDevice, ctx->stream));
@@ -1220,6 +1307,14 @@ int reattn_plan_run_host(reattn_plan* p, const float* q_host, float* out_host) {
         return set_err(ctx, REATTN_EINVAL, "plan: append mode takes the step's K/V too (reattn_plan_step_host)");
     int rc = check_plan(p);
     if (rc) return rc;
+    const void* key[4] = {q_host, nullptr, nullptr, out_host};
+    const bool io_ready = p->io_exec && !p->io_append && std::equal(key, key + 4, p->io_key);
+    if (io_ready || (zero_copy_enabled() && host_pinned(q_host) && host_pinned(out_host))) {
+        if ((rc = ensure_io_graph(p, q_host, nullptr, nullptr, out_host))) return rc;
+        CU(ctx, cudaGraphLaunch(p->io_exec, ctx->stream));
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+        return REATTN_OK;
+    }
     CU(ctx, cudaMemcpyAsync(p->q, q_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
     CU(ctx, cudaGraphLaunch(p->exec, ctx->stream));
     CU(ctx, cudaMemcpyAsync(out_host, p->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));

@@ -4,6 +4,8 @@
 // entropy reduction in the reference's accumulation order (engine.hpp:100-106).
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -140,7 +142,53 @@ __global__ void __launch_bounds__(256) cache_append_step_kernel(const float* __r
 }
 
 __global__ void set_u32_kernel(uint32_t* p, uint32_t v) { *p = v; }
+
+// Zero-copy host I/O of a decode step (reattn_plan_step_host / run_host on pinned buffers):
+// up to three host arrays read straight over the bus into device buffers, or one written
+// back, by a few CTAs -- no DMA set-up per array.  16-byte vectors when everything is
+// aligned.
+struct HostIo {
+    const float* src[3];
+    float* dst[3];
+    uint32_t n[3];
+    int count;
+};
+
+__global__ void __launch_bounds__(256) host_io_kernel(const HostIo io) {
+    const uint32_t stride = gridDim.x * blockDim.x, t0 = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll 1
+    for (int a = 0; a < io.count; ++a) {
+        const float* src = io.src[a];
+        float* dst = io.dst[a];
+        const uint32_t n = io.n[a];
+        if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+            const uint32_t n4 = n / 4;
+            for (uint32_t i = t0; i < n4; i += stride)
+                reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
+            for (uint32_t i = 4 * n4 + t0; i < n; i += stride) dst[i] = src[i];
+        } else {
+            for (uint32_t i = t0; i < n; i += stride) dst[i] = src[i];
+        }
+    }
+}
 }  // namespace
+
+cudaError_t launch_host_io(const float* const* src, float* const* dst, const uint64_t* n, int count,
+                           cudaStream_t s) {
+    HostIo io{};
+    uint64_t total = 0;
+    for (int a = 0; a < count && a < 3; ++a) {
+        io.src[a] = src[a];
+        io.dst[a] = dst[a];
+        io.n[a] = (uint32_t)n[a];
+        total += n[a];
+    }
+    io.count = count < 3 ? count : 3;
+    if (total == 0) return cudaSuccess;
+    const int g = (int)std::min<uint64_t>(16, (total / 4 + 255) / 256 + 1);
+    host_io_kernel<<<g, 256, 0, s>>>(io);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_cache_append_step(const float* k_in, const float* v_in, void* keys, void* values,
                                      int dtype, uint64_t n_kv, uint64_t d, uint64_t head_stride,
