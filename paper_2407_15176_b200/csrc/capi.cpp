@@ -495,38 +495,30 @@ bool host_pinned(const void* p) {
     return at.type == cudaMemoryTypeHost;
 }
 
-// The I/O graph: host q (and K/V rows) -> device, the plan's own graph as a child, device
-// output -> host.  Rebuilt when the host pointers, the append mode or the plan graph change.
-int ensure_io_graph(reattn_plan* p, const float* q_host, const float* k_host, const float* v_host,
-                    float* out_host) {
-    const void* key[4] = {q_host, k_host, v_host, out_host};
-    if (p->io_exec && p->io_append == p->append && std::equal(key, key + 4, p->io_key)) return REATTN_OK;
-    reattn_ctx* ctx = p->ctx;
-    if (p->io_exec) cudaGraphExecDestroy(p->io_exec);
-    p->io_exec = nullptr;
-    const uint64_t qn = p->P.n_q * p->P.n_head * p->cache->d, kn = p->cache->n_kv * p->cache->d;
+// An I/O graph: host arrays -> device (zero-copy reads), `body` as a child graph, device
+// output -> host.  Used by the plans' run_host / step_host on pinned buffers.
+int build_io_exec(reattn_ctx* ctx, cudaGraph_t body, const float* const* in_src, float* const* in_dst,
+                  const uint64_t* in_n, int n_in, const float* out_src, float* out_dst, uint64_t out_n,
+                  cudaGraphExec_t* exec) {
+    *exec = nullptr;
     cudaStream_t cs;
     CU(ctx, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     CU(ctx, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    const float* src[3] = {q_host, k_host, v_host};
-    float* dst[3] = {p->q, p->k_in, p->v_in};
-    const uint64_t n[3] = {qn, kn, kn};
-    cudaError_t e = launch_host_io(src, dst, n, p->append ? 3 : 1, cs);
-    cudaGraphNode_t child = nullptr;
+    cudaError_t e = launch_host_io(in_src, in_dst, in_n, n_in, cs);
     if (e == cudaSuccess) {
-        // the plan's graph as a child node of the capture
         cudaGraph_t cap = nullptr;
         const cudaGraphNode_t* deps = nullptr;
         size_t nd = 0;
         cudaStreamCaptureStatus st;
+        cudaGraphNode_t child = nullptr;
         e = cudaStreamGetCaptureInfo(cs, &st, nullptr, &cap, &deps, &nd);
-        if (e == cudaSuccess) e = cudaGraphAddChildGraphNode(&child, cap, deps, nd, p->graph);
+        if (e == cudaSuccess) e = cudaGraphAddChildGraphNode(&child, cap, deps, nd, body);
         if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(cs, &child, 1, cudaStreamSetCaptureDependencies);
     }
     if (e == cudaSuccess) {
-        const float* osrc[1] = {p->out};
-        float* odst[1] = {out_host};
-        const uint64_t on[1] = {qn};
+        const float* osrc[1] = {out_src};
+        float* odst[1] = {out_dst};
+        const uint64_t on[1] = {out_n};
         e = launch_host_io(osrc, odst, on, 1, cs);
     }
     cudaGraph_t g = nullptr;
@@ -537,12 +529,29 @@ int ensure_io_graph(reattn_plan* p, const float* q_host, const float* k_host, co
         return set_err(ctx, REATTN_ECUDA, std::string("host I/O graph: ") +
                                               cudaGetErrorString(e != cudaSuccess ? e : ce));
     }
-    e = cudaGraphInstantiate(&p->io_exec, g, 0);
+    e = cudaGraphInstantiate(exec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) {
-        p->io_exec = nullptr;
+        *exec = nullptr;
         return set_err(ctx, REATTN_ECUDA, std::string("host I/O graph instantiate: ") + cudaGetErrorString(e));
     }
+    return REATTN_OK;
+}
+
+// the plan's I/O graph for these host pointers (rebuilt when they, the append mode or the
+// plan graph change)
+int ensure_io_graph(reattn_plan* p, const float* q_host, const float* k_host, const float* v_host,
+                    float* out_host) {
+    const void* key[4] = {q_host, k_host, v_host, out_host};
+    if (p->io_exec && p->io_append == p->append && std::equal(key, key + 4, p->io_key)) return REATTN_OK;
+    if (p->io_exec) cudaGraphExecDestroy(p->io_exec);
+    p->io_exec = nullptr;
+    const uint64_t qn = p->P.n_q * p->P.n_head * p->cache->d, kn = p->cache->n_kv * p->cache->d;
+    const float* src[3] = {q_host, k_host, v_host};
+    float* dst[3] = {p->q, p->k_in, p->v_in};
+    const uint64_t n[3] = {qn, kn, kn};
+    int rc = build_io_exec(p->ctx, p->graph, src, dst, n, p->append ? 3 : 1, p->out, out_host, qn, &p->io_exec);
+    if (rc) return rc;
     std::copy(key, key + 4, p->io_key);
     p->io_append = p->append;
     return REATTN_OK;
@@ -1444,7 +1453,10 @@ struct reattn_batch_plan {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     uint64_t kernels = 0;
+    cudaGraphExec_t io_exec = nullptr;  // zero-copy run_host for io_key's pinned buffers
+    const void* io_key[2] = {nullptr, nullptr};
     ~reattn_batch_plan() {
+        if (io_exec) cudaGraphExecDestroy(io_exec);
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
         for (auto e : ev) cudaEventDestroy(e);
@@ -1575,6 +1587,22 @@ int reattn_batch_plan_launch(reattn_batch_plan* p) {
 int reattn_batch_plan_run_host(reattn_batch_plan* p, const float* q_host, float* out_host) {
     const size_t bytes = p->P.size() * p->n_head * p->d * sizeof(float);
     reattn_ctx* ctx = p->ctx;
+    const bool io_ready = p->io_exec && p->io_key[0] == q_host && p->io_key[1] == out_host;
+    if (io_ready || (zero_copy_enabled() && host_pinned(q_host) && host_pinned(out_host))) {
+        if (!io_ready) {
+            if (p->io_exec) cudaGraphExecDestroy(p->io_exec);
+            const float* src[1] = {q_host};
+            float* dst[1] = {p->q};
+            const uint64_t n[1] = {bytes / sizeof(float)};
+            int rc = build_io_exec(ctx, p->graph, src, dst, n, 1, p->out, out_host, n[0], &p->io_exec);
+            if (rc) return rc;
+            p->io_key[0] = q_host;
+            p->io_key[1] = out_host;
+        }
+        CU(ctx, cudaGraphLaunch(p->io_exec, ctx->stream));
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+        return REATTN_OK;
+    }
     CU(ctx, cudaMemcpyAsync(p->q, q_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
     CU(ctx, cudaGraphLaunch(p->exec, ctx->stream));
     CU(ctx, cudaMemcpyAsync(out_host, p->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
