@@ -509,9 +509,10 @@ def run_ours(args) -> None:
         "e2e": {"value": e2e_us, "unit": UNIT,
                 "h2d_bytes_per_step": n_head * D * 4 + 2 * meta["n_kv"] * D * 4,
                 "d2h_bytes_per_step": n_head * D * 4,
-                "path": "reattn_plan_step_host (C-ABI): H2D q + the step's K/V rows from pinned "
-                        "host, one graph replay (append node + attend_step), D2H output, "
-                        "synchronise; the cache grows by one row per step"},
+                "path": "reattn_plan_step_host (C-ABI) on pinned host buffers: one graph launch "
+                        "that reads q and the step's K/V rows from host memory (zero-copy kernel), "
+                        "appends the rows, runs attend_step and writes the output back to host "
+                        "memory; then synchronise.  The cache grows by one row per step"},
         "gpu_launches": int(info["kernels_per_step"]) * K,
         "kernels_per_step": int(info["kernels_per_step"]),
         "wall_s_timed_region": t_wall,
