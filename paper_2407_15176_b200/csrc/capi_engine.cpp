@@ -363,14 +363,22 @@ int forward_block(reattn_engine* e, uint64_t rows) {
         reattn_cache* cache = e->caches[l];
         int rc;
         reattn_plan* pl = nullptr;
-        if (token && cache->dtype == REATTN_BF16) {
+        if (token) {
+            // q -> the plan's query buffer; K / V rows written straight into the cache at its
+            // length (the append of engine.hpp:196-198, kv_cache.hpp:54-68, fused into the
+            // projection's epilogue), and the cache's device length advanced by the launch
             if ((rc = ensure_capacity(e, cache, 1))) return rc;
             pl = layer_plan(e, l);
-            const GemvDesc m[3] = {{cslot(e->w, REATTN_W_WQ, l), QW, QW, pl ? reattn_plan_q(pl) : e->q, 0.0f},
-                                   {cslot(e->w, REATTN_W_WK, l), KW, KW, e->kb, 0.0f},
-                                   {cslot(e->w, REATTN_W_WV, l), KW, KW, e->vb, 0.0f}};
-            CU(ctx, launch_gemv_batch(e->h, D, m, 3, false, e->gemv_ws, e->gemv_n_max, ctx->stream));
-            if ((rc = reattn_cache_append(ctx, cache, e->kb, e->vb, 1, 1))) return rc;  // engine.hpp:196-198
+            const int kind = cache->dtype == REATTN_BF16 ? 1 : 2;
+            const GemvDesc m[3] = {
+                {cslot(e->w, REATTN_W_WQ, l), QW, QW, pl ? reattn_plan_q(pl) : e->q, 0.0f, 0, 0, 0, 0},
+                {cslot(e->w, REATTN_W_WK, l), KW, KW, (float*)cache->keys, 0.0f, kind, c.d_head, cache->total,
+                 cache->capacity},
+                {cslot(e->w, REATTN_W_WV, l), KW, KW, (float*)cache->values, 0.0f, kind, c.d_head, cache->total,
+                 cache->capacity}};
+            CU(ctx, launch_gemv_batch(e->h, D, m, 3, false, e->gemv_ws, e->gemv_n_max, ctx->stream,
+                                      cache->dev_total, (uint32_t)(cache->total + 1)));
+            cache->total += 1;
         } else {
             if ((rc = append_kv(e, cache, l, rows))) return rc;  // before attend_step (engine.hpp:196-198)
             pl = rows == 1 ? layer_plan(e, l) : nullptr;
@@ -396,8 +404,8 @@ int forward_block(reattn_engine* e, uint64_t rows) {
             return rc;
         CU(ctx, launch_rmsnorm(e->x, rows, D, cslot(e->w, REATTN_W_NORM_FFN, l), e->h, ctx->stream));
         if (token) {
-            const GemvDesc m[2] = {{cslot(e->w, REATTN_W_GATE, l), F, F, e->gate, 0.0f},
-                                   {cslot(e->w, REATTN_W_UP, l), F, F, e->up, 0.0f}};
+            const GemvDesc m[2] = {{cslot(e->w, REATTN_W_GATE, l), F, F, e->gate, 0.0f, 0, 0, 0, 0},
+                                   {cslot(e->w, REATTN_W_UP, l), F, F, e->up, 0.0f, 0, 0, 0, 0}};
             CU(ctx, launch_gemv_batch(e->h, D, m, 2, true, e->gemv_ws, e->gemv_n_max, ctx->stream));
         } else {
             if ((rc = gemm(e, rows, F, D, e->h, D, cslot(e->w, REATTN_W_GATE, l), F, e->gate, F, 0.0f)))
@@ -688,7 +696,7 @@ int reattn_engine_create(reattn_ctx* ctx, const reattn_weights* w, const reattn_
                               mc.n_kv_head * mc.d_head});
     CU(ctx, cudaMalloc(&e->gemv_ws, gemv_workspace_bytes(e->gemv_n_max)));
     CU(ctx, cudaMemsetAsync(e->gemv_ws, 0, gemv_workspace_bytes(e->gemv_n_max), ctx->stream));
-    e->gemv_ok = mc.d_model % 4 == 0 && mc.d_ff % 4 == 0 && (mc.n_head * mc.d_head) % 4 == 0 &&
+    e->gemv_ok = mc.d_model % 4 == 0 && mc.d_ff % 4 == 0 && mc.d_head % 4 == 0 && (mc.n_head * mc.d_head) % 4 == 0 &&
                  (mc.n_kv_head * mc.d_head) % 4 == 0 && getenv("REATTN_ENGINE_CUBLAS") == nullptr;
     if ((rc = reattn_engine_reset(e.get()))) return rc;
     *out = e.release();

@@ -303,10 +303,15 @@ struct GemvDesc {
     uint64_t ldw, N;
     float* y;
     float beta;
+    int kind;              // 0: y dense fp32; 1 / 2: y is a bf16 / fp32 cache's K or V base and
+    uint64_t d, row;       //   column c lands in head c / d, element c % d of cache row `row`
+    uint64_t head_stride;  //   (the cache capacity)
 };
-// up to 3 matrices sharing x in one launch; silu_pair: mats = {gate, up}, gate <- silu(g) * u
+// up to 3 matrices sharing x in one launch; silu_pair: mats = {gate, up}, gate <- silu(g) * u;
+// total_ptr (optional): written with total_val by the launch (a cache's device length)
 cudaError_t launch_gemv_batch(const float* x, uint64_t K, const GemvDesc* mats, int count, bool silu_pair,
-                              void* ws, uint64_t n_max, cudaStream_t s);
+                              void* ws, uint64_t n_max, cudaStream_t s, uint32_t* total_ptr = nullptr,
+                              uint32_t total_val = 0);
 
 // ---- timeline trace (diagnostics): REATTN_TRACE=1 at plan / launch time makes the decode
 // kernels stamp %globaltimer into a device buffer (layout in misc.cu); null otherwise.

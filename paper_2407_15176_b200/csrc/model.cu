@@ -247,9 +247,12 @@ __device__ __forceinline__ void add4(float4& a, const float4& b) {
 struct GemvMat {
     const float* W;
     uint64_t ldw;
-    float* y;
+    float* y;           // kind 0: y[N]; kinds 1 / 2: the cache's K or V base ([n_kv][cap][d])
     uint32_t N, tile0;  // columns; first global tile of this matrix
     float beta;
+    int kind;           // 0 dense fp32, 1 bf16 cache row, 2 fp32 cache row
+    uint32_t d, row;    // cache row layout: column c -> head c / d, element c % d of row `row`
+    uint64_t head_stride;
 };
 
 struct GemvBatch {
@@ -259,7 +262,37 @@ struct GemvBatch {
     uint32_t K, upt;    // rows; units per tile
     uint32_t tiles;     // tiles over all matrices
     uint64_t units;     // tiles * upt
+    uint32_t* total_ptr;  // non-null: CTA 0 writes total_val (a cache's device length)
+    uint32_t total_val;
 };
+
+// y columns [col, col + 4) of M (the matrix's own column index), beta-accumulated for dense
+// outputs; cache rows take the bf16 (round to nearest even, as the cache append) or fp32 value
+__device__ __forceinline__ void gemv_store(const GemvMat& M, uint32_t col, float4 p) {
+    if (M.kind == 0) {
+        float4* yp = reinterpret_cast<float4*>(M.y + col);
+        if (M.beta != 0.0f) {
+            const float4 o = *yp;
+            p.x = fmaf(M.beta, o.x, p.x);
+            p.y = fmaf(M.beta, o.y, p.y);
+            p.z = fmaf(M.beta, o.z, p.z);
+            p.w = fmaf(M.beta, o.w, p.w);
+        }
+        *yp = p;
+        return;
+    }
+    const uint32_t h = col / M.d, c = col % M.d;
+    const size_t o = ((size_t)h * M.head_stride + M.row) * M.d + c;
+    if (M.kind == 1) {
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(p.x, p.y), hi = __floats2bfloat162_rn(p.z, p.w);
+        uint2 w;
+        w.x = *reinterpret_cast<const uint32_t*>(&lo);
+        w.y = *reinterpret_cast<const uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(M.y) + o) = w;
+    } else {
+        *reinterpret_cast<float4*>(M.y + o) = p;
+    }
+}
 
 __device__ __forceinline__ uint32_t unit_begin(uint64_t c, uint64_t units, uint32_t G) {
     return (uint32_t)(c * units / G);
@@ -330,16 +363,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(const float* _
         const uint32_t cf = unit_owner((uint64_t)t * B.upt, B.units, G);
         const uint32_t cl = unit_owner((uint64_t)(t + 1) * B.upt - 1, B.units, G);
         if (!pair && cf == cl) {
-            if (!ok) return;
-            float4* yp = reinterpret_cast<float4*>(M.y + col);
-            if (M.beta != 0.0f) {
-                const float4 o = *yp;
-                p.x = fmaf(M.beta, o.x, p.x);
-                p.y = fmaf(M.beta, o.y, p.y);
-                p.z = fmaf(M.beta, o.z, p.z);
-                p.w = fmaf(M.beta, o.w, p.w);
-            }
-            *yp = p;
+            if (ok) gemv_store(M, col, p);
             return;
         }
         if (ok) reinterpret_cast<float4*>(ws)[(uint64_t)(c + t) * 32 + lane] = p;
@@ -375,23 +399,17 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(const float* _
                 make_float4(silu(g.x, u.x), silu(g.y, u.y), silu(g.z, u.z), silu(g.w, u.w));
             return;
         }
-        p = total_of(t);
-        float4* yp = reinterpret_cast<float4*>(M.y + col);
-        if (M.beta != 0.0f) {
-            const float4 o = *yp;
-            p.x = fmaf(M.beta, o.x, p.x);
-            p.y = fmaf(M.beta, o.y, p.y);
-            p.z = fmaf(M.beta, o.z, p.z);
-            p.w = fmaf(M.beta, o.w, p.w);
-        }
-        *yp = p;
+        gemv_store(M, col, total_of(t));
     };
     if (u0 >= u1) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (B.total_ptr && c == 0 && threadIdx.x == 0) *B.total_ptr = B.total_val;
         return;
     }
     load_w(u0, 0);                                      // weights: constant
     asm volatile("griddepcontrol.wait;" ::: "memory");  // x, y, workspace: the kernel before
+    // the cache's new device length: read only by kernels after this grid completes
+    if (B.total_ptr && c == 0 && threadIdx.x == 0) *B.total_ptr = B.total_val;
     load_x(u0, 0);
     for (uint32_t u = u0;;) {
         if (u + 1 < u1) {
@@ -437,14 +455,17 @@ bool gemv_supported(uint64_t N, uint64_t K, uint64_t ldw, const void* x, const v
 }
 
 cudaError_t launch_gemv_batch(const float* x, uint64_t K, const GemvDesc* mats, int count, bool silu_pair,
-                              void* ws, uint64_t n_max, cudaStream_t s) {
+                              void* ws, uint64_t n_max, cudaStream_t s, uint32_t* total_ptr,
+                              uint32_t total_val) {
     if (count < 1 || count > 3 || (silu_pair && (count != 2 || mats[0].N != mats[1].N)))
         return cudaErrorInvalidValue;
     GemvBatch B{};
     uint32_t tiles = 0;
     for (int i = 0; i < count; ++i) {
         if (mats[i].N > n_max) return cudaErrorInvalidValue;
-        B.m[i] = GemvMat{mats[i].W, mats[i].ldw, mats[i].y, (uint32_t)mats[i].N, tiles, mats[i].beta};
+        B.m[i] = GemvMat{mats[i].W, mats[i].ldw, mats[i].y, (uint32_t)mats[i].N, tiles, mats[i].beta,
+                         mats[i].kind, (uint32_t)mats[i].d, (uint32_t)mats[i].row, mats[i].head_stride};
+        if (mats[i].kind != 0 && (mats[i].d == 0 || mats[i].d % 4 != 0)) return cudaErrorInvalidValue;
         tiles += (uint32_t)((mats[i].N + kGemvCols - 1) / kGemvCols);
     }
     if (tiles == 0) return cudaSuccess;
@@ -454,6 +475,8 @@ cudaError_t launch_gemv_batch(const float* x, uint64_t K, const GemvDesc* mats, 
     B.K = (uint32_t)K;
     B.upt = (uint32_t)((K + kGemvUnitRows - 1) / kGemvUnitRows);
     B.units = (uint64_t)tiles * B.upt;
+    B.total_ptr = total_ptr;
+    B.total_val = total_val;
     if (B.units > UINT32_MAX) return cudaErrorInvalidValue;
     const uint32_t G = (uint32_t)std::min<uint64_t>(std::min(gemv_ctas(), 148 * 8), B.units);
     const uint64_t tiles_max = 3 * ((n_max + kGemvCols - 1) / kGemvCols);
@@ -474,7 +497,7 @@ cudaError_t launch_gemv_batch(const float* x, uint64_t K, const GemvDesc* mats, 
 cudaError_t launch_gemv(const float* x, const float* W, uint64_t ldw, uint64_t N, uint64_t K, float* y,
                         float beta, void* ws, uint64_t n_max, cudaStream_t s) {
     if (N == 0) return cudaSuccess;
-    const GemvDesc m{W, ldw, N, y, beta};
+    const GemvDesc m{W, ldw, N, y, beta, 0, 0, 0, 0};
     return launch_gemv_batch(x, K, &m, 1, false, ws, n_max, s);
 }
 
