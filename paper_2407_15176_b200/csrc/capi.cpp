@@ -1371,22 +1371,25 @@ size_t staged_bytes(const StepPlan& P) {
 }
 }  // namespace
 
-int reattn_plan_stage_result(reattn_plan* p) {
+// one zero-copy kernel writes the header, entropies and spans into the pinned staging area
+int plan_stage_result_on(reattn_plan* p, cudaStream_t s) {
     reattn_ctx* ctx = p->ctx;
     const StepPlan& P = p->P;
     if (!p->staged) CU(ctx, cudaHostAlloc(&p->staged, staged_bytes(P), cudaHostAllocDefault));
     uint8_t* h = (uint8_t*)p->staged;
     const uint64_t kp = std::max<uint64_t>(1, P.cfg.k_prime);
     const size_t ent = P.n_q * P.n_head * sizeof(double);
-    CU(ctx, cudaMemcpyAsync(h, P.hdr, sizeof(ScopeHeader), cudaMemcpyDeviceToHost, ctx->stream));
-    h += sizeof(ScopeHeader);
-    if (ent) CU(ctx, cudaMemcpyAsync(h, P.entropy, ent, cudaMemcpyDeviceToHost, ctx->stream));
-    h += ent;
-    CU(ctx, cudaMemcpyAsync(h, P.span_b, kp * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaMemcpyAsync(h + kp * 4, P.span_e, kp * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    const float* src[4] = {(const float*)P.hdr, (const float*)P.entropy, (const float*)P.span_b,
+                           (const float*)P.span_e};
+    float* dst[4] = {(float*)h, (float*)(h + sizeof(ScopeHeader)), (float*)(h + sizeof(ScopeHeader) + ent),
+                     (float*)(h + sizeof(ScopeHeader) + ent + kp * 4)};
+    const uint64_t n[4] = {sizeof(ScopeHeader) / 4, ent / 4, kp, kp};
+    CU(ctx, launch_host_io(src, dst, n, 4, s));
     p->staged_pending = true;
     return REATTN_OK;
 }
+
+int reattn_plan_stage_result(reattn_plan* p) { return plan_stage_result_on(p, p->ctx->stream); }
 
 int reattn_plan_staged_result(reattn_plan* p, reattn_step_stats* st, uint64_t* span_b_host,
                               uint64_t* span_e_host, double* entropy_host) {

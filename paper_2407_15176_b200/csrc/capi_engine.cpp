@@ -209,11 +209,16 @@ struct reattn_engine {
     // launched without a host synchronisation; their stats are read once per forward block
     std::vector<reattn_plan*> plans;
     std::vector<reattn_plan*> pending;  // plans whose staged results the next sync completes
+    cudaStream_t side = nullptr;        // stats staging beside the main stream
+    cudaEvent_t ev_stage = nullptr;
     // decode-token projections: GEMV workspace (split-k partials + self-resetting tickets)
     void* gemv_ws = nullptr;
     uint64_t gemv_n_max = 0;
     bool gemv_ok = false;  // every projection width a multiple of 4 (float4 columns)
     ~reattn_engine() {
+        if (side) cudaStreamSynchronize(side);
+        if (ev_stage) cudaEventDestroy(ev_stage);
+        if (side) cudaStreamDestroy(side);
         if (gemv_ws) cudaFree(gemv_ws);
         for (auto* p : plans) reattn_plan_destroy(p);
         for (auto* c : caches) reattn_cache_destroy(c);
@@ -389,7 +394,10 @@ int forward_block(reattn_engine* e, uint64_t rows) {
         const float* attn = e->attn;
         if (pl) {  // the graph replay, no host synchronisation; stats after the block
             if ((rc = reattn_plan_launch(pl))) return rc;
-            if ((rc = reattn_plan_stage_result(pl))) return rc;
+            // the step's stats are copied to the host beside the main stream
+            CU(ctx, cudaEventRecord(e->ev_stage, ctx->stream));
+            CU(ctx, cudaStreamWaitEvent(e->side, e->ev_stage, 0));
+            if ((rc = plan_stage_result_on(pl, e->side))) return rc;
             launched[l] = pl;
             attn = reattn_plan_out(pl);
         } else {
@@ -427,6 +435,7 @@ int forward_block(reattn_engine* e, uint64_t rows) {
 // fold the staged results of the last block's plans (engine.hpp:100-112, layer order); the
 // caller has synchronised the context stream
 int fold_pending(reattn_engine* e) {
+    if (!e->pending.empty()) CU(e->ctx, cudaStreamSynchronize(e->side));
     for (uint64_t l = 0; l < e->pending.size(); ++l) {
         if (!e->pending[l]) continue;
         reattn_step_stats st{};
@@ -691,6 +700,8 @@ int reattn_engine_create(reattn_ctx* ctx, const reattn_weights* w, const reattn_
     if ((rc = reattn_rope_create(ctx, w->cfg.d_head, w->cfg.rope_base, w->cfg.pretrain_window, &e->rope)))
         return rc;
     CU(ctx, cudaMalloc(&e->next, sizeof(uint32_t)));
+    CU(ctx, cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+    CU(ctx, cudaEventCreateWithFlags(&e->ev_stage, cudaEventDisableTiming));
     const reattn_model_config& mc = w->cfg;
     e->gemv_n_max = std::max({mc.vocab_size, mc.d_ff, mc.d_model, mc.n_head * mc.d_head,
                               mc.n_kv_head * mc.d_head});

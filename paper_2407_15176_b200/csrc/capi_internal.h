@@ -101,6 +101,9 @@ inline int ensure_arena(reattn_ctx* ctx, size_t bytes) {
 }
 
 // enqueue the device mirror of cache->total (stream-ordered with the plans that read it)
+// reattn_plan_stage_result on a given stream (the engine stages beside its main stream)
+extern "C" int plan_stage_result_on(reattn_plan* p, cudaStream_t s);
+
 inline int cache_sync_total(reattn_ctx* ctx, reattn_cache* c, cudaStream_t s) {
     if (c->dev_total) CU(ctx, launch_set_u32(c->dev_total, (uint32_t)c->total, s));
     return REATTN_OK;

@@ -269,7 +269,7 @@ cudaError_t launch_cache_append_step(const float* k_in, const float* v_in, void*
                                      int dtype, uint64_t n_kv, uint64_t d, uint64_t head_stride,
                                      uint32_t* dev_total, cudaStream_t s);
 cudaError_t launch_set_u32(uint32_t* p, uint32_t v, cudaStream_t s);
-// copies count (<= 3) arrays src[i] -> dst[i] of n[i] floats (pinned host <-> device, zero-copy)
+// copies count (<= 4) arrays src[i] -> dst[i] of n[i] floats (pinned host <-> device, zero-copy)
 cudaError_t launch_host_io(const float* const* src, float* const* dst, const uint64_t* n, int count,
                            cudaStream_t s);
 // scope gather to fp32 [n_kv][L][d] (assemble_scope's copies, scope.hpp:63-76).

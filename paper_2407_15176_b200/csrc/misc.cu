@@ -144,13 +144,12 @@ __global__ void __launch_bounds__(256) cache_append_step_kernel(const float* __r
 __global__ void set_u32_kernel(uint32_t* p, uint32_t v) { *p = v; }
 
 // Zero-copy host I/O of a decode step (reattn_plan_step_host / run_host on pinned buffers):
-// up to three host arrays read straight over the bus into device buffers, or one written
-// back, by a few CTAs -- no DMA set-up per array.  16-byte vectors when everything is
+// up to four host arrays read straight over the bus into device buffers, or written back, by a few CTAs -- no DMA set-up per array.  16-byte vectors when everything is
 // aligned.
 struct HostIo {
-    const float* src[3];
-    float* dst[3];
-    uint32_t n[3];
+    const float* src[4];
+    float* dst[4];
+    uint32_t n[4];
     int count;
 };
 
@@ -177,13 +176,13 @@ cudaError_t launch_host_io(const float* const* src, float* const* dst, const uin
                            cudaStream_t s) {
     HostIo io{};
     uint64_t total = 0;
-    for (int a = 0; a < count && a < 3; ++a) {
+    for (int a = 0; a < count && a < 4; ++a) {
         io.src[a] = src[a];
         io.dst[a] = dst[a];
         io.n[a] = (uint32_t)n[a];
         total += n[a];
     }
-    io.count = count < 3 ? count : 3;
+    io.count = count < 4 ? count : 4;
     if (total == 0) return cudaSuccess;
     const int g = (int)std::min<uint64_t>(16, (total / 4 + 255) / 256 + 1);
     host_io_kernel<<<g, 256, 0, s>>>(io);
