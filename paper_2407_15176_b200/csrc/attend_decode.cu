@@ -130,6 +130,7 @@ __device__ __noinline__ void merge_parts(const BulkArgs& B, int kv, int role, ui
             return B.part + (((size_t)p * a.n_kv + kv) * G + g) * kBPartBytes;
         };
         const int n_slots = B.n_slots;
+        RA_ASSERT(n_slots <= kBMaxParts);
         double hm = -INFINITY, ha = 0.0, hb = 0.0;  // header of slot `lane` (first page)
         if (lane < n_slots) {
             const double* hd = (const double*)prow(lane);
@@ -369,9 +370,11 @@ __global__ void __launch_bounds__(kBThreads, 1) attend_decode_bulk_kernel(const 
             const uint32_t heads = __ballot_sync(0xFFFFFFFFu, head);
             const uint32_t breaks = heads | __ballot_sync(0xFFFFFFFFu, !own);
             if (head) {
+                RA_ASSERT(cr < a.head_stride);
                 const uint32_t later = lane == 31 ? 0u : breaks & ~((2u << lane) - 1u);
                 const int end = later ? __ffs(later) - 1 : 32;
                 const uint32_t bytes_run = (uint32_t)(end - lane) * kBD * 2u;
+                RA_ASSERT(cr + (uint32_t)(end - lane) <= a.head_stride);
                 const size_t row = ((size_t)kv * a.head_stride + cr) * kBD;
                 bulk_g2s(st + lane * kBD * 2, (const __nv_bfloat16*)a.k_base + row, bytes_run, &full[s]);
                 bulk_g2s(st + kBKVBytes + lane * kBD * 2, (const __nv_bfloat16*)a.v_base + row, bytes_run,

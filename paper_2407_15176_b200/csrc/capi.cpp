@@ -580,7 +580,13 @@ int check_plan(reattn_plan* p) {
 
 extern "C" {
 
-const char* reattn_version(void) { return "reattn-b200 0.1 (sm_100a)"; }
+const char* reattn_version(void) {
+#ifdef REATTN_DEBUG
+    return "reattn-b200 0.1 (sm_100a, debug: device asserts, trapping mbarrier timeouts)";
+#else
+    return "reattn-b200 0.1 (sm_100a)";
+#endif
+}
 
 int reattn_ctx_create(int device, reattn_ctx** out) {
     auto* ctx = new reattn_ctx();

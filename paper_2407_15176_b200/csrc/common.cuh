@@ -1,6 +1,7 @@
 // Shared sm_100a device helpers: mbarrier / TMA PTX wrappers, packed f32x2 math,
 // total-order keys for (score desc, index asc) selection.
 #pragma once
+#include <cstdio>
 
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -123,6 +124,42 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifdef REATTN_DEBUG
+// Debug build (make DEBUG=1 -> libreattn_cuda_debug.so): a wait that has not completed after
+// ~4 s of polling traps with its location instead of hanging the GPU; RA_ASSERT traps on a
+// violated bound.  The product library compiles both away.
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const long long t0 = clock64();
+    while (!mbar_try_wait(bar, parity)) {
+        if (clock64() - t0 > 8000000000ll) {
+            printf("reattn debug: mbarrier wait timed out (block %d,%d,%d thread %d, parity %u)\n",
+                   blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, parity);
+            __trap();
+        }
+    }
+}
+#define RA_ASSERT(cond)                                                                     \
+    do {                                                                                    \
+        if (!(cond)) {                                                                      \
+            printf("reattn debug: %s:%d: assertion failed: %s (block %d,%d thread %d)\n", \
+                   __FILE__, __LINE__, #cond, blockIdx.x, blockIdx.y, threadIdx.x);         \
+            __trap();                                                                       \
+        }                                                                                   \
+    } while (0)
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -134,6 +171,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+#define RA_ASSERT(cond) \
+    do {                \
+    } while (0)
+#endif
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0,
                                             int32_t c1, uint64_t* bar, uint64_t policy) {
     asm volatile(

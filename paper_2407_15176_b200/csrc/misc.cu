@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(256) cache_append_step_kernel(const float* __r
                                                                 uint32_t d, uint64_t head_stride,
                                                                 uint32_t* dev_total) {
     const uint32_t row = *(volatile uint32_t*)dev_total;
+    RA_ASSERT(row < head_stride);  // the plan checked capacity on the host mirror
     for (uint32_t e = threadIdx.x; e < n_kv * d; e += blockDim.x) {
         const uint32_t h = e / d, c = e % d;
         const size_t o = ((size_t)h * head_stride + row) * d + c;

@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(const float* _
             if (ok) gemv_store(M, col, p);
             return;
         }
+        RA_ASSERT(c + t < G + B.tiles);
         if (ok) reinterpret_cast<float4*>(ws)[(uint64_t)(c + t) * 32 + lane] = p;
         // units of tile t in this CTA
         const uint64_t tb = (uint64_t)t * B.upt, te = tb + B.upt;

@@ -719,6 +719,7 @@ __global__ void __launch_bounds__(256) scan_generic_kernel(const GenArgs a) {
     }
     const size_t o = ((size_t)kv * a.n_q + qi) * a.k;
     for (uint32_t j = tid; j < r; j += blockDim.x) {
+        RA_ASSERT(key_index(buf[j]) < a.count);
         a.idx_out[o + j] = key_index(buf[j]);
         a.score_out[o + j] = key_score(buf[j]);
     }

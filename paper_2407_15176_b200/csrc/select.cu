@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectArgs a)
                 } else {
                     src = a.l_start + (r - g - cov);
                 }
+                RA_ASSERT(r < a.window && src < a.total);
                 a.scope_src[r] = src;
             }
         }

@@ -222,6 +222,7 @@ __device__ __forceinline__ void small_select_scope_smem(const SmallSelectIO& io,
     if ((sm.err == 0 || dry) && io.scope_src) {
         const uint32_t g = io.g_end, cov = sm.cov, ns = min(sm.ns, 32u);
         const uint32_t L = dry ? min(sm.L, g + cov + 64u) : sm.L;
+        RA_ASSERT(dry || L <= io.window);
         const uint32_t nthr = blockDim.x, warp = (uint32_t)tid >> 5, lane = (uint32_t)tid & 31u;
         for (uint32_t r = tid; r < g; r += nthr)
             if (!dry) io.scope_src[r] = r;
@@ -229,6 +230,7 @@ __device__ __forceinline__ void small_select_scope_smem(const SmallSelectIO& io,
             const uint32_t o = sm.off[sp], e0 = sp + 1 < ns ? sm.off[sp + 1] : cov;
             const uint32_t e = dry ? min(e0, o + 32u) : e0;
             const uint32_t src0 = g + sm.b[sp];
+            RA_ASSERT(dry || sm.b[sp] + (e0 - o) <= io.middle_len);
             for (uint32_t j = o + lane; j < e; j += 32)
                 if (!dry) io.scope_src[g + j] = src0 + (j - o);
         }
