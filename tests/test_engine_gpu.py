@@ -233,6 +233,32 @@ def test_selection_active_matches_reference_engine(ctx):
     assert abs(gs.entropy_max - rs["entropy_max"]) <= 1e-4
 
 
+@pytest.mark.parametrize("cache_dtype", [N.F32, N.BF16])
+def test_decode_projection_shapes_match_reference_engine(ctx, cache_dtype):
+    """Decode tokens at widths that are not multiples of the GEMV's 128-column tiles or
+    64-row units (d_model 260 = 5 heads x 52, d_ff 1000, vocab 1032, one kv head): the
+    fused q/k/v GEMV with the K/V rows written into the cache from its epilogue, the
+    gate/up pair with silu in the epilogue, the stream-K fix-up across tile boundaries --
+    logits within 1e-4 of the reference Engine (fp32 cache) and the same greedy tokens."""
+    cfg = toy_config(d_model=260, n_head=5, n_kv_head=1, d_head=52, d_ff=1000, vocab_size=1032)
+    w, r = pair(ctx, cfg, 41)
+    tokens = ob.random_tokens(600, cfg.vocab_size, 410)
+    sel = toy_selection(k_prime=8)
+    eng = N.Engine(ctx, w, sel, cache_dtype=cache_dtype)
+    ref = ob.RefEngine(r, sel, d_model=cfg.d_model, vocab=cfg.vocab_size)
+    gh, rh = eng.prefill(tokens), ref.prefill(tokens)
+    tol = 1e-4 if cache_dtype == N.F32 else 2e-2
+    assert np.abs(gh - rh).max() <= tol
+    feed = int(tokens[-1])
+    for _ in range(5):
+        a = eng.decode_step(feed)
+        b, lb = ref.decode_step(feed)
+        assert np.abs(eng.last_logits() - lb).max() <= tol
+        if cache_dtype == N.F32:
+            assert a == b
+        feed = b
+
+
 def test_long_context_never_leaves_pretrain_range(ctx):  # test_engine.cpp:173-195
     cfg = toy_config()
     w = N.Weights.init_random(ctx, cfg, 26)
