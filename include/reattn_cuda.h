@@ -278,6 +278,12 @@ int reattn_plan_staged_result(reattn_plan* plan, reattn_step_stats* stats, uint6
  * is built, the decode kernels stamp %globaltimer (ns) into a device trace buffer; this
  * synchronises the device and copies its first n words (n <= 4096) to the host. */
 int reattn_debug_trace(uint64_t* host_out, uint64_t n);
+/* Diagnostics: the decoder's fp32 GEMV (y[N] = x[K] . W[K][N] + beta y) on the context
+ * stream, for benchmarking the projection kernel alone (tools/bench_gemv.py); ws is a device
+ * workspace of reattn_debug_gemv_workspace(N) bytes, zeroed once. */
+size_t reattn_debug_gemv_workspace(uint64_t n);
+int reattn_debug_gemv(reattn_ctx* ctx, const float* x, const float* w, uint64_t ldw, uint64_t n,
+                      uint64_t k, float* y, float beta, void* ws);
 /* kernels per replay, and the algorithmic bytes of the dominant kernel (the K scan) */
 int reattn_plan_info(const reattn_plan* plan, uint64_t* kernels_per_step,
                      uint64_t* scan_bytes, uint64_t* scope_bytes);

@@ -117,6 +117,10 @@ const float* cslot(const reattn_weights* w, int kind, uint64_t layer) {
     return *slot(const_cast<reattn_weights*>(w), kind, layer);
 }
 
+// the GEMV weight map of (kind, layer), or nullptr when it cannot be encoded
+constexpr int kMapKinds = REATTN_W_DOWN + 1;
+const CUtensorMap* wmap(reattn_engine* e, int kind, uint64_t layer);
+
 int alloc_weights(reattn_ctx* ctx, const reattn_model_config& c, std::unique_ptr<reattn_weights>& w) {
     int rc = validate_model(ctx, c);
     if (rc) return rc;
@@ -211,6 +215,10 @@ struct reattn_engine {
     std::vector<reattn_plan*> pending;  // plans whose staged results the next sync completes
     cudaStream_t side = nullptr;        // stats staging beside the main stream
     cudaEvent_t ev_stage = nullptr;
+    // TMA tensor maps of the projection weights for the GEMV (built on first use; the weight
+    // storage never moves): [layer * kMapKinds + kind], lm_head at the end
+    std::vector<CUtensorMap> wmaps;
+    std::vector<uint8_t> wmap_ok;
     // decode-token projections: GEMV workspace (split-k partials + self-resetting tickets)
     void* gemv_ws = nullptr;
     uint64_t gemv_n_max = 0;
@@ -241,11 +249,29 @@ namespace {
     } while (0)
 
 // row-major C[M x N] = A[M x K] · B[K x N] + beta·C, leading dimensions in elements
+const CUtensorMap* wmap(reattn_engine* e, int kind, uint64_t layer) {
+    const reattn_model_config& c = e->w->cfg;
+    const size_t n = c.n_layer * kMapKinds + 1;
+    if (e->wmaps.size() != n) {
+        e->wmaps.assign(n, CUtensorMap{});
+        e->wmap_ok.assign(n, 0);
+    }
+    const size_t i = kind == REATTN_W_LM_HEAD ? n - 1 : layer * kMapKinds + kind;
+    if (!e->wmap_ok[i]) {
+        uint64_t rows, cols;
+        shape_of(c, kind, &rows, &cols);
+        e->wmap_ok[i] = gemv_weight_map(&e->wmaps[i], cslot(e->w, kind, layer), cols, cols, rows) ? 1 : 2;
+    }
+    return e->wmap_ok[i] == 1 ? &e->wmaps[i] : nullptr;
+}
+
 int gemm(reattn_engine* e, uint64_t M, uint64_t N, uint64_t K, const float* A, uint64_t lda,
-         const float* B, uint64_t ldb, float* C, uint64_t ldc, float beta) {
+         const float* B, uint64_t ldb, float* C, uint64_t ldc, float beta, const CUtensorMap* map = nullptr) {
     if (M == 0 || N == 0) return REATTN_OK;
     if (M == 1 && e->gemv_ok && N <= e->gemv_n_max && gemv_supported(N, K, ldb, A, B, C)) {
-        CU(e->ctx, launch_gemv(A, B, ldb, N, K, C, beta, e->gemv_ws, e->gemv_n_max, e->ctx->stream));
+        const GemvDesc m{B, ldb, N, C, beta, 0, 0, 0, 0};
+        CU(e->ctx, launch_gemv_batch(A, K, &m, 1, false, e->gemv_ws, e->gemv_n_max, e->ctx->stream, nullptr, 0,
+                                     map));
         return REATTN_OK;
     }
     const float one = 1.0f;
@@ -381,8 +407,18 @@ int forward_block(reattn_engine* e, uint64_t rows) {
                  cache->capacity},
                 {cslot(e->w, REATTN_W_WV, l), KW, KW, (float*)cache->values, 0.0f, kind, c.d_head, cache->total,
                  cache->capacity}};
+            const CUtensorMap* mq = wmap(e, REATTN_W_WQ, l);
+            const CUtensorMap* mk = wmap(e, REATTN_W_WK, l);
+            const CUtensorMap* mv = wmap(e, REATTN_W_WV, l);
+            CUtensorMap maps[3];
+            const bool tma = mq && mk && mv;
+            if (tma) {
+                maps[0] = *mq;
+                maps[1] = *mk;
+                maps[2] = *mv;
+            }
             CU(ctx, launch_gemv_batch(e->h, D, m, 3, false, e->gemv_ws, e->gemv_n_max, ctx->stream,
-                                      cache->dev_total, (uint32_t)(cache->total + 1)));
+                                      cache->dev_total, (uint32_t)(cache->total + 1), tma ? maps : nullptr));
             cache->total += 1;
         } else {
             if ((rc = append_kv(e, cache, l, rows))) return rc;  // before attend_step (engine.hpp:196-198)
@@ -408,13 +444,22 @@ int forward_block(reattn_engine* e, uint64_t rows) {
             fold_stats(e, l, st);
         }
         // x += attn · wo
-        if ((rc = gemm(e, rows, D, D, attn, D, cslot(e->w, REATTN_W_WO, l), D, e->x, D, 1.0f)))
+        if ((rc = gemm(e, rows, D, D, attn, D, cslot(e->w, REATTN_W_WO, l), D, e->x, D, 1.0f,
+                       token ? wmap(e, REATTN_W_WO, l) : nullptr)))
             return rc;
         CU(ctx, launch_rmsnorm(e->x, rows, D, cslot(e->w, REATTN_W_NORM_FFN, l), e->h, ctx->stream));
         if (token) {
             const GemvDesc m[2] = {{cslot(e->w, REATTN_W_GATE, l), F, F, e->gate, 0.0f, 0, 0, 0, 0},
                                    {cslot(e->w, REATTN_W_UP, l), F, F, e->up, 0.0f, 0, 0, 0, 0}};
-            CU(ctx, launch_gemv_batch(e->h, D, m, 2, true, e->gemv_ws, e->gemv_n_max, ctx->stream));
+            const CUtensorMap* mg = wmap(e, REATTN_W_GATE, l);
+            const CUtensorMap* mu = wmap(e, REATTN_W_UP, l);
+            CUtensorMap maps[2];
+            if (mg && mu) {
+                maps[0] = *mg;
+                maps[1] = *mu;
+            }
+            CU(ctx, launch_gemv_batch(e->h, D, m, 2, true, e->gemv_ws, e->gemv_n_max, ctx->stream, nullptr, 0,
+                                      mg && mu ? maps : nullptr));
         } else {
             if ((rc = gemm(e, rows, F, D, e->h, D, cslot(e->w, REATTN_W_GATE, l), F, e->gate, F, 0.0f)))
                 return rc;
@@ -422,7 +467,8 @@ int forward_block(reattn_engine* e, uint64_t rows) {
                 return rc;
             CU(ctx, launch_silu_mul(e->gate, e->up, rows * F, ctx->stream));
         }
-        if ((rc = gemm(e, rows, D, F, e->gate, F, cslot(e->w, REATTN_W_DOWN, l), D, e->x, D, 1.0f)))
+        if ((rc = gemm(e, rows, D, F, e->gate, F, cslot(e->w, REATTN_W_DOWN, l), D, e->x, D, 1.0f,
+                       token ? wmap(e, REATTN_W_DOWN, l) : nullptr)))
             return rc;
     }
     // the plans' results are copied behind the block; folded in layer order after the next
@@ -460,7 +506,7 @@ int logits_of_x(reattn_engine* e, uint64_t rows) {
     CU(ctx, launch_rmsnorm(e->x, rows, c.d_model, cslot(e->w, REATTN_W_NORM_FINAL, 0), e->h,
                            ctx->stream));
     return gemm(e, rows, c.vocab_size, c.d_model, e->h, c.d_model, cslot(e->w, REATTN_W_LM_HEAD, 0),
-                c.vocab_size, e->logits, c.vocab_size, 0.0f);
+                c.vocab_size, e->logits, c.vocab_size, 0.0f, rows == 1 ? wmap(e, REATTN_W_LM_HEAD, 0) : nullptr);
 }
 
 }  // namespace
@@ -861,6 +907,18 @@ int reattn_engine_synth_context(reattn_engine* e, uint64_t total, uint64_t seed)
         if ((rc = reattn_cache_set_total(ctx, cache, total))) return rc;
     }
     CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+size_t reattn_debug_gemv_workspace(uint64_t n) { return gemv_workspace_bytes(n); }
+
+int reattn_debug_gemv(reattn_ctx* ctx, const float* x, const float* w, uint64_t ldw, uint64_t n,
+                      uint64_t k, float* y, float beta, void* ws) {
+    if (!gemv_supported(n, k, ldw, x, w, y)) return set_err(ctx, REATTN_EINVAL, "gemv: unsupported shape");
+    CUtensorMap map;
+    const bool tma = gemv_weight_map(&map, w, ldw, n, k);
+    const GemvDesc m{w, ldw, n, y, beta, 0, 0, 0, 0};
+    CU(ctx, launch_gemv_batch(x, k, &m, 1, false, ws, n, ctx->stream, nullptr, 0, tma ? &map : nullptr));
     return REATTN_OK;
 }
 

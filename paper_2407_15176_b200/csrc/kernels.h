@@ -307,11 +307,17 @@ struct GemvDesc {
     uint64_t d, row;       //   column c lands in head c / d, element c % d of cache row `row`
     uint64_t head_stride;  //   (the cache capacity)
 };
+// a plain (unswizzled) 2-D tensor map: `outer` rows of `inner` elements, row_bytes apart
+bool make_tensor_map_2d(CUtensorMap* map, const void* base, int dtype, uint64_t inner, uint64_t outer,
+                        uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer);
+// the GEMV's weight tile map (64 rows x 128 fp32 columns) for W[K][N] with row stride ldw
+bool gemv_weight_map(CUtensorMap* map, const float* W, uint64_t ldw, uint64_t N, uint64_t K);
 // up to 3 matrices sharing x in one launch; silu_pair: mats = {gate, up}, gate <- silu(g) * u;
+// maps (optional, one per matrix, from gemv_weight_map): the TMA-fed kernel when K fits;
 // total_ptr (optional): written with total_val by the launch (a cache's device length)
 cudaError_t launch_gemv_batch(const float* x, uint64_t K, const GemvDesc* mats, int count, bool silu_pair,
                               void* ws, uint64_t n_max, cudaStream_t s, uint32_t* total_ptr = nullptr,
-                              uint32_t total_val = 0);
+                              uint32_t total_val = 0, const CUtensorMap* maps = nullptr);
 
 // ---- timeline trace (diagnostics): REATTN_TRACE=1 at plan / launch time makes the decode
 // kernels stamp %globaltimer into a device buffer (layout in misc.cu); null otherwise.

@@ -11,6 +11,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+using namespace reattn_dev;
+
 namespace reattn_impl {
 
 namespace {
@@ -264,6 +266,7 @@ struct GemvBatch {
     uint64_t units;     // tiles * upt
     uint32_t* total_ptr;  // non-null: CTA 0 writes total_val (a cache's device length)
     uint32_t total_val;
+    uint32_t prefetch;    // units prefetched into L2 ahead of the register double buffer
 };
 
 // y columns [col, col + 4) of M (the matrix's own column index), beta-accumulated for dense
@@ -325,6 +328,20 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(const float* _
         for (int i = 0; i < kGemvRows; ++i)
             w[b][i] = col < M.N && r0 + i * kGemvWarps < B.K ? ld_stream4(wp + (uint64_t)i * kGemvWarps * M.ldw)
                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    // L2 prefetch of a later unit's rows: DRAM requests in flight beyond the register buffers
+    auto prefetch_w = [&](uint32_t u) {
+        const uint32_t t = u / B.upt;
+        const GemvMat& M = B.m[mat_of(B, t)];
+        const uint32_t col = (t - M.tile0) * kGemvCols + lane * 4;
+        const uint32_t r0 = (u % B.upt) * kGemvUnitRows + warp;
+        const float* wp = M.W + (uint64_t)r0 * M.ldw + col;
+        if ((lane & 7) == 0 && col < M.N) {  // one lane per 128-byte line
+#pragma unroll
+            for (int i = 0; i < kGemvRows; ++i)
+                if (r0 + i * kGemvWarps < B.K)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(wp + (uint64_t)i * kGemvWarps * M.ldw));
+        }
     };
     auto load_x = [&](uint32_t u, int b) {
         const uint32_t r0 = (u % B.upt) * kGemvUnitRows + warp;
@@ -412,11 +429,15 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(const float* _
     // the cache's new device length: read only by kernels after this grid completes
     if (B.total_ptr && c == 0 && threadIdx.x == 0) *B.total_ptr = B.total_val;
     load_x(u0, 0);
+    const uint32_t pd = B.prefetch;
+    if (pd)
+        for (uint32_t v = u0 + 1; v < min(u1, u0 + 1 + pd); ++v) prefetch_w(v);
     for (uint32_t u = u0;;) {
         if (u + 1 < u1) {
             load_w(u + 1, 1);
             load_x(u + 1, 1);
         }
+        if (pd && u + 1 + pd < u1) prefetch_w(u + 1 + pd);
         fma_rows(0);
         if (u + 1 >= u1 || (u + 1) / B.upt != u / B.upt) epilogue(u / B.upt);
         if (++u >= u1) break;
@@ -424,9 +445,147 @@ __global__ void __launch_bounds__(kGemvWarps * 32, 2) gemv_kernel(const float* _
             load_w(u + 1, 0);
             load_x(u + 1, 0);
         }
+        if (pd && u + 1 + pd < u1) prefetch_w(u + 1 + pd);
         fma_rows(1);
         if (u + 1 >= u1 || (u + 1) / B.upt != u / B.upt) epilogue(u / B.upt);
         if (++u >= u1) break;
+    }
+}
+
+// The TMA-fed variant (weights of every unit staged in shared memory by the tensor-memory
+// accelerator): one CTA per SM, a producer thread keeps kTStages units (32 KB each) in flight
+// -- 160 KB per SM, issued before griddepcontrol.wait since the weights do not depend on the
+// kernel before -- and 8 consumer warps accumulate from shared memory with x staged once.
+// Same stream-K split, epilogue and determinism as gemv_kernel.
+constexpr int kTStages = 5, kTConsumers = 8, kTThreads = (kTConsumers + 1) * 32;
+constexpr int kTStageBytes = kGemvUnitRows * kGemvCols * 4;  // 32 KB
+constexpr int kTMaxK = 14336;                                 // x staged in shared memory
+constexpr size_t kTSmem = 1024 + (size_t)kTStages * kTStageBytes + (size_t)kTMaxK * 4 + 256;
+
+__global__ void __launch_bounds__(kTThreads, 1) gemv_tma_kernel(
+    const __grid_constant__ CUtensorMap map0, const __grid_constant__ CUtensorMap map1,
+    const __grid_constant__ CUtensorMap map2, const float* __restrict__ x, GemvBatch B, float* ws,
+    uint32_t* tickets) {
+    extern __shared__ uint8_t tsm_raw[];
+    uint8_t* sm = (uint8_t*)(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
+    float* ring = (float*)sm;                                            // [stages][64][128]
+    float* sx = (float*)(sm + (size_t)kTStages * kTStageBytes);          // [K]
+    uint64_t* full = (uint64_t*)(sx + kTMaxK);
+    uint64_t* empty = full + kTStages;
+    __shared__ float4 red[2][kTConsumers * 32];
+    asm volatile("griddepcontrol.launch_dependents;");
+    const uint32_t G = gridDim.x, c = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t u0 = unit_begin(c, B.units, G), u1 = unit_begin(c + 1, B.units, G);
+    if (tid == 0) {
+        for (int i = 0; i < kTStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kTConsumers);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == kTConsumers) {  // ===== producer: one TMA load per unit =====
+        if (lane == 0) {
+            prefetch_tensormap(&map0);
+            if (B.count > 1) prefetch_tensormap(&map1);
+            if (B.count > 2) prefetch_tensormap(&map2);
+            const uint64_t pol = policy_evict_first();
+            for (uint32_t u = u0; u < u1; ++u) {
+                const uint32_t i = u - u0, s = i % kTStages;
+                if (i >= kTStages) mbar_wait(&empty[s], ((i / kTStages) - 1) & 1u);
+                const uint32_t t = u / B.upt;
+                const int mi = mat_of(B, t);
+                const CUtensorMap* mp = mi == 0 ? &map0 : mi == 1 ? &map1 : &map2;
+                mbar_arrive_expect_tx(&full[s], kTStageBytes);
+                tma_load_2d(ring + (size_t)s * (kTStageBytes / 4), mp, (int32_t)((t - B.m[mi].tile0) * kGemvCols),
+                            (int32_t)((u % B.upt) * kGemvUnitRows), &full[s], pol);
+            }
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        return;
+    }
+    // ===== consumers =====
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // x, y, workspace: the kernel before
+    if (B.total_ptr && c == 0 && tid == 0) *B.total_ptr = B.total_val;
+    for (uint32_t i = tid; i < B.K; i += kTConsumers * 32) sx[i] = x[i];
+    named_bar_sync(1, kTConsumers * 32);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int rb = 0;
+    auto silu = [](float gv, float uv) { return __fmul_rn(__fdiv_rn(gv, __fadd_rn(1.0f, expf(-gv))), uv); };
+    auto epilogue = [&](uint32_t t) {
+        red[rb][warp * 32 + lane] = acc;
+        acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        named_bar_sync(1, kTConsumers * 32);
+        const int b = rb;
+        rb ^= 1;
+        if (warp != 0) return;
+        float4 p = red[b][lane];
+#pragma unroll
+        for (int i = 1; i < kTConsumers; ++i) add4(p, red[b][i * 32 + lane]);
+        const bool pair = B.silu_pair != 0;
+        const GemvMat& M = B.m[mat_of(B, t)];
+        const uint32_t col = (t - M.tile0) * kGemvCols + lane * 4;
+        const bool ok = col < M.N;
+        const uint32_t cf = unit_owner((uint64_t)t * B.upt, B.units, G);
+        const uint32_t cl = unit_owner((uint64_t)(t + 1) * B.upt - 1, B.units, G);
+        if (!pair && cf == cl) {
+            if (ok) gemv_store(M, col, p);
+            return;
+        }
+        RA_ASSERT(c + t < G + B.tiles);
+        if (ok) reinterpret_cast<float4*>(ws)[(uint64_t)(c + t) * 32 + lane] = p;
+        const uint64_t tb = (uint64_t)t * B.upt, te = tb + B.upt;
+        const uint32_t mine = (uint32_t)((te < u1 ? te : (uint64_t)u1) - (tb > u0 ? tb : (uint64_t)u0));
+        const uint32_t pt = pair ? B.m[1].tile0 : 0;
+        const uint32_t ticket = pair ? t % pt : t;
+        const uint32_t need = pair ? 2 * B.upt : B.upt;
+        __threadfence();
+        __syncwarp();
+        uint32_t last = 0;
+        if (lane == 0) {
+            last = atomicAdd(&tickets[ticket], mine) + mine == need;
+            if (last) tickets[ticket] = 0;
+        }
+        if (!__shfl_sync(0xFFFFFFFFu, last, 0)) return;
+        __threadfence();
+        auto total_of = [&](uint32_t tt) {
+            const uint32_t f = unit_owner((uint64_t)tt * B.upt, B.units, G);
+            const uint32_t l = unit_owner((uint64_t)(tt + 1) * B.upt - 1, B.units, G);
+            float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (!ok) return q;
+            for (uint32_t j = f; j <= l; ++j)
+                add4(q, __ldcg(reinterpret_cast<const float4*>(ws) + (uint64_t)(j + tt) * 32 + lane));
+            return q;
+        };
+        if (!ok) return;
+        if (pair) {
+            const uint32_t tg = t % pt;
+            const float4 g = total_of(tg), u = total_of(tg + pt);
+            *reinterpret_cast<float4*>(B.m[0].y + col) =
+                make_float4(silu(g.x, u.x), silu(g.y, u.y), silu(g.z, u.z), silu(g.w, u.w));
+            return;
+        }
+        gemv_store(M, col, total_of(t));
+    };
+    for (uint32_t u = u0; u < u1; ++u) {
+        const uint32_t i = u - u0, s = i % kTStages;
+        mbar_wait(&full[s], (i / kTStages) & 1u);
+        const float* st = ring + (size_t)s * (kTStageBytes / 4);
+        const uint32_t r0 = (u % B.upt) * kGemvUnitRows;
+#pragma unroll
+        for (int j = 0; j < kGemvRows; ++j) {
+            const uint32_t r = warp + j * kTConsumers, row = r0 + r;
+            const float4 w = reinterpret_cast<const float4*>(st + r * kGemvCols)[lane];
+            const float xv = row < B.K ? sx[row] : 0.f;  // rows past K: zero-filled by the TMA
+            acc.x = fmaf(xv, w.x, acc.x);
+            acc.y = fmaf(xv, w.y, acc.y);
+            acc.z = fmaf(xv, w.z, acc.z);
+            acc.w = fmaf(xv, w.w, acc.w);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (u + 1 >= u1 || (u + 1) / B.upt != u / B.upt) epilogue(u / B.upt);
     }
 }
 
@@ -443,6 +602,10 @@ int gemv_ctas() {
 }
 }  // namespace
 
+bool gemv_weight_map(CUtensorMap* map, const float* W, uint64_t ldw, uint64_t N, uint64_t K) {
+    return make_tensor_map_2d(map, W, kF32, N, K, ldw * sizeof(float), kGemvCols, kGemvUnitRows);
+}
+
 size_t gemv_workspace_bytes(uint64_t n_max) {
     // partial slots cta + tile < ctas + tiles; one ticket per tile
     const uint64_t tiles = 3 * ((n_max + kGemvCols - 1) / kGemvCols);
@@ -457,7 +620,7 @@ bool gemv_supported(uint64_t N, uint64_t K, uint64_t ldw, const void* x, const v
 
 cudaError_t launch_gemv_batch(const float* x, uint64_t K, const GemvDesc* mats, int count, bool silu_pair,
                               void* ws, uint64_t n_max, cudaStream_t s, uint32_t* total_ptr,
-                              uint32_t total_val) {
+                              uint32_t total_val, const CUtensorMap* maps) {
     if (count < 1 || count > 3 || (silu_pair && (count != 2 || mats[0].N != mats[1].N)))
         return cudaErrorInvalidValue;
     GemvBatch B{};
@@ -478,6 +641,8 @@ cudaError_t launch_gemv_batch(const float* x, uint64_t K, const GemvDesc* mats, 
     B.units = (uint64_t)tiles * B.upt;
     B.total_ptr = total_ptr;
     B.total_val = total_val;
+    static const uint32_t pf = getenv("REATTN_GEMV_PREFETCH") ? (uint32_t)atoi(getenv("REATTN_GEMV_PREFETCH")) : 0u;
+    B.prefetch = pf;
     if (B.units > UINT32_MAX) return cudaErrorInvalidValue;
     const uint32_t G = (uint32_t)std::min<uint64_t>(std::min(gemv_ctas(), 148 * 8), B.units);
     const uint64_t tiles_max = 3 * ((n_max + kGemvCols - 1) / kGemvCols);
@@ -492,6 +657,28 @@ cudaError_t launch_gemv_batch(const float* x, uint64_t K, const GemvDesc* mats, 
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = gemv_pdl_env() ? 1 : 0;
+    static const bool no_tma = getenv("REATTN_GEMV_NO_TMA") != nullptr;
+    if (maps && K <= (uint64_t)kTMaxK && !no_tma) {
+        static int sms = [] {
+            int dev = 0, n = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+            return n;
+        }();
+        static bool attr = [] {
+            return cudaFuncSetAttribute(gemv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kTSmem) == cudaSuccess;
+        }();
+        if (!attr) return cudaErrorInvalidValue;
+        const uint32_t GT = (uint32_t)std::min<uint64_t>((uint64_t)sms, B.units);
+        cfg.gridDim = dim3(GT);
+        cfg.blockDim = dim3(kTThreads);
+        cfg.dynamicSmemBytes = kTSmem;
+        const CUtensorMap& m0 = maps[0];
+        const CUtensorMap& m1 = count > 1 ? maps[1] : maps[0];
+        const CUtensorMap& m2 = count > 2 ? maps[2] : maps[0];
+        return cudaLaunchKernelEx(&cfg, gemv_tma_kernel, m0, m1, m2, x, B, part, tickets);
+    }
     return cudaLaunchKernelEx(&cfg, gemv_kernel, x, B, part, tickets);
 }
 
