@@ -199,6 +199,34 @@ inline ModelWeights load_weights(const std::string& path) {
     return detail::DeviceWeights(w).to_host();
 }
 
+// rmsnorm (model.hpp:155-167): the mean square in f64, then two fp32 multiplies per element
+inline DenseMatrix rmsnorm(const DenseMatrix& x, std::span<const float> weight) {
+    if (x.cols != weight.size()) throw std::invalid_argument("rmsnorm: weight width mismatch");
+    DenseMatrix out(x.rows, x.cols);
+    if (out.values.empty()) return out;
+    gpu::DeviceBuffer<float> dx, dw, dout(out.values.size());
+    dx.upload(x.values.data(), x.values.size());
+    dw.upload(weight.data(), weight.size());
+    gpu::check(reattn_rmsnorm(gpu::context(), dx.get(), x.rows, x.cols, dw.get(), dout.get()));
+    out.values = dout.to_vector(out.values.size());
+    return out;
+}
+
+// feed_forward (model.hpp:169-178): (silu(x Wg) * (x Wu)) Wd with the reference's k-ordered
+// matmul and fp32 activation
+inline DenseMatrix feed_forward(const DenseMatrix& x, const LayerWeights& layer) {
+    DenseMatrix gate = matmul(x, layer.w_gate);
+    const DenseMatrix up = matmul(x, layer.w_up);
+    if (!gate.values.empty()) {
+        gpu::DeviceBuffer<float> dg, du;
+        dg.upload(gate.values.data(), gate.values.size());
+        du.upload(up.values.data(), up.values.size());
+        gpu::check(reattn_silu_mul(gpu::context(), dg.get(), du.get(), gate.values.size()));
+        gate.values = dg.to_vector(gate.values.size());
+    }
+    return matmul(gate, layer.w_down);
+}
+
 // embed (model.hpp:181-190)
 inline DenseMatrix embed(std::span<const std::uint32_t> tokens, const ModelWeights& w) {
     DenseMatrix out(tokens.size(), w.config.d_model);

@@ -278,6 +278,16 @@ int reattn_plan_staged_result(reattn_plan* plan, reattn_step_stats* stats, uint6
  * is built, the decode kernels stamp %globaltimer (ns) into a device trace buffer; this
  * synchronises the device and copies its first n words (n <= 4096) to the host. */
 int reattn_debug_trace(uint64_t* host_out, uint64_t n);
+/* model.hpp:155-178 rmsnorm and the gated feed-forward's activation, on device arrays:
+ * out[r][c] = x[r][c] * float(1 / sqrt(mean_c(x^2 in f64) + 1e-5)) * w[c]; gate[i] <-
+ * gate[i] / (1 + exp(-gate[i])) * up[i] (fp32, the reference's operation order). */
+int reattn_rmsnorm(reattn_ctx* ctx, const float* x_dev, uint64_t rows, uint64_t cols, const float* w_dev,
+                   float* out_dev);
+int reattn_silu_mul(reattn_ctx* ctx, float* gate_dev, const float* up_dev, uint64_t n);
+/* softmax.hpp:13-36 stable_softmax (max-subtracted, f64 sums) and attention_entropy of one
+ * device vector; entropy_out: one double on the device. */
+int reattn_stable_softmax(reattn_ctx* ctx, const float* logits_dev, uint64_t n, float* out_dev);
+int reattn_attention_entropy(reattn_ctx* ctx, const float* weights_dev, uint64_t n, double* entropy_out_dev);
 /* Diagnostics: the decoder's fp32 GEMV (y[N] = x[K] . W[K][N] + beta y) on the context
  * stream, for benchmarking the projection kernel alone (tools/bench_gemv.py); ws is a device
  * workspace of reattn_debug_gemv_workspace(N) bytes, zeroed once. */

@@ -248,7 +248,10 @@ void carve_step(StepPlan& P, const reattn_cache* cache, const reattn_rope* rope,
     P.attn_tc_ws = c.take<uint8_t>(P.attn_tc_bytes);
     P.entropy = c.take<double>(std::max<uint64_t>(1, P.n_q * P.n_head));
     P.vote_ws = c.take<uint8_t>(P.vote_ws_bytes);
-    P.scratch_bytes = c.off;
+    // the scan's scratch, what the reference's ScratchMeter meters (inside fused_topk_scores
+    // only, selection.hpp:168-248, via engine.hpp:60-66): the candidate lists and the scan's
+    // workspace -- not the vote, the scope table or the attention's partial rows
+    P.scratch_bytes = ncand * (sizeof(uint32_t) + sizeof(float)) + P.scan.ws_bytes;
 }
 
 // The selection half of a step: the local-window fork (when planned), K1 (+ fused K3) or the
@@ -968,6 +971,45 @@ int reattn_matmul(reattn_ctx* ctx, const float* a, const float* b, uint64_t m, u
                   uint64_t n, float* c) {
     if (m * n == 0) return REATTN_OK;
     CU(ctx, launch_matmul(a, b, m, k, n, c, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_rmsnorm(reattn_ctx* ctx, const float* x_dev, uint64_t rows, uint64_t cols, const float* w_dev,
+                   float* out_dev) {
+    if (rows == 0 || cols == 0) return REATTN_OK;
+    CU(ctx, launch_rmsnorm(x_dev, rows, cols, w_dev, out_dev, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_silu_mul(reattn_ctx* ctx, float* gate_dev, const float* up_dev, uint64_t n) {
+    if (n == 0) return REATTN_OK;
+    CU(ctx, launch_silu_mul(gate_dev, up_dev, n, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_stable_softmax(reattn_ctx* ctx, const float* logits_dev, uint64_t n, float* out_dev) {
+    if (n == 0) return set_err(ctx, REATTN_EINVAL, "empty logits");
+    if (n >= (1ull << 31)) return set_err(ctx, REATTN_EINVAL, "stable_softmax: too many logits");
+    int rc = ensure_arena(ctx, n * sizeof(double) + 256);
+    if (rc) return rc;
+    CU(ctx, launch_stable_softmax(logits_dev, n, out_dev, (double*)ctx->arena, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return REATTN_OK;
+}
+
+int reattn_attention_entropy(reattn_ctx* ctx, const float* weights_dev, uint64_t n, double* entropy_out_dev) {
+    if (n >= (1ull << 31)) return set_err(ctx, REATTN_EINVAL, "attention_entropy: too many weights");
+    if (n == 0) {
+        CU(ctx, cudaMemsetAsync(entropy_out_dev, 0, sizeof(double), ctx->stream));
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+        return REATTN_OK;
+    }
+    int rc = ensure_arena(ctx, n * sizeof(double) + 256);
+    if (rc) return rc;
+    CU(ctx, launch_attention_entropy(weights_dev, n, entropy_out_dev, (double*)ctx->arena, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     return REATTN_OK;
 }

@@ -146,6 +146,57 @@ __global__ void naive_select_kernel(const float* scores, uint32_t count, uint32_
 
 int grid_of(uint64_t n) { return (int)std::min<uint64_t>((n + 255) / 256, 148 * 32); }
 
+// softmax.hpp:13-27 stable_softmax of one vector, one CTA: the max, exp(l - max) in f64 for
+// every element in parallel, then the f64 sum in element order by one thread (the reference's
+// bits), then float(float(e) / sum)
+__global__ void __launch_bounds__(1024) softmax_kernel(const float* __restrict__ l, uint32_t n, float* out,
+                                                       double* scratch) {
+    __shared__ float s_max[32];
+    __shared__ double s_sum;
+    float m = -INFINITY;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) m = fmaxf(m, l[i]);
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < (blockDim.x >> 5) ? s_max[threadIdx.x] : -INFINITY;
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+        if (threadIdx.x == 0) s_max[0] = m;
+    }
+    __syncthreads();
+    const double mx = (double)s_max[0];
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double e = exp((double)l[i] - mx);
+        scratch[i] = e;
+        out[i] = (float)e;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+        for (uint32_t i = 0; i < n; ++i) sum += scratch[i];
+        s_sum = sum;
+    }
+    __syncthreads();
+    const double sum = s_sum;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = (float)((double)out[i] / sum);
+}
+
+// softmax.hpp:29-36 attention_entropy: -sum w ln w over w > 0 in element order, clamped at 0
+__global__ void __launch_bounds__(1024) entropy_kernel(const float* __restrict__ w, uint32_t n, double* out,
+                                                       double* scratch) {
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const float v = w[i];
+        scratch[i] = v > 0.0f ? (double)v * log((double)v) : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double h = 0.0;
+        for (uint32_t i = 0; i < n; ++i)
+            if (w[i] > 0.0f) h -= scratch[i];
+        *out = h < 0.0 ? 0.0 : h;
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_dot_f32(const float* a, const float* b, uint64_t n, uint64_t d, int lanes,
@@ -173,6 +224,16 @@ cudaError_t launch_group_mean(const float* q, uint64_t n_q, uint64_t n_heads, ui
                               uint64_t d, float* out, cudaStream_t s) {
     group_mean_kernel<<<grid_of(n_q * n_kv * d), 256, 0, s>>>(q, n_q, (uint32_t)n_heads,
                                                               (uint32_t)n_kv, (uint32_t)d, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stable_softmax(const float* l, uint64_t n, float* out, double* scratch, cudaStream_t s) {
+    softmax_kernel<<<1, 1024, 0, s>>>(l, (uint32_t)n, out, scratch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_attention_entropy(const float* w, uint64_t n, double* out, double* scratch, cudaStream_t s) {
+    entropy_kernel<<<1, 1024, 0, s>>>(w, (uint32_t)n, out, scratch);
     return cudaGetLastError();
 }
 

@@ -290,6 +290,9 @@ cudaError_t launch_embed(const uint32_t* tokens, uint64_t rows, const float* emb
 cudaError_t launch_rmsnorm(const float* x, uint64_t rows, uint64_t cols, const float* w, float* out,
                            cudaStream_t s);
 cudaError_t launch_silu_mul(float* gate, const float* up, uint64_t n, cudaStream_t s);
+// softmax.hpp utilities (scratch: n doubles)
+cudaError_t launch_stable_softmax(const float* l, uint64_t n, float* out, double* scratch, cudaStream_t s);
+cudaError_t launch_attention_entropy(const float* w, uint64_t n, double* out, double* scratch, cudaStream_t s);
 cudaError_t launch_argmax(const float* v, uint64_t n, uint32_t* out, cudaStream_t s);
 cudaError_t launch_scale(float* x, uint64_t n, float a, cudaStream_t s);
 // decode projections: y[N] = x[K] . W[K][N] (+ beta y), workspace sized for N <= n_max

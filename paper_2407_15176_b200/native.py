@@ -159,6 +159,10 @@ SIGNATURES = [
     ("reattn_plan_launch", C.c_int, [vp]),
     ("reattn_plan_launch_scan", C.c_int, [vp]),
     ("reattn_debug_trace", C.c_int, [C.POINTER(u64), u64]),
+    ("reattn_rmsnorm", C.c_int, [vp, vp, u64, u64, vp, vp]),
+    ("reattn_silu_mul", C.c_int, [vp, vp, vp, u64]),
+    ("reattn_stable_softmax", C.c_int, [vp, vp, u64, vp]),
+    ("reattn_attention_entropy", C.c_int, [vp, vp, u64, vp]),
     ("reattn_debug_gemv_workspace", C.c_size_t, [u64]),
     ("reattn_debug_gemv", C.c_int, [vp, vp, vp, u64, u64, u64, vp, C.c_float, vp]),
     ("reattn_plan_run_host", C.c_int, [vp, vp, vp]),
