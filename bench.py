@@ -406,7 +406,7 @@ def prefill_config3_line(ctx) -> dict:
     try:
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         import bench_prefill_layer as bpl
-        a = argparse.Namespace(ctx=256 * 1024, chunk=4096, every=1, start=0)
+        a = argparse.Namespace(ctx=256 * 1024, chunk=4096, every=1, start=0, stop=1 << 30)
         r = bpl.run(ctx, a)
         r.pop("last_chunk", None)
         return r

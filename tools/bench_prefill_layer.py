@@ -52,12 +52,13 @@ def run(ctx, args) -> dict:
         return e0.elapsed_time(e1)
 
     ctx.set_prefill(N.PREFILL_TENSOR)
+    start, stop = getattr(args, "start", 0), getattr(args, "stop", 1 << 30)
     rows = []
     prev = 0
     for ci, end in enumerate(ends):
         n_q = end - prev
         timed = ci == 0 or ci == len(ends) - 1 or ci % args.every == 0
-        if timed and args.start <= ci <= args.stop:
+        if timed and start <= ci <= stop:
             dbg = (lambda *m: print(ci, *m, file=sys.stderr, flush=True)) if os.environ.get("VERBOSE") else (lambda *m: None)
             cache.set_total(end)
             plan = N.Plan(ctx, cache, rope, n_q, nh, cfg)
@@ -82,7 +83,7 @@ def run(ctx, args) -> dict:
             del plan
         prev = end
     ctx.set_prefill(N.PREFILL_DEFAULT)
-    if args.start or args.stop < len(ends) - 1:  # debugging / profiling a few chunks: no total
+    if start or stop < len(ends) - 1:  # debugging / profiling a few chunks: no total
         return {"rows": rows}
     # interpolate untimed chunks linearly in the chunk index between timed neighbours
     timed_idx = [r["chunk"] for r in rows]
