@@ -467,7 +467,13 @@ cudaError_t launch_vote_large(const SelectArgs& a, void* ws, cudaStream_t s) {
         cudaError_t e = launch_vote_sorted(a, ws, s);
         if (e != cudaSuccess) return e;
     }
-    // spans + scope from the device-resident winners
+    // spans + scope from the device-resident winners (the standalone vote / tally APIs ask
+    // for neither)
+    if (!a.span_b) {  // the header's error field is the select's to write: clear it here
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        return cudaMemsetAsync(&a.hdr->error, 0, sizeof(a.hdr->error), s);
+    }
     SelectArgs b = a;
     b.cand_idx = nullptr;
     b.cand_score = nullptr;

@@ -364,6 +364,34 @@ def test_vote_large_candidate_sets(ctx):
         assert np.array_equal(w.cpu().numpy()[:nw].astype(np.uint64), want), n
 
 
+def test_tally_large_unbounded_indices(ctx):
+    """reattn_tally over > 8192 candidates with indices spread over the whole u32 range (the
+    standalone path: hand-written radix sorts): every distinct index once, ranked by (votes
+    desc, max score desc, index asc) as the oracle's vote with k' = n, with its vote count and
+    max score (selection.hpp:252-286)."""
+    rng = np.random.default_rng(91)
+    for n, span in ((9000, 2500), (40000, 40000)):
+        base = rng.integers(0, 1 << 31, span).astype(np.uint64)
+        idx = base[rng.integers(0, span, n)]
+        score = (rng.integers(0, 3000, n) / 1500.0 - 1.0).astype(np.float32)
+        want = ob.vote(idx, score, n)
+        io = torch.zeros(n, dtype=torch.int32, device="cuda")
+        vo = torch.zeros(n, dtype=torch.int32, device="cuda")
+        so = torch.zeros(n, dtype=torch.float32, device="cuda")
+        nu = ctx.tally(dev(idx.astype(np.uint32).view(np.int32)), dev(score), io, vo, so)
+        got = io.cpu().numpy()[:nu].view(np.uint32).astype(np.uint64)
+        assert np.array_equal(got, want), n
+        uniq, counts = np.unique(idx, return_counts=True)
+        cnt = dict(zip(uniq.tolist(), counts.tolist()))
+        mx = {}
+        for i, sc in zip(idx.tolist(), score.tolist()):
+            mx[i] = max(mx.get(i, -np.inf), sc)
+        v = vo.cpu().numpy()[:nu]
+        sv = so.cpu().numpy()[:nu]
+        for j in range(0, nu, max(1, nu // 500)):
+            assert v[j] == cnt[int(got[j])] and sv[j] == np.float32(mx[int(got[j])]), (n, j)
+
+
 def test_attend_step_prefill_chunk_large_vote(ctx):
     """test_engine.cpp-style k = k' = 100 prefill chunk: 2 x 100 x 100 = 20,000 candidates."""
     cfg = N.SelectionConfig(k=100, k_prime=100, span_m=16, l_global=16, l_local=256, l_chunk=128)
