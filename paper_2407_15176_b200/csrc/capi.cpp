@@ -921,7 +921,6 @@ int reattn_naive_topk(reattn_ctx* ctx, const float* q_dev, uint64_t n_q, uint64_
     if (n_kv == 0 || n_heads % n_kv != 0)
         return set_err(ctx, REATTN_EINVAL, "naive_topk_scores: n_heads must be a multiple of kv heads");
     if (k == 0) return set_err(ctx, REATTN_EINVAL, "selection: k must be >= 1");
-    if (k > 64) return set_err(ctx, REATTN_EINVAL, "naive_topk_scores: k exceeds device capacity (64)");
     if (count >= (1ull << 32)) return set_err(ctx, REATTN_EINVAL, "naive_topk_scores: middle too long");
     if (n_out) *n_out = std::min(k, count);
     // the reference's meter (selection_reference.hpp:37-41): mq + the score matrix (+ its

@@ -103,24 +103,28 @@ __global__ void naive_scores_kernel(const float* mq, uint32_t n_q, uint32_t n_kv
     }
 }
 
-// one CTA per (kv, q) row: k rounds of block argmax under (score desc, index asc), skipping the
-// entries already taken
+// one CTA per (kv, q) row: k rounds of block argmax under (score desc, index asc), each round
+// the best entry strictly behind the previous round's pick (the order is total: indices are
+// distinct), so any k needs no record of the entries taken
 __global__ void naive_select_kernel(const float* scores, uint32_t count, uint32_t kk, uint32_t k,
                                     uint32_t* idx_out, float* score_out) {
     const uint64_t row = blockIdx.x;
     const float* s = scores + row * count;
-    __shared__ uint32_t taken[64];
     __shared__ float ws[32];
     __shared__ uint32_t wi[32];
+    __shared__ float s_ps;
+    __shared__ uint32_t s_pi;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    float ps = INFINITY;  // previous pick (score, index); none yet
+    uint32_t pi = kNoIndex;
     for (uint32_t r = 0; r < kk; ++r) {
         float bs = -INFINITY;
         uint32_t bi = kNoIndex;
         for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
-            bool skip = false;
-            for (uint32_t t = 0; t < r; ++t) skip |= taken[t] == i;
-            if (!skip && better(s[i], i, bs, bi)) {
-                bs = s[i];
+            const float v = s[i];
+            const bool behind = pi == kNoIndex || better(ps, pi, v, i);
+            if (behind && better(v, i, bs, bi)) {
+                bs = v;
                 bi = i;
             }
         }
@@ -135,12 +139,15 @@ __global__ void naive_select_kernel(const float* scores, uint32_t count, uint32_
             bi = lane < nw ? wi[lane] : kNoIndex;
             warp_best(bs, bi);
             if (lane == 0) {
-                taken[r] = bi;
                 idx_out[row * k + r] = bi;
                 score_out[row * k + r] = bs;
+                s_ps = bs;
+                s_pi = bi;
             }
         }
         __syncthreads();
+        ps = s_ps;
+        pi = s_pi;
     }
 }
 

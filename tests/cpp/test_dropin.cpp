@@ -666,7 +666,7 @@ static void test_dense_and_naive() {
     // (test_selection.cpp:89-103); its scratch grows with the middle, the fused one's does not
     std::size_t naive_small = 0, naive_large = 0, fused_small = 0, fused_large = 0;
     for (std::size_t count : {0, 1, 4, 5, 127, 1000, 2049, 10000}) {
-        for (std::size_t k : {1, 4, 8}) {
+        for (std::size_t k : {1, 4, 8, 100}) {  // k > 64: the naive select has no capacity limit
             const std::size_t n_kv = 2, nh = 4, d = 32;
             std::vector<std::vector<float>> heads(n_kv, std::vector<float>(std::max<std::size_t>(1, count) * d));
             for (auto& h : heads)
