@@ -364,6 +364,18 @@ def test_vote_large_candidate_sets(ctx):
         assert np.array_equal(w.cpu().numpy()[:nw].astype(np.uint64), want), n
 
 
+def test_vote_small_path_large_k_prime(ctx):
+    """<= 8192 candidates (the shared-memory select) with k' up to the candidate count."""
+    rng = np.random.default_rng(17)
+    for n, span, kp in ((8192, 9000, 8192), (5000, 300, 4000), (3000, 3000, 2999)):
+        idx = rng.integers(0, span, n).astype(np.uint64)
+        score = (rng.integers(0, 5000, n) / 2500.0 - 1.0).astype(np.float32)
+        want = ob.vote(idx, score, kp)
+        w = torch.zeros(kp, dtype=torch.int32, device="cuda")
+        nw = ctx.vote(dev(idx.astype(np.int32)), dev(score), kp, w)
+        assert np.array_equal(w.cpu().numpy()[:nw].astype(np.uint64), want), (n, kp)
+
+
 def test_tally_large_unbounded_indices(ctx):
     """reattn_tally over > 8192 candidates with indices spread over the whole u32 range (the
     standalone path: hand-written radix sorts): every distinct index once, ranked by (votes
