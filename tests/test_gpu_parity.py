@@ -272,6 +272,31 @@ def test_attend_step_llama_geometry_bf16(ctx, total):
     assert bool(res.stats.coverage_total) == bool(st.coverage_total)
 
 
+@pytest.mark.parametrize("n_kv,nh,d,dtype,total", [(96, 96, 128, N.BF16, 20000),  # > 64 kv heads
+                                                    (8, 32, 64, N.BF16, 30000),     # d = 64
+                                                    (4, 16, 256, N.F32, 12000),     # d = 256
+                                                    (2, 14, 128, N.BF16, 50000)])   # group 7
+def test_attend_step_decode_geometries(ctx, n_kv, nh, d, dtype, total):
+    """Decode steps away from the LLaMA geometry: more than 64 kv heads (the decode
+    attention's per-head tickets), head dims 64 / 256 (the generic scan and
+    attention), group 7 -- spans, L' and outputs against the oracle; then a plan replayed
+    twice on the same cache."""
+    cfg = N.SelectionConfig()
+    res, out, st, spans = step_vs_oracle(ctx, n_kv, nh, d, total, cfg, dtype, 333 + d, 8192)
+    assert res.stats.scope_len == st.scope_len
+    assert np.array_equal(res.spans[0], spans[0]) and np.array_equal(res.spans[1], spans[1])
+    assert np.abs(res.out.cpu().numpy() - out).max() <= ATTN_TOL
+    cache, _, _ = make_cache(ctx, n_kv, d, total, cfg, dtype, 333 + d)
+    rope = N.Rope(ctx, d, 500000.0, 8192)
+    plan = N.Plan(ctx, cache, rope, 1, nh, cfg)
+    plan.q.copy_(dev(synth.uniform(333 + d + 7, nh * d).reshape(1, nh * d)))
+    for _ in range(2):
+        plan.launch()
+        r = plan.result(cfg.k_prime)
+        assert r.stats.scope_len == st.scope_len
+        assert np.abs(r.out.cpu().numpy() - out).max() <= ATTN_TOL
+
+
 @pytest.mark.parametrize("case", range(8))
 def test_attend_step_toy_geometries(ctx, case):
     """test_engine.cpp toy_selection-like configs, fp32 caches, prefill-sized n_q, both span
