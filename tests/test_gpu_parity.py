@@ -297,6 +297,21 @@ def test_attend_step_decode_geometries(ctx, n_kv, nh, d, dtype, total):
         assert np.abs(r.out.cpu().numpy() - out).max() <= ATTN_TOL
 
 
+@pytest.mark.parametrize("k,n_q,total", [(4, 160, 16000), (16, 96, 12000), (4, 129, 5000), (4, 256, 4200)])
+def test_attend_step_prefill_default_mode(ctx, k, n_q, total):
+    """A fresh context's prefill path (REATTN_PREFILL_TENSOR: the tcgen05 score GEMM where
+    k <= 8, the exact scan otherwise; tcgen05 scope attention) against the oracle: spans and
+    L' exactly, outputs within 2e-4 (north_star bf16 bar 1e-2); a middle that is empty or
+    shorter than k' spans included."""
+    c = N.Context(0)  # default prefill mode
+    cfg = N.SelectionConfig(k=k)
+    res, out, st, spans = step_vs_oracle(c, 8, 32, 128, total, cfg, N.BF16, 900 + k + n_q, 8192,
+                                         base=1e6, n_q=n_q)
+    assert res.stats.scope_len == st.scope_len
+    assert np.array_equal(res.spans[0], spans[0]) and np.array_equal(res.spans[1], spans[1])
+    assert np.abs(res.out.cpu().numpy() - out).max() <= 2e-4
+
+
 @pytest.mark.parametrize("case", range(8))
 def test_attend_step_toy_geometries(ctx, case):
     """test_engine.cpp toy_selection-like configs, fp32 caches, prefill-sized n_q, both span
