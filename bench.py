@@ -558,7 +558,7 @@ def run_sharded(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl")
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     dev = f"cuda:{local}"
     stream = torch.cuda.Stream(device=dev)
     ctx = N.Context(local, stream=stream.cuda_stream)

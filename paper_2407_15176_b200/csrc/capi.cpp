@@ -489,6 +489,15 @@ int capture_plan(reattn_plan* p) {
     return REATTN_OK;
 }
 
+}  // namespace
+
+namespace reattn_capi {
+
+bool zero_copy_enabled() {
+    static const bool off = std::getenv("REATTN_NO_ZERO_COPY") != nullptr;
+    return !off;
+}
+
 bool host_pinned(const void* p) {
     cudaPointerAttributes at;
     if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -541,6 +550,10 @@ int build_io_exec(reattn_ctx* ctx, cudaGraph_t body, const float* const* in_src,
     return REATTN_OK;
 }
 
+}  // namespace reattn_capi
+
+namespace {
+
 // the plan's I/O graph for these host pointers (rebuilt when they, the append mode or the
 // plan graph change)
 int ensure_io_graph(reattn_plan* p, const float* q_host, const float* k_host, const float* v_host,
@@ -560,10 +573,6 @@ int ensure_io_graph(reattn_plan* p, const float* q_host, const float* k_host, co
     return REATTN_OK;
 }
 
-bool zero_copy_enabled() {
-    static const bool off = std::getenv("REATTN_NO_ZERO_COPY") != nullptr;
-    return !off;
-}
 
 // A plan replays the graph it captured: the cache storage must be the one it was built over
 // (reserve reallocates), and a frozen plan also its length (replays used to attend

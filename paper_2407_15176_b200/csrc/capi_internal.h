@@ -103,6 +103,12 @@ inline int ensure_arena(reattn_ctx* ctx, size_t bytes) {
 // enqueue the device mirror of cache->total (stream-ordered with the plans that read it)
 // reattn_plan_stage_result on a given stream (the engine stages beside its main stream)
 extern "C" int plan_stage_result_on(reattn_plan* p, cudaStream_t s);
+// zero-copy host I/O around a captured graph (run_host / step_host on pinned buffers)
+bool zero_copy_enabled();
+bool host_pinned(const void* p);
+int build_io_exec(reattn_ctx* ctx, cudaGraph_t body, const float* const* in_src, float* const* in_dst,
+                  const uint64_t* in_n, int n_in, const float* out_src, float* out_dst, uint64_t out_n,
+                  cudaGraphExec_t* exec);
 
 inline int cache_sync_total(reattn_ctx* ctx, reattn_cache* c, cudaStream_t s) {
     if (c->dev_total) CU(ctx, launch_set_u32(c->dev_total, (uint32_t)c->total, s));
