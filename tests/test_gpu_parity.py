@@ -312,6 +312,59 @@ def test_attend_step_prefill_default_mode(ctx, k, n_q, total):
     assert np.abs(res.out.cpu().numpy() - out).max() <= 2e-4
 
 
+@pytest.mark.parametrize("seed", range(64))
+def test_attend_step_randomized_vs_oracle(ctx, seed):
+    """Random geometries and selection settings (kv heads, group, head dim, dtype, cache
+    length, k, k', span_m, both span modes, l_global, l_local, decode or a prefill block),
+    each against the oracle: spans and L' exactly, stats, outputs within 1e-6 (exact paths)
+    or 2e-4 (the tcgen05 prefill attention on bf16 d=128).  Errors must match too: when the
+    oracle raises (e.g. the query block longer than the scope) the device raises the same."""
+    rng = np.random.default_rng(1000 + seed)
+    n_kv = int(rng.choice([1, 2, 4, 8]))
+    group = int(rng.choice([1, 2, 3, 4]))
+    d = int(rng.choice([16, 32, 64, 128]))
+    dtype = N.BF16 if rng.random() < 0.6 else N.F32
+    l_local = int(rng.choice([16, 64, 256, 512]))
+    l_global = int(rng.integers(0, 65))
+    span_m = int(rng.choice([1, 4, 16, 32, 64]))
+    k = int(rng.integers(1, 9))
+    k_prime = int(rng.integers(0, 65))
+    window = 8192
+    while l_global + k_prime * span_m + l_local > window:
+        k_prime //= 2
+    n_q = 1 if rng.random() < 0.6 else int(rng.integers(2, min(64, l_local) + 1))
+    cfg = N.SelectionConfig(k=k, k_prime=k_prime, span_m=span_m, l_global=l_global, l_local=l_local,
+                            l_chunk=max(1, min(l_local, 128)), span_mode=int(rng.integers(0, 2)))
+    total = int(rng.integers(n_q, 20000))
+    nh = n_kv * group
+    label = (n_kv, nh, d, dtype, total, n_q, k, k_prime, span_m, l_global, l_local, cfg.span_mode)
+    ocfg = ob.SelectionConfig(cfg.k, cfg.k_prime, cfg.span_m, cfg.tile_size, cfg.l_global,
+                              cfg.l_local, cfg.l_chunk, cfg.span_mode)
+    cache, hk, hv = make_cache(ctx, n_kv, d, total, cfg, dtype, 2000 + seed)
+    rope = N.Rope(ctx, d, 10000.0, window)
+    q = synth.uniform(2100 + seed, n_q * nh * d).reshape(n_q, nh * d)
+    try:
+        out, st, spans = ob.attend_step(q, nh, hk, hv, total, ocfg, 10000.0, window)
+    except Exception as e:  # the reference's error: the device must raise it too
+        with pytest.raises(N.ReattnError):
+            N.attend_step(ctx, cache, rope, dev(q), nh, cfg)
+        return
+    res = N.attend_step(ctx, cache, rope, dev(q), nh, cfg)
+    assert res.stats.scope_len == st.scope_len, label
+    assert np.array_equal(res.spans[0], spans[0]) and np.array_equal(res.spans[1], spans[1]), label
+    tol = 2e-4 if (n_q > 1 and dtype == N.BF16 and d == 128) else ATTN_TOL
+    assert np.abs(res.out.cpu().numpy() - out).max() <= tol, label
+    # the same step as a plan (decode plans follow the device cache length), replayed twice
+    plan = N.Plan(ctx, cache, rope, n_q, nh, cfg)
+    plan.q.copy_(dev(q))
+    for _ in range(2):
+        plan.launch()
+        r = plan.result(max(1, k_prime))
+        assert r.stats.scope_len == st.scope_len, label
+        assert np.array_equal(r.spans[0], spans[0]) and np.array_equal(r.spans[1], spans[1]), label
+        assert np.abs(r.out.cpu().numpy() - out).max() <= tol, label
+
+
 @pytest.mark.parametrize("case", range(8))
 def test_attend_step_toy_geometries(ctx, case):
     """test_engine.cpp toy_selection-like configs, fp32 caches, prefill-sized n_q, both span
