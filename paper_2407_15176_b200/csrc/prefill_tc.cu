@@ -164,9 +164,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint64_t* q_full = bars;
     uint64_t* full = bars + 1;
     uint64_t* empty = full + kPStages;
-    uint64_t* tfull = empty + kPStages;   // [kPPairs]: both query tiles' accumulators ready
-    uint64_t* tempty = tfull + kPPairs;
-    uint32_t* s_tmem = (uint32_t*)(tempty + kPPairs);
+    // per (pair, query tile): the MMA and the two query tiles' epilogue warps run as two
+    // independent pipelines over the shared K stages, so a slow warp of one query tile does
+    // not hold back the other's next accumulator
+    uint64_t* tfull = empty + kPStages;   // [kPPairs][kPQT]: accumulator ready
+    uint64_t* tempty = tfull + kPPairs * kPQT;
+    uint32_t* s_tmem = (uint32_t*)(tempty + kPPairs * kPQT);
     float* s_thr = (float*)((uint8_t*)bars + 256);  // [kPQT][2 halves][128] KT-th best S_hi
     uint8_t* aux = s_k;  // half-merge lists, after the tile loop (the K ring is idle then)
 
@@ -183,9 +186,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);  // MMA commit: the stage has been read
         }
-        for (int b = 0; b < kPPairs; ++b) {
+        for (int b = 0; b < kPPairs * kPQT; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], kPEpi * 32);
+            mbar_init(&tempty[b], kPEpi * 32 / kPQT);
         }
         fence_barrier_init();
     }
@@ -230,13 +233,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const uint32_t ph = (t / kPStages) & 1u;
                 const int p = t % kPPairs;
                 const uint32_t pph = (t / kPPairs) & 1u;
-                if (t >= kPPairs) mbar_wait(&tempty[p], pph ^ 1u);
                 mbar_wait(&full[s], ph);
-                tc_fence_after();
                 const uint32_t kbase = smem_u32(s_k + (size_t)s * kPKBytes);
-                if (!a.no_mma)
 #pragma unroll
-                    for (int qt = 0; qt < kPQT; ++qt) {
+                for (int qt = 0; qt < kPQT; ++qt) {
+                    if (t >= kPPairs) mbar_wait(&tempty[p * kPQT + qt], pph ^ 1u);
+                    tc_fence_after();
+                    if (!a.no_mma) {
                         const uint32_t d_tmem = tmem + (uint32_t)((p * kPQT + qt) * kPN);
 #pragma unroll
                         for (int kb = 0; kb < 2; ++kb)
@@ -247,8 +250,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
                                 mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | ks) ? 1u : 0u);
                             }
                     }
-                mma_commit(&empty[s]);  // K stage consumed
-                mma_commit(&tfull[p]);  // both accumulators ready for the epilogue
+                    mma_commit(&tfull[p * kPQT + qt]);  // this query tile's accumulator is ready
+                }
+                mma_commit(&empty[s]);  // K stage consumed (both query tiles' MMAs)
             }
         }
     } else {
@@ -292,7 +296,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             }
             const int p = t % kPPairs;
             const uint32_t pph = (t / kPPairs) & 1u;
-            mbar_wait(&tfull[p], pph);
+            mbar_wait(&tfull[p * kPQT + qt], pph);
             tc_fence_after();
             const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) +
                                    (uint32_t)((p * kPQT + qt) * kPN + half * 64);
@@ -303,7 +307,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 tmem_wait_ld();
                 if (r[0] == 0x7FFFFFFFu && r[63] == 0x7FFFFFFFu) dropped = 1.0f;
                 tc_fence_before();
-                mbar_arrive(&tempty[p]);
+                mbar_arrive(&tempty[p * kPQT + qt]);
                 continue;
             }
             // 8 group maxima, 32 columns at a time (register pressure)
@@ -385,12 +389,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty[p]);  // accumulator no longer read: the MMA warp may reuse it
+            mbar_arrive(&tempty[p * kPQT + qt]);  // accumulator no longer read: the MMA warp may reuse it
         }
         // merge the two column halves of each row (disjoint key sets): top L under better(),
         // anything pushed off the end raises `dropped`.  The K ring is idle now (every MMA
         // that read it has completed: its tfull commit was waited on above); query tile qt
         // uses its own part of it.
+        // every MMA has completed once both query tiles' warps have seen their last tfull:
+        // only then may the K ring be overwritten
+        named_bar_sync(2, kPEpi * 32);
         uint8_t* aq = aux + (size_t)qt * kPM * (kPL * 8 + 4);
         float* m_s = (float*)aq;                               // [128][L] scores
         uint32_t* m_i = (uint32_t*)(aq + kPM * kPL * 4);       // [128][L] indices
