@@ -615,11 +615,29 @@ __global__ void __launch_bounds__(256, 4) prefill_exact_merge_kernel(const Prefi
     const int n = m.splits * kPL;
     float* sc = s_sc[wib];
     uint32_t* ix = s_ix[wib];
-    for (int i = lane; i < n; i += 32) {
-        const size_t o = (((size_t)(i / kPL) * m.n_kv + kv) * m.n_qpad + query) * kPL + (i % kPL);
-        const uint32_t id = m.part_idx[o];
-        ix[i] = id;
-        sc[i] = id == kNoIndex ? -INFINITY : m.part_score[o];
+    {  // every list entry's index and score loaded before any is used (no dependent load)
+        constexpr int kU = kPMaxSplits * kPL / 32;
+        uint32_t id[kU];
+        float sv[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = lane + 32 * u;
+            id[u] = kNoIndex;
+            sv[u] = -INFINITY;
+            if (i < n) {
+                const size_t o = (((size_t)(i / kPL) * m.n_kv + kv) * m.n_qpad + query) * kPL + (i % kPL);
+                id[u] = m.part_idx[o];
+                sv[u] = m.part_score[o];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = lane + 32 * u;
+            if (i < n) {
+                ix[i] = id[u];
+                sc[i] = id[u] == kNoIndex ? -INFINITY : sv[u];
+            }
+        }
     }
     __syncwarp();
     // T: k rounds of "best list head" across the (sorted) part lists, lane s owns part s
