@@ -79,6 +79,20 @@ def build_decode(ctx, cid: int, total: int | None = None, extra_rows: int = 0):
     return cache, rope, plan, cfg, dict(c, total=total, cid=cid)
 
 
+def load_read_ceiling() -> dict | None:
+    """The read-only bandwidth of K1's own access pattern without its arithmetic (TMA boxes,
+    ring and CTA count of the scan; tools/micro/hbm_read.cu, committed measurement)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_hbm_read_ceiling.txt")) as f:
+            for line in f:
+                if line.startswith("tma 256r x 3 ef1 144 CTAs"):
+                    return {"gbs": float(line.split()[7]),
+                            "source": "profiles/r2_hbm_read_ceiling.txt (tools/micro/hbm_read.cu)"}
+    except Exception:
+        pass
+    return None
+
+
 def load_traffic() -> dict | None:
     """dram read+write bytes per scan launch from the committed ncu --set full capture."""
     try:
@@ -505,6 +519,10 @@ def run_ours(args) -> None:
                      "launch_us": scan_ms * 1000.0, "peak_source": peaks["source"],
                      "peak_note": "peak is the measured copy (read+write) bandwidth; the scan "
                                   "only reads, so frac can exceed 1",
+                     "read_ceiling_gbs": (load_read_ceiling() or {}).get("gbs"),
+                     "frac_of_read_ceiling": (achieved / load_read_ceiling()["gbs"]
+                                              if load_read_ceiling() else None),
+                     "read_ceiling_source": (load_read_ceiling() or {}).get("source"),
                      "share_of_step": scan_ms / ms_per_step},
         "e2e": {"value": e2e_us, "unit": UNIT,
                 "h2d_bytes_per_step": n_head * D * 4 + 2 * meta["n_kv"] * D * 4,
