@@ -45,11 +45,15 @@ struct FastCfg {
     // evenly loaded); thread 0 also issues the TMA loads, so ptxas keeps 255 registers per
     // thread for the 128-float query held in registers (9 warps would cap it at 168).
     static constexpr int ROWS = ESZ == 2 ? 256 : 128;
+    // fp32: two threads per key row, each summing four of the reference's eight lanes (half
+    // the query in registers), so the CTA keeps 8 warps like bf16 -- the merger CTA's merge
+    // and select run on 8 warps, and twice the loads are in flight per stage
+    static constexpr int ROW_THREADS = ESZ == 2 ? 1 : 2;
     static constexpr int NBOX = ROW_BYTES / 128;    // 128-byte TMA boxes per row
     static constexpr int BOX_ELEMS = 128 / ESZ;
     static constexpr int STAGE_BYTES = ROWS * ROW_BYTES;
     static constexpr int STAGES = 3;
-    static constexpr int CONSUMERS = ROWS;
+    static constexpr int CONSUMERS = ROWS * ROW_THREADS;
     static constexpr int CWARPS = CONSUMERS / 32;
     static constexpr int THREADS = CONSUMERS;  // thread 0 doubles as the TMA producer
     static constexpr int KMAX = 8;
@@ -281,14 +285,16 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
         for (uint32_t it = 0; it < (uint32_t)C::STAGES && t_begin + it < t_end; ++it) issue(it);
     }
     {
-        // ===== consumers: one key row per thread per tile =====
-        f2_t qv[C::D / 2];
+        // ===== consumers: one key row per thread (bf16) or per thread pair (fp32) per tile =====
+        constexpr int RT = C::ROW_THREADS;
+        const uint32_t rrow = (uint32_t)tid / RT, half = (uint32_t)tid % RT;
+        f2_t qv[C::D / 2 / RT];
         float ts[KMAX];
         uint32_t ti[KMAX];
         float thr = -INFINITY;
         topk_reset<KMAX>(ts, ti);
         uint32_t cur_kv = kNoIndex;
-        const uint32_t sw = (uint32_t)tid & 7u;
+        const uint32_t sw = rrow & 7u;
 
         auto flush = [&](uint32_t kv) {
             // warp-level top-k of the warp's 32 lists, then warp 0 merges the warps
@@ -366,44 +372,54 @@ __global__ void __launch_bounds__(FastCfg<KT>::THREADS, 1)
                     s_mq[tid] = __fmul_rn(acc, inv);
                 }
                 named_bar_sync(1, C::CONSUMERS);
+                if (RT == 1) {
 #pragma unroll
-                for (int p = 0; p < C::D / 2; ++p) qv[p] = f2_packf(s_mq[2 * p], s_mq[2 * p + 1]);
+                    for (int p = 0; p < C::D / 2 / RT; ++p) qv[p] = f2_packf(s_mq[2 * p], s_mq[2 * p + 1]);
+                } else {  // this thread's lanes 4h..4h+3: elements 8c + 4h + {0..3}
+#pragma unroll
+                    for (int c = 0; c < C::D / 8; ++c) {
+                        qv[(2 * c) % (C::D / 2 / RT)] = f2_packf(s_mq[8 * c + 4 * half], s_mq[8 * c + 4 * half + 1]);
+                        qv[(2 * c + 1) % (C::D / 2 / RT)] =
+                            f2_packf(s_mq[8 * c + 4 * half + 2], s_mq[8 * c + 4 * half + 3]);
+                    }
+                }
                 cur_kv = kv;
             }
             const int s = it % C::STAGES;
             const uint32_t ph = (it / C::STAGES) & 1u;
             mbar_wait(&full[s], ph);
-            const uint32_t row = j * C::ROWS + (uint32_t)tid;
-            if (row < fg.count) {
-                const uint32_t sbase =
-                    smem_u32(stages + (size_t)s * C::STAGE_BYTES) + (uint32_t)tid * 128u;
-                f2_t a0 = f2_pack(0u, 0u), a1 = a0, a2 = a0, a3 = a0;
+            const uint32_t row = j * C::ROWS + rrow;
+            const bool live = row < fg.count;  // the same for both threads of a row
+            const uint32_t sbase = smem_u32(stages + (size_t)s * C::STAGE_BYTES) + rrow * 128u;
+            f2_t a0 = f2_pack(0u, 0u), a1 = a0, a2 = a0, a3 = a0;
+            if (live) {
 #pragma unroll
                 for (int c = 0; c < C::D / 8; ++c) {
-                    f2_t k0, k1, k2, k3;
                     if (C::ESZ == 2) {
                         const int box = c >> 3, cb = c & 7;
                         const uint4 w = lds128(sbase + box * C::ROWS * 128 + (((uint32_t)cb ^ sw) << 4));
-                        k0 = bf16x2_to_f2(w.x);
-                        k1 = bf16x2_to_f2(w.y);
-                        k2 = bf16x2_to_f2(w.z);
-                        k3 = bf16x2_to_f2(w.w);
-                    } else {
-                        const int box = c >> 2, u0 = (c & 3) * 2;
-                        const uint32_t bb = sbase + box * C::ROWS * 128;
-                        const uint4 w0 = lds128(bb + (((uint32_t)u0 ^ sw) << 4));
-                        const uint4 w1 = lds128(bb + (((uint32_t)(u0 + 1) ^ sw) << 4));
-                        k0 = f2_pack(w0.x, w0.y);
-                        k1 = f2_pack(w0.z, w0.w);
-                        k2 = f2_pack(w1.x, w1.y);
-                        k3 = f2_pack(w1.z, w1.w);
+                        lane_step<LANES>(a0, qv[(4 * c + 0) % (C::D / 2 / RT)], bf16x2_to_f2(w.x));
+                        lane_step<LANES>(a1, qv[(4 * c + 1) % (C::D / 2 / RT)], bf16x2_to_f2(w.y));
+                        lane_step<LANES>(a2, qv[(4 * c + 2) % (C::D / 2 / RT)], bf16x2_to_f2(w.z));
+                        lane_step<LANES>(a3, qv[(4 * c + 3) % (C::D / 2 / RT)], bf16x2_to_f2(w.w));
+                    } else {  // 16 bytes: the row's elements 8c + 4h .. 8c + 4h + 3 (lanes 4h..4h+3)
+                        const int box = c >> 2, u = (c & 3) * 2 + (int)half;
+                        const uint4 w = lds128(sbase + box * C::ROWS * 128 + (((uint32_t)u ^ sw) << 4));
+                        lane_step<LANES>(a0, qv[(2 * c) % (C::D / 2 / RT)], f2_pack(w.x, w.y));
+                        lane_step<LANES>(a1, qv[(2 * c + 1) % (C::D / 2 / RT)], f2_pack(w.z, w.w));
                     }
-                    lane_step<LANES>(a0, qv[4 * c + 0], k0);
-                    lane_step<LANES>(a1, qv[4 * c + 1], k1);
-                    lane_step<LANES>(a2, qv[4 * c + 2], k2);
-                    lane_step<LANES>(a3, qv[4 * c + 3], k3);
                 }
-                const float score = lane_tree(a0, a1, a2, a3);
+            }
+            float score;
+            if (RT == 1) {
+                score = lane_tree(a0, a1, a2, a3);
+            } else {
+                // ((l0+l1)+(l2+l3)) on the even thread, ((l4+l5)+(l6+l7)) on the odd one, and
+                // their sum on both (IEEE addition commutes): the reference's tree, bit for bit
+                const float part = __fadd_rn(__fadd_rn(f2_lo(a0), f2_hi(a0)), __fadd_rn(f2_lo(a1), f2_hi(a1)));
+                score = __fadd_rn(part, __shfl_xor_sync(0xFFFFFFFFu, part, 1));
+            }
+            if (live && half == 0) {
                 if (score > thr) {
                     topk_insert<KMAX>(ts, ti, k, score, row);
                     thr = topk_threshold<KMAX>(ts, k);
