@@ -615,6 +615,8 @@ __global__ void __launch_bounds__(256, 4) prefill_exact_merge_kernel(const Prefi
     const int n = m.splits * kPL;
     float* sc = s_sc[wib];
     uint32_t* ix = s_ix[wib];
+    const float dsp = lane < m.splits ? m.part_dropped[(((size_t)lane * m.n_kv + kv) * m.n_qpad + query)]
+                                      : -INFINITY;
     {  // every list entry's index and score loaded before any is used (no dependent load)
         constexpr int kU = kPMaxSplits * kPL / 32;
         uint32_t id[kU];
@@ -673,11 +675,8 @@ __global__ void __launch_bounds__(256, 4) prefill_exact_merge_kernel(const Prefi
         if (lane == bl) ++pos;
     }
     const float w = T - 2.0f * m.dl[qrow] * __uint_as_float(m.kmax[kv]);
-    uint32_t rescan = 0;  // parts to re-scan exactly
-    for (int s = 0; s < m.splits; ++s) {
-        const float d = m.part_dropped[(((size_t)s * m.n_kv + kv) * m.n_qpad + query)];
-        if (d > -INFINITY && d >= w) rescan |= 1u << s;
-    }
+    // parts to re-scan exactly (bit s = lane s; the dropped values were loaded up front)
+    const uint32_t rescan = __ballot_sync(0xFFFFFFFFu, lane < m.splits && dsp > -INFINITY && dsp >= w);
     // compact the candidates (listed, S_hi >= w, part not re-scanned) to the front of ix
     int nc = 0;
     for (int i0 = 0; i0 < n; i0 += 32) {
